@@ -1,0 +1,79 @@
+"""Oracle: velocity moment, periodic 1D Poisson solve and cell-averaged E.  TEST INFRASTRUCTURE ONLY.
+
+  rho_i = 1 - dv * sum_j f_ij
+  30 phi_i - 16 (phi_{i+1} + phi_{i-1}) + (phi_{i+2} + phi_{i-2}) = 12 dx^2 rho_i
+        (printed "12 dx": reading #2 takes dx^2)
+  periodic null space: project rho to mean zero; phi normalised to mean zero
+  E_i = -[8 (phi_{i+1} - phi_{i-1}) - phi_{i+2} + phi_{i-2}] / (12 dx)
+        (printed with "+": reading #1 takes E = -d_x phi, consistent with
+         P:192)
+
+The linear system is LU-factorised once per (n, dx) and stored.  The singular
+periodic matrix is made regular by bordering it with the constraint sum(phi) = 0.
+"""
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+import scipy.linalg as sla
+
+G = 2
+
+
+def moment_rho(f_interior, dv_volume):
+    """rho = 1 - V_v sum over all velocity cells (V_v = product of velocity spacings,
+    P:1072).  Velocity axes are the trailing half of the axes."""
+    ndim = f_interior.ndim
+    vel_axes = tuple(range(ndim // 2, ndim))
+    return 1.0 - dv_volume * np.sum(f_interior, axis=vel_axes)
+
+
+def poisson_matrix(n):
+    """Periodic pentadiagonal matrix of eq. (discrete_potential)."""
+    if n < 5:
+        raise ValueError("periodic 5-point Poisson needs n >= 5")
+    A = np.zeros((n, n))
+    for i in range(n):
+        A[i, i] = 30.0
+        A[i, (i + 1) % n] += -16.0
+        A[i, (i - 1) % n] += -16.0
+        A[i, (i + 2) % n] += 1.0
+        A[i, (i - 2) % n] += 1.0
+    return A
+
+
+@functools.lru_cache(maxsize=16)
+def _bordered_lu(n):
+    """LU factors of [[A, 1], [1^T, 0]] (A periodic, singular with null space = constants)."""
+    A = poisson_matrix(n)
+    B = np.zeros((n + 1, n + 1))
+    B[:n, :n] = A
+    B[:n, n] = 1.0
+    B[n, :n] = 1.0
+    return sla.lu_factor(B)
+
+
+def solve_potential(rho, dx):
+    """Mean-zero phi solving the periodic system with the projected rho."""
+    rho = np.asarray(rho, dtype=np.float64)
+    n = rho.size
+    rho_proj = rho - rho.mean()                       # project out the null-space component
+    rhs = np.concatenate([12.0 * dx * dx * rho_proj, [0.0]])
+    sol = sla.lu_solve(_bordered_lu(n), rhs)
+    return sol[:n]
+
+
+def efield_from_potential(phi, dx):
+    """E_i = -D4 phi (reading #1), periodic."""
+    p = lambda s: np.roll(phi, -s)   # p(s)[i] = phi[i+s]
+    return -(8.0 * (p(1) - p(-1)) - p(2) + p(-2)) / (12.0 * dx)
+
+
+def efield_from_rho(rho, dx):
+    return efield_from_potential(solve_potential(rho, dx), dx)
+
+
+def ghost_periodic(a, g=G):
+    """Periodic ghost extension of a configuration-space array along every axis."""
+    return np.pad(a, [(g, g)] * a.ndim, mode="wrap")
