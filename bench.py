@@ -1,0 +1,278 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 phase-space cell-updates/s per RK4 step of the uniform 1D+1V Vlasov-Poisson hot
+path (BASELINE.json metric) on the C4 workload (2048 x 4096 bump-on-tail, 64x64 patches), plus the
+achieved HBM bandwidth of the dominant kernel (the fused RK4 stage kernel) against the measured
+B200 copy bandwidth.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--workload C4]
+
+N > 1 runs under torchrun: every rank advances its own C4 problem (replicas; see DESIGN.md
+"Multi-GPU"), the time is the max over ranks, value = all cells updated / time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# algorithmic DRAM bytes per cell of the fused stage kernel:
+#   stage 1: read f_n, write f2                    16 B
+#   stage 2: read f2, f_n; write u, f3             32 B
+#   stage 3: read f3, f_n; write f4                24 B
+#   stage 4: read f4, u, f_n; write f_{n+1}        32 B
+STAGE_BYTES = {1: 16, 2: 32, 3: 24, 4: 32}
+STEP_BYTES = sum(STAGE_BYTES.values())          # 104 B per cell per RK4 step
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_baseline(workload_name, budget_s=20.0):
+    """Oracle (as it stands) on the host: full-size C4 RK4 steps until ~budget_s."""
+    import inputs
+    from oracle import uniform
+    w = inputs.get(workload_name)
+    prob = uniform.problem_for(w)
+    f = inputs.initial_cell_averages(w)
+    dt = inputs.fixed_dt(w)
+    E_bc = prob.constraints(f)
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        f, E_bc, _ = prob.step(f, E_bc, dt)
+        steps += 1
+        if time.perf_counter() - t0 > budget_s or steps >= 3:
+            break
+    el = time.perf_counter() - t0
+    return {"value": w.cells * steps / el, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+            "sample": f"{steps} full-size {workload_name} RK4 step(s) of the numpy fp64 oracle "
+                      f"({w.ncells[0]}x{w.ncells[1]}), {el:.1f} s, single thread"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    base = cpu_baseline(args.workload, budget_s=max(5.0, 60.0 / max(1, args.steps + args.warmup)))
+    import inputs
+    w = inputs.get(args.workload)
+    line = {"impl": "reference", "metric": "fp64 phase-space cell-updates/s per RK4 step",
+            "value": base["value"], "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * w.cells / base["value"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "cells": w.cells, "grid": list(w.ncells)},
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="C4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    assert args.warmup >= 3, "warm-up must be >= 3 steps"
+
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    from paper_1204_3853_b200 import api
+    from paper_1204_3853_b200.solver import UniformVlasov1D
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = inputs.get(args.workload)
+    h = inputs.spacing(w)
+    dt = inputs.fixed_dt(w)
+    f0 = inputs.initial_cell_averages(w)
+    S = UniformVlasov1D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w))
+    S.set_state(f0)
+    S.capture(dt, steps=1)                       # one warm-up step inside
+    for _ in range(args.warmup - 1):
+        S.replay()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- device-timed region
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(S.stream)
+    for _ in range(args.steps):
+        S.replay()
+    ev1.record(S.stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = w.cells * world * args.steps / (ms / 1e3)
+
+    # ---------------------------------------------------------------- dominant-kernel timing
+    # eager replay of the same launches with events bracketing every stage kernel on its stream
+    with torch.cuda.stream(S.stream):
+        ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(4)]
+              for _ in range(args.steps)]
+        L = S.level.h
+        barrier()
+        for k in range(args.steps):
+            for s in (1, 2, 3, 4):
+                f_s, f_next = {1: (S.A, S.B), 2: (S.B, S.C), 3: (S.C, S.B), 4: (S.B, S.A)}[s]
+                E_cur, E_bc = (S.E[1], S.E[0]) if s % 2 == 1 else (S.E[0], S.E[1])
+                api.vlasov_reduce_moment([L], None, S.partials, S.rho)
+                S._field(E_cur)
+                api.vlasov_fill_ghosts(L, f_s, None, None, E_bc, S.f0v)
+                ev[k][s - 1][0].record(S.stream)
+                api.vlasov_rk4_stage(L, s, dt, S.A, f_s, S.U, f_next, E_cur, S.recon, S.partials)
+                ev[k][s - 1][1].record(S.stream)
+        barrier()
+    stage_ms = np.array([[a.elapsed_time(b) for a, b in row] for row in ev])      # (steps, 4)
+    per_stage_avg = stage_ms.mean(axis=0)
+    kern_ms_step = float(per_stage_avg.sum())
+    achieved = STEP_BYTES * w.cells / (kern_ms_step / 1e3) / 1e9                   # GB/s over the 4 launches
+    peak, peak_kind = read_peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "stage_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_step_per_cell")
+            traffic = None if traffic is None else float(traffic) * w.cells
+        except Exception:
+            traffic = None
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nE = max(3, args.steps // 4)
+    h2d_bytes = S.A.numel() * 8
+    d2h_bytes = S.A.numel() * 8
+    host_state = torch.empty(S.A.numel(), dtype=torch.float64).pin_memory()
+    host_state.copy_(S.A)
+    barrier()
+    with torch.cuda.stream(S.stream):
+        e0.record(S.stream)
+        for _ in range(nE):
+            S.A.copy_(host_state, non_blocking=True)                 # H2D of the step's input state
+            S.graph.replay()
+            host_state.copy_(S.A, non_blocking=True)                 # D2H of the step's result
+        e1.record(S.stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / nE
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = w.cells * world / (e2e_ms / 1e3)
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(args.workload)
+    if rank == 0:
+        line = {
+            "metric": "fp64 phase-space cell-updates/s per RK4 step",
+            "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "grid": list(w.ncells), "patches": "64x64 (merged single block)",
+                       "cells": w.cells, "recon": "centered4", "dt": dt,
+                       "l2": "inputs larger than L2 (4 x 64 MiB fields per step > 126 MB)",
+                       "parallelism": f"replicas x{world}", "graph": "CUDA graph, 1 RK4 step (24 launches)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "k_stage_1d1v (4 launches per step)",
+                         "algorithmic_bytes_per_cell_step": STEP_BYTES,
+                         "stage_ms": [float(x) for x in per_stage_avg],
+                         "share_of_step": kern_ms_step / ms_step},
+            "e2e": {"value": e2e_value, "unit": "cell-updates/s", "h2d_bytes_per_step": h2d_bytes,
+                    "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms},
+            "gpu_launches": S.launches_per_step() * args.steps,
+            "clocks": clk,
+            "cpu_baseline": base,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

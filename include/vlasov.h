@@ -1,0 +1,227 @@
+/*
+ * vlasov.h -- C ABI of libvlasov, the B200 (sm_100a, fp64) hot path of the block-structured
+ * AMR Vlasov-Poisson method of Hittinger & Banks, arXiv:1204.3853.
+ *
+ * Citations "P:n" are lines of the paper's text; "reading #k" refers to the list of
+ * interpretations of garbled / silent passages in DESIGN.md.
+ *
+ * ---- Conventions -----------------------------------------------------------------------------
+ * Status:     every int-returning call returns VLASOV_OK (0) or a negative VLASOV_E* code; the
+ *             message of the last failure on the calling host thread is vlasov_last_error().
+ *             Kernel faults are asynchronous: they surface as VLASOV_ECUDA at a later call.
+ * Ownership:  every phase-space or configuration-space FIELD array (f, k, u, E, rho, partials,
+ *             flux registers, tags) is a caller-owned DEVICE buffer of the length reported by
+ *             vlasov_level_get_info(), passed as a raw pointer.  The library owns only level
+ *             metadata (box lists, tiles, ghost/transfer task lists, Green's functions) on host and
+ *             device; it is freed by the matching *_destroy.  No call other than *_create
+ *             allocates device memory.
+ * Streams:    a level (and a Poisson plan) is bound to the cudaStream_t given at creation (passed
+ *             as void*; NULL = legacy default stream).  Every compute call is enqueued on that
+ *             stream and returns without synchronising, so the calls can be captured in a CUDA
+ *             graph.  Only *_create and the host queries block.  One host thread per level.
+ * Indexing:   phase space has D = 2*C dims, configuration dims first then velocity dims
+ *             (P:1056-1059); C = 1 (1D+1V) or C = 2 (2D+2V).  Boxes are inclusive [lo, hi]
+ *              in the level's own global index space; level l is refined by
+ *             ratio_to_level0 with respect to level 0.  Configuration dims are
+ *             periodic, velocity dims are truncated with the characteristic boundary condition
+ *             (P:222-231).  The velocity dim is the fastest-varying (contiguous) one.
+ * Layout:     a level stores its cells in one device array of fp64 with a ghost frame of G = 2
+ *             cells on every side of every storage block; vlasov_level_layout() reports, per
+ *             patch, the offset of the patch's interior cell `lo` and the strides (in doubles).
+ *             A level whose boxes exactly tile their bounding box is stored as ONE block (the
+ *             patches are then views into it); otherwise each patch is its own block.
+ * Precision:  all arithmetic is IEEE fp64.  No CPU fallback exists: without a CUDA device of
+ *             compute capability 10.0 every compute call returns VLASOV_ECUDA.
+ */
+#ifndef VLASOV_H
+#define VLASOV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------------------------------- */
+#define VLASOV_OK            0
+#define VLASOV_EINVAL       -1  /* bad argument or shape (empty box, nboxes < 1, n < 5 for Poisson) */
+#define VLASOV_ENOMEM       -2  /* host or device allocation failed                                 */
+#define VLASOV_ECUDA        -3  /* CUDA runtime / launch error, or no usable sm_100 device          */
+#define VLASOV_ENEST        -4  /* boxes overlap, leave the domain, or are not properly nested      */
+#define VLASOV_ESTALE       -5  /* a transfer between levels whose metadata no longer match         */
+#define VLASOV_ESTENCIL     -6  /* a coarse-fine stencil needs coarse data outside the coarse level */
+#define VLASOV_EUNSUPPORTED -7  /* valid request that this build does not implement                 */
+
+/* ---- options ----------------------------------------------------------------------------------- */
+enum { VLASOV_CENTERED4 = 0,   /* ideal weights 1/2, 1/2: centered 4th order face average */
+       VLASOV_UPWIND = 1 };    /* WENO provisional weights, larger weight upwind; #4-#5   */
+enum { VLASOV_LINEAR5 = 0,     /* unlimited quintic-stencil interpolation b_j(s); #12     */
+       VLASOV_WENO5 = 1 };     /* limited WENO5 conservative interpolation; #8-#10        */
+enum { VLASOV_GHOST_INTERIOR = 0, VLASOV_GHOST_SIBLING = 1, VLASOV_GHOST_COARSE = 2,
+       VLASOV_GHOST_PHYS = 3 };
+
+/* ---- plain data --------------------------------------------------------------------------------- */
+typedef struct { int32_t lo[4], hi[4]; } vlasov_box;   /* inclusive; entries >= ndim unused */
+
+typedef struct {
+    int32_t    ndim;        /* 2 (1D+1V) or 4 (2D+2V)                                         */
+    vlasov_box domain;      /* level-0 index domain, lo = 0                                  */
+    double     lower[4];    /* physical coordinate of the domain's lower corner              */
+    double     dx0[4];      /* level-0 mesh spacings                                          */
+} vlasov_geom;
+
+typedef struct {
+    int64_t field_doubles;    /* length of every phase-space field array of this level          */
+    int64_t e_doubles;        /* length of this level's E array: C * prod(ncfg_d + 4)             */
+    int64_t cfg_cells;        /* configuration cells of this level (prod ncfg_d)                 */
+    int64_t partial_doubles;  /* length of rho_partials accepted by vlasov_rk4_stage              */
+    int64_t fluxreg_doubles;  /* flux-register length of this level w.r.t. its coarser level      */
+    int64_t tag_bytes;        /* length of the tag array of vlasov_tag_cells (level domain)      */
+    int32_t nblocks, npatches, ntiles, ndim;
+    int32_t ratio[4];         /* ratio to level 0                                               */
+    int32_t ncfg[2];          /* configuration cells per config dim at this level               */
+    int32_t domain_cells[4];  /* level domain cells per dim                                      */
+} vlasov_level_info;
+
+typedef struct vlasov_level vlasov_level;
+typedef struct vlasov_poisson vlasov_poisson;
+
+/* ---- levels ------------------------------------------------------------------------------------- *
+ * Create the metadata of one refinement level from its box list (patch id = index
+ * in `boxes`).  Boxes must be disjoint and inside the level domain (refined level-0 domain);
+ * `coarser` (NULL for level 0) must be the next coarser level, and the level must be properly
+ * nested in it (Fig.1 caption): else VLASOV_ENEST / VLASOV_ESTENCIL.  Level 0 must
+ * tile the whole domain.  Builds the ghost-fill, coarse-fine, flux-register and average-down
+ * task lists and the stage-kernel tile table, uploads them to the device (on `stream`).       */
+int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4],
+                        const vlasov_box* boxes, int32_t nboxes, const vlasov_level* coarser,
+                        void* cuda_stream, vlasov_level** out);
+int vlasov_level_destroy(vlasov_level* level);
+int vlasov_level_get_info(const vlasov_level* level, vlasov_level_info* info);
+
+/* Offset (doubles) of patch `patch`'s interior cell `lo` in the level field array, and the
+ * strides (doubles) of that array per dim (entries >= ndim are 0).                             */
+int vlasov_level_layout(const vlasov_level* level, int32_t patch, int64_t* offset,
+                        int64_t strides[4]);
+
+/* Dense ghost map of patch `patch` over grow(box, 2), row-major (last dim fastest).  Host
+ * arrays of prod(size+4) entries.  kind[]: VLASOV_GHOST_*.  src_patch/src_cell:
+ *   INTERIOR: patch, row-major index in the patch box;
+ *   SIBLING : same-level patch holding the cell after the periodic wrap of the configuration
+ *             indices (may be `patch` itself), index of the wrapped cell in it;
+ *   COARSE  : coarser-level patch holding the coarse parent of the wrapped cell, index of that
+ *             parent in it;
+ *   PHYS    : -1, 2*(velocity dim number) + (0 low | 1 high) for the first velocity dim outside
+ *             the domain.
+ * Precedence (reading #15): PHYS, then SIBLING, then COARSE.                                   */
+int vlasov_level_ghost_map(const vlasov_level* level, int32_t patch, int32_t* kind,
+                           int32_t* src_patch, int64_t* src_cell);
+
+/* Alg.7 ComputeSubPatches of patch `patch` of levels[level_index] against all
+ * finer levels of the hierarchy `levels[0..nlev-1]`; boxes in the patch's index space, sorted
+ * lexicographically by (lo, hi).  *n receives the count; at most `cap` are written.          */
+int vlasov_subpatches(const vlasov_level* const* levels, int32_t nlev, int32_t level_index,
+                      int32_t patch, vlasov_box* out, int32_t cap, int32_t* n);
+
+/* ---- ghost fill (Alg.2) --------------------------- *
+ * Fill the ghost frame of every block of `level` in `f`: same-level and periodic copies, then
+ * coarse-fine interpolation from `f_coarse` on `coarser` (whose ghosts must be current;
+ * `interp` = VLASOV_LINEAR5 | VLASOV_WENO5, dimension by dimension, x first), then the
+ * characteristic velocity boundary condition: per configuration column the speed a_d = -E_d
+ * (E_bc: this level's E array, reading #6b) decides outgoing (cubic extrapolation, reading #6)
+ * or incoming / zero (the cell averages `f0v` of the unperturbed profile on the level's ghosted
+ * velocity range: (nv+4) doubles for 1V, (nvx+4)*(nvy+4) for 2V).                              */
+int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coarser,
+                       const double* f_coarse, const double* E_bc, const double* f0v,
+                       int32_t interp);
+
+/* ---- right-hand side and RK4 stage ------------------------------------------------- *
+ * vlasov_rhs: k = L(f) on every interior cell (face averages P:322-368, fluxes P:263-282 with
+ * the +1/48 reading #3, divergence P:246-250); `f` ghosts must be filled; `E` is this level's
+ * E array.  k has the level layout (ghost cells of k untouched).
+ *
+ * vlasov_rk4_stage: one stage of classic RK4 in the minimum-traffic rearrangement
+ * (identical to the flux-accumulation form P:399-410 in exact arithmetic):
+ *   stage 1: f_next = f_n + dt/2 k(f_n)                         (f_s == f_n)
+ *   stage 2: u = f_n + (f_s - f_n)/3 + dt/3 k(f_s);  f_next = f_n + dt/2 k(f_s)
+ *   stage 3: f_next = f_n + dt k(f_s)
+ *   stage 4: f_next = u + (f_s - f_n)/3 + dt/6 k(f_s)           (f_next may alias f_n)
+ * f_s ghosts must be filled.  If rho_partials != NULL the kernel also writes, for every
+ * configuration cell and every velocity tile, the sum of f_next over the tile
+ * (partial_doubles entries) for vlasov_reduce_moment.                                          */
+int vlasov_rhs(vlasov_level* level, const double* f, const double* E, double* k, int32_t recon);
+int vlasov_rk4_stage(vlasov_level* level, int32_t stage, double dt, double* f_n, const double* f_s,
+                     double* u, double* f_next, const double* E, int32_t recon,
+                     double* rho_partials);
+
+/* ---- reduction ------------------------------------------------------ *
+ * rho on the finest configuration mesh: rho = 1 - sum_levels dv_l sum_v f (reading #13).
+ * Single level with rho_partials != NULL: sums the fused per-tile partial sums of
+ * vlasov_rk4_stage in a fixed order.  Otherwise Alg.8 Sub-Patch Reduction over the hierarchy
+ * levels[0..nlev-1] with the (host array of) device field pointers f[l] whose x-ghosts must be
+ * current: per sub-patch, v-sums including 2 ghost columns in x (reading #16), linear5
+ * refinement to the finest x resolution, deposit; fixed summation order (level, patch,
+ * sub-patch).                                                                                   */
+int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
+                         const double* rho_partials, double* rho_finest);
+
+/* ---- periodic Poisson + E -------------------------------------------------------- *
+ * Plan for n >= 5 periodic cells of width dx (1D configuration space).  solve: projects rho to
+ * mean zero, solves 30 phi_i - 16(phi_{i+1}+phi_{i-1}) + (phi_{i+2}+phi_{i-2}) = 12 dx^2 rho_i
+ * (reading #2) with mean-zero phi, and E_i = -[8(phi_{i+1}-phi_{i-1}) - phi_{i+2} + phi_{i-2}]
+ * /(12 dx) (reading #1).  Implemented as circulant convolutions with the exact discrete
+ * Green's functions (computed on the host at plan creation).  phi or E may be NULL.             */
+int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisson** out);
+int vlasov_poisson_solve(vlasov_poisson* plan, const double* rho, double* phi, double* E);
+int vlasov_poisson_destroy(vlasov_poisson* plan);
+
+/* ---- injection ----------------------------------------------------------------- *
+ * E_lvl (this level's ghosted E array, 1D) from the finest configuration field E_finest of
+ * n_finest cells: mean of the R finest values per level cell, periodic ghosts.
+ * For 2D configuration space (prescribed field), E_finest holds C components of n_finest[0] x
+ * n_finest[1] cells.                                                                          */
+int vlasov_inject_field(vlasov_level* level, const double* E_finest, const int32_t n_finest[2],
+                        double* E_lvl);
+
+/* ---- AMR transfers -------------------------------------------------------------- *
+ * Flux registers of `fine` with respect to its coarser level: for every coarse face on the
+ * coarse-fine interface, regs += b_s * (F_coarse - mean of the overlying fine F) evaluated on
+ * the stage states (ghosts filled) with the stage field.  Zero them (cudaMemsetAsync) at the
+ * start of a step.  vlasov_average_down then applies the Alg.4 flux substitution to the coarse
+ * cells next to the interface (f_coarse += +-dt * regs / h) and replaces every coarse cell
+ * covered by `fine` by the mean of its fine cells (reading #14).  regs may be NULL
+ * in vlasov_average_down (plain average-down).                                                 */
+int vlasov_flux_register_accumulate(vlasov_level* fine, const double* f_fine, const double* E_fine,
+                                    const double* f_coarse, const double* E_coarse, double b_s,
+                                    double* regs, int32_t recon);
+int vlasov_average_down(vlasov_level* fine, const double* f_fine, double* f_coarse,
+                        const double* regs, double dt);
+
+/* ---- tagging and regrid -------------------------------------------- *
+ * tags[cell of the level domain] = (delta1 f + delta2 f > tol), dilated by `buffer` cells
+ * (Chebyshev, periodic in configuration dims, clipped in velocity); f ghosts must be filled;
+ * the level must tile its domain.  Evaluated without FMA contraction in the fixed order stated in
+ * DESIGN.md so that tags are bit-identical to the oracle's.                                      */
+int vlasov_tag_cells(vlasov_level* level, const double* f, double tol, int32_t buffer,
+                     uint8_t* tags);
+/* Host: fixed-tile rule of the C3 workload (reading #18): boxes of `tile` fine cells (fine =
+ * level domain refined by `ratio`) whose coarse footprint holds a tag; sorted lexicographically. */
+int vlasov_tags_to_boxes(const uint8_t* tags_host, const int32_t domain_cells[4], int32_t ndim,
+                         const int32_t ratio[4], int32_t tile, vlasov_box* out, int32_t cap,
+                         int32_t* n);
+/* Regrid data motion: interior of every patch of `level` (new) from `old` (same resolution,
+ * may be NULL) where the old patches overlap, else by conservative interpolation from
+ * `coarser` (ghosts of f_coarse current).                                                         */
+int vlasov_level_fill_from(vlasov_level* level, double* f, const vlasov_level* old,
+                           const double* f_old, const vlasov_level* coarser,
+                           const double* f_coarse, int32_t interp);
+
+/* ---- misc ------------------------------------------------------------------------------------ */
+const char* vlasov_last_error(void);
+int vlasov_device_ok(void);         /* 1 if a compute-capability 10.x device is current, else 0 */
+int vlasov_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VLASOV_H */

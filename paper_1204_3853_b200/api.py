@@ -1,0 +1,252 @@
+"""Thin Python binding of the libvlasov C ABI (include/vlasov.h): same names, argument marshalling
+only.  Field arguments are torch CUDA float64 tensors (or None); every compute step runs in the
+library's CUDA kernels on the level's stream.  PyTorch provides device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import Box, Geom, LevelInfo, check, lib
+
+__all__ = [
+    "Level", "Poisson", "make_geom", "vlasov_level_create", "vlasov_level_destroy",
+    "vlasov_level_get_info", "vlasov_level_layout", "vlasov_level_ghost_map", "vlasov_subpatches",
+    "vlasov_fill_ghosts", "vlasov_rhs", "vlasov_rk4_stage", "vlasov_reduce_moment",
+    "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
+    "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes",
+    "vlasov_level_fill_from", "vlasov_device_ok", "vlasov_last_error",
+]
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libvlasov fields must be CUDA tensors")
+    if t.dtype not in (torch.float64, torch.uint8):
+        raise ValueError("libvlasov fields are float64 (tags: uint8)")
+    if not t.is_contiguous():
+        raise ValueError("libvlasov fields must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream) if torch.cuda.is_available() else None
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def make_geom(ndim, ncells, lower, dx0) -> Geom:
+    g = Geom()
+    g.ndim = ndim
+    for d in range(4):
+        g.domain.lo[d] = 0
+        g.domain.hi[d] = (ncells[d] - 1) if d < ndim else 0
+        g.lower[d] = lower[d] if d < ndim else 0.0
+        g.dx0[d] = dx0[d] if d < ndim else 0.0
+    return g
+
+
+def _boxes(boxes) -> C.Array:
+    arr = (Box * len(boxes))()
+    for i, (lo, hi) in enumerate(boxes):
+        for d in range(4):
+            arr[i].lo[d] = lo[d] if d < len(lo) else 0
+            arr[i].hi[d] = hi[d] if d < len(hi) else 0
+    return arr
+
+
+# ----------------------------------------------------------------------------- raw names
+def vlasov_level_create(geom, ratio, boxes, coarser=None, stream=None):
+    out = C.c_void_p()
+    r = (C.c_int32 * 4)(*(list(ratio) + [1] * (4 - len(ratio))))
+    bx = _boxes(boxes)
+    check(lib.vlasov_level_create(C.byref(geom), r, bx, len(boxes), coarser, _stream_ptr(stream), C.byref(out)))
+    return out
+
+
+def vlasov_level_destroy(h):
+    return check(lib.vlasov_level_destroy(h))
+
+
+def vlasov_level_get_info(h) -> LevelInfo:
+    info = LevelInfo()
+    check(lib.vlasov_level_get_info(h, C.byref(info)))
+    return info
+
+
+def vlasov_level_layout(h, patch):
+    off = C.c_int64()
+    st = (C.c_int64 * 4)()
+    check(lib.vlasov_level_layout(h, patch, C.byref(off), st))
+    return off.value, tuple(st)
+
+
+def vlasov_level_ghost_map(h, patch, ncells_grown):
+    kind = np.zeros(ncells_grown, np.int32)
+    sp = np.zeros(ncells_grown, np.int32)
+    sc = np.zeros(ncells_grown, np.int64)
+    check(lib.vlasov_level_ghost_map(h, patch, kind.ctypes.data_as(_lib.PI32), sp.ctypes.data_as(_lib.PI32),
+                                     sc.ctypes.data_as(_lib.PI64)))
+    return kind, sp, sc
+
+
+def vlasov_subpatches(levels, level_index, patch, cap=4096):
+    arr = (C.c_void_p * len(levels))(*[l.value if isinstance(l, C.c_void_p) else l for l in levels])
+    out = (Box * cap)()
+    n = C.c_int32()
+    check(lib.vlasov_subpatches(arr, len(levels), level_index, patch, out, cap, C.byref(n)))
+    return [(tuple(out[i].lo), tuple(out[i].hi)) for i in range(min(n.value, cap))]
+
+
+def vlasov_fill_ghosts(h, f, coarser=None, f_coarse=None, E_bc=None, f0v=None, interp=_lib.LINEAR5):
+    return check(lib.vlasov_fill_ghosts(h, _ptr(f), coarser, _ptr(f_coarse), _ptr(E_bc), _ptr(f0v), interp))
+
+
+def vlasov_rhs(h, f, E, k, recon=_lib.CENTERED4):
+    return check(lib.vlasov_rhs(h, _ptr(f), _ptr(E), _ptr(k), recon))
+
+
+def vlasov_rk4_stage(h, stage, dt, f_n, f_s, u, f_next, E, recon=_lib.CENTERED4, rho_partials=None):
+    return check(lib.vlasov_rk4_stage(h, stage, float(dt), _ptr(f_n), _ptr(f_s), _ptr(u), _ptr(f_next), _ptr(E),
+                                      recon, _ptr(rho_partials)))
+
+
+def vlasov_reduce_moment(levels, f_list, rho_partials, rho_finest):
+    arr = (C.c_void_p * len(levels))(*[l.value if isinstance(l, C.c_void_p) else l for l in levels])
+    fp = (C.c_void_p * len(levels))(*[(t.data_ptr() if t is not None else None) for t in f_list]) \
+        if f_list is not None else None
+    return check(lib.vlasov_reduce_moment(arr, len(levels), fp, _ptr(rho_partials), _ptr(rho_finest)))
+
+
+def vlasov_poisson_create(n, dx, stream=None):
+    out = C.c_void_p()
+    check(lib.vlasov_poisson_create(n, float(dx), _stream_ptr(stream), C.byref(out)))
+    return out
+
+
+def vlasov_poisson_solve(p, rho, phi=None, E=None):
+    return check(lib.vlasov_poisson_solve(p, _ptr(rho), _ptr(phi), _ptr(E)))
+
+
+def vlasov_poisson_destroy(p):
+    return check(lib.vlasov_poisson_destroy(p))
+
+
+def vlasov_inject_field(h, E_finest, n_finest, E_lvl):
+    n = (C.c_int32 * 2)(*(list(n_finest) + [1] * (2 - len(n_finest))))
+    return check(lib.vlasov_inject_field(h, _ptr(E_finest), n, _ptr(E_lvl)))
+
+
+def vlasov_flux_register_accumulate(fine, f_fine, E_fine, f_coarse, E_coarse, b_s, regs, recon=_lib.CENTERED4):
+    return check(lib.vlasov_flux_register_accumulate(fine, _ptr(f_fine), _ptr(E_fine), _ptr(f_coarse),
+                                                     _ptr(E_coarse), float(b_s), _ptr(regs), recon))
+
+
+def vlasov_average_down(fine, f_fine, f_coarse, regs, dt):
+    return check(lib.vlasov_average_down(fine, _ptr(f_fine), _ptr(f_coarse), _ptr(regs), float(dt)))
+
+
+def vlasov_tag_cells(h, f, tol, buffer, tags):
+    return check(lib.vlasov_tag_cells(h, _ptr(f), float(tol), int(buffer), _ptr(tags)))
+
+
+def vlasov_tags_to_boxes(tags_host: np.ndarray, domain_cells, ratio, tile, cap=65536):
+    t = np.ascontiguousarray(tags_host, dtype=np.uint8)
+    dc = (C.c_int32 * 4)(*(list(domain_cells) + [0] * (4 - len(domain_cells))))
+    r = (C.c_int32 * 4)(*(list(ratio) + [1] * (4 - len(ratio))))
+    out = (Box * cap)()
+    n = C.c_int32()
+    check(lib.vlasov_tags_to_boxes(t.ctypes.data_as(C.c_void_p), dc, len(domain_cells), r, tile, out, cap,
+                                   C.byref(n)))
+    return [(tuple(out[i].lo[:2]), tuple(out[i].hi[:2])) for i in range(min(n.value, cap))]
+
+
+def vlasov_level_fill_from(h, f, old=None, f_old=None, coarser=None, f_coarse=None, interp=_lib.LINEAR5):
+    return check(lib.vlasov_level_fill_from(h, _ptr(f), old, _ptr(f_old), coarser, _ptr(f_coarse), interp))
+
+
+def vlasov_device_ok() -> bool:
+    return bool(lib.vlasov_device_ok())
+
+
+def vlasov_last_error() -> str:
+    return lib.vlasov_last_error().decode()
+
+
+# ----------------------------------------------------------------------------- objects
+class Level:
+    """Owns one vlasov_level handle; helpers to allocate fields and view patches."""
+
+    def __init__(self, ndim, ncells0, lower, dx0, ratio, boxes, coarser: Optional["Level"] = None, stream=None):
+        self.geom = make_geom(ndim, ncells0, lower, dx0)
+        self.ndim = ndim
+        self.ratio = tuple(ratio)
+        self.boxes = [(tuple(lo), tuple(hi)) for lo, hi in boxes]
+        self.coarser = coarser
+        self.h = vlasov_level_create(self.geom, ratio, self.boxes, coarser.h if coarser else None, stream)
+        self.info = vlasov_level_get_info(self.h)
+        self.layouts = [vlasov_level_layout(self.h, p) for p in range(len(self.boxes))]
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib.vlasov_level_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def field(self, fill=float("nan")):
+        return torch.full((self.info.field_doubles,), fill, dtype=torch.float64, device="cuda")
+
+    def efield(self):
+        return torch.zeros(self.info.e_doubles, dtype=torch.float64, device="cuda")
+
+    def patch_view(self, f: torch.Tensor, p: int, ghost: int = 0):
+        off, st = self.layouts[p]
+        lo, hi = self.boxes[p]
+        size = [hi[d] - lo[d] + 1 + 2 * ghost for d in range(self.ndim)]
+        start = off - sum(ghost * st[d] for d in range(self.ndim))
+        return torch.as_strided(f, size, st[:self.ndim], start)
+
+    def set_patches(self, f: torch.Tensor, arrays):
+        for p, a in enumerate(arrays):
+            self.patch_view(f, p).copy_(torch.as_tensor(a, dtype=torch.float64))
+
+    def get_patches(self, f: torch.Tensor, ghost: int = 0):
+        return [self.patch_view(f, p, ghost).cpu().numpy() for p in range(len(self.boxes))]
+
+    def set_domain(self, f: torch.Tensor, full: np.ndarray):
+        """Scatter a whole-domain array (level index space) into the patches."""
+        for p, (lo, hi) in enumerate(self.boxes):
+            sl = tuple(slice(lo[d], hi[d] + 1) for d in range(self.ndim))
+            self.patch_view(f, p).copy_(torch.as_tensor(np.ascontiguousarray(full[sl])))
+
+    def get_domain(self, f: torch.Tensor) -> np.ndarray:
+        out = np.full(tuple(self.info.domain_cells[d] for d in range(self.ndim)), np.nan)
+        for p, (lo, hi) in enumerate(self.boxes):
+            sl = tuple(slice(lo[d], hi[d] + 1) for d in range(self.ndim))
+            out[sl] = self.patch_view(f, p).cpu().numpy()
+        return out
+
+
+class Poisson:
+    def __init__(self, n, dx, stream=None):
+        self.n = n
+        self.h = vlasov_poisson_create(n, dx, stream)
+
+    def solve(self, rho, phi=None, E=None):
+        vlasov_poisson_solve(self.h, rho, phi, E)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib.vlasov_poisson_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass

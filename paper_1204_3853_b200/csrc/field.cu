@@ -1,0 +1,162 @@
+// Configuration-space kernels: fused-partial moment sum, periodic Poisson + E as
+// circulant convolutions with exact discrete Green's functions (readings #1, #2),
+// injection to a level.
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace vk {
+
+// rho[x] = 1 - dv * sum_{vt} partials[vt][x]   (fixed order vt = 0..n-1)
+__global__ void k_sum_partials(const double* __restrict__ partials, int nvt, int nx, double dv,
+                               double* __restrict__ rho) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= nx) return;
+    double s = 0.0;
+    for (int t = 0; t < nvt; ++t) s += partials[(int64_t)t * nx + x];
+    rho[x] = 1.0 - dv * s;
+}
+
+// rho[x] = 1 - dv * sum_v f[x][v] on a single block covering the domain (one warp per x row;
+// lane-strided sums combined by a fixed butterfly: deterministic)
+__global__ void k_moment_direct(const double* __restrict__ f, int64_t off, int pitch, int nx, int nv, double dv,
+                                double* __restrict__ rho) {
+    const int lane = threadIdx.x & 31;
+    const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (x >= nx) return;
+    const double* row = f + off + (int64_t)(x + G) * pitch + G;
+    double s = 0.0;
+    for (int j = lane; j < nv; j += 32) s += row[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) rho[x] = 1.0 - dv * s;
+}
+
+int launch_moment_direct(const vlasov_level* L, const double* f, double* rho) {
+    const int nx = L->dom[0], nv = L->dom[1];
+    k_moment_direct<<<(nx + 7) / 8, 256, 0, L->stream>>>(f, L->block_off[0], (int)L->block_str[0][0], nx, nv,
+                                                          L->h[1], rho);
+    VK_LAUNCH("k_moment_direct");
+    return VLASOV_OK;
+}
+
+int launch_sum_partials(const vlasov_level* L, const double* partials, double* rho) {
+    const int nx = L->dom[0];
+    k_sum_partials<<<(nx + 255) / 256, 256, 0, L->stream>>>(partials, L->n_vtiles, nx, L->h[1], rho);
+    VK_LAUNCH("k_sum_partials");
+    return VLASOV_OK;
+}
+
+// out[i] = sum_k g[(i - k) mod n] (rho[k] - mean(rho)).  One warp per output; every CTA
+// stages the whole projected rho in shared memory (n <= 8192) and reduces the mean itself in a
+// fixed order, so the result is deterministic.
+__global__ void k_circulant(const double* __restrict__ rho, const double* __restrict__ g, int n,
+                            double* __restrict__ out) {
+    extern __shared__ double s_rho[];
+    __shared__ double s_red[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    double acc = 0.0;
+    for (int k = tid; k < n; k += blockDim.x) {
+        const double v = rho[k];
+        s_rho[k] = v;
+        acc += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) s_red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += s_red[w];
+        s_red[0] = s / (double)n;
+    }
+    __syncthreads();
+    const double mean = s_red[0];
+    for (int k = tid; k < n; k += blockDim.x) s_rho[k] -= mean;      // projection
+    __syncthreads();
+    const int per_block = nw * 4;
+    for (int o = 0; o < 4; ++o) {
+        const int i = blockIdx.x * per_block + warp * 4 + o;
+        if (i >= n) break;
+        double s = 0.0;
+        for (int k = lane; k < n; k += 32) {
+            int d = i - k;
+            d += (d < 0) ? n : 0;
+            s = fma(__ldg(g + d), s_rho[k], s);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) out[i] = s;
+    }
+}
+
+int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E) {
+    const int threads = 256, per_block = (threads / 32) * 4;
+    const int blocks = (P->n + per_block - 1) / per_block;
+    const size_t smem = (size_t)P->n * sizeof(double);
+    if (smem > 48 * 1024) {
+        static bool conf = false;
+        if (!conf) {
+            VK_CUDA(cudaFuncSetAttribute(k_circulant, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            conf = true;
+        }
+    }
+    if (E) {
+        k_circulant<<<blocks, threads, smem, P->stream>>>(rho, P->d_gE, P->n, E);
+        VK_LAUNCH("k_circulant(E)");
+    }
+    if (phi) {
+        k_circulant<<<blocks, threads, smem, P->stream>>>(rho, P->d_gphi, P->n, phi);
+        VK_LAUNCH("k_circulant(phi)");
+    }
+    return VLASOV_OK;
+}
+
+// E_lvl[i + 2] = mean_{s<R} E_f[R i + s]; periodic ghosts i = -2, -1, n, n+1.
+__global__ void k_inject_1d(const double* __restrict__ Ef, int nf, int R, int n, double* __restrict__ El) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n + 4) return;
+    int i = t - 2;
+    i = (i < 0) ? i + n : (i >= n ? i - n : i);
+    double s = 0.0;
+    for (int q = 0; q < R; ++q) s += Ef[(int64_t)i * R + q];
+    El[t] = (R == 1) ? s : s / (double)R;
+}
+
+int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest, double* E_lvl) {
+    const int n = L->dom[0];
+    if (n_finest % n) return fail(VLASOV_EINVAL, "inject: finest size not a multiple of the level size");
+    const int R = n_finest / n;
+    k_inject_1d<<<(n + 4 + 127) / 128, 128, 0, L->stream>>>(E_finest, n_finest, R, n, E_lvl);
+    VK_LAUNCH("k_inject_1d");
+    return VLASOV_OK;
+}
+
+// 2D configuration space, C = 2 components: El[c][(i+2)*(ny+4) + (k+2)] = mean over Rx x Ry.
+__global__ void k_inject_2d(const double* __restrict__ Ef, int nfx, int nfy, int Rx, int Ry, int nx,
+                            int ny, double* __restrict__ El) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nxg = nx + 4, nyg = ny + 4;
+    if (t >= 2 * nxg * nyg) return;
+    const int c = t / (nxg * nyg), rem = t % (nxg * nyg);
+    int i = rem / nyg - 2, k = rem % nyg - 2;
+    i = (i < 0) ? i + nx : (i >= nx ? i - nx : i);
+    k = (k < 0) ? k + ny : (k >= ny ? k - ny : k);
+    double s = 0.0;
+    for (int a = 0; a < Rx; ++a)
+        for (int b = 0; b < Ry; ++b)
+            s += Ef[(int64_t)c * nfx * nfy + (int64_t)(i * Rx + a) * nfy + (k * Ry + b)];
+    El[t] = (Rx * Ry == 1) ? s : s / (double)(Rx * Ry);
+}
+
+int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest, double* E_lvl) {
+    const int nx = L->dom[0], ny = L->dom[1];
+    if (n_finest[0] % nx || n_finest[1] % ny) return fail(VLASOV_EINVAL, "inject: size mismatch");
+    const int tot = 2 * (nx + 4) * (ny + 4);
+    k_inject_2d<<<(tot + 255) / 256, 256, 0, L->stream>>>(E_finest, n_finest[0], n_finest[1],
+                                                            n_finest[0] / nx, n_finest[1] / ny, nx, ny, E_lvl);
+    VK_LAUNCH("k_inject_2d");
+    return VLASOV_OK;
+}
+
+}  // namespace vk

@@ -1,0 +1,151 @@
+// Internal declarations of libvlasov (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <array>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "vlasov.h"
+
+namespace vk {
+
+constexpr int G = 2;              // ghost width (reading #7)
+constexpr int MAXR = 16;          // largest refinement ratio per dim supported by the transfers
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_check(cudaError_t e, const char* what);
+#define VK_CUDA(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return ::vk::cuda_check(_e, #call); } while (0)
+#define VK_LAUNCH(what) do { cudaError_t _e = cudaGetLastError(); if (_e != cudaSuccess) return ::vk::cuda_check(_e, what); } while (0)
+
+// ------------------------------------------------------------------ boxes
+struct Box {
+    int lo[4] = {0, 0, 0, 0}, hi[4] = {-1, -1, -1, -1};
+};
+int box_ncells_dim(const Box& b, int d);
+int64_t box_ncells(const Box& b, int nd);
+bool box_empty(const Box& b, int nd);
+Box box_intersect(const Box& a, const Box& b, int nd);
+bool box_contains(const Box& b, const int* c, int nd);
+Box box_refine(const Box& b, const int* r, int nd);
+Box box_coarsen(const Box& b, const int* r, int nd);
+Box box_grow(const Box& b, int g, int nd);
+std::vector<Box> box_subtract(const Box& a, const Box& b, int nd);
+bool box_less(const Box& a, const Box& b, int nd);
+int64_t box_index(const Box& b, const int* c, int nd);   // row-major, last dim fastest
+inline int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+
+// ------------------------------------------------------------------ device task structs
+struct Block1 {               // one storage block of a 1D+1V level
+    int64_t off;              // index of the ghosted origin (x = lo-2, v = lo-2)
+    int32_t pitch;            // doubles per ghosted x-row
+    int32_t lo_x, lo_v, nx, nv;
+};
+struct Tile1 {                // one CTA of the 1D+1V stage kernel
+    int32_t block, x0, nrows, j0, ncols, pvt;   // pvt = partial v-tile index (-1: none)
+};
+struct CFTask {               // one coarse-fine ghost value
+    int64_t dst;              // fine index in the level array
+    int64_t csrc;             // coarse index of the parent cell in the coarse level array
+    int32_t cstride[4];       // coarse strides (doubles) per dim
+    int8_t sub[4];            // sub-cell offsets per dim
+};
+struct PhysTask {             // characteristic v-BC of one column side (1D+1V)
+    int64_t cell0;            // index of the boundary cell (j = 0 for low, j = n-1 for high)
+    int32_t e_idx;            // index into the level E array (wrapped x + 2)
+    int32_t side;             // 0 low, 1 high
+};
+struct RedEntry {             // one sub-patch of Alg.8
+    int64_t base;             // index of cell (x = s.lo_x - 2, v = s.lo_v) in its level array
+    int32_t level, pitch, ncols_g, nrows_v;  // ncols_g = nx_s + 4 (grown), nrows_v = v extent
+    int32_t R;                // x ratio to the finest level
+    int32_t xf0;              // finest x of the first fine cell (s.lo_x * R)
+    int32_t buf_off;          // offset of its refined values in the scratch buffer
+    double dv;                // velocity spacing of its level
+};
+struct RefluxTask {           // one coarse face on the coarse-fine interface
+    int64_t ccell;            // coarse cell (uncovered) whose face is corrected
+    int64_t cface_lo;         // coarse: index of the 4-cell stencil start along the face normal
+    int32_t dir;              // 0: x-face, 1: v-face
+    int32_t sign;             // +1: face is the cell's high face, -1: low face
+    int32_t c_e_idx;          // E index of the coarse column (x-faces: -1)
+    int32_t nfine;            // transverse fine faces (R_transverse)
+    int64_t fface_lo[MAXR];   // fine stencil starts (index of the first of 4 cells)
+    int32_t f_e_idx[MAXR];    // fine E indices of the fine faces' columns
+};
+struct AvgTask {              // one covered coarse cell
+    int64_t ccell;
+    int64_t fcell0;           // first fine cell
+    int32_t fpitch;           // fine x stride
+};
+
+}  // namespace vk
+
+// ------------------------------------------------------------------ opaque structs
+struct vlasov_level {
+    int ndim = 2, ncfg = 1;
+    double lower[4] = {0, 0, 0, 0}, h[4] = {0, 0, 0, 0};
+    int ratio[4] = {1, 1, 1, 1};
+    int dom[4] = {0, 0, 0, 0};            // level domain cells per dim
+    std::vector<vk::Box> boxes;           // logical patches
+    std::vector<int> patch_block;         // patch -> block
+    std::vector<vk::Box> blocks;          // storage blocks (interior boxes)
+    std::vector<int64_t> block_off;       // ghosted-origin offset per block
+    std::vector<std::array<int64_t, 4>> block_str;  // strides per block
+    int64_t field_doubles = 0;
+    const vlasov_level* coarser = nullptr;
+    uint64_t uid = 0, coarser_uid = 0;
+    cudaStream_t stream = nullptr;
+    bool single_block = false;            // one block covering the whole domain
+    // 1D+1V stage tables
+    std::vector<vk::Block1> h_blocks1;
+    vk::Block1* d_blocks1 = nullptr;
+    std::vector<vk::Tile1> h_tiles_wide, h_tiles_narrow;
+    vk::Tile1* d_tiles_wide = nullptr;
+    vk::Tile1* d_tiles_narrow = nullptr;
+    int tile_rows = 0;
+    int n_vtiles = 0;                     // partial v-tiles (single-block only)
+    // ghost fill
+    int64_t n_copy = 0, n_cf = 0, n_phys = 0;
+    int64_t* d_copy = nullptr;            // pairs (dst, src)
+    vk::CFTask* d_cf = nullptr;
+    vk::PhysTask* d_phys = nullptr;
+    int coarse_ratio[4] = {1, 1, 1, 1};   // ratio to the coarser level
+    // AMR transfers w.r.t. the coarser level
+    int64_t n_reflux = 0, n_avg = 0;
+    vk::RefluxTask* d_reflux = nullptr;
+    vk::AvgTask* d_avg = nullptr;
+    int avg_count = 1;                    // fine cells per coarse cell
+    // 2D+2V
+    int64_t e_doubles = 0;
+    // scratch (device): interpolation tables
+    double* d_b5 = nullptr;               // linear5 weights for coarse_ratio, [dim][s][5]
+};
+
+struct vlasov_poisson {
+    int n = 0;
+    double dx = 0;
+    cudaStream_t stream = nullptr;
+    double* d_gE = nullptr;
+    double* d_gphi = nullptr;
+};
+
+namespace vk {
+// ------------------------------------------------------------------ kernels (launchers)
+int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s,
+                      double* u, double* f_next, const double* E, int recon, double* partials);
+int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double* E_bc,
+                const double* f0v, int interp);
+int launch_sum_partials(const vlasov_level* L, const double* partials, double* rho);
+int launch_moment_direct(const vlasov_level* L, const double* f, double* rho);
+int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E);
+int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest, double* E_lvl);
+int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest,
+                     double* E_lvl);
+int linear5_weights(int R, double* out /* R*5 */);
+}  // namespace vk

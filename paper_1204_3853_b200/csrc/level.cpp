@@ -1,0 +1,814 @@
+// libvlasov host side: errors, box calculus, level metadata (layout, tiles, ghost / transfer task
+// lists), Poisson plans, C ABI entry points.  See include/vlasov.h for the contract.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using vk::Box;
+
+// ====================================================================== errors
+namespace vk {
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+int fail(int code, const std::string& m) {
+    g_err = m;
+    return code;
+}
+int cuda_check(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return VLASOV_ECUDA;
+}
+
+// ====================================================================== boxes
+int box_ncells_dim(const Box& b, int d) { return b.hi[d] - b.lo[d] + 1; }
+bool box_empty(const Box& b, int nd) {
+    for (int d = 0; d < nd; ++d)
+        if (b.lo[d] > b.hi[d]) return true;
+    return false;
+}
+int64_t box_ncells(const Box& b, int nd) {
+    if (box_empty(b, nd)) return 0;
+    int64_t n = 1;
+    for (int d = 0; d < nd; ++d) n *= box_ncells_dim(b, d);
+    return n;
+}
+Box box_intersect(const Box& a, const Box& b, int nd) {
+    Box r;
+    for (int d = 0; d < nd; ++d) {
+        r.lo[d] = std::max(a.lo[d], b.lo[d]);
+        r.hi[d] = std::min(a.hi[d], b.hi[d]);
+    }
+    return r;
+}
+bool box_contains(const Box& b, const int* c, int nd) {
+    for (int d = 0; d < nd; ++d)
+        if (c[d] < b.lo[d] || c[d] > b.hi[d]) return false;
+    return true;
+}
+Box box_refine(const Box& b, const int* r, int nd) {
+    Box o;
+    for (int d = 0; d < nd; ++d) {
+        o.lo[d] = b.lo[d] * r[d];
+        o.hi[d] = (b.hi[d] + 1) * r[d] - 1;
+    }
+    return o;
+}
+Box box_coarsen(const Box& b, const int* r, int nd) {
+    Box o;
+    for (int d = 0; d < nd; ++d) {
+        o.lo[d] = floordiv(b.lo[d], r[d]);
+        o.hi[d] = floordiv(b.hi[d], r[d]);
+    }
+    return o;
+}
+Box box_grow(const Box& b, int g, int nd) {
+    Box o = b;
+    for (int d = 0; d < nd; ++d) {
+        o.lo[d] -= g;
+        o.hi[d] += g;
+    }
+    return o;
+}
+// a \ b: split dim 0 first, low fragment before high (deterministic, same rule as the oracle)
+std::vector<Box> box_subtract(const Box& a, const Box& b, int nd) {
+    std::vector<Box> out;
+    if (box_empty(box_intersect(a, b, nd), nd)) {
+        out.push_back(a);
+        return out;
+    }
+    Box rem = a;
+    for (int d = 0; d < nd; ++d) {
+        if (rem.lo[d] < b.lo[d]) {
+            Box f = rem;
+            f.hi[d] = b.lo[d] - 1;
+            out.push_back(f);
+            rem.lo[d] = b.lo[d];
+        }
+        if (rem.hi[d] > b.hi[d]) {
+            Box f = rem;
+            f.lo[d] = b.hi[d] + 1;
+            out.push_back(f);
+            rem.hi[d] = b.hi[d];
+        }
+    }
+    return out;
+}
+bool box_less(const Box& a, const Box& b, int nd) {
+    for (int d = 0; d < nd; ++d)
+        if (a.lo[d] != b.lo[d]) return a.lo[d] < b.lo[d];
+    for (int d = 0; d < nd; ++d)
+        if (a.hi[d] != b.hi[d]) return a.hi[d] < b.hi[d];
+    return false;
+}
+int64_t box_index(const Box& b, const int* c, int nd) {
+    int64_t idx = 0;
+    for (int d = 0; d < nd; ++d) idx = idx * box_ncells_dim(b, d) + (c[d] - b.lo[d]);
+    return idx;
+}
+
+// linear5 weights b_j(s), j=-2..2 with p_k(s) = ((s+1)^{k+1} - s^{k+1}) / R^k
+// (reading #12).  For R = 2^m the values are dyadic and exact in fp64.
+int linear5_weights(int R, double* out) {
+    for (int s = 0; s < R; ++s) {
+        double p[5];
+        for (int k = 0; k <= 4; ++k) {
+            const double a = std::pow((double)(s + 1), k + 1) - std::pow((double)s, k + 1);
+            p[k] = a / std::pow((double)R, k);
+        }
+        out[5 * s + 0] = (p[4] - 5 * p[3] + 5 * p[2] + 5 * p[1] - 6) / 120.0;
+        out[5 * s + 1] = (-4 * p[4] + 15 * p[3] + 10 * p[2] - 75 * p[1] + 54) / 120.0;
+        out[5 * s + 2] = (6 * p[4] - 15 * p[3] - 40 * p[2] + 75 * p[1] + 94) / 120.0;
+        out[5 * s + 3] = (-4 * p[4] + 5 * p[3] + 30 * p[2] - 5 * p[1] - 26) / 120.0;
+        out[5 * s + 4] = (p[4] - 5 * p[2] + 4) / 120.0;
+    }
+    return 0;
+}
+}  // namespace vk
+
+// ====================================================================== device helpers
+namespace {
+std::atomic<uint64_t> g_uid{1};
+
+template <class T>
+int upload(T** dptr, const std::vector<T>& h, cudaStream_t st) {
+    *dptr = nullptr;
+    if (h.empty()) return VLASOV_OK;
+    VK_CUDA(cudaMalloc((void**)dptr, h.size() * sizeof(T)));
+    VK_CUDA(cudaMemcpyAsync(*dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return VLASOV_OK;
+}
+
+void free_level(vlasov_level* L) {
+    if (!L) return;
+    cudaFree(L->d_blocks1);
+    cudaFree(L->d_tiles_wide);
+    cudaFree(L->d_tiles_narrow);
+    cudaFree(L->d_copy);
+    cudaFree(L->d_cf);
+    cudaFree(L->d_phys);
+    cudaFree(L->d_reflux);
+    cudaFree(L->d_avg);
+    cudaFree(L->d_b5);
+    delete L;
+}
+
+inline int wrap(int x, int n) { return ((x % n) + n) % n; }
+
+int device_ok_impl() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return p.major == 10 ? 1 : 0;
+}
+
+// owner lookup over the level domain: which block (or patch) holds a cell (-1: none)
+struct Owner {
+    int nd = 2;
+    int dom[4] = {0, 0, 0, 0};
+    std::vector<int32_t> id;
+    int64_t lin(const int* c) const {
+        int64_t i = 0;
+        for (int d = 0; d < nd; ++d) i = i * dom[d] + c[d];
+        return i;
+    }
+    int find(const int* c) const {
+        for (int d = 0; d < nd; ++d)
+            if (c[d] < 0 || c[d] >= dom[d]) return -1;
+        return id[lin(c)];
+    }
+};
+
+Owner make_owner(const vlasov_level* L, const std::vector<Box>& bs) {
+    Owner o;
+    o.nd = L->ndim;
+    int64_t tot = 1;
+    for (int d = 0; d < L->ndim; ++d) {
+        o.dom[d] = L->dom[d];
+        tot *= L->dom[d];
+    }
+    o.id.assign(tot, -1);
+    for (size_t p = 0; p < bs.size(); ++p) {
+        const Box& b = bs[p];
+        int c[4];
+        if (L->ndim == 2) {
+            for (c[0] = b.lo[0]; c[0] <= b.hi[0]; ++c[0])
+                for (c[1] = b.lo[1]; c[1] <= b.hi[1]; ++c[1]) o.id[o.lin(c)] = (int32_t)p;
+        } else {
+            for (c[0] = b.lo[0]; c[0] <= b.hi[0]; ++c[0])
+                for (c[1] = b.lo[1]; c[1] <= b.hi[1]; ++c[1])
+                    for (c[2] = b.lo[2]; c[2] <= b.hi[2]; ++c[2])
+                        for (c[3] = b.lo[3]; c[3] <= b.hi[3]; ++c[3]) o.id[o.lin(c)] = (int32_t)p;
+        }
+    }
+    return o;
+}
+
+// index of a (block-local interior) cell c of block b in the level array
+inline int64_t cell_addr(const vlasov_level* L, int b, const int* c) {
+    const Box& B = L->blocks[b];
+    int64_t a = L->block_off[b];
+    for (int d = 0; d < L->ndim; ++d) a += (int64_t)(c[d] - B.lo[d] + vk::G) * L->block_str[b][d];
+    return a;
+}
+
+// wrap configuration dims into the domain
+inline void wrap_cfg(const vlasov_level* L, const int* c, int* w) {
+    for (int d = 0; d < L->ndim; ++d) w[d] = (d < L->ncfg) ? wrap(c[d], L->dom[d]) : c[d];
+}
+
+int phys_code(const vlasov_level* L, const int* c) {
+    for (int d = L->ncfg; d < L->ndim; ++d) {
+        if (c[d] < 0) return 2 * (d - L->ncfg);
+        if (c[d] >= L->dom[d]) return 2 * (d - L->ncfg) + 1;
+    }
+    return -1;
+}
+
+void for_each_cell(const Box& b, int nd, const std::function<void(const int*)>& fn) {
+    int c[4] = {0, 0, 0, 0};
+    if (vk::box_empty(b, nd)) return;
+    for (int d = 0; d < nd; ++d) c[d] = b.lo[d];
+    while (true) {
+        fn(c);
+        int d = nd - 1;
+        while (d >= 0) {
+            if (++c[d] <= b.hi[d]) break;
+            c[d] = b.lo[d];
+            --d;
+        }
+        if (d < 0) break;
+    }
+}
+
+// ------------------------------------------------------------------ task-list construction
+int build_tiles_1d(vlasov_level* L) {
+    const bool wide = [&] {
+        int mx = 0;
+        for (const Box& b : L->blocks) mx = std::max(mx, vk::box_ncells_dim(b, 1));
+        return mx >= 256;
+    }();
+    const int TV = wide ? 256 : 64;
+    int64_t strips_total = 0;
+    for (const Box& b : L->blocks) {
+        const int nvt = (vk::box_ncells_dim(b, 1) + TV - 1) / TV;
+        strips_total += (int64_t)vk::box_ncells_dim(b, 0) * nvt;
+    }
+    int rows = (int)((strips_total + 591) / 592);
+    rows = ((rows + 3) / 4) * 4;
+    rows = std::max(8, std::min(64, rows));
+    if (const char* e = std::getenv("VLASOV_TILE_ROWS")) rows = std::max(4, std::min(256, atoi(e)));
+    L->tile_rows = rows;
+    std::vector<vk::Tile1>& tiles = wide ? L->h_tiles_wide : L->h_tiles_narrow;
+    tiles.clear();
+    L->n_vtiles = 0;
+    for (size_t b = 0; b < L->blocks.size(); ++b) {
+        const int nx = vk::box_ncells_dim(L->blocks[b], 0), nv = vk::box_ncells_dim(L->blocks[b], 1);
+        const int nvt = (nv + TV - 1) / TV;
+        if (L->single_block) L->n_vtiles = nvt;
+        for (int x0 = 0; x0 < nx; x0 += rows)
+            for (int vt = 0; vt < nvt; ++vt) {
+                vk::Tile1 t;
+                t.block = (int)b;
+                t.x0 = x0;
+                t.nrows = std::min(rows, nx - x0);
+                t.j0 = vt * TV;
+                t.ncols = std::min(TV, nv - vt * TV);
+                t.pvt = L->single_block ? vt : -1;
+                tiles.push_back(t);
+            }
+    }
+    L->h_blocks1.clear();
+    for (size_t b = 0; b < L->blocks.size(); ++b) {
+        vk::Block1 B;
+        B.off = L->block_off[b];
+        B.pitch = (int32_t)L->block_str[b][0];
+        B.lo_x = L->blocks[b].lo[0];
+        B.lo_v = L->blocks[b].lo[1];
+        B.nx = vk::box_ncells_dim(L->blocks[b], 0);
+        B.nv = vk::box_ncells_dim(L->blocks[b], 1);
+        L->h_blocks1.push_back(B);
+    }
+    return VLASOV_OK;
+}
+
+// ghost-fill tasks of every block: copies (siblings / periodic), CF interpolation, PHYS columns
+int build_ghost_tasks(vlasov_level* L, const vlasov_level* C, std::vector<int64_t>& copies,
+                      std::vector<vk::CFTask>& cfs, std::vector<vk::PhysTask>& phys) {
+    const int nd = L->ndim;
+    Owner own;
+    if (!L->single_block) own = make_owner(L, L->blocks);
+    Owner cown;
+    if (C) cown = make_owner(C, C->blocks);
+    int rr[4] = {1, 1, 1, 1};
+    if (C)
+        for (int d = 0; d < nd; ++d) rr[d] = L->ratio[d] / C->ratio[d];
+    int err = VLASOV_OK;
+    for (size_t b = 0; b < L->blocks.size(); ++b) {
+        const Box& B = L->blocks[b];
+        const Box GB = vk::box_grow(B, vk::G, nd);
+        for_each_cell(GB, nd, [&](const int* c) {
+            if (err) return;
+            if (vk::box_contains(B, c, nd)) return;
+            if (phys_code(L, c) >= 0) return;                     // PHYS: handled per column
+            int w[4];
+            wrap_cfg(L, c, w);
+            const int q = L->single_block ? (vk::box_contains(L->blocks[0], w, nd) ? 0 : -1) : own.find(w);
+            const int64_t dst = cell_addr(L, (int)b, c);
+            if (q >= 0) {
+                copies.push_back(dst);
+                copies.push_back(cell_addr(L, q, w));
+                return;
+            }
+            if (!C) {
+                err = vk::fail(VLASOV_ENEST, "ghost cell without a source on a level without a coarser level");
+                return;
+            }
+            int cc[4];
+            for (int d = 0; d < nd; ++d) cc[d] = vk::floordiv(w[d], rr[d]);
+            const int cq = cown.find(cc);
+            if (cq < 0) {
+                err = vk::fail(VLASOV_ESTENCIL, "coarse-fine ghost: coarse parent not on the coarser level");
+                return;
+            }
+            vk::CFTask t;
+            t.dst = dst;
+            t.csrc = cell_addr(C, cq, cc);
+            for (int d = 0; d < 4; ++d) {
+                t.cstride[d] = d < nd ? (int32_t)C->block_str[cq][d] : 0;
+                t.sub[d] = d < nd ? (int8_t)(w[d] - cc[d] * rr[d]) : 0;
+            }
+            cfs.push_back(t);
+        });
+        if (err) return err;
+        if (nd == 2) {
+            const int nv = L->dom[1];
+            for (int side = 0; side < 2; ++side) {
+                if (side == 0 && B.lo[1] != 0) continue;
+                if (side == 1 && B.hi[1] != nv - 1) continue;
+                if (vk::box_ncells_dim(B, 1) < 4)
+                    return vk::fail(VLASOV_EINVAL, "blocks touching the v-boundary need >= 4 v-cells");
+                for (int x = B.lo[0] - vk::G; x <= B.hi[0] + vk::G; ++x) {
+                    int c[4] = {x, side == 0 ? 0 : nv - 1, 0, 0};
+                    vk::PhysTask t;
+                    t.cell0 = cell_addr(L, (int)b, c);
+                    t.e_idx = wrap(x, L->dom[0]) + vk::G;
+                    t.side = side;
+                    phys.push_back(t);
+                }
+            }
+        }
+    }
+    return VLASOV_OK;
+}
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* vlasov_last_error(void) { return vk::g_err.c_str(); }
+int vlasov_version(void) { return 1; }
+int vlasov_device_ok(void) { return device_ok_impl(); }
+
+int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4], const vlasov_box* boxes,
+                        int32_t nboxes, const vlasov_level* coarser, void* cuda_stream, vlasov_level** out) {
+    if (!geom || !ratio_to_level0 || !boxes || !out) return vk::fail(VLASOV_EINVAL, "null argument");
+    *out = nullptr;
+    const int nd = geom->ndim;
+    if (nd != 2 && nd != 4) return vk::fail(VLASOV_EINVAL, "ndim must be 2 or 4");
+    if (nboxes < 1) return vk::fail(VLASOV_EINVAL, "nboxes < 1");
+    vlasov_level* L = new vlasov_level();
+    L->ndim = nd;
+    L->ncfg = nd / 2;
+    L->stream = (cudaStream_t)cuda_stream;
+    L->uid = g_uid++;
+    L->coarser = coarser;
+    L->coarser_uid = coarser ? coarser->uid : 0;
+    for (int d = 0; d < nd; ++d) {
+        if (ratio_to_level0[d] < 1) { free_level(L); return vk::fail(VLASOV_EINVAL, "ratio < 1"); }
+        if (geom->domain.lo[d] != 0 || geom->domain.hi[d] < 0) {
+            free_level(L);
+            return vk::fail(VLASOV_EINVAL, "level-0 domain must start at 0 and be non-empty");
+        }
+        L->ratio[d] = ratio_to_level0[d];
+        L->dom[d] = (geom->domain.hi[d] + 1) * L->ratio[d];
+        L->lower[d] = geom->lower[d];
+        L->h[d] = geom->dx0[d] / L->ratio[d];
+    }
+    if (coarser) {
+        if (coarser->ndim != nd) { free_level(L); return vk::fail(VLASOV_EINVAL, "coarser level ndim mismatch"); }
+        for (int d = 0; d < nd; ++d) {
+            if (L->ratio[d] % coarser->ratio[d]) {
+                free_level(L);
+                return vk::fail(VLASOV_EINVAL, "ratio not a multiple of the coarser level's ratio");
+            }
+            L->coarse_ratio[d] = L->ratio[d] / coarser->ratio[d];
+            if (L->coarse_ratio[d] > vk::MAXR) { free_level(L); return vk::fail(VLASOV_EUNSUPPORTED, "ratio > 16"); }
+        }
+    }
+    // boxes: inside the domain, non-empty, disjoint
+    Box bbox;
+    int64_t total = 0;
+    for (int p = 0; p < nboxes; ++p) {
+        Box b;
+        for (int d = 0; d < nd; ++d) {
+            b.lo[d] = boxes[p].lo[d];
+            b.hi[d] = boxes[p].hi[d];
+            if (b.lo[d] > b.hi[d]) { free_level(L); return vk::fail(VLASOV_EINVAL, "empty box"); }
+            if (b.lo[d] < 0 || b.hi[d] >= L->dom[d]) { free_level(L); return vk::fail(VLASOV_ENEST, "box outside the level domain"); }
+            bbox.lo[d] = p ? std::min(bbox.lo[d], b.lo[d]) : b.lo[d];
+            bbox.hi[d] = p ? std::max(bbox.hi[d], b.hi[d]) : b.hi[d];
+        }
+        total += vk::box_ncells(b, nd);
+        L->boxes.push_back(b);
+    }
+    {   // disjointness via an owner map
+        Owner o;
+        o.nd = nd;
+        int64_t tot = 1;
+        for (int d = 0; d < nd; ++d) { o.dom[d] = L->dom[d]; tot *= L->dom[d]; }
+        std::vector<uint8_t> cnt(tot, 0);
+        bool overlap = false;
+        for (const Box& b : L->boxes)
+            for_each_cell(b, nd, [&](const int* c) { if (cnt[o.lin(c)]++) overlap = true; });
+        if (overlap) { free_level(L); return vk::fail(VLASOV_ENEST, "boxes overlap"); }
+        if (!coarser && total != tot) { free_level(L); return vk::fail(VLASOV_ENEST, "level 0 must tile the domain"); }
+        if (coarser) {   // proper nesting: coarse parents of every fine cell on the coarser level
+            Owner co = make_owner(coarser, coarser->boxes);
+            bool bad = false;
+            for (const Box& b : L->boxes) {
+                Box cb = vk::box_coarsen(b, L->coarse_ratio, nd);
+                for_each_cell(cb, nd, [&](const int* c) { if (co.find(c) < 0) bad = true; });
+            }
+            if (bad) { free_level(L); return vk::fail(VLASOV_ENEST, "level not nested in the coarser level"); }
+        }
+    }
+    // storage blocks
+    L->single_block = (total == vk::box_ncells(bbox, nd));
+    if (L->single_block) {
+        L->blocks.push_back(bbox);
+        L->patch_block.assign(nboxes, 0);
+    } else {
+        L->blocks = L->boxes;
+        for (int p = 0; p < nboxes; ++p) L->patch_block.push_back(p);
+    }
+    bool covers_domain = L->single_block;
+    for (int d = 0; d < nd && covers_domain; ++d) covers_domain = (bbox.lo[d] == 0 && bbox.hi[d] == L->dom[d] - 1);
+    L->single_block = covers_domain && L->single_block;
+    if (!covers_domain && L->blocks.size() == 1 && nboxes > 1) {
+        // a single rectangle not covering the domain still stores as one block
+    }
+    int64_t off = 0;
+    for (const Box& b : L->blocks) {
+        std::array<int64_t, 4> st = {0, 0, 0, 0};
+        int64_t ext[4];
+        for (int d = 0; d < nd; ++d) ext[d] = vk::box_ncells_dim(b, d) + 2 * vk::G;
+        ext[nd - 1] = (ext[nd - 1] + 1) & ~int64_t(1);                // even pitch (16-B rows)
+        st[nd - 1] = 1;
+        for (int d = nd - 2; d >= 0; --d) st[d] = st[d + 1] * ext[d + 1];
+        L->block_off.push_back(off);
+        L->block_str.push_back(st);
+        off += ((st[0] * ext[0] + 31) / 32) * 32;                        // 256-B aligned blocks
+    }
+    L->field_doubles = off;
+    L->e_doubles = (nd == 2) ? (int64_t)(L->dom[0] + 4) : (int64_t)2 * (L->dom[0] + 4) * (L->dom[1] + 4);
+
+    int rc = VLASOV_OK;
+    std::vector<int64_t> copies;
+    std::vector<vk::CFTask> cfs;
+    std::vector<vk::PhysTask> phys;
+    if (nd == 2) {
+        rc = build_tiles_1d(L);
+        if (!rc) rc = build_ghost_tasks(L, coarser, copies, cfs, phys);
+    } else {
+        rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V levels: not in this build yet");
+    }
+    if (rc) { free_level(L); return rc; }
+    L->n_copy = (int64_t)copies.size() / 2;
+    L->n_cf = (int64_t)cfs.size();
+    L->n_phys = (int64_t)phys.size();
+    std::vector<double> b5(2 * vk::MAXR * 5, 0.0);
+    vk::linear5_weights(L->coarse_ratio[0], b5.data());
+    vk::linear5_weights(L->coarse_ratio[1], b5.data() + 5 * vk::MAXR);
+    if (!device_ok_impl()) {            // host metadata only (queries work, compute calls fail)
+        *out = L;
+        return VLASOV_OK;
+    }
+    if ((rc = upload(&L->d_blocks1, L->h_blocks1, L->stream)) ||
+        (rc = upload(&L->d_tiles_wide, L->h_tiles_wide, L->stream)) ||
+        (rc = upload(&L->d_tiles_narrow, L->h_tiles_narrow, L->stream)) ||
+        (rc = upload(&L->d_copy, copies, L->stream)) || (rc = upload(&L->d_cf, cfs, L->stream)) ||
+        (rc = upload(&L->d_phys, phys, L->stream)) || (rc = upload(&L->d_b5, b5, L->stream))) {
+        free_level(L);
+        return rc;
+    }
+    cudaError_t e = cudaStreamSynchronize(L->stream);
+    if (e != cudaSuccess) { free_level(L); return vk::cuda_check(e, "level_create upload"); }
+    *out = L;
+    return VLASOV_OK;
+}
+
+int vlasov_level_destroy(vlasov_level* level) {
+    if (level) {
+        cudaStreamSynchronize(level->stream);
+        free_level(level);
+    }
+    return VLASOV_OK;
+}
+
+int vlasov_level_get_info(const vlasov_level* L, vlasov_level_info* info) {
+    if (!L || !info) return vk::fail(VLASOV_EINVAL, "null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->field_doubles = L->field_doubles;
+    info->e_doubles = L->e_doubles;
+    info->cfg_cells = (L->ndim == 2) ? L->dom[0] : (int64_t)L->dom[0] * L->dom[1];
+    info->partial_doubles = L->single_block ? (int64_t)L->n_vtiles * L->dom[0] : 0;
+    info->fluxreg_doubles = L->n_reflux;
+    info->tag_bytes = 1;
+    for (int d = 0; d < L->ndim; ++d) info->tag_bytes *= L->dom[d];
+    info->nblocks = (int32_t)L->blocks.size();
+    info->npatches = (int32_t)L->boxes.size();
+    info->ntiles = (int32_t)(L->h_tiles_wide.size() + L->h_tiles_narrow.size());
+    info->ndim = L->ndim;
+    for (int d = 0; d < 4; ++d) {
+        info->ratio[d] = L->ratio[d];
+        info->domain_cells[d] = d < L->ndim ? L->dom[d] : 0;
+    }
+    info->ncfg[0] = L->dom[0];
+    info->ncfg[1] = L->ndim == 4 ? L->dom[1] : 1;
+    return VLASOV_OK;
+}
+
+int vlasov_level_layout(const vlasov_level* L, int32_t patch, int64_t* offset, int64_t strides[4]) {
+    if (!L || !offset || !strides) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (patch < 0 || patch >= (int)L->boxes.size()) return vk::fail(VLASOV_EINVAL, "patch out of range");
+    const int b = L->patch_block[patch];
+    *offset = cell_addr(L, b, L->boxes[patch].lo);
+    for (int d = 0; d < 4; ++d) strides[d] = d < L->ndim ? L->block_str[b][d] : 0;
+    return VLASOV_OK;
+}
+
+int vlasov_level_ghost_map(const vlasov_level* L, int32_t patch, int32_t* kind, int32_t* src_patch,
+                           int64_t* src_cell) {
+    if (!L || !kind || !src_patch || !src_cell) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (patch < 0 || patch >= (int)L->boxes.size()) return vk::fail(VLASOV_EINVAL, "patch out of range");
+    const int nd = L->ndim;
+    const Box& B = L->boxes[patch];
+    Owner own = make_owner(L, L->boxes);
+    Owner cown;
+    const vlasov_level* C = L->coarser;
+    if (C) cown = make_owner(C, C->boxes);
+    int64_t t = 0;
+    int err = VLASOV_OK;
+    for_each_cell(vk::box_grow(B, vk::G, nd), nd, [&](const int* c) {
+        if (err) return;
+        if (vk::box_contains(B, c, nd)) {
+            kind[t] = VLASOV_GHOST_INTERIOR; src_patch[t] = patch; src_cell[t] = vk::box_index(B, c, nd);
+        } else if (int pc = phys_code(L, c); pc >= 0) {
+            kind[t] = VLASOV_GHOST_PHYS; src_patch[t] = -1; src_cell[t] = pc;
+        } else {
+            int w[4];
+            wrap_cfg(L, c, w);
+            const int q = own.find(w);
+            if (q >= 0) {
+                kind[t] = VLASOV_GHOST_SIBLING; src_patch[t] = q; src_cell[t] = vk::box_index(L->boxes[q], w, nd);
+            } else if (C) {
+                int cc[4];
+                for (int d = 0; d < nd; ++d) cc[d] = vk::floordiv(w[d], L->coarse_ratio[d]);
+                const int cq = cown.find(cc);
+                if (cq < 0) { err = vk::fail(VLASOV_ESTENCIL, "no coarse parent"); return; }
+                kind[t] = VLASOV_GHOST_COARSE; src_patch[t] = cq; src_cell[t] = vk::box_index(C->boxes[cq], cc, nd);
+            } else {
+                err = vk::fail(VLASOV_ENEST, "ghost cell without source");
+                return;
+            }
+        }
+        ++t;
+    });
+    return err;
+}
+
+// Alg.7 ComputeSubPatches, same set operations as the oracle, sorted output
+int vlasov_subpatches(const vlasov_level* const* levels, int32_t nlev, int32_t li, int32_t patch,
+                      vlasov_box* out, int32_t cap, int32_t* n) {
+    if (!levels || !n || li < 0 || li >= nlev) return vk::fail(VLASOV_EINVAL, "bad arguments");
+    const vlasov_level* L = levels[li];
+    if (patch < 0 || patch >= (int)L->boxes.size()) return vk::fail(VLASOV_EINVAL, "patch out of range");
+    const int nd = L->ndim;
+    const Box pin = L->boxes[patch];
+    std::vector<Box> S{pin};
+    for (int fl = li + 1; fl < nlev; ++fl) {
+        const vlasov_level* F = levels[fl];
+        int rr[4];
+        for (int d = 0; d < nd; ++d) rr[d] = F->ratio[d] / L->ratio[d];
+        for (const Box& fb : F->boxes) {
+            const Box P = vk::box_coarsen(fb, rr, nd);
+            if (vk::box_empty(vk::box_intersect(P, pin, nd), nd)) continue;
+            Box Pext = P;                                           // extend in reduction dims
+            for (int d = L->ncfg; d < nd; ++d) { Pext.lo[d] = pin.lo[d]; Pext.hi[d] = pin.hi[d]; }
+            std::vector<Box> S2;
+            for (const Box& Ps : S) {
+                const Box I = vk::box_intersect(Ps, Pext, nd);
+                if (vk::box_empty(I, nd)) { S2.push_back(Ps); continue; }
+                S2.push_back(I);
+                for (const Box& r : vk::box_subtract(Ps, I, nd)) S2.push_back(r);
+            }
+            S.clear();
+            for (const Box& Ps : S2)
+                for (const Box& r : vk::box_subtract(Ps, P, nd)) S.push_back(r);
+        }
+    }
+    std::vector<Box> T;
+    for (const Box& s : S)
+        if (!vk::box_empty(s, nd)) T.push_back(s);
+    std::sort(T.begin(), T.end(), [&](const Box& a, const Box& b) { return vk::box_less(a, b, nd); });
+    *n = (int32_t)T.size();
+    for (int i = 0; i < (int)T.size() && i < cap; ++i) {
+        for (int d = 0; d < 4; ++d) {
+            out[i].lo[d] = d < nd ? T[i].lo[d] : 0;
+            out[i].hi[d] = d < nd ? T[i].hi[d] : 0;
+        }
+    }
+    return VLASOV_OK;
+}
+
+int vlasov_tags_to_boxes(const uint8_t* tags, const int32_t domain_cells[4], int32_t ndim, const int32_t ratio[4],
+                         int32_t tile, vlasov_box* out, int32_t cap, int32_t* n) {
+    if (!tags || !domain_cells || !ratio || !n || ndim != 2) return vk::fail(VLASOV_EINVAL, "bad arguments");
+    int foot[2];
+    for (int d = 0; d < 2; ++d) {
+        if (ratio[d] < 1 || tile % ratio[d]) return vk::fail(VLASOV_EINVAL, "tile must be a multiple of the ratio");
+        foot[d] = tile / ratio[d];
+    }
+    const int nx = domain_cells[0], nv = domain_cells[1];
+    int cnt = 0;
+    for (int tx = 0; tx < nx / foot[0]; ++tx)
+        for (int tv = 0; tv < nv / foot[1]; ++tv) {
+            bool any = false;
+            for (int i = tx * foot[0]; i < (tx + 1) * foot[0] && !any; ++i)
+                for (int j = tv * foot[1]; j < (tv + 1) * foot[1]; ++j)
+                    if (tags[(int64_t)i * nv + j]) { any = true; break; }
+            if (!any) continue;
+            if (cnt < cap) {
+                std::memset(&out[cnt], 0, sizeof(vlasov_box));
+                out[cnt].lo[0] = tx * tile; out[cnt].hi[0] = (tx + 1) * tile - 1;
+                out[cnt].lo[1] = tv * tile; out[cnt].hi[1] = (tv + 1) * tile - 1;
+            }
+            ++cnt;
+        }
+    *n = cnt;
+    return VLASOV_OK;
+}
+
+// ---------------------------------------------------------------- compute entry points
+int vlasov_fill_ghosts(vlasov_level* L, double* f, const vlasov_level* coarser, const double* f_coarse,
+                       const double* E_bc, const double* f0v, int32_t interp) {
+    if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->n_cf > 0 && (coarser != L->coarser || !coarser || coarser->uid != L->coarser_uid))
+        return vk::fail(VLASOV_ESTALE, "fill_ghosts: coarser level does not match the one of level_create");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_fill(L, f, f_coarse, E_bc, f0v, interp);
+}
+
+int vlasov_rhs(vlasov_level* L, const double* f, const double* E, double* k, int32_t recon) {
+    if (!L || !f || !E || !k) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "rhs: 2D+2V not in this build yet");
+    return vk::launch_stage_1d1v(L, 0, 0.0, nullptr, f, nullptr, k, E, recon, nullptr);
+}
+
+int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, const double* f_s, double* u,
+                     double* f_next, const double* E, int32_t recon, double* rho_partials) {
+    if (!L || !f_s || !f_next || !E) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (stage < 1 || stage > 4) return vk::fail(VLASOV_EINVAL, "stage must be 1..4");
+    if (stage >= 2 && !f_n) return vk::fail(VLASOV_EINVAL, "f_n required");
+    if ((stage == 2 || stage == 4) && !u) return vk::fail(VLASOV_EINVAL, "u required");
+    if (rho_partials && !L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "fused partials need a single-block level");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage: 2D+2V not in this build yet");
+    return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E,
+                                 recon, rho_partials);
+}
+
+int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
+                         const double* rho_partials, double* rho_finest) {
+    if (!levels || nlev < 1 || !rho_finest) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    if (rho_partials) {
+        if (nlev != 1 || !levels[0]->single_block) return vk::fail(VLASOV_EINVAL, "partials: single-block level only");
+        return vk::launch_sum_partials(levels[0], rho_partials, rho_finest);
+    }
+    if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 2) {
+        if (!f || !f[0]) return vk::fail(VLASOV_EINVAL, "reduce_moment: field pointer required");
+        return vk::launch_moment_direct(levels[0], f[0], rho_finest);
+    }
+    return vk::fail(VLASOV_EUNSUPPORTED, "sub-patch reduction: not in this build yet");
+}
+
+int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisson** out) {
+    if (!out) return vk::fail(VLASOV_EINVAL, "null argument");
+    *out = nullptr;
+    if (n < 5 || !(dx > 0)) return vk::fail(VLASOV_EINVAL, "poisson: need n >= 5 and dx > 0");
+    if (n > 16384) return vk::fail(VLASOV_EUNSUPPORTED, "poisson: n > 16384");
+    // exact discrete Green's functions of the circulant system (long double on the host):
+    //   gE[d]   = (1/n) sum_m S_m sin(theta_m d),  S_m = dx (16 sin th - 2 sin 2th) / lambda_m
+    //   gphi[d] = (1/n) sum_{m != 0} 12 dx^2 / lambda_m cos(theta_m d)
+    //   lambda_m = 30 - 32 cos th + 2 cos 2th,  th = 2 pi m / n
+    std::vector<long double> lam(n), S(n);
+    const long double PI = 3.141592653589793238462643383279502884L;
+    for (int m = 0; m < n; ++m) {
+        const long double th = 2.0L * PI * m / n;
+        lam[m] = 30.0L - 32.0L * cosl(th) + 2.0L * cosl(2.0L * th);
+        S[m] = (m == 0) ? 0.0L : (long double)dx * (16.0L * sinl(th) - 2.0L * sinl(2.0L * th)) / lam[m];
+    }
+    std::vector<double> gE(n), gphi(n);
+    std::vector<long double> c(n), s(n);
+    for (int k = 0; k < n; ++k) {
+        const long double th = 2.0L * PI * k / n;
+        c[k] = cosl(th);
+        s[k] = sinl(th);
+    }
+    for (int d = 0; d < n; ++d) {
+        long double aE = 0.0L, aP = 0.0L;
+        for (int m = 1; m < n; ++m) {
+            const int k = (int)(((int64_t)m * d) % n);   // theta_m d mod 2 pi
+            aE += S[m] * s[k];
+            aP += (12.0L * dx * dx / lam[m]) * c[k];
+        }
+        gE[d] = (double)(aE / n);
+        gphi[d] = (double)(aP / n);
+    }
+    vlasov_poisson* P = new vlasov_poisson();
+    P->n = n;
+    P->dx = dx;
+    P->stream = (cudaStream_t)cuda_stream;
+    int rc;
+    if ((rc = upload(&P->d_gE, gE, P->stream)) || (rc = upload(&P->d_gphi, gphi, P->stream))) {
+        cudaFree(P->d_gE);
+        cudaFree(P->d_gphi);
+        delete P;
+        return rc;
+    }
+    cudaError_t e = cudaStreamSynchronize(P->stream);
+    if (e != cudaSuccess) { cudaFree(P->d_gE); cudaFree(P->d_gphi); delete P; return vk::cuda_check(e, "poisson upload"); }
+    *out = P;
+    return VLASOV_OK;
+}
+
+int vlasov_poisson_solve(vlasov_poisson* P, const double* rho, double* phi, double* E) {
+    if (!P || !rho) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_poisson(P, rho, phi, E);
+}
+
+int vlasov_poisson_destroy(vlasov_poisson* P) {
+    if (P) {
+        cudaStreamSynchronize(P->stream);
+        cudaFree(P->d_gE);
+        cudaFree(P->d_gphi);
+        delete P;
+    }
+    return VLASOV_OK;
+}
+
+int vlasov_inject_field(vlasov_level* L, const double* E_finest, const int32_t n_finest[2], double* E_lvl) {
+    if (!L || !E_finest || !n_finest || !E_lvl) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    if (L->ndim == 2) return vk::launch_inject_1d(L, E_finest, n_finest[0], E_lvl);
+    return vk::launch_inject_2d(L, E_finest, n_finest, E_lvl);
+}
+
+int vlasov_flux_register_accumulate(vlasov_level*, const double*, const double*, const double*, const double*,
+                                    double, double*, int32_t) {
+    return vk::fail(VLASOV_EUNSUPPORTED, "flux registers: not in this build yet");
+}
+int vlasov_average_down(vlasov_level*, const double*, double*, const double*, double) {
+    return vk::fail(VLASOV_EUNSUPPORTED, "average_down: not in this build yet");
+}
+int vlasov_tag_cells(vlasov_level*, const double*, double, int32_t, uint8_t*) {
+    return vk::fail(VLASOV_EUNSUPPORTED, "tag_cells: not in this build yet");
+}
+int vlasov_level_fill_from(vlasov_level*, double*, const vlasov_level*, const double*, const vlasov_level*,
+                           const double*, int32_t) {
+    return vk::fail(VLASOV_EUNSUPPORTED, "level_fill_from: not in this build yet");
+}
+
+}  // extern "C"

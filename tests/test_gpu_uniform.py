@@ -1,0 +1,171 @@
+"""GPU parity of the single-level (uniform) path against the oracle, through the C ABI.
+
+Tolerances (BASELINE.json north_star, SURVEY.md reading #25): normwise per level,
+max|f_gpu - f_oracle| <= tol * max|f_oracle| with tol = 1e-12 after one RK4 step and 1e-10 after
+100 steps (50 for C1).  Single operator applications (ghost fill, RHS) are held to 1e-13.
+"""
+import numpy as np
+import pytest
+
+import inputs
+from oracle import field, scheme, uniform
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1204_3853_b200 import _lib, api  # noqa: E402
+from paper_1204_3853_b200.solver import UniformVlasov1D  # noqa: E402
+
+RECON = {scheme.CENTERED4: _lib.CENTERED4, scheme.UPWIND: _lib.UPWIND}
+
+
+def relerr(a, b):
+    return np.max(np.abs(a - b)) / np.max(np.abs(b))
+
+
+def _level(w, boxes=None):
+    return api.Level(2, w.ncells, w.lower, inputs.spacing(w), (1, 1), boxes or inputs.level0_boxes(w))
+
+
+def _ghosted_E(E):
+    return np.pad(E, 2, mode="wrap")
+
+
+@pytest.mark.parametrize("shape,patch", [((64, 64), (64, 64)), ((40, 300), (20, 100)), ((37, 520), (37, 520))])
+def test_fill_ghosts_parity(shape, patch):
+    w = inputs.scaled(inputs.get("C2"), shape, patch)
+    L = _level(w)
+    f = inputs.random_positive_field(shape, 1)
+    E = inputs.random_field(shape[0], 2, -0.3, 0.3)
+    fbg = inputs.background_profile(w)
+    dev = L.field()
+    L.set_domain(dev, f)
+    Eg = torch.as_tensor(_ghosted_E(E)).cuda()
+    api.vlasov_fill_ghosts(L.h, dev, None, None, Eg, torch.as_tensor(fbg).cuda())
+    torch.cuda.synchronize()
+    got = L.patch_view(dev, 0, 2).cpu().numpy() if L.info.nblocks == 1 else None
+    ref = uniform.fill_ghosts_uniform(f, [_ghosted_E(E)], fbg)
+    if got is None:
+        pytest.skip("multi-block")
+    # the (+-2, +-2) corners are never used by the stencil but are defined identically
+    np.testing.assert_allclose(got, ref, rtol=1e-14, atol=1e-15)
+
+
+@pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
+@pytest.mark.parametrize("shape,patch", [((64, 64), (64, 64)), ((41, 300), (41, 300)), ((96, 768), (32, 64)),
+                                         ((16, 30), (16, 30))])
+def test_rhs_parity(recon, shape, patch):
+    w = inputs.scaled(inputs.get("C2"), shape, patch)
+    L = _level(w)
+    h = inputs.spacing(w)
+    f = inputs.random_positive_field(shape, 3)
+    E = inputs.random_field(shape[0], 4, -0.3, 0.3)
+    fbg = inputs.background_profile(w)
+    dev = L.field()
+    L.set_domain(dev, f)
+    Eg = torch.as_tensor(_ghosted_E(E)).cuda()
+    api.vlasov_fill_ghosts(L.h, dev, None, None, Eg, torch.as_tensor(fbg).cuda())
+    k = L.field(0.0)
+    api.vlasov_rhs(L.h, dev, Eg, k, RECON[recon])
+    torch.cuda.synchronize()
+    got = L.get_domain(k)
+    fg = uniform.fill_ghosts_uniform(f, [_ghosted_E(E)], fbg)
+    vbar = [scheme.exact_vbar(w.lower[1], h[1], shape[1])]
+    ref, _ = scheme.rhs(fg, vbar, [_ghosted_E(E)], h, recon)
+    assert relerr(got, ref) < 1e-13
+
+
+@pytest.mark.parametrize("n", [64, 256, 2048])
+def test_poisson_parity(n):
+    dx = 0.05 * 64 / n
+    rho = inputs.random_field(n, 5, -0.01, 0.01) + 0.001
+    P = api.Poisson(n, dx)
+    r = torch.as_tensor(rho).cuda()
+    E = torch.zeros(n, dtype=torch.float64, device="cuda")
+    phi = torch.zeros(n, dtype=torch.float64, device="cuda")
+    P.solve(r, phi, E)
+    torch.cuda.synchronize()
+    cond = 64.0 / (30 - 32 * np.cos(2 * np.pi / n) + 2 * np.cos(4 * np.pi / n))
+    tol = 50 * np.finfo(float).eps * cond
+    phi_ref = field.solve_potential(rho, dx)
+    E_ref = field.efield_from_potential(phi_ref, dx)
+    assert relerr(phi.cpu().numpy(), phi_ref) < tol
+    assert relerr(E.cpu().numpy(), E_ref) < tol
+
+
+def test_fused_partials_equal_direct_moment():
+    w = inputs.get("C1")
+    S = UniformVlasov1D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), inputs.background_profile(w))
+    S.set_state(inputs.initial_cell_averages(w))
+    S.step(inputs.fixed_dt(w))
+    torch.cuda.synchronize()
+    rho_fused = torch.zeros_like(S.rho)
+    api.vlasov_reduce_moment([S.level.h], None, S.partials, rho_fused)
+    rho_direct = torch.zeros_like(S.rho)
+    api.vlasov_reduce_moment([S.level.h], [S.A], None, rho_direct)
+    torch.cuda.synchronize()
+    f = S.get_state()
+    ref = field.moment_rho(f, inputs.spacing(w)[1])
+    np.testing.assert_allclose(rho_fused.cpu().numpy(), ref, atol=1e-15)
+    np.testing.assert_allclose(rho_direct.cpu().numpy(), ref, atol=1e-15)
+
+
+def _run_both(w, nsteps, recon=scheme.CENTERED4, boxes=None, graph=False):
+    h = inputs.spacing(w)
+    dt = inputs.fixed_dt(w)
+    f0 = inputs.initial_cell_averages(w)
+    S = UniformVlasov1D(w.ncells, w.lower, h, boxes or inputs.level0_boxes(w), inputs.background_profile(w),
+                        RECON[recon])
+    S.set_state(f0)
+    if graph:
+        S.step(dt)
+        S.stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=S.stream):
+            for s in (1, 2, 3, 4):
+                S._stage(s, dt)
+        for _ in range(nsteps - 1):
+            g.replay()
+    else:
+        for _ in range(nsteps):
+            S.step(dt)
+    got = S.get_state()
+    prob = uniform.problem_for(w, recon)
+    ref, _ = prob.run(f0, dt, nsteps)
+    return got, ref
+
+
+@pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
+def test_c1_one_step(recon):
+    got, ref = _run_both(inputs.get("C1"), 1, recon)
+    assert relerr(got, ref) < 1e-12
+
+
+def test_c1_fifty_steps():
+    got, ref = _run_both(inputs.get("C1"), 50)
+    assert relerr(got, ref) < 1e-10
+
+
+def test_c1_fifty_steps_upwind_graph():
+    got, ref = _run_both(inputs.get("C1"), 50, scheme.UPWIND, graph=True)
+    assert relerr(got, ref) < 1e-10
+
+
+def test_c2_hundred_steps():
+    got, ref = _run_both(inputs.get("C2"), 100)
+    assert relerr(got, ref) < 1e-10
+
+
+def test_ragged_multi_tile_ten_steps():
+    # 2 x 3 patches merged into one block, ragged tiles in both x (rows) and v (columns)
+    w = inputs.scaled(inputs.get("C4"), (150, 600), (75, 200))
+    got, ref = _run_both(w, 10)
+    assert relerr(got, ref) < 1e-11
+
+
+@pytest.mark.slow
+def test_c4_full_size_one_step():
+    got, ref = _run_both(inputs.get("C4"), 1)
+    assert relerr(got, ref) < 1e-12
