@@ -9,12 +9,12 @@
  * Status:     every int-returning call returns VLASOV_OK (0) or a negative VLASOV_E* code; the
  *             message of the last failure on the calling host thread is vlasov_last_error().
  *             Kernel faults are asynchronous: they surface as VLASOV_ECUDA at a later call.
- * Ownership:  every phase-space or configuration-space FIELD array (f, k, u, E, rho, partials,
- *             flux registers, tags) is a caller-owned DEVICE buffer of the length reported by
+ * Ownership:  every phase-space or configuration-space FIELD array (f, k, u, E, rho, flux
+ *             registers, tags) is a caller-owned DEVICE buffer of the length reported by
  *             vlasov_level_get_info(), passed as a raw pointer.  The library owns only level
- *             metadata (box lists, tiles, ghost/transfer task lists, Green's functions) on host and
- *             device; it is freed by the matching *_destroy.  No call other than *_create
- *             allocates device memory.
+ *             metadata (box lists, tiles, ghost/transfer task lists, Green's functions) and small
+ *             scratch (moment partial sums) on host and device, freed by the matching *_destroy.
+ *             No call other than *_create allocates device memory.
  * Streams:    a level (and a Poisson plan) is bound to the cudaStream_t given at creation (passed
  *             as void*; NULL = legacy default stream).  Every compute call is enqueued on that
  *             stream and returns without synchronising, so the calls can be captured in a CUDA
@@ -74,7 +74,6 @@ typedef struct {
     int64_t field_doubles;    /* length of every phase-space field array of this level          */
     int64_t e_doubles;        /* length of this level's E array: C * prod(ncfg_d + 4)             */
     int64_t cfg_cells;        /* configuration cells of this level (prod ncfg_d)                 */
-    int64_t partial_doubles;  /* length of rho_partials accepted by vlasov_rk4_stage              */
     int64_t fluxreg_doubles;  /* flux-register length of this level w.r.t. its coarser level      */
     int64_t tag_bytes;        /* length of the tag array of vlasov_tag_cells (level domain)      */
     int32_t nblocks, npatches, ntiles, ndim;
@@ -146,33 +145,40 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
  *   stage 2: u = f_n + (f_s - f_n)/3 + dt/3 k(f_s);  f_next = f_n + dt/2 k(f_s)
  *   stage 3: f_next = f_n + dt k(f_s)
  *   stage 4: f_next = u + (f_s - f_n)/3 + dt/6 k(f_s)           (f_next may alias f_n)
- * f_s ghosts must be filled.  If rho_partials != NULL the kernel also writes, for every
- * configuration cell and every velocity tile, the sum of f_next over the tile
- * (partial_doubles entries) for vlasov_reduce_moment.                                          */
+ * Ghosts of f_s: if E_bc and f0v are both non-NULL the level must be ONE block covering the
+ * (periodic) domain with an even number of velocity cells; the kernel then derives the ghost
+ * values itself (periodic wrap in x, characteristic v-boundary condition with E_bc, exactly as
+ * vlasov_fill_ghosts(E_bc, f0v) would) and never reads the ghost frame.  Otherwise (NULL) the
+ * ghost frame of f_s must have been filled by vlasov_fill_ghosts.
+ * rho_next (nullable; single block covering the domain only): receives the velocity moment of
+ * f_next, rho = 1 - dv sum_v f_next, fused into the stage: per-(row, v-tile) partial
+ * sums combined in a fixed order by the last CTA of each row strip (deterministic).            */
 int vlasov_rhs(vlasov_level* level, const double* f, const double* E, double* k, int32_t recon);
 int vlasov_rk4_stage(vlasov_level* level, int32_t stage, double dt, double* f_n, const double* f_s,
-                     double* u, double* f_next, const double* E, int32_t recon,
-                     double* rho_partials);
+                     double* u, double* f_next, const double* E, const double* E_bc,
+                     const double* f0v, int32_t recon, double* rho_next);
 
 /* ---- reduction ------------------------------------------------------ *
- * rho on the finest configuration mesh: rho = 1 - sum_levels dv_l sum_v f (reading #13).
- * Single level with rho_partials != NULL: sums the fused per-tile partial sums of
- * vlasov_rk4_stage in a fixed order.  Otherwise Alg.8 Sub-Patch Reduction over the hierarchy
- * levels[0..nlev-1] with the (host array of) device field pointers f[l] whose x-ghosts must be
- * current: per sub-patch, v-sums including 2 ghost columns in x (reading #16), linear5
- * refinement to the finest x resolution, deposit; fixed summation order (level, patch,
- * sub-patch).                                                                                   */
+ * rho on the finest configuration mesh: rho = 1 - sum_levels dv_l sum_v f (reading #13), from the
+ * (host array of) device field pointers f[l] of the hierarchy levels[0..nlev-1].  One level
+ * covering the domain: direct velocity sums.  Otherwise Alg.8 Sub-Patch Reduction: x-ghosts of
+ * every level must be current; per sub-patch, v-sums including 2 ghost columns in x (reading
+ * #16), linear5 refinement to the finest x resolution, deposit; fixed summation order (level,
+ * patch, sub-patch).  The sub-patch plan is rebuilt lazily when any level changed.*/
 int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
-                         const double* rho_partials, double* rho_finest);
+                         double* rho_finest);
 
 /* ---- periodic Poisson + E -------------------------------------------------------- *
  * Plan for n >= 5 periodic cells of width dx (1D configuration space).  solve: projects rho to
  * mean zero, solves 30 phi_i - 16(phi_{i+1}+phi_{i-1}) + (phi_{i+2}+phi_{i-2}) = 12 dx^2 rho_i
  * (reading #2) with mean-zero phi, and E_i = -[8(phi_{i+1}-phi_{i-1}) - phi_{i+2} + phi_{i-2}]
  * /(12 dx) (reading #1).  Implemented as circulant convolutions with the exact discrete
- * Green's functions (computed on the host at plan creation).  phi or E may be NULL.             */
+ * Green's functions (computed on the host at plan creation).  phi or E may be NULL.  Both are
+ * written with `ghost` periodic ghost cells on each side (length n + 2*ghost), so that with
+ * ghost = 2 the E of a level at the finest x resolution is produced directly.                  */
 int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisson** out);
-int vlasov_poisson_solve(vlasov_poisson* plan, const double* rho, double* phi, double* E);
+int vlasov_poisson_solve(vlasov_poisson* plan, const double* rho, double* phi, double* E,
+                         int32_t ghost);
 int vlasov_poisson_destroy(vlasov_poisson* plan);
 
 /* ---- injection ----------------------------------------------------------------- *

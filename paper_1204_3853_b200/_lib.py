@@ -35,7 +35,7 @@ class Geom(C.Structure):
 
 class LevelInfo(C.Structure):
     _fields_ = [("field_doubles", C.c_int64), ("e_doubles", C.c_int64), ("cfg_cells", C.c_int64),
-                ("partial_doubles", C.c_int64), ("fluxreg_doubles", C.c_int64), ("tag_bytes", C.c_int64),
+                ("fluxreg_doubles", C.c_int64), ("tag_bytes", C.c_int64),
                 ("nblocks", C.c_int32), ("npatches", C.c_int32), ("ntiles", C.c_int32), ("ndim", C.c_int32),
                 ("ratio", C.c_int32 * 4), ("ncfg", C.c_int32 * 2), ("domain_cells", C.c_int32 * 4)]
 
@@ -61,10 +61,10 @@ _SIGS = {
     "vlasov_subpatches": (I32, [C.POINTER(P), I32, I32, I32, C.POINTER(Box), I32, PI32]),
     "vlasov_fill_ghosts": (I32, [P, P, P, P, P, P, I32]),
     "vlasov_rhs": (I32, [P, P, P, P, I32]),
-    "vlasov_rk4_stage": (I32, [P, I32, D, P, P, P, P, P, I32, P]),
-    "vlasov_reduce_moment": (I32, [C.POINTER(P), I32, C.POINTER(P), P, P]),
+    "vlasov_rk4_stage": (I32, [P, I32, D, P, P, P, P, P, P, P, I32, P]),
+    "vlasov_reduce_moment": (I32, [C.POINTER(P), I32, C.POINTER(P), P]),
     "vlasov_poisson_create": (I32, [I32, D, P, C.POINTER(P)]),
-    "vlasov_poisson_solve": (I32, [P, P, P, P]),
+    "vlasov_poisson_solve": (I32, [P, P, P, P, I32]),
     "vlasov_poisson_destroy": (I32, [P]),
     "vlasov_inject_field": (I32, [P, P, PI32, P]),
     "vlasov_flux_register_accumulate": (I32, [P, P, P, P, P, D, P, I32]),

@@ -112,16 +112,16 @@ def vlasov_rhs(h, f, E, k, recon=_lib.CENTERED4):
     return check(lib.vlasov_rhs(h, _ptr(f), _ptr(E), _ptr(k), recon))
 
 
-def vlasov_rk4_stage(h, stage, dt, f_n, f_s, u, f_next, E, recon=_lib.CENTERED4, rho_partials=None):
+def vlasov_rk4_stage(h, stage, dt, f_n, f_s, u, f_next, E, E_bc=None, f0v=None, recon=_lib.CENTERED4,
+                     rho_next=None):
     return check(lib.vlasov_rk4_stage(h, stage, float(dt), _ptr(f_n), _ptr(f_s), _ptr(u), _ptr(f_next), _ptr(E),
-                                      recon, _ptr(rho_partials)))
+                                      _ptr(E_bc), _ptr(f0v), recon, _ptr(rho_next)))
 
 
-def vlasov_reduce_moment(levels, f_list, rho_partials, rho_finest):
+def vlasov_reduce_moment(levels, f_list, rho_finest):
     arr = (C.c_void_p * len(levels))(*[l.value if isinstance(l, C.c_void_p) else l for l in levels])
-    fp = (C.c_void_p * len(levels))(*[(t.data_ptr() if t is not None else None) for t in f_list]) \
-        if f_list is not None else None
-    return check(lib.vlasov_reduce_moment(arr, len(levels), fp, _ptr(rho_partials), _ptr(rho_finest)))
+    fp = (C.c_void_p * len(levels))(*[(t.data_ptr() if t is not None else None) for t in f_list])
+    return check(lib.vlasov_reduce_moment(arr, len(levels), fp, _ptr(rho_finest)))
 
 
 def vlasov_poisson_create(n, dx, stream=None):
@@ -130,8 +130,8 @@ def vlasov_poisson_create(n, dx, stream=None):
     return out
 
 
-def vlasov_poisson_solve(p, rho, phi=None, E=None):
-    return check(lib.vlasov_poisson_solve(p, _ptr(rho), _ptr(phi), _ptr(E)))
+def vlasov_poisson_solve(p, rho, phi=None, E=None, ghost=0):
+    return check(lib.vlasov_poisson_solve(p, _ptr(rho), _ptr(phi), _ptr(E), int(ghost)))
 
 
 def vlasov_poisson_destroy(p):
@@ -227,6 +227,17 @@ class Level:
             sl = tuple(slice(lo[d], hi[d] + 1) for d in range(self.ndim))
             self.patch_view(f, p).copy_(torch.as_tensor(np.ascontiguousarray(full[sl])))
 
+    def block_view(self, f: torch.Tensor, ghost: int = 2):
+        """Whole ghosted block of a single-block level."""
+        assert self.info.nblocks == 1
+        off, st = self.layouts[0]
+        lo, _ = self.boxes[0]
+        lo_all = [min(b[0][d] for b in self.boxes) for d in range(self.ndim)]
+        hi_all = [max(b[1][d] for b in self.boxes) for d in range(self.ndim)]
+        start = off - sum((lo[d] - lo_all[d] + ghost) * st[d] for d in range(self.ndim))
+        size = [hi_all[d] - lo_all[d] + 1 + 2 * ghost for d in range(self.ndim)]
+        return torch.as_strided(f, size, st[:self.ndim], start)
+
     def get_domain(self, f: torch.Tensor) -> np.ndarray:
         out = np.full(tuple(self.info.domain_cells[d] for d in range(self.ndim)), np.nan)
         for p, (lo, hi) in enumerate(self.boxes):
@@ -240,8 +251,8 @@ class Poisson:
         self.n = n
         self.h = vlasov_poisson_create(n, dx, stream)
 
-    def solve(self, rho, phi=None, E=None):
-        vlasov_poisson_solve(self.h, rho, phi, E)
+    def solve(self, rho, phi=None, E=None, ghost=0):
+        vlasov_poisson_solve(self.h, rho, phi, E, ghost)
 
     def __del__(self):
         try:

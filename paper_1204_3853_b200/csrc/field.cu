@@ -7,16 +7,6 @@
 
 namespace vk {
 
-// rho[x] = 1 - dv * sum_{vt} partials[vt][x]   (fixed order vt = 0..n-1)
-__global__ void k_sum_partials(const double* __restrict__ partials, int nvt, int nx, double dv,
-                               double* __restrict__ rho) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= nx) return;
-    double s = 0.0;
-    for (int t = 0; t < nvt; ++t) s += partials[(int64_t)t * nx + x];
-    rho[x] = 1.0 - dv * s;
-}
-
 // rho[x] = 1 - dv * sum_v f[x][v] on a single block covering the domain (one warp per x row;
 // lane-strided sums combined by a fixed butterfly: deterministic)
 __global__ void k_moment_direct(const double* __restrict__ f, int64_t off, int pitch, int nx, int nv, double dv,
@@ -40,18 +30,14 @@ int launch_moment_direct(const vlasov_level* L, const double* f, double* rho) {
     return VLASOV_OK;
 }
 
-int launch_sum_partials(const vlasov_level* L, const double* partials, double* rho) {
-    const int nx = L->dom[0];
-    k_sum_partials<<<(nx + 255) / 256, 256, 0, L->stream>>>(partials, L->n_vtiles, nx, L->h[1], rho);
-    VK_LAUNCH("k_sum_partials");
-    return VLASOV_OK;
-}
+// out[i + ghost] = sum_k g[(i - k) mod n] (rho[k] - mean(rho)), plus periodic ghost copies.
+// One warp per output (OPW outputs per warp); every CTA stages the whole projected rho in
+// shared memory and reduces the mean itself in a fixed order, so the result is deterministic.
+constexpr int CIRC_THREADS = 256, CIRC_OPW = 2;
 
-// out[i] = sum_k g[(i - k) mod n] (rho[k] - mean(rho)).  One warp per output; every CTA
-// stages the whole projected rho in shared memory (n <= 8192) and reduces the mean itself in a
-// fixed order, so the result is deterministic.
-__global__ void k_circulant(const double* __restrict__ rho, const double* __restrict__ g, int n,
-                            double* __restrict__ out) {
+__global__ void __launch_bounds__(CIRC_THREADS) k_circulant(const double* __restrict__ rho,
+                                                             const double* __restrict__ g, int n, int ghost,
+                                                             double* __restrict__ out) {
     extern __shared__ double s_rho[];
     __shared__ double s_red[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -74,9 +60,10 @@ __global__ void k_circulant(const double* __restrict__ rho, const double* __rest
     const double mean = s_red[0];
     for (int k = tid; k < n; k += blockDim.x) s_rho[k] -= mean;      // projection
     __syncthreads();
-    const int per_block = nw * 4;
-    for (int o = 0; o < 4; ++o) {
-        const int i = blockIdx.x * per_block + warp * 4 + o;
+    const int per_block = nw * CIRC_OPW;
+#pragma unroll
+    for (int o = 0; o < CIRC_OPW; ++o) {
+        const int i = blockIdx.x * per_block + warp * CIRC_OPW + o;
         if (i >= n) break;
         double s = 0.0;
         for (int k = lane; k < n; k += 32) {
@@ -86,12 +73,16 @@ __global__ void k_circulant(const double* __restrict__ rho, const double* __rest
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) out[i] = s;
+        if (lane == 0) {
+            out[i + ghost] = s;
+            if (i < ghost) out[i + ghost + n] = s;
+            if (i >= n - ghost) out[i + ghost - n] = s;
+        }
     }
 }
 
-int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E) {
-    const int threads = 256, per_block = (threads / 32) * 4;
+int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E, int ghost) {
+    const int per_block = (CIRC_THREADS / 32) * CIRC_OPW;
     const int blocks = (P->n + per_block - 1) / per_block;
     const size_t smem = (size_t)P->n * sizeof(double);
     if (smem > 48 * 1024) {
@@ -102,11 +93,11 @@ int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E)
         }
     }
     if (E) {
-        k_circulant<<<blocks, threads, smem, P->stream>>>(rho, P->d_gE, P->n, E);
+        k_circulant<<<blocks, CIRC_THREADS, smem, P->stream>>>(rho, P->d_gE, P->n, ghost, E);
         VK_LAUNCH("k_circulant(E)");
     }
     if (phi) {
-        k_circulant<<<blocks, threads, smem, P->stream>>>(rho, P->d_gphi, P->n, phi);
+        k_circulant<<<blocks, CIRC_THREADS, smem, P->stream>>>(rho, P->d_gphi, P->n, ghost, phi);
         VK_LAUNCH("k_circulant(phi)");
     }
     return VLASOV_OK;

@@ -47,7 +47,8 @@ struct Block1 {               // one storage block of a 1D+1V level
     int32_t lo_x, lo_v, nx, nv;
 };
 struct Tile1 {                // one CTA of the 1D+1V stage kernel
-    int32_t block, x0, nrows, j0, ncols, pvt;   // pvt = partial v-tile index (-1: none)
+    int32_t block, x0, nrows, j0, ncols;
+    int32_t pvt, strip;       // v-tile index and row-strip index (moment partials; single block)
 };
 struct CFTask {               // one coarse-fine ghost value
     int64_t dst;              // fine index in the level array
@@ -110,6 +111,10 @@ struct vlasov_level {
     vk::Tile1* d_tiles_narrow = nullptr;
     int tile_rows = 0;
     int n_vtiles = 0;                     // partial v-tiles (single-block only)
+    int n_strips = 0;
+    double* d_partials = nullptr;         // moment scratch [n_vtiles][dom_x]
+    unsigned* d_tickets = nullptr;        // per-strip arrival tickets
+    bool self_ghost_ok = false;           // single periodic block, even nv: in-kernel ghosts
     // ghost fill
     int64_t n_copy = 0, n_cf = 0, n_phys = 0;
     int64_t* d_copy = nullptr;            // pairs (dst, src)
@@ -138,12 +143,13 @@ struct vlasov_poisson {
 namespace vk {
 // ------------------------------------------------------------------ kernels (launchers)
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s,
-                      double* u, double* f_next, const double* E, int recon, double* partials);
+                      double* u, double* f_next, const double* E, const double* E_bc,
+                      const double* f0v, int recon, double* rho);
+int stage_1d1v_ctas_per_sm(bool wide, int tile_rows);
 int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double* E_bc,
                 const double* f0v, int interp);
-int launch_sum_partials(const vlasov_level* L, const double* partials, double* rho);
 int launch_moment_direct(const vlasov_level* L, const double* f, double* rho);
-int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E);
+int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E, int ghost);
 int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest, double* E_lvl);
 int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest,
                      double* E_lvl);

@@ -161,12 +161,14 @@ void free_level(vlasov_level* L) {
     cudaFree(L->d_reflux);
     cudaFree(L->d_avg);
     cudaFree(L->d_b5);
+    cudaFree(L->d_partials);
+    cudaFree(L->d_tickets);
     delete L;
 }
 
 inline int wrap(int x, int n) { return ((x % n) + n) % n; }
 
-int device_ok_impl() {
+int device_ok_uncached() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) {
         cudaGetLastError();
@@ -178,6 +180,23 @@ int device_ok_impl() {
         return 0;
     }
     return p.major == 10 ? 1 : 0;
+}
+
+// cached per current device (cudaGetDeviceProperties costs milliseconds)
+int device_ok_impl() {
+    static int cache[64];
+    static bool init[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (dev < 0 || dev >= 64) return device_ok_uncached();
+    if (!init[dev]) {
+        cache[dev] = device_ok_uncached();
+        init[dev] = true;
+    }
+    return cache[dev];
 }
 
 // owner lookup over the level domain: which block (or patch) holds a cell (-1: none)
@@ -260,7 +279,7 @@ void for_each_cell(const Box& b, int nd, const std::function<void(const int*)>& 
 }
 
 // ------------------------------------------------------------------ task-list construction
-int build_tiles_1d(vlasov_level* L) {
+int build_tiles_1d(vlasov_level* L, bool have_device) {
     const bool wide = [&] {
         int mx = 0;
         for (const Box& b : L->blocks) mx = std::max(mx, vk::box_ncells_dim(b, 1));
@@ -272,29 +291,46 @@ int build_tiles_1d(vlasov_level* L) {
         const int nvt = (vk::box_ncells_dim(b, 1) + TV - 1) / TV;
         strips_total += (int64_t)vk::box_ncells_dim(b, 0) * nvt;
     }
-    int rows = (int)((strips_total + 591) / 592);
-    rows = ((rows + 3) / 4) * 4;
-    rows = std::max(8, std::min(64, rows));
-    if (const char* e = std::getenv("VLASOV_TILE_ROWS")) rows = std::max(4, std::min(256, atoi(e)));
+    // one-wave tiling: as many row strips as resident CTAs allow (occupancy of the stage-4
+    // instance, the one with the largest shared-memory ring)
+    int nsm = 148, per_sm = 3;
+    if (have_device) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int occ = vk::stage_1d1v_ctas_per_sm(wide, 128);
+        if (occ > 0) per_sm = occ;
+    }
+    const int64_t slots = (int64_t)nsm * per_sm;
+    int rows = (int)((strips_total + slots - 1) / slots);
+    rows = std::max(8, std::min(128, rows));
+    if (const char* e = std::getenv("VLASOV_TILE_ROWS")) rows = std::max(4, std::min(128, atoi(e)));
     L->tile_rows = rows;
     std::vector<vk::Tile1>& tiles = wide ? L->h_tiles_wide : L->h_tiles_narrow;
     tiles.clear();
     L->n_vtiles = 0;
+    L->n_strips = 0;
     for (size_t b = 0; b < L->blocks.size(); ++b) {
         const int nx = vk::box_ncells_dim(L->blocks[b], 0), nv = vk::box_ncells_dim(L->blocks[b], 1);
         const int nvt = (nv + TV - 1) / TV;
+        // balance the strips: equal row counts (+-1) instead of a short last strip
+        const int nstrip = (nx + rows - 1) / rows;
         if (L->single_block) L->n_vtiles = nvt;
-        for (int x0 = 0; x0 < nx; x0 += rows)
+        for (int s = 0; s < nstrip; ++s) {
+            const int x0 = (int)((int64_t)nx * s / nstrip), x1 = (int)((int64_t)nx * (s + 1) / nstrip);
             for (int vt = 0; vt < nvt; ++vt) {
                 vk::Tile1 t;
                 t.block = (int)b;
                 t.x0 = x0;
-                t.nrows = std::min(rows, nx - x0);
+                t.nrows = x1 - x0;
                 t.j0 = vt * TV;
                 t.ncols = std::min(TV, nv - vt * TV);
                 t.pvt = L->single_block ? vt : -1;
+                t.strip = L->n_strips;
                 tiles.push_back(t);
             }
+            ++L->n_strips;
+        }
     }
     L->h_blocks1.clear();
     for (size_t b = 0; b < L->blocks.size(); ++b) {
@@ -307,6 +343,7 @@ int build_tiles_1d(vlasov_level* L) {
         B.nv = vk::box_ncells_dim(L->blocks[b], 1);
         L->h_blocks1.push_back(B);
     }
+    L->self_ghost_ok = L->single_block && (L->dom[1] % 2 == 0) && L->dom[1] >= 4;
     return VLASOV_OK;
 }
 
@@ -496,7 +533,7 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
     std::vector<vk::CFTask> cfs;
     std::vector<vk::PhysTask> phys;
     if (nd == 2) {
-        rc = build_tiles_1d(L);
+        rc = build_tiles_1d(L, device_ok_impl() != 0);
         if (!rc) rc = build_ghost_tasks(L, coarser, copies, cfs, phys);
     } else {
         rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V levels: not in this build yet");
@@ -511,6 +548,11 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
     if (!device_ok_impl()) {            // host metadata only (queries work, compute calls fail)
         *out = L;
         return VLASOV_OK;
+    }
+    if (L->single_block && L->ndim == 2) {
+        VK_CUDA(cudaMalloc((void**)&L->d_partials, sizeof(double) * (size_t)L->n_vtiles * L->dom[0]));
+        VK_CUDA(cudaMalloc((void**)&L->d_tickets, sizeof(unsigned) * (size_t)std::max(1, L->n_strips)));
+        VK_CUDA(cudaMemsetAsync(L->d_tickets, 0, sizeof(unsigned) * (size_t)std::max(1, L->n_strips), L->stream));
     }
     if ((rc = upload(&L->d_blocks1, L->h_blocks1, L->stream)) ||
         (rc = upload(&L->d_tiles_wide, L->h_tiles_wide, L->stream)) ||
@@ -540,7 +582,6 @@ int vlasov_level_get_info(const vlasov_level* L, vlasov_level_info* info) {
     info->field_doubles = L->field_doubles;
     info->e_doubles = L->e_doubles;
     info->cfg_cells = (L->ndim == 2) ? L->dom[0] : (int64_t)L->dom[0] * L->dom[1];
-    info->partial_doubles = L->single_block ? (int64_t)L->n_vtiles * L->dom[0] : 0;
     info->fluxreg_doubles = L->n_reflux;
     info->tag_bytes = 1;
     for (int d = 0; d < L->ndim; ++d) info->tag_bytes *= L->dom[d];
@@ -692,32 +733,33 @@ int vlasov_rhs(vlasov_level* L, const double* f, const double* E, double* k, int
     if (!L || !f || !E || !k) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "rhs: 2D+2V not in this build yet");
-    return vk::launch_stage_1d1v(L, 0, 0.0, nullptr, f, nullptr, k, E, recon, nullptr);
+    return vk::launch_stage_1d1v(L, 0, 0.0, nullptr, f, nullptr, k, E, nullptr, nullptr, recon, nullptr);
 }
 
 int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, const double* f_s, double* u,
-                     double* f_next, const double* E, int32_t recon, double* rho_partials) {
+                     double* f_next, const double* E, const double* E_bc, const double* f0v, int32_t recon,
+                     double* rho_next) {
     if (!L || !f_s || !f_next || !E) return vk::fail(VLASOV_EINVAL, "null argument");
     if (stage < 1 || stage > 4) return vk::fail(VLASOV_EINVAL, "stage must be 1..4");
     if (stage >= 2 && !f_n) return vk::fail(VLASOV_EINVAL, "f_n required");
     if ((stage == 2 || stage == 4) && !u) return vk::fail(VLASOV_EINVAL, "u required");
-    if (rho_partials && !L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "fused partials need a single-block level");
+    if (recon != VLASOV_CENTERED4 && recon != VLASOV_UPWIND) return vk::fail(VLASOV_EINVAL, "bad recon");
+    if (rho_next && !L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "fused moment needs a single-block level");
+    if ((E_bc == nullptr) != (f0v == nullptr)) return vk::fail(VLASOV_EINVAL, "E_bc and f0v go together");
+    if (E_bc && !L->self_ghost_ok)
+        return vk::fail(VLASOV_EUNSUPPORTED, "in-kernel ghosts need one periodic block with even nv");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage: 2D+2V not in this build yet");
     return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E,
-                                 recon, rho_partials);
+                                 E_bc, f0v, recon, rho_next);
 }
 
 int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
-                         const double* rho_partials, double* rho_finest) {
-    if (!levels || nlev < 1 || !rho_finest) return vk::fail(VLASOV_EINVAL, "null argument");
+                         double* rho_finest) {
+    if (!levels || nlev < 1 || !rho_finest || !f) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
-    if (rho_partials) {
-        if (nlev != 1 || !levels[0]->single_block) return vk::fail(VLASOV_EINVAL, "partials: single-block level only");
-        return vk::launch_sum_partials(levels[0], rho_partials, rho_finest);
-    }
     if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 2) {
-        if (!f || !f[0]) return vk::fail(VLASOV_EINVAL, "reduce_moment: field pointer required");
+        if (!f[0]) return vk::fail(VLASOV_EINVAL, "reduce_moment: field pointer required");
         return vk::launch_moment_direct(levels[0], f[0], rho_finest);
     }
     return vk::fail(VLASOV_EUNSUPPORTED, "sub-patch reduction: not in this build yet");
@@ -773,10 +815,11 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
     return VLASOV_OK;
 }
 
-int vlasov_poisson_solve(vlasov_poisson* P, const double* rho, double* phi, double* E) {
+int vlasov_poisson_solve(vlasov_poisson* P, const double* rho, double* phi, double* E, int32_t ghost) {
     if (!P || !rho) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (ghost < 0 || ghost > P->n) return vk::fail(VLASOV_EINVAL, "bad ghost width");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
-    return vk::launch_poisson(P, rho, phi, E);
+    return vk::launch_poisson(P, rho, phi, E, ghost);
 }
 
 int vlasov_poisson_destroy(vlasov_poisson* P) {

@@ -1,17 +1,23 @@
-// 1D+1V fused RK4 stage kernel: face averages -> fluxes -> divergence -> RK4 stage combine ->
-// per-(x-row, v-tile) partial sums of the new stage state.
+// 1D+1V fused RK4 stage kernel: (ghost values) -> face averages -> fluxes -> divergence -> RK4
+// stage combine -> velocity moment of the new stage state.
 //
 // PAPER.md: face averages P:322-368, fluxes P:263-282 (+1/48, reading #3), divergence
 // P:246-250, RK4 P:389-410 (minimum-traffic rearrangement, see include/vlasov.h), moment
-// P:295-297.
+// P:295-297, periodic x and characteristic v-boundary P:222-231 (reading #6).
 //
 // Design (B200): one CTA owns a v-segment of TV = 2*NT contiguous cells and marches along x
-// over `nrows` rows.  A producer warp streams each ghosted row segment of f_s (and the matching
-// f_n / u rows) into an NSLOT-deep shared-memory ring with cp.async.bulk (TMA engine) completing
-// on mbarriers; NT consumer threads own two adjacent v-cells each, keep a 4-row register window
-// of f_s, compute every face once per row from registers, and release ring slots through
-// "empty" mbarriers.  Every HBM byte of f_s is read once per tile (+4 halo rows, L2 hits),
-// f_n / u are read once, f_next / u written once: 16/32/24/32 B per cell for stages 1..4.
+// over `nrows` rows.  A producer warp streams each row segment of f_s (with its 2+2 halo
+// columns) and the matching f_n / u rows into an NSLOT-deep shared-memory ring with
+// cp.async.bulk (TMA engine), completing on mbarriers; NSLOT is sized so that ~64 KB per CTA
+// are in flight.  NT consumer threads own two adjacent v-cells each, keep a 4-row register
+// window of f_s, compute every face once per row from registers, and release ring slots via
+// "empty" mbarriers.  f_s is read once per tile (+4 halo rows, L2 hits), f_n / u once, f_next / u
+// written once: 16/32/24/32 B per cell for stages 1..4 (DESIGN.md roofline).
+// SELF mode (single block covering the periodic domain): the producer wraps halo rows
+// periodically and the two edge threads of the edge tiles compute the characteristic v-ghosts
+// in registers, so no ghost-fill kernel and no ghost-frame traffic are needed.
+// Moment: per-(row, tile) warp-shuffle + cross-warp sums -> scratch; the last CTA of a row strip
+// (atomic ticket) adds the v-tiles in tile order -> rho = 1 - dv sum (deterministic).
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -26,11 +32,15 @@ struct StageArgs1 {
     double* u_out;
     double* f_next;
     const double* E;           // level E array, index x + 2
-    double* partials;          // [n_vtiles][dom_x] or null
+    const double* E_bc;        // SELF: field deciding the characteristic direction
+    const double* f0v;         // SELF: unperturbed profile on the ghosted v range
+    double* rho;               // nullable: moment of f_next
+    double* partials;          // scratch [n_vtiles][dom_x]
+    unsigned* tickets;         // scratch [n_strips]
     const Tile1* tiles;
     const Block1* blocks;
     double dt, dx, dv, v_lo;   // v_lo: physical lower velocity of the level domain
-    int dom_x;
+    int dom_x, dom_v, n_vtiles;
 };
 
 template <int RECON>
@@ -53,18 +63,28 @@ __device__ __forceinline__ double face_avg(double fm1, double f0, double fp1, do
     }
 }
 
-template <int STAGE, int RECON, int NT, int NSLOT>
+template <int STAGE, int NT>
+struct StageGeom {
+    static constexpr int TV = 2 * NT;
+    static constexpr int SEG = TV + 4;
+    static constexpr int SLOT = SEG + (STAGE >= 2 ? TV : 0) + (STAGE == 4 ? TV : 0);
+    // ring depth: ~64 KB of row data per CTA, at least 8 and at most 32 slots
+    static constexpr int NSLOT_RAW = (64 * 1024) / (SLOT * 8);
+    static constexpr int NSLOT = NSLOT_RAW < 8 ? 8 : (NSLOT_RAW > 32 ? 32 : NSLOT_RAW);
+};
+
+template <int STAGE, int RECON, int NT, bool SELF>
 __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
-    constexpr int TV = 2 * NT;
-    constexpr int SEG = TV + 4;
+    using SG = StageGeom<STAGE, NT>;
+    constexpr int TV = SG::TV, SEG = SG::SEG, SLOT = SG::SLOT, NSLOT = SG::NSLOT;
     constexpr bool NEED_FN = (STAGE >= 2);
     constexpr bool NEED_U = (STAGE == 4);
-    constexpr int SLOT = SEG + (NEED_FN ? TV : 0) + (NEED_U ? TV : 0);
     constexpr int NW = NT / 32;
 
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) uint64_t full_bar[NSLOT];
     __shared__ __align__(8) uint64_t empty_bar[NSLOT];
+    __shared__ unsigned s_ticket;
     double* psum = smem + NSLOT * SLOT;          // [NW][nrows]
 
     const Tile1 T = A.tiles[blockIdx.x];
@@ -94,16 +114,17 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
                 const int slot = q % NSLOT;
                 if (q >= NSLOT) mbar_wait(&empty_bar[slot], ((q / NSLOT) - 1) & 1);
                 const int r = T.x0 - 2 + q;
+                int rs = r;
+                if (SELF) rs = (r < 0) ? r + B.nx : (r >= B.nx ? r - B.nx : r);
                 const bool out_row = (q >= 2) && (q < T.nrows + 2);
                 uint32_t bytes = seg_bytes;
                 if (NEED_FN && out_row) bytes += row_bytes;
                 if (NEED_U && out_row) bytes += row_bytes;
                 double* dst = smem + slot * SLOT;
-                const int64_t rb = rowbase(r) + T.j0;
                 mbar_arrive_expect_tx(&full_bar[slot], bytes);
-                bulk_g2s(dst, A.f_s + rb - 2, seg_bytes, &full_bar[slot]);
-                if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rb, row_bytes, &full_bar[slot]);
-                if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rb, row_bytes, &full_bar[slot]);
+                bulk_g2s(dst, A.f_s + rowbase(rs) + T.j0 - 2, seg_bytes, &full_bar[slot]);
+                if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(r) + T.j0, row_bytes, &full_bar[slot]);
+                if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(r) + T.j0, row_bytes, &full_bar[slot]);
             }
         }
         return;
@@ -119,6 +140,11 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
     const double dv24 = A.dv * (1.0 / 24.0);
     const double rdx = 1.0 / A.dx, rdv = 1.0 / A.dv;
     const double* E = A.E + B.lo_x + G;          // E[i] for block-local row i (i >= -2)
+    // SELF: the thread holding domain cells (0,1) computes the low v-ghosts, the one holding
+    // (nv-2, nv-1) the high ones
+    const bool lo_edge = SELF && (B.lo_v + c0 == 0);
+    const bool hi_edge = SELF && (B.lo_v + c0 + 1 == A.dom_v - 1);
+    const double* Ebc = SELF ? (A.E_bc + B.lo_x + G) : nullptr;
 
     double W[4][4];                              // f_s rows r-3..r at columns c0-1..c0+2
     double vfm[3], vf0[3], vfp[3];               // v-faces c0-1/2, c0+1/2, c0+3/2 of rows i-1, i, i+1
@@ -132,15 +158,36 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
 
     for (int q = 0; q < Q; ++q) {
         const int slot = q % NSLOT;
+        const int r = T.x0 - 2 + q;
         mbar_wait(&full_bar[slot], (q / NSLOT) & 1);
         const double* seg = smem + slot * SLOT;
         const double2 pa = lds2(seg + cl), pb = lds2(seg + cl + 2), pc = lds2(seg + cl + 4);
         // columns c0-2 .. c0+3
-        const double v0 = pa.x, v1 = pa.y, v2 = pb.x, v3 = pb.y, v4 = pc.x, v5 = pc.y;
+        double v0 = pa.x, v1 = pa.y, v2 = pb.x, v3 = pb.y, v4 = pc.x, v5 = pc.y;
+        if (SELF && (lo_edge || hi_edge)) {      // characteristic BC (reading #6), a = -E_bc
+            const double a = -__ldg(Ebc + r);
+            if (lo_edge) {
+                if (a < 0.0) {
+                    v1 = 4.0 * v2 - 6.0 * v3 + 4.0 * v4 - v5;
+                    v0 = 10.0 * v2 - 20.0 * v3 + 15.0 * v4 - 4.0 * v5;
+                } else {
+                    v1 = __ldg(A.f0v + 1);
+                    v0 = __ldg(A.f0v + 0);
+                }
+            }
+            if (hi_edge) {
+                if (a > 0.0) {
+                    v4 = 4.0 * v3 - 6.0 * v2 + 4.0 * v1 - v0;
+                    v5 = 10.0 * v3 - 20.0 * v2 + 15.0 * v1 - 4.0 * v0;
+                } else {
+                    v4 = __ldg(A.f0v + A.dom_v + 2);
+                    v5 = __ldg(A.f0v + A.dom_v + 3);
+                }
+            }
+        }
 #pragma unroll
         for (int b = 0; b < 4; ++b) { W[0][b] = W[1][b]; W[1][b] = W[2][b]; W[2][b] = W[3][b]; }
         W[3][0] = v1; W[3][1] = v2; W[3][2] = v3; W[3][3] = v4;
-        const int r = T.x0 - 2 + q;
 
         double Fxn0 = 0.0, Fxn1 = 0.0;
         if (q >= 3) {                            // x-face (r-2)+1/2 from rows r-3..r
@@ -190,7 +237,7 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
             double* op = A.f_next + rowbase(i) + c0;
             if (act1) *reinterpret_cast<double2*>(op) = make_double2(o0, o1);
             else if (act0) op[0] = o0;
-            if (A.partials != nullptr) {
+            if (A.rho != nullptr) {
                 double s = (act0 ? o0 : 0.0) + (act1 ? o1 : 0.0);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -211,7 +258,7 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
         vfp[2] = face_avg<RECON>(v2, v3, v4, v5, ar);
     }
 
-    if (A.partials != nullptr && T.pvt >= 0) {
+    if (A.rho != nullptr) {
         named_bar_sync(1, NT);
         for (int rr = tid; rr < T.nrows; rr += NT) {
             double s = psum[rr];
@@ -219,16 +266,29 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
             for (int w = 1; w < NW; ++w) s += psum[w * T.nrows + rr];
             A.partials[(int64_t)T.pvt * A.dom_x + B.lo_x + T.x0 + rr] = s;
         }
+        // last CTA of this row strip finalises rho in v-tile order (deterministic)
+        __threadfence();
+        named_bar_sync(1, NT);
+        if (tid == 0) s_ticket = atomicAdd(A.tickets + T.strip, 1u);
+        named_bar_sync(1, NT);
+        if (s_ticket == (unsigned)(A.n_vtiles - 1)) {
+            __threadfence();
+            for (int rr = tid; rr < T.nrows; rr += NT) {
+                const int x = B.lo_x + T.x0 + rr;
+                double s = 0.0;
+                for (int t = 0; t < A.n_vtiles; ++t) s += __ldcg(A.partials + (int64_t)t * A.dom_x + x);
+                A.rho[x] = 1.0 - A.dv * s;
+            }
+            if (tid == 0) A.tickets[T.strip] = 0u;     // reset for the next launch
+        }
     }
 }
 
-template <int STAGE, int RECON, int NT, int NSLOT>
+template <int STAGE, int RECON, int NT, bool SELF>
 static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
-    constexpr int TV = 2 * NT;
-    constexpr int SEG = TV + 4;
-    constexpr int SLOT = SEG + (STAGE >= 2 ? TV : 0) + (STAGE == 4 ? TV : 0);
-    const size_t smem = (size_t)(NSLOT * SLOT + (NT / 32) * tile_rows) * sizeof(double);
-    auto kern = k_stage_1d1v<STAGE, RECON, NT, NSLOT>;
+    using SG = StageGeom<STAGE, NT>;
+    const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + (NT / 32) * tile_rows) * sizeof(double);
+    auto kern = k_stage_1d1v<STAGE, RECON, NT, SELF>;
     static bool configured = false;   // per template instantiation
     if (!configured) {
         VK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -239,21 +299,51 @@ static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t
     return VLASOV_OK;
 }
 
-template <int RECON, int NT>
+template <int RECON, int NT, bool SELF>
 static int dispatch_stage(int stage, const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
-    constexpr int NSLOT = 8;
     switch (stage) {
-        case 0: return launch_t<0, RECON, NT, NSLOT>(A, ntiles, tile_rows, st);
-        case 1: return launch_t<1, RECON, NT, NSLOT>(A, ntiles, tile_rows, st);
-        case 2: return launch_t<2, RECON, NT, NSLOT>(A, ntiles, tile_rows, st);
-        case 3: return launch_t<3, RECON, NT, NSLOT>(A, ntiles, tile_rows, st);
-        case 4: return launch_t<4, RECON, NT, NSLOT>(A, ntiles, tile_rows, st);
+        case 0: return launch_t<0, RECON, NT, SELF>(A, ntiles, tile_rows, st);
+        case 1: return launch_t<1, RECON, NT, SELF>(A, ntiles, tile_rows, st);
+        case 2: return launch_t<2, RECON, NT, SELF>(A, ntiles, tile_rows, st);
+        case 3: return launch_t<3, RECON, NT, SELF>(A, ntiles, tile_rows, st);
+        case 4: return launch_t<4, RECON, NT, SELF>(A, ntiles, tile_rows, st);
     }
     return fail(VLASOV_EINVAL, "stage must be 1..4");
 }
 
-int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s,
-                      double* u, double* f_next, const double* E, int recon, double* partials) {
+template <int NT, bool SELF>
+static int dispatch_recon(int recon, int stage, const StageArgs1& A, int nt, int rows, cudaStream_t st) {
+    return recon == VLASOV_UPWIND ? dispatch_stage<VLASOV_UPWIND, NT, SELF>(stage, A, nt, rows, st)
+                                  : dispatch_stage<VLASOV_CENTERED4, NT, SELF>(stage, A, nt, rows, st);
+}
+
+// CTAs per SM of the most demanding stage instance (stage 4), for one-wave tiling.
+int stage_1d1v_ctas_per_sm(bool wide, int tile_rows) {
+    int n = 0;
+    cudaError_t e;
+    if (wide) {
+        using SG = StageGeom<4, 128>;
+        const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + 4 * tile_rows) * sizeof(double);
+        auto k = k_stage_1d1v<4, VLASOV_CENTERED4, 128, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 128 + 32, smem);
+    } else {
+        using SG = StageGeom<4, 32>;
+        const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + 1 * tile_rows) * sizeof(double);
+        auto k = k_stage_1d1v<4, VLASOV_CENTERED4, 32, true>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 32 + 32, smem);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
+                      double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
+                      double* rho) {
     StageArgs1 A;
     A.f_s = f_s;
     A.f_n = f_n;
@@ -261,23 +351,31 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.u_out = u;
     A.f_next = f_next;
     A.E = E;
-    A.partials = partials;
+    A.E_bc = E_bc;
+    A.f0v = f0v;
+    A.rho = rho;
+    A.partials = L->d_partials;
+    A.tickets = L->d_tickets;
     A.blocks = L->d_blocks1;
     A.dt = dt;
     A.dx = L->h[0];
     A.dv = L->h[1];
     A.v_lo = L->lower[1];
     A.dom_x = L->dom[0];
+    A.dom_v = L->dom[1];
+    A.n_vtiles = L->n_vtiles;
+    const bool self = (E_bc != nullptr && f0v != nullptr);
     const bool wide = !L->h_tiles_wide.empty();
     A.tiles = wide ? L->d_tiles_wide : L->d_tiles_narrow;
     const int nt = (int)(wide ? L->h_tiles_wide.size() : L->h_tiles_narrow.size());
     if (nt == 0) return VLASOV_OK;
+    const int rows = L->tile_rows;
     if (wide) {
-        return recon == VLASOV_UPWIND ? dispatch_stage<VLASOV_UPWIND, 128>(stage, A, nt, L->tile_rows, L->stream)
-                                      : dispatch_stage<VLASOV_CENTERED4, 128>(stage, A, nt, L->tile_rows, L->stream);
+        return self ? dispatch_recon<128, true>(recon, stage, A, nt, rows, L->stream)
+                    : dispatch_recon<128, false>(recon, stage, A, nt, rows, L->stream);
     }
-    return recon == VLASOV_UPWIND ? dispatch_stage<VLASOV_UPWIND, 32>(stage, A, nt, L->tile_rows, L->stream)
-                                  : dispatch_stage<VLASOV_CENTERED4, 32>(stage, A, nt, L->tile_rows, L->stream);
+    return self ? dispatch_recon<32, true>(recon, stage, A, nt, rows, L->stream)
+                : dispatch_recon<32, false>(recon, stage, A, nt, rows, L->stream);
 }
 
 }  // namespace vk

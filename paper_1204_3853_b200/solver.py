@@ -1,14 +1,16 @@
 """Step orchestration for a single uniform level (1D+1V Vlasov-Poisson), issuing only libvlasov
 C-ABI calls on one CUDA stream (optionally captured in a CUDA graph).
 
-One RK4 step = Alg.5 with one hierarchy and one level, per stage s = 1..4:
-    vlasov_reduce_moment (fused partials of the previous stage)      rho
-    vlasov_poisson_solve                                             E
-    vlasov_inject_field                                              E_lvl
-    vlasov_fill_ghosts(f_s, E_bc = E of the previous evaluation)      (Alg.2; reading #6b)
-    vlasov_rk4_stage(s)  -> f_{s+1} and its per-tile partial sums    (Alg.3 + P:389-410)
-Buffers: A = f_n, B = f2/f4, C = f3, U = u.  E_lvl alternates between two buffers so that the
-ghost fill of stage s reads the field of stage s-1 while stage s uses its own.
+One RK4 step = Alg.5 with one hierarchy and one level.  Per stage s = 1..4:
+    vlasov_poisson_solve(rho_s -> E_s, 2 periodic ghosts)          (injection at the
+                                                                    finest x resolution is the
+                                                                    identity)
+    vlasov_rk4_stage(s, f_s, E_s, E_bc = E_{s-1})  -> f_{s+1}, rho_{s+1}
+        (ghosts of f_s derived in-kernel = Alg.2 exchange + BC with the latest field, reading #6b;
+         face averages, fluxes, divergence, RK4 combine P:233-410; moment P:295-297)
+With ``self_ghost=False`` the ghost frame is filled by vlasov_fill_ghosts instead (generic path).
+Buffers: A = f_n, B = f2/f4, C = f3, U = u.  E alternates between two buffers so that stage s
+reads E_{s-1} for the boundary condition while it uses E_s for the fluxes.
 """
 from __future__ import annotations
 
@@ -23,15 +25,16 @@ from ._lib import CENTERED4
 
 class UniformVlasov1D:
     def __init__(self, ncells: Sequence[int], lower: Sequence[float], dx: Sequence[float], boxes,
-                 f0v: np.ndarray, recon: int = CENTERED4, stream: Optional[torch.cuda.Stream] = None):
+                 f0v: np.ndarray, recon: int = CENTERED4, stream: Optional[torch.cuda.Stream] = None,
+                 self_ghost: bool = True):
         self.stream = stream or torch.cuda.Stream()
         self.ncells = tuple(ncells)
         self.dx = tuple(dx)
         self.recon = recon
+        self.self_ghost = self_ghost
         with torch.cuda.stream(self.stream):
             self.level = api.Level(2, ncells, lower, dx, (1, 1), boxes, stream=self.stream)
-            info = self.level.info
-            if info.partial_doubles == 0:
+            if self.level.info.nblocks != 1:
                 raise ValueError("UniformVlasov1D needs boxes that tile the domain")
             self.poisson = api.Poisson(ncells[0], dx[0], self.stream)
             self.A = self.level.field()
@@ -40,20 +43,17 @@ class UniformVlasov1D:
             self.U = self.level.field()
             self.E = [self.level.efield(), self.level.efield()]
             self.rho = torch.zeros(ncells[0], dtype=torch.float64, device="cuda")
-            self.Efin = torch.zeros(ncells[0], dtype=torch.float64, device="cuda")
-            self.partials = torch.zeros(info.partial_doubles, dtype=torch.float64, device="cuda")
             self.f0v = torch.as_tensor(np.ascontiguousarray(f0v), dtype=torch.float64).cuda()
         self.graph = None
-        self.graph_steps = 0
         self.dt = None
 
     # ------------------------------------------------------------------ state
     def set_state(self, f_full: np.ndarray):
         with torch.cuda.stream(self.stream):
             self.level.set_domain(self.A, f_full)
-            # first constraint evaluation (t = 0): direct moment of f_n
-            api.vlasov_reduce_moment([self.level.h], [self.A], None, self.rho)
-            self._field(self.E[0])
+            # first constraint evaluation (t = 0): moment of f_n, field -> E_bc of stage 1
+            api.vlasov_reduce_moment([self.level.h], [self.A], self.rho)
+            self.poisson.solve(self.rho, None, self.E[0], 2)
         self.stream.synchronize()
 
     def get_state(self) -> np.ndarray:
@@ -66,41 +66,44 @@ class UniformVlasov1D:
         return self.E[0][2:-2].cpu().numpy()
 
     # ------------------------------------------------------------------ step
-    def _field(self, E_out):
-        self.poisson.solve(self.rho, None, self.Efin)
-        api.vlasov_inject_field(self.level.h, self.Efin, (self.ncells[0],), E_out)
-
-    def _stage(self, s, dt):
-        L = self.level.h
-        A, B, C, U = self.A, self.B, self.C, self.U
+    def buffers(self, s):
+        A, B, C = self.A, self.B, self.C
         f_s, f_next = {1: (A, B), 2: (B, C), 3: (C, B), 4: (B, A)}[s]
         E_cur, E_bc = (self.E[1], self.E[0]) if s % 2 == 1 else (self.E[0], self.E[1])
-        if s > 1 or self._have_partials:
-            api.vlasov_reduce_moment([L], None, self.partials, self.rho)
+        return f_s, f_next, E_cur, E_bc
+
+    def field_launch(self, s):
+        _, _, E_cur, _ = self.buffers(s)
+        self.poisson.solve(self.rho, None, E_cur, 2)
+
+    def stage_launch(self, s, dt):
+        L = self.level.h
+        f_s, f_next, E_cur, E_bc = self.buffers(s)
+        if self.self_ghost:
+            api.vlasov_rk4_stage(L, s, dt, self.A, f_s, self.U, f_next, E_cur, E_bc, self.f0v, self.recon, self.rho)
         else:
-            api.vlasov_reduce_moment([L], [A], None, self.rho)
-        self._field(E_cur)
-        api.vlasov_fill_ghosts(L, f_s, None, None, E_bc, self.f0v)
-        api.vlasov_rk4_stage(L, s, dt, A, f_s, U, f_next, E_cur, self.recon, self.partials)
+            api.vlasov_fill_ghosts(L, f_s, None, None, E_bc, self.f0v)
+            api.vlasov_rk4_stage(L, s, dt, self.A, f_s, self.U, f_next, E_cur, None, None, self.recon, self.rho)
+
+    def _stage(self, s, dt):
+        self.field_launch(s)
+        self.stage_launch(s, dt)
 
     def step(self, dt: float):
         with torch.cuda.stream(self.stream):
             for s in (1, 2, 3, 4):
                 self._stage(s, dt)
-        self._have_partials = True
-
-    _have_partials = False
 
     def capture(self, dt: float, steps: int = 1):
-        """Capture `steps` RK4 steps (16*steps... launches) in a CUDA graph."""
-        self.step(dt)                         # warm-up (also makes fused partials available)
+        """Warm up one step, then capture `steps` RK4 steps in a CUDA graph."""
+        self.step(dt)
         self.stream.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=self.stream):
             for _ in range(steps):
                 for s in (1, 2, 3, 4):
                     self._stage(s, dt)
-        self.graph, self.graph_steps, self.dt = g, steps, dt
+        self.graph, self.dt = g, dt
         return g
 
     def replay(self):
@@ -108,5 +111,5 @@ class UniformVlasov1D:
             self.graph.replay()
 
     def launches_per_step(self) -> int:
-        # per stage: sum_partials, circulant(E), inject, fill(copy+phys = 2), stage
-        return 4 * 6
+        # per stage: circulant (E with ghosts) + fused stage kernel  (+ 2 ghost-fill kernels)
+        return 4 * (2 if self.self_ghost else 4)
