@@ -303,6 +303,12 @@ int build_tiles_1d(vlasov_level* L, bool have_device) {
     }
     const int64_t slots = (int64_t)nsm * per_sm;
     int rows = (int)((strips_total + slots - 1) / slots);
+    if (L->blocks.size() == 1) {              // exact one-wave tiling of a single block
+        const int nx = vk::box_ncells_dim(L->blocks[0], 0);
+        const int nvt = (vk::box_ncells_dim(L->blocks[0], 1) + TV - 1) / TV;
+        const int64_t max_strips = std::max<int64_t>(1, slots / nvt);
+        rows = (int)((nx + max_strips - 1) / max_strips);
+    }
     rows = std::max(8, std::min(128, rows));
     if (const char* e = std::getenv("VLASOV_TILE_ROWS")) rows = std::max(4, std::min(128, atoi(e)));
     L->tile_rows = rows;

@@ -40,7 +40,7 @@ struct StageArgs1 {
     const Tile1* tiles;
     const Block1* blocks;
     double dt, dx, dv, v_lo;   // v_lo: physical lower velocity of the level domain
-    int dom_x, dom_v, n_vtiles;
+    int dom_x, dom_v, n_vtiles, tile_rows;
 };
 
 template <int RECON>
@@ -93,6 +93,13 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
     const int warp = tid >> 5, lane = tid & 31;
     const int Q = T.nrows + 4;
     const int wpad = (T.ncols + 1) & ~1;
+    double* sE = psum + NW * A.tile_rows;        // E of rows x0-2 .. x0+nrows+1
+    double* sEbc = sE + (A.tile_rows + 4);       // E_bc of the same rows (SELF)
+    for (int t = tid; t < Q; t += blockDim.x) {
+        const int gi = B.lo_x + T.x0 - 2 + t + G;  // index in the ghosted level E array
+        sE[t] = __ldg(A.E + gi);
+        if (SELF) sEbc[t] = __ldg(A.E_bc + gi);
+    }
 
     if (tid == 0) {
         for (int s = 0; s < NSLOT; ++s) {
@@ -139,12 +146,12 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
     const double vbm = vb0 - A.dv, vbp = vb1 + A.dv;
     const double dv24 = A.dv * (1.0 / 24.0);
     const double rdx = 1.0 / A.dx, rdv = 1.0 / A.dv;
-    const double* E = A.E + B.lo_x + G;          // E[i] for block-local row i (i >= -2)
+    const double* E = sE + 2 - T.x0;             // E[i] for block-local row i (x0-2 <= i <= x0+nrows+1)
     // SELF: the thread holding domain cells (0,1) computes the low v-ghosts, the one holding
     // (nv-2, nv-1) the high ones
     const bool lo_edge = SELF && (B.lo_v + c0 == 0);
     const bool hi_edge = SELF && (B.lo_v + c0 + 1 == A.dom_v - 1);
-    const double* Ebc = SELF ? (A.E_bc + B.lo_x + G) : nullptr;
+    const double* Ebc = sEbc + 2 - T.x0;
 
     double W[4][4];                              // f_s rows r-3..r at columns c0-1..c0+2
     double vfm[3], vf0[3], vfp[3];               // v-faces c0-1/2, c0+1/2, c0+3/2 of rows i-1, i, i+1
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
         // columns c0-2 .. c0+3
         double v0 = pa.x, v1 = pa.y, v2 = pb.x, v3 = pb.y, v4 = pc.x, v5 = pc.y;
         if (SELF && (lo_edge || hi_edge)) {      // characteristic BC (reading #6), a = -E_bc
-            const double a = -__ldg(Ebc + r);
+            const double a = -Ebc[r];
             if (lo_edge) {
                 if (a < 0.0) {
                     v1 = 4.0 * v2 - 6.0 * v3 + 4.0 * v4 - v5;
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
         }
         if (q >= 4) {                            // output row i = r - 2
             const int i = r - 2;
-            const double Ei = __ldg(E + i), Em = __ldg(E + i - 1), Ep = __ldg(E + i + 1);
+            const double Ei = E[i], Em = E[i - 1], Ep = E[i + 1];
             const double c48 = (Ep - Em) * (1.0 / 48.0);
             const double Fv0 = Ei * vf0[0] + c48 * (vfp[0] - vfm[0]);
             const double Fv1 = Ei * vf0[1] + c48 * (vfp[1] - vfm[1]);
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
         }
         Fxp0 = Fxn0; Fxp1 = Fxn1;
         // v-faces of row r (c0-1/2, c0+1/2, c0+3/2); speed a = -E_r
-        const double ar = -__ldg(E + r);
+        const double ar = -E[r];
 #pragma unroll
         for (int m = 0; m < 3; ++m) { vfm[m] = vf0[m]; vf0[m] = vfp[m]; }
         vfp[0] = face_avg<RECON>(v0, v1, v2, v3, ar);
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
 template <int STAGE, int RECON, int NT, bool SELF>
 static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
     using SG = StageGeom<STAGE, NT>;
-    const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + (NT / 32) * tile_rows) * sizeof(double);
+    const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + (NT / 32) * tile_rows + 2 * (tile_rows + 4)) * sizeof(double);
     auto kern = k_stage_1d1v<STAGE, RECON, NT, SELF>;
     static bool configured = false;   // per template instantiation
     if (!configured) {
@@ -323,13 +330,13 @@ int stage_1d1v_ctas_per_sm(bool wide, int tile_rows) {
     cudaError_t e;
     if (wide) {
         using SG = StageGeom<4, 128>;
-        const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + 4 * tile_rows) * sizeof(double);
+        const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + 4 * tile_rows + 2 * (tile_rows + 4)) * sizeof(double);
         auto k = k_stage_1d1v<4, VLASOV_CENTERED4, 128, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 128 + 32, smem);
     } else {
         using SG = StageGeom<4, 32>;
-        const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + 1 * tile_rows) * sizeof(double);
+        const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + 1 * tile_rows + 2 * (tile_rows + 4)) * sizeof(double);
         auto k = k_stage_1d1v<4, VLASOV_CENTERED4, 32, true>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 32 + 32, smem);
@@ -364,6 +371,7 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.dom_x = L->dom[0];
     A.dom_v = L->dom[1];
     A.n_vtiles = L->n_vtiles;
+    A.tile_rows = L->tile_rows;
     const bool self = (E_bc != nullptr && f0v != nullptr);
     const bool wide = !L->h_tiles_wide.empty();
     A.tiles = wide ? L->d_tiles_wide : L->d_tiles_narrow;
