@@ -146,7 +146,7 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
  *   stage 3: f_next = f_n + dt k(f_s)
  *   stage 4: f_next = u + (f_s - f_n)/3 + dt/6 k(f_s)           (f_next may alias f_n)
  * Ghosts of f_s: if E_bc and f0v are both non-NULL the level must be ONE block covering the
- * (periodic) domain with an even number of velocity cells; the kernel then derives the ghost
+ * (periodic) domain with a number of velocity cells divisible by 4; the kernel then derives the ghost
  * values itself (periodic wrap in x, characteristic v-boundary condition with E_bc, exactly as
  * vlasov_fill_ghosts(E_bc, f0v) would) and never reads the ghost frame.  Otherwise (NULL) the
  * ghost frame of f_s must have been filled by vlasov_fill_ghosts.

@@ -221,8 +221,17 @@ class Level:
     def get_patches(self, f: torch.Tensor, ghost: int = 0):
         return [self.patch_view(f, p, ghost).cpu().numpy() for p in range(len(self.boxes))]
 
+    def _covers_domain_as_one_block(self):
+        return self.info.nblocks == 1 and all(
+            min(b[0][d] for b in self.boxes) == 0 and max(b[1][d] for b in self.boxes) == self.info.domain_cells[d] - 1
+            for d in range(self.ndim))
+
     def set_domain(self, f: torch.Tensor, full: np.ndarray):
         """Scatter a whole-domain array (level index space) into the patches."""
+        if self._covers_domain_as_one_block():
+            g = [slice(2, -2)] * self.ndim
+            self.block_view(f, 2)[tuple(g)].copy_(torch.as_tensor(np.ascontiguousarray(full)))
+            return
         for p, (lo, hi) in enumerate(self.boxes):
             sl = tuple(slice(lo[d], hi[d] + 1) for d in range(self.ndim))
             self.patch_view(f, p).copy_(torch.as_tensor(np.ascontiguousarray(full[sl])))
@@ -239,6 +248,9 @@ class Level:
         return torch.as_strided(f, size, st[:self.ndim], start)
 
     def get_domain(self, f: torch.Tensor) -> np.ndarray:
+        if self._covers_domain_as_one_block():
+            g = [slice(2, -2)] * self.ndim
+            return self.block_view(f, 2)[tuple(g)].cpu().numpy()
         out = np.full(tuple(self.info.domain_cells[d] for d in range(self.ndim)), np.nan)
         for p, (lo, hi) in enumerate(self.boxes):
             sl = tuple(slice(lo[d], hi[d] + 1) for d in range(self.ndim))

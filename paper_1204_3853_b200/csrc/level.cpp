@@ -159,7 +159,10 @@ void free_level(vlasov_level* L) {
     cudaFree(L->d_cf);
     cudaFree(L->d_phys);
     cudaFree(L->d_reflux);
+    cudaFree(L->d_reflux_cells);
+    cudaFree(L->d_reflux_off);
     cudaFree(L->d_avg);
+    vk::free_red_plan(L->red_plan);
     cudaFree(L->d_b5);
     cudaFree(L->d_partials);
     cudaFree(L->d_tickets);
@@ -283,9 +286,9 @@ int build_tiles_1d(vlasov_level* L, bool have_device) {
     const bool wide = [&] {
         int mx = 0;
         for (const Box& b : L->blocks) mx = std::max(mx, vk::box_ncells_dim(b, 1));
-        return mx >= 256;
+        return mx >= 512;
     }();
-    const int TV = wide ? 256 : 64;
+    const int TV = vk::stage_1d1v_tile_width(wide);
     int64_t strips_total = 0;
     for (const Box& b : L->blocks) {
         const int nvt = (vk::box_ncells_dim(b, 1) + TV - 1) / TV;
@@ -349,7 +352,7 @@ int build_tiles_1d(vlasov_level* L, bool have_device) {
         B.nv = vk::box_ncells_dim(L->blocks[b], 1);
         L->h_blocks1.push_back(B);
     }
-    L->self_ghost_ok = L->single_block && (L->dom[1] % 2 == 0) && L->dom[1] >= 4;
+    L->self_ghost_ok = L->single_block && (L->dom[1] % 4 == 0) && L->dom[1] >= 4;
     return VLASOV_OK;
 }
 
@@ -420,6 +423,152 @@ int build_ghost_tasks(vlasov_level* L, const vlasov_level* C, std::vector<int64_
             }
         }
     }
+    return VLASOV_OK;
+}
+
+// Alg.7 ComputeSubPatches (P:1196-1209), same set operations as the oracle, sorted output
+std::vector<Box> subpatches_of(const vlasov_level* const* levels, int nlev, int li, int patch) {
+    const vlasov_level* L = levels[li];
+    const int nd = L->ndim;
+    const Box pin = L->boxes[patch];
+    std::vector<Box> S{pin};
+    for (int fl = li + 1; fl < nlev; ++fl) {
+        const vlasov_level* F = levels[fl];
+        int rr[4];
+        for (int d = 0; d < nd; ++d) rr[d] = F->ratio[d] / L->ratio[d];
+        for (const Box& fb : F->boxes) {
+            const Box P = vk::box_coarsen(fb, rr, nd);
+            if (vk::box_empty(vk::box_intersect(P, pin, nd), nd)) continue;
+            Box Pext = P;                                           // extend in reduction dims
+            for (int d = L->ncfg; d < nd; ++d) { Pext.lo[d] = pin.lo[d]; Pext.hi[d] = pin.hi[d]; }
+            std::vector<Box> S2;
+            for (const Box& Ps : S) {
+                const Box I = vk::box_intersect(Ps, Pext, nd);
+                if (vk::box_empty(I, nd)) { S2.push_back(Ps); continue; }
+                S2.push_back(I);
+                for (const Box& r : vk::box_subtract(Ps, I, nd)) S2.push_back(r);
+            }
+            S.clear();
+            for (const Box& Ps : S2)
+                for (const Box& r : vk::box_subtract(Ps, P, nd)) S.push_back(r);
+        }
+    }
+    std::vector<Box> T;
+    for (const Box& b : S)
+        if (!vk::box_empty(b, nd)) T.push_back(b);
+    std::sort(T.begin(), T.end(), [&](const Box& a, const Box& b) { return vk::box_less(a, b, nd); });
+    return T;
+}
+
+// Flux-register tasks (Alg.4 flux substitution as refluxing) and average-down tasks
+// of a 1D+1V fine level L with respect to its coarser level C.
+int build_amr_tasks(const vlasov_level* L, const vlasov_level* C, std::vector<vk::RefluxTask>& tasks,
+                    std::vector<int64_t>& cells, std::vector<int32_t>& offs, std::vector<vk::AvgTask>& avg) {
+    const int nd = 2;
+    const int* rr = L->coarse_ratio;
+    for (const Box& fb : L->boxes)
+        for (int d = 0; d < nd; ++d)
+            if (fb.lo[d] % rr[d] || (fb.hi[d] + 1) % rr[d])
+                return vk::fail(VLASOV_EINVAL, "fine boxes must be unions of refined coarse cells");
+    Owner cown = make_owner(C, C->blocks);
+    std::vector<uint8_t> covered((size_t)C->dom[0] * C->dom[1], 0);
+    for (const Box& fb : L->boxes) {
+        const Box cb = vk::box_coarsen(fb, rr, nd);
+        for (int x = cb.lo[0]; x <= cb.hi[0]; ++x)
+            for (int v = cb.lo[1]; v <= cb.hi[1]; ++v) covered[(size_t)x * C->dom[1] + v] = 1;
+    }
+    auto is_cov = [&](int x, int v) { return covered[(size_t)x * C->dom[1] + v] != 0; };
+    std::vector<vk::RefluxTask> T;
+    for (size_t q = 0; q < L->boxes.size(); ++q) {
+        const Box& fb = L->boxes[q];
+        const int fblk = L->patch_block[q];
+        const int64_t fpitch = L->block_str[fblk][0];
+        const Box cb = vk::box_coarsen(fb, rr, nd);
+        for (int side = 0; side < 2; ++side) {                   // x-faces
+            const int ux = wrap(side == 0 ? cb.lo[0] - 1 : cb.hi[0] + 1, C->dom[0]);
+            for (int jc = cb.lo[1]; jc <= cb.hi[1]; ++jc) {
+                if (is_cov(ux, jc)) continue;
+                int uc[4] = {ux, jc, 0, 0};
+                const int cq = cown.find(uc);
+                if (cq < 0) return vk::fail(VLASOV_ESTENCIL, "coarse cell next to a fine patch not on the coarser level");
+                vk::RefluxTask t;
+                std::memset(&t, 0, sizeof(t));
+                t.ccell = cell_addr(C, cq, uc);
+                t.dir = 0;
+                t.sign = side == 0 ? +1 : -1;
+                int cs[4] = {side == 0 ? ux - 1 : ux - 2, jc, 0, 0};
+                t.cf.s0 = cell_addr(C, cq, cs);
+                t.cf.pitch = (int32_t)C->block_str[cq][0];
+                t.cf.g = jc;
+                t.nfine = rr[1];
+                for (int s = 0; s < rr[1]; ++s) {
+                    const int jf = jc * rr[1] + s;
+                    int fs[4] = {side == 0 ? fb.lo[0] - 2 : fb.hi[0] - 1, jf, 0, 0};
+                    t.ff[s].s0 = cell_addr(L, fblk, fs);
+                    t.ff[s].pitch = (int32_t)fpitch;
+                    t.ff[s].g = jf;
+                }
+                T.push_back(t);
+            }
+        }
+        for (int side = 0; side < 2; ++side) {                   // v-faces
+            const int uv = side == 0 ? cb.lo[1] - 1 : cb.hi[1] + 1;
+            if (uv < 0 || uv >= C->dom[1]) continue;             // physical v boundary
+            for (int xc = cb.lo[0]; xc <= cb.hi[0]; ++xc) {
+                if (is_cov(xc, uv)) continue;
+                int uc[4] = {xc, uv, 0, 0};
+                const int cq = cown.find(uc);
+                if (cq < 0) return vk::fail(VLASOV_ESTENCIL, "coarse cell next to a fine patch not on the coarser level");
+                vk::RefluxTask t;
+                std::memset(&t, 0, sizeof(t));
+                t.ccell = cell_addr(C, cq, uc);
+                t.dir = 1;
+                t.sign = side == 0 ? +1 : -1;
+                int cs[4] = {xc, side == 0 ? uv - 1 : uv - 2, 0, 0};
+                t.cf.s0 = cell_addr(C, cq, cs);
+                t.cf.pitch = (int32_t)C->block_str[cq][0];
+                t.cf.g = xc + vk::G;
+                t.nfine = rr[0];
+                for (int s = 0; s < rr[0]; ++s) {
+                    const int xf = xc * rr[0] + s;
+                    int fs[4] = {xf, side == 0 ? fb.lo[1] - 2 : fb.hi[1] - 1, 0, 0};
+                    t.ff[s].s0 = cell_addr(L, fblk, fs);
+                    t.ff[s].pitch = (int32_t)fpitch;
+                    t.ff[s].g = xf + vk::G;
+                }
+                T.push_back(t);
+            }
+        }
+        for (int xc = cb.lo[0]; xc <= cb.hi[0]; ++xc)            // average-down
+            for (int jc = cb.lo[1]; jc <= cb.hi[1]; ++jc) {
+                int uc[4] = {xc, jc, 0, 0};
+                const int cq = cown.find(uc);
+                if (cq < 0) return vk::fail(VLASOV_ENEST, "fine patch not covered by the coarser level");
+                int fc[4] = {xc * rr[0], jc * rr[1], 0, 0};
+                vk::AvgTask a;
+                a.ccell = cell_addr(C, cq, uc);
+                a.fcell0 = cell_addr(L, fblk, fc);
+                a.fpitch = (int32_t)fpitch;
+                a.pad = 0;
+                avg.push_back(a);
+            }
+    }
+    // group by corrected coarse cell (stable: the face order above within a cell)
+    std::vector<size_t> idx(T.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return T[a].ccell < T[b].ccell; });
+    tasks.clear();
+    cells.clear();
+    offs.clear();
+    for (size_t k = 0; k < idx.size(); ++k) {
+        const vk::RefluxTask& t = T[idx[k]];
+        if (cells.empty() || cells.back() != t.ccell) {
+            cells.push_back(t.ccell);
+            offs.push_back((int32_t)tasks.size());
+        }
+        tasks.push_back(t);
+    }
+    offs.push_back((int32_t)tasks.size());
     return VLASOV_OK;
 }
 }  // namespace
@@ -538,9 +687,14 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
     std::vector<int64_t> copies;
     std::vector<vk::CFTask> cfs;
     std::vector<vk::PhysTask> phys;
+    std::vector<vk::RefluxTask> reflux;
+    std::vector<int64_t> reflux_cells;
+    std::vector<int32_t> reflux_off;
+    std::vector<vk::AvgTask> avg;
     if (nd == 2) {
         rc = build_tiles_1d(L, device_ok_impl() != 0);
         if (!rc) rc = build_ghost_tasks(L, coarser, copies, cfs, phys);
+        if (!rc && coarser) rc = build_amr_tasks(L, coarser, reflux, reflux_cells, reflux_off, avg);
     } else {
         rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V levels: not in this build yet");
     }
@@ -548,6 +702,10 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
     L->n_copy = (int64_t)copies.size() / 2;
     L->n_cf = (int64_t)cfs.size();
     L->n_phys = (int64_t)phys.size();
+    L->n_reflux = (int64_t)reflux.size();
+    L->n_reflux_cells = (int64_t)reflux_cells.size();
+    L->n_avg = (int64_t)avg.size();
+    L->avg_count = L->coarse_ratio[0] * L->coarse_ratio[1];
     std::vector<double> b5(2 * vk::MAXR * 5, 0.0);
     vk::linear5_weights(L->coarse_ratio[0], b5.data());
     vk::linear5_weights(L->coarse_ratio[1], b5.data() + 5 * vk::MAXR);
@@ -564,7 +722,9 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         (rc = upload(&L->d_tiles_wide, L->h_tiles_wide, L->stream)) ||
         (rc = upload(&L->d_tiles_narrow, L->h_tiles_narrow, L->stream)) ||
         (rc = upload(&L->d_copy, copies, L->stream)) || (rc = upload(&L->d_cf, cfs, L->stream)) ||
-        (rc = upload(&L->d_phys, phys, L->stream)) || (rc = upload(&L->d_b5, b5, L->stream))) {
+        (rc = upload(&L->d_phys, phys, L->stream)) || (rc = upload(&L->d_b5, b5, L->stream)) ||
+        (rc = upload(&L->d_reflux, reflux, L->stream)) || (rc = upload(&L->d_reflux_cells, reflux_cells, L->stream)) ||
+        (rc = upload(&L->d_reflux_off, reflux_off, L->stream)) || (rc = upload(&L->d_avg, avg, L->stream))) {
         free_level(L);
         return rc;
     }
@@ -653,40 +813,14 @@ int vlasov_level_ghost_map(const vlasov_level* L, int32_t patch, int32_t* kind, 
     return err;
 }
 
-// Alg.7 ComputeSubPatches (P:1196-1209), same set operations as the oracle, sorted output
+// Alg.7 ComputeSubPatches
 int vlasov_subpatches(const vlasov_level* const* levels, int32_t nlev, int32_t li, int32_t patch,
                       vlasov_box* out, int32_t cap, int32_t* n) {
     if (!levels || !n || li < 0 || li >= nlev) return vk::fail(VLASOV_EINVAL, "bad arguments");
     const vlasov_level* L = levels[li];
     if (patch < 0 || patch >= (int)L->boxes.size()) return vk::fail(VLASOV_EINVAL, "patch out of range");
     const int nd = L->ndim;
-    const Box pin = L->boxes[patch];
-    std::vector<Box> S{pin};
-    for (int fl = li + 1; fl < nlev; ++fl) {
-        const vlasov_level* F = levels[fl];
-        int rr[4];
-        for (int d = 0; d < nd; ++d) rr[d] = F->ratio[d] / L->ratio[d];
-        for (const Box& fb : F->boxes) {
-            const Box P = vk::box_coarsen(fb, rr, nd);
-            if (vk::box_empty(vk::box_intersect(P, pin, nd), nd)) continue;
-            Box Pext = P;                                           // extend in reduction dims
-            for (int d = L->ncfg; d < nd; ++d) { Pext.lo[d] = pin.lo[d]; Pext.hi[d] = pin.hi[d]; }
-            std::vector<Box> S2;
-            for (const Box& Ps : S) {
-                const Box I = vk::box_intersect(Ps, Pext, nd);
-                if (vk::box_empty(I, nd)) { S2.push_back(Ps); continue; }
-                S2.push_back(I);
-                for (const Box& r : vk::box_subtract(Ps, I, nd)) S2.push_back(r);
-            }
-            S.clear();
-            for (const Box& Ps : S2)
-                for (const Box& r : vk::box_subtract(Ps, P, nd)) S.push_back(r);
-        }
-    }
-    std::vector<Box> T;
-    for (const Box& s : S)
-        if (!vk::box_empty(s, nd)) T.push_back(s);
-    std::sort(T.begin(), T.end(), [&](const Box& a, const Box& b) { return vk::box_less(a, b, nd); });
+    const std::vector<Box> T = subpatches_of(levels, nlev, li, patch);
     *n = (int32_t)T.size();
     for (int i = 0; i < (int)T.size() && i < cap; ++i) {
         for (int d = 0; d < 4; ++d) {
@@ -753,7 +887,7 @@ int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, con
     if (rho_next && !L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "fused moment needs a single-block level");
     if ((E_bc == nullptr) != (f0v == nullptr)) return vk::fail(VLASOV_EINVAL, "E_bc and f0v go together");
     if (E_bc && !L->self_ghost_ok)
-        return vk::fail(VLASOV_EUNSUPPORTED, "in-kernel ghosts need one periodic block with even nv");
+        return vk::fail(VLASOV_EUNSUPPORTED, "in-kernel ghosts need one periodic block with nv a multiple of 4");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage: 2D+2V not in this build yet");
     return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E,

@@ -22,6 +22,7 @@
 
 #include "internal.h"
 #include "ptx.cuh"
+#include "scheme.cuh"
 
 namespace vk {
 
@@ -43,49 +44,40 @@ struct StageArgs1 {
     int dom_x, dom_v, n_vtiles, tile_rows;
 };
 
-template <int RECON>
-__device__ __forceinline__ double face_avg(double fm1, double f0, double fp1, double fp2, double upw) {
-    if (RECON == VLASOV_CENTERED4) {
-        return (7.0 * (f0 + fp1) - (fm1 + fp2)) * (1.0 / 12.0);
-    } else {
-        const double L = (-fm1 + 5.0 * f0 + 2.0 * fp1) * (1.0 / 6.0);
-        const double R = (2.0 * f0 + 5.0 * fp1 - fp2) * (1.0 / 6.0);
-        const double d2l = fm1 - 2.0 * f0 + fp1, d1l = fp1 - fm1;
-        const double d2r = f0 - 2.0 * fp1 + fp2, d1r = fp2 - f0;
-        const double sl = 1.0e-6 + ((13.0 / 12.0) * d2l * d2l + 0.25 * d1l * d1l);
-        const double sr = 1.0e-6 + ((13.0 / 12.0) * d2r * d2r + 0.25 * d1r * d1r);
-        // hat w_L = alpha_L/(alpha_L+alpha_R), alpha = 0.5/s^2  ==  s_R^2/(s_L^2 + s_R^2)
-        const double ql = sl * sl, qr = sr * sr;
-        const double inv = 1.0 / (ql + qr);
-        const double wl = qr * inv, wr = ql * inv;
-        const double big = fmax(wl, wr), small = fmin(wl, wr);
-        return (upw > 0.0) ? (big * L + small * R) : (small * L + big * R);
-    }
-}
+// CPT = 4 cells per consumer thread, TV = 4*NT cells per v-tile.
+constexpr int CPT = 4;
+constexpr int NT_WIDE = 128, NT_NARROW = 32;   // consumer threads per CTA
 
 template <int STAGE, int NT>
 struct StageGeom {
-    static constexpr int TV = 2 * NT;
-    static constexpr int SEG = TV + 4;
-    static constexpr int SLOT = SEG + (STAGE >= 2 ? TV : 0) + (STAGE == 4 ? TV : 0);
-    // ring depth: ~64 KB of row data per CTA, at least 8 and at most 32 slots
-    static constexpr int NSLOT_RAW = (64 * 1024) / (SLOT * 8);
-    static constexpr int NSLOT = NSLOT_RAW < 8 ? 8 : (NSLOT_RAW > 32 ? 32 : NSLOT_RAW);
+    static constexpr int TV = CPT * NT;
+    static constexpr int SEG = TV + 4;                       // f_s row segment incl. 2+2 halo columns
+    static constexpr int NFN = (STAGE >= 2 ? 1 : 0) + (STAGE == 4 ? 1 : 0);
+    static constexpr int SLOT = SEG + NFN * TV;              // doubles per ring slot
+    // ring depth: ~40 KB of row data per CTA, 3..16 slots (a slot is consumed in one row step)
+    static constexpr int NSLOT_RAW = (40 * 1024) / (SLOT * 8);
+    static constexpr int NSLOT = NSLOT_RAW < 3 ? 3 : (NSLOT_RAW > 16 ? 16 : NSLOT_RAW);
+    static constexpr int NW = NT / 32;
+    static size_t smem_bytes(int tile_rows) {
+        return (size_t)(NSLOT * SLOT + NW * tile_rows + 2 * (tile_rows + 4)) * sizeof(double);
+    }
 };
 
+// Ring slot of row step q (row r = x0 - 2 + q): [ f_s(r, j0-2 .. j0+TV+1) | f_n(r-2, j0..) | u(r-2, j0..) ];
+// the f_n / u rows are those of the output row i = r - 2 (q >= 4), so every slot is consumed
+// completely in its own row step and released at once.
 template <int STAGE, int RECON, int NT, bool SELF>
-__global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
+__global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
     using SG = StageGeom<STAGE, NT>;
-    constexpr int TV = SG::TV, SEG = SG::SEG, SLOT = SG::SLOT, NSLOT = SG::NSLOT;
+    constexpr int TV = SG::TV, SEG = SG::SEG, SLOT = SG::SLOT, NSLOT = SG::NSLOT, NW = SG::NW;
     constexpr bool NEED_FN = (STAGE >= 2);
     constexpr bool NEED_U = (STAGE == 4);
-    constexpr int NW = NT / 32;
 
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) uint64_t full_bar[NSLOT];
     __shared__ __align__(8) uint64_t empty_bar[NSLOT];
     __shared__ unsigned s_ticket;
-    double* psum = smem + NSLOT * SLOT;          // [NW][nrows]
+    double* psum = smem + NSLOT * SLOT;          // [NW][tile_rows]
 
     const Tile1 T = A.tiles[blockIdx.x];
     const Block1 B = A.blocks[T.block];
@@ -100,7 +92,6 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
         sE[t] = __ldg(A.E + gi);
         if (SELF) sEbc[t] = __ldg(A.E_bc + gi);
     }
-
     if (tid == 0) {
         for (int s = 0; s < NSLOT; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -117,152 +108,190 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
         if (lane == 0) {
             const uint32_t seg_bytes = (uint32_t)(wpad + 4) * 8u;
             const uint32_t row_bytes = (uint32_t)wpad * 8u;
+            int slot = 0;
+            uint32_t phase = 0;
             for (int q = 0; q < Q; ++q) {
-                const int slot = q % NSLOT;
-                if (q >= NSLOT) mbar_wait(&empty_bar[slot], ((q / NSLOT) - 1) & 1);
+                if (q >= NSLOT) mbar_wait(&empty_bar[slot], phase ^ 1u);
                 const int r = T.x0 - 2 + q;
                 int rs = r;
                 if (SELF) rs = (r < 0) ? r + B.nx : (r >= B.nx ? r - B.nx : r);
-                const bool out_row = (q >= 2) && (q < T.nrows + 2);
+                const bool out_row = (q >= 4);
                 uint32_t bytes = seg_bytes;
                 if (NEED_FN && out_row) bytes += row_bytes;
                 if (NEED_U && out_row) bytes += row_bytes;
                 double* dst = smem + slot * SLOT;
                 mbar_arrive_expect_tx(&full_bar[slot], bytes);
                 bulk_g2s(dst, A.f_s + rowbase(rs) + T.j0 - 2, seg_bytes, &full_bar[slot]);
-                if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(r) + T.j0, row_bytes, &full_bar[slot]);
-                if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(r) + T.j0, row_bytes, &full_bar[slot]);
+                if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(r - 2) + T.j0, row_bytes, &full_bar[slot]);
+                if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(r - 2) + T.j0, row_bytes, &full_bar[slot]);
+                if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
             }
         }
         return;
     }
 
     // ---------------------------------------------------------------- consumers
-    const int cl = 2 * tid;                      // tile-local column of my first cell
-    const bool act0 = cl < T.ncols, act1 = (cl + 1) < T.ncols;
+    const int cl = CPT * tid;                    // tile-local column of my first cell
     const int c0 = T.j0 + cl;                    // block-local interior column
-    const double vb0 = A.v_lo + ((double)(B.lo_v + c0) + 0.5) * A.dv;   // exact cell averages
-    const double vb1 = vb0 + A.dv;
-    const double vbm = vb0 - A.dv, vbp = vb1 + A.dv;
+    const int nact = min(CPT, T.ncols - cl);     // active cells of this thread (may be <= 0)
+    double vb[CPT + 2];                          // exact cell-average velocities of c0-1 .. c0+4
+#pragma unroll
+    for (int n = 0; n < CPT + 2; ++n) vb[n] = A.v_lo + ((double)(B.lo_v + c0 + n - 1) + 0.5) * A.dv;
     const double dv24 = A.dv * (1.0 / 24.0);
     const double rdx = 1.0 / A.dx, rdv = 1.0 / A.dv;
     const double* E = sE + 2 - T.x0;             // E[i] for block-local row i (x0-2 <= i <= x0+nrows+1)
-    // SELF: the thread holding domain cells (0,1) computes the low v-ghosts, the one holding
-    // (nv-2, nv-1) the high ones
-    const bool lo_edge = SELF && (B.lo_v + c0 == 0);
-    const bool hi_edge = SELF && (B.lo_v + c0 + 1 == A.dom_v - 1);
     const double* Ebc = sEbc + 2 - T.x0;
+    // SELF: the thread holding domain cells 0..3 computes the low v-ghosts, the one holding
+    // nv-4 .. nv-1 the high ones (level nv % 4 == 0)
+    const bool lo_edge = SELF && (B.lo_v + c0 == 0);
+    const bool hi_edge = SELF && (B.lo_v + c0 + CPT == A.dom_v);
 
-    double W[4][4];                              // f_s rows r-3..r at columns c0-1..c0+2
-    double vfm[3], vf0[3], vfp[3];               // v-faces c0-1/2, c0+1/2, c0+3/2 of rows i-1, i, i+1
-    double Fxp0 = 0.0, Fxp1 = 0.0;               // x-fluxes at i-1/2
+    double W[4][CPT + 2];                        // f_s rows (mod 4) at columns c0-1 .. c0+4
+    double VF[4][CPT + 1];                       // v-faces (mod 4) at c0-1/2 .. c0+CPT-1/2
+    double Fxp[CPT];                             // x-fluxes at i-1/2
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) W[a][b] = 0.0;
+        for (int b = 0; b < CPT + 2; ++b) W[a][b] = 0.0;
 #pragma unroll
-    for (int m = 0; m < 3; ++m) { vfm[m] = vf0[m] = vfp[m] = 0.0; }
+        for (int b = 0; b < CPT + 1; ++b) VF[a][b] = 0.0;
+    }
+#pragma unroll
+    for (int n = 0; n < CPT; ++n) Fxp[n] = 0.0;
 
-    for (int q = 0; q < Q; ++q) {
-        const int slot = q % NSLOT;
-        const int r = T.x0 - 2 + q;
-        mbar_wait(&full_bar[slot], (q / NSLOT) & 1);
-        const double* seg = smem + slot * SLOT;
-        const double2 pa = lds2(seg + cl), pb = lds2(seg + cl + 2), pc = lds2(seg + cl + 4);
-        // columns c0-2 .. c0+3
-        double v0 = pa.x, v1 = pa.y, v2 = pb.x, v3 = pb.y, v4 = pc.x, v5 = pc.y;
-        if (SELF && (lo_edge || hi_edge)) {      // characteristic BC (reading #6), a = -E_bc
-            const double a = -Ebc[r];
-            if (lo_edge) {
-                if (a < 0.0) {
-                    v1 = 4.0 * v2 - 6.0 * v3 + 4.0 * v4 - v5;
-                    v0 = 10.0 * v2 - 20.0 * v3 + 15.0 * v4 - 4.0 * v5;
-                } else {
-                    v1 = __ldg(A.f0v + 1);
-                    v0 = __ldg(A.f0v + 0);
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int q0 = 0; q0 < Q; q0 += 4) {
+#pragma unroll
+        for (int K = 0; K < 4; ++K) {           // K == q mod 4 == row r mod 4 (shifted by 2)
+            const int q = q0 + K;
+            if (q < Q) {
+                const int r = T.x0 - 2 + q;
+                mbar_wait(&full_bar[slot], phase);
+                const double* seg = smem + slot * SLOT;
+                double v[CPT + 4];               // columns c0-2 .. c0+5
+#pragma unroll
+                for (int m = 0; m < CPT + 4; m += 2) {
+                    const double2 p = lds2(seg + cl + m);
+                    v[m] = p.x; v[m + 1] = p.y;
                 }
-            }
-            if (hi_edge) {
-                if (a > 0.0) {
-                    v4 = 4.0 * v3 - 6.0 * v2 + 4.0 * v1 - v0;
-                    v5 = 10.0 * v3 - 20.0 * v2 + 15.0 * v1 - 4.0 * v0;
-                } else {
-                    v4 = __ldg(A.f0v + A.dom_v + 2);
-                    v5 = __ldg(A.f0v + A.dom_v + 3);
-                }
-            }
-        }
+                double fn[CPT], uu[CPT];
+                if (q >= 4) {
+                    if (NEED_FN) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) { W[0][b] = W[1][b]; W[1][b] = W[2][b]; W[2][b] = W[3][b]; }
-        W[3][0] = v1; W[3][1] = v2; W[3][2] = v3; W[3][3] = v4;
+                        for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + cl + m); fn[m] = p.x; fn[m + 1] = p.y; }
+                    }
+                    if (NEED_U) {
+#pragma unroll
+                        for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + TV + cl + m); uu[m] = p.x; uu[m + 1] = p.y; }
+                    }
+                }
+                if (SELF && (lo_edge || hi_edge)) {   // characteristic BC (reading #6), a = -E_bc
+                    const double a = -Ebc[r];
+                    if (lo_edge) {
+                        if (a < 0.0) {
+                            v[1] = 4.0 * v[2] - 6.0 * v[3] + 4.0 * v[4] - v[5];
+                            v[0] = 10.0 * v[2] - 20.0 * v[3] + 15.0 * v[4] - 4.0 * v[5];
+                        } else {
+                            v[1] = __ldg(A.f0v + 1);
+                            v[0] = __ldg(A.f0v + 0);
+                        }
+                    }
+                    if (hi_edge) {
+                        constexpr int L = CPT + 1;   // last interior column of the thread
+                        if (a > 0.0) {
+                            v[L + 1] = 4.0 * v[L] - 6.0 * v[L - 1] + 4.0 * v[L - 2] - v[L - 3];
+                            v[L + 2] = 10.0 * v[L] - 20.0 * v[L - 1] + 15.0 * v[L - 2] - 4.0 * v[L - 3];
+                        } else {
+                            v[L + 1] = __ldg(A.f0v + A.dom_v + 2);
+                            v[L + 2] = __ldg(A.f0v + A.dom_v + 3);
+                        }
+                    }
+                }
+                // register window: row r -> W[K]
+#pragma unroll
+                for (int b = 0; b < CPT + 2; ++b) W[K][b] = v[b + 1];
 
-        double Fxn0 = 0.0, Fxn1 = 0.0;
-        if (q >= 3) {                            // x-face (r-2)+1/2 from rows r-3..r
-            const double xm = face_avg<RECON>(W[0][0], W[1][0], W[2][0], W[3][0], vbm);
-            const double x0 = face_avg<RECON>(W[0][1], W[1][1], W[2][1], W[3][1], vb0);
-            const double x1 = face_avg<RECON>(W[0][2], W[1][2], W[2][2], W[3][2], vb1);
-            const double xp = face_avg<RECON>(W[0][3], W[1][3], W[2][3], W[3][3], vbp);
-            Fxn0 = vb0 * x0 + dv24 * (x1 - xm);
-            Fxn1 = vb1 * x1 + dv24 * (xp - x0);
-        }
-        if (q >= 4) {                            // output row i = r - 2
-            const int i = r - 2;
-            const double Ei = E[i], Em = E[i - 1], Ep = E[i + 1];
-            const double c48 = (Ep - Em) * (1.0 / 48.0);
-            const double Fv0 = Ei * vf0[0] + c48 * (vfp[0] - vfm[0]);
-            const double Fv1 = Ei * vf0[1] + c48 * (vfp[1] - vfm[1]);
-            const double Fv2 = Ei * vf0[2] + c48 * (vfp[2] - vfm[2]);
-            const double k0 = (Fv1 - Fv0) * rdv - (Fxn0 - Fxp0) * rdx;
-            const double k1 = (Fv2 - Fv1) * rdv - (Fxn1 - Fxp1) * rdx;
-            const double fs0 = W[1][1], fs1 = W[1][2];
-            const double* oseg = smem + ((q - 2) % NSLOT) * SLOT;
-            double o0, o1;
-            if (STAGE == 0) {
-                o0 = k0; o1 = k1;
-            } else if (STAGE == 1) {
-                o0 = fs0 + (0.5 * A.dt) * k0;
-                o1 = fs1 + (0.5 * A.dt) * k1;
-            } else {
-                const double2 fn = lds2(oseg + SEG + cl);
-                if (STAGE == 2) {
-                    const double u0 = fn.x + (fs0 - fn.x) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * k0;
-                    const double u1 = fn.y + (fs1 - fn.y) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * k1;
+                if (q >= 4) {                    // output row i = r - 2
+                    const int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;   // rows r-3, r-2, r-1
+                    const int i = r - 2;
+                    // x-faces at i + 1/2 (rows i-1 .. i+2 = r-3 .. r) for columns c0-1 .. c0+4
+                    double XF[CPT + 2];
+#pragma unroll
+                    for (int n = 0; n < CPT + 2; ++n)
+                        XF[n] = face_avg<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vb[n]);
+                    const double Ei = E[i], Em = E[i - 1], Ep = E[i + 1];
+                    const double c48 = (Ep - Em) * (1.0 / 48.0);
+                    // v-fluxes of row i from the v-faces of rows i-1 (R... see below), i, i+1
+                    const int VM = (K + 1) & 3, V0 = (K + 2) & 3, VP = (K + 3) & 3;  // rows r-3, r-2, r-1
+                    double Fv[CPT + 1];
+#pragma unroll
+                    for (int m = 0; m < CPT + 1; ++m) Fv[m] = Ei * VF[V0][m] + c48 * (VF[VP][m] - VF[VM][m]);
+                    double o[CPT];
+#pragma unroll
+                    for (int n = 0; n < CPT; ++n) {
+                        const double Fxn = vb[n + 1] * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
+                        const double k = (Fv[n + 1] - Fv[n]) * rdv - (Fxn - Fxp[n]) * rdx;
+                        Fxp[n] = Fxn;
+                        const double fs = W[R1][n + 1];
+                        if (STAGE == 0) {
+                            o[n] = k;
+                        } else if (STAGE == 1) {
+                            o[n] = fs + (0.5 * A.dt) * k;
+                        } else if (STAGE == 2) {
+                            uu[n] = fn[n] + (fs - fn[n]) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * k;
+                            o[n] = fn[n] + (0.5 * A.dt) * k;
+                        } else if (STAGE == 3) {
+                            o[n] = fn[n] + A.dt * k;
+                        } else {
+                            o[n] = uu[n] + (fs - fn[n]) * (1.0 / 3.0) + (A.dt * (1.0 / 6.0)) * k;
+                        }
+                    }
+                    double* op = A.f_next + rowbase(i) + c0;
                     double* up = A.u_out + rowbase(i) + c0;
-                    if (act1) *reinterpret_cast<double2*>(up) = make_double2(u0, u1);
-                    else if (act0) up[0] = u0;
-                    o0 = fn.x + (0.5 * A.dt) * k0;
-                    o1 = fn.y + (0.5 * A.dt) * k1;
-                } else if (STAGE == 3) {
-                    o0 = fn.x + A.dt * k0;
-                    o1 = fn.y + A.dt * k1;
-                } else {
-                    const double2 uu = lds2(oseg + SEG + TV + cl);
-                    o0 = uu.x + (fs0 - fn.x) * (1.0 / 3.0) + (A.dt * (1.0 / 6.0)) * k0;
-                    o1 = uu.y + (fs1 - fn.y) * (1.0 / 3.0) + (A.dt * (1.0 / 6.0)) * k1;
+                    if (nact == CPT) {
+#pragma unroll
+                        for (int m = 0; m < CPT; m += 2) {
+                            *reinterpret_cast<double2*>(op + m) = make_double2(o[m], o[m + 1]);
+                            if (STAGE == 2) *reinterpret_cast<double2*>(up + m) = make_double2(uu[m], uu[m + 1]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < CPT; ++m)
+                            if (m < nact) {
+                                op[m] = o[m];
+                                if (STAGE == 2) up[m] = uu[m];
+                            }
+                    }
+                    if (A.rho != nullptr) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int m = 0; m < CPT; ++m) s += (m < nact) ? o[m] : 0.0;
+#pragma unroll
+                        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                        if (lane == 0) psum[warp * A.tile_rows + (i - T.x0)] = s;
+                    }
+                } else if (q == 3) {             // x-fluxes at x0 - 1/2 (rows x0-2 .. x0+1)
+                    const int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;
+                    double XF[CPT + 2];
+#pragma unroll
+                    for (int n = 0; n < CPT + 2; ++n)
+                        XF[n] = face_avg<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vb[n]);
+#pragma unroll
+                    for (int n = 0; n < CPT; ++n) Fxp[n] = vb[n + 1] * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
                 }
-            }
-            double* op = A.f_next + rowbase(i) + c0;
-            if (act1) *reinterpret_cast<double2*>(op) = make_double2(o0, o1);
-            else if (act0) op[0] = o0;
-            if (A.rho != nullptr) {
-                double s = (act0 ? o0 : 0.0) + (act1 ? o1 : 0.0);
+                // v-faces of row r (c0-1/2 .. c0+CPT-1/2); speed a = -E_r; stored in VF[K]
+                const double ar = -E[r];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                if (lane == 0) psum[warp * T.nrows + (i - T.x0)] = s;
+                for (int m = 0; m < CPT + 1; ++m) VF[K][m] = face_avg<RECON>(v[m], v[m + 1], v[m + 2], v[m + 3], ar);
+                // release the slot only now: every value loaded from it has been consumed by an
+                // instruction of this (converged) warp, so no shared-memory read of the slot is
+                // still in flight when the producer overwrites it
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[slot]);
+                if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
             }
         }
-        if (q >= 2) {                            // slot of row r-2 fully consumed
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[(q - 2) % NSLOT]);
-        }
-        Fxp0 = Fxn0; Fxp1 = Fxn1;
-        // v-faces of row r (c0-1/2, c0+1/2, c0+3/2); speed a = -E_r
-        const double ar = -E[r];
-#pragma unroll
-        for (int m = 0; m < 3; ++m) { vfm[m] = vf0[m]; vf0[m] = vfp[m]; }
-        vfp[0] = face_avg<RECON>(v0, v1, v2, v3, ar);
-        vfp[1] = face_avg<RECON>(v1, v2, v3, v4, ar);
-        vfp[2] = face_avg<RECON>(v2, v3, v4, v5, ar);
     }
 
     if (A.rho != nullptr) {
@@ -270,7 +299,7 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
         for (int rr = tid; rr < T.nrows; rr += NT) {
             double s = psum[rr];
 #pragma unroll
-            for (int w = 1; w < NW; ++w) s += psum[w * T.nrows + rr];
+            for (int w = 1; w < NW; ++w) s += psum[w * A.tile_rows + rr];
             A.partials[(int64_t)T.pvt * A.dom_x + B.lo_x + T.x0 + rr] = s;
         }
         // last CTA of this row strip finalises rho in v-tile order (deterministic)
@@ -294,7 +323,7 @@ __global__ void __launch_bounds__(NT + 32) k_stage_1d1v(const StageArgs1 A) {
 template <int STAGE, int RECON, int NT, bool SELF>
 static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
     using SG = StageGeom<STAGE, NT>;
-    const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + (NT / 32) * tile_rows + 2 * (tile_rows + 4)) * sizeof(double);
+    const size_t smem = SG::smem_bytes(tile_rows);
     auto kern = k_stage_1d1v<STAGE, RECON, NT, SELF>;
     static bool configured = false;   // per template instantiation
     if (!configured) {
@@ -325,28 +354,24 @@ static int dispatch_recon(int recon, int stage, const StageArgs1& A, int nt, int
 }
 
 // CTAs per SM of the most demanding stage instance (stage 4), for one-wave tiling.
-int stage_1d1v_ctas_per_sm(bool wide, int tile_rows) {
+template <int NT>
+static int ctas_per_sm_t(int tile_rows) {
     int n = 0;
-    cudaError_t e;
-    if (wide) {
-        using SG = StageGeom<4, 128>;
-        const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + 4 * tile_rows + 2 * (tile_rows + 4)) * sizeof(double);
-        auto k = k_stage_1d1v<4, VLASOV_CENTERED4, 128, true>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 128 + 32, smem);
-    } else {
-        using SG = StageGeom<4, 32>;
-        const size_t smem = (size_t)(SG::NSLOT * SG::SLOT + 1 * tile_rows + 2 * (tile_rows + 4)) * sizeof(double);
-        auto k = k_stage_1d1v<4, VLASOV_CENTERED4, 32, true>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, 32 + 32, smem);
-    }
-    if (e != cudaSuccess) {
+    using SG = StageGeom<4, NT>;
+    auto k = k_stage_1d1v<4, VLASOV_CENTERED4, NT, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT + 32, SG::smem_bytes(tile_rows)) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     return n;
 }
+
+int stage_1d1v_ctas_per_sm(bool wide, int tile_rows) {
+    return wide ? ctas_per_sm_t<NT_WIDE>(tile_rows) : ctas_per_sm_t<NT_NARROW>(tile_rows);
+}
+
+int stage_1d1v_tile_width(bool wide) { return CPT * (wide ? NT_WIDE : NT_NARROW); }
 
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
@@ -379,11 +404,11 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     if (nt == 0) return VLASOV_OK;
     const int rows = L->tile_rows;
     if (wide) {
-        return self ? dispatch_recon<128, true>(recon, stage, A, nt, rows, L->stream)
-                    : dispatch_recon<128, false>(recon, stage, A, nt, rows, L->stream);
+        return self ? dispatch_recon<NT_WIDE, true>(recon, stage, A, nt, rows, L->stream)
+                    : dispatch_recon<NT_WIDE, false>(recon, stage, A, nt, rows, L->stream);
     }
-    return self ? dispatch_recon<32, true>(recon, stage, A, nt, rows, L->stream)
-                : dispatch_recon<32, false>(recon, stage, A, nt, rows, L->stream);
+    return self ? dispatch_recon<NT_NARROW, true>(recon, stage, A, nt, rows, L->stream)
+                : dispatch_recon<NT_NARROW, false>(recon, stage, A, nt, rows, L->stream);
 }
 
 }  // namespace vk
