@@ -1,0 +1,199 @@
+"""Step orchestration for a 1D+1V phase-space hierarchy (block-structured AMR), issuing only
+libvlasov C-ABI calls on one CUDA stream.
+
+One RK4 step = Alg.5 with one hierarchy, Alg.1-4 over the levels:
+
+    zero the interface flux registers of every fine level
+    for s = 1..4:                                   (f_s = f_n, f2, f3, f4 per level)
+        vlasov_fill_ghosts  level 0 .. L-1          Alg.2: siblings / periodic, CF interpolation
+                                                    from the (already filled) coarser level,
+                                                    characteristic v-BC with E_bc (reading #6b)
+        vlasov_reduce_moment                         Alg.8 sub-patch reduction -> rho (finest x)
+        vlasov_poisson_solve                         P:283-311 -> E on the finest x mesh
+        vlasov_inject_field per level
+        vlasov_rk4_stage per level                   Alg.3: faces, fluxes, divergence, RK4 combine
+        vlasov_flux_register_accumulate per fine level   += b_s (F_coarse - <F_fine>) on the
+                                                    coarse-fine interface (Alg.3 F_accum)
+    vlasov_average_down level L-1 .. 1              Alg.4: refluxing (flux substitution) and
+                                                    coarse := mean of fine
+
+Regrid (C3 rule, reading #18): tags on level 0, dilation, fixed fine tiles,
+vlasov_level_fill_from (copy old fine where it overlaps, else interpolate from level 0), then a
+constraint evaluation on the new hierarchy (Alg.5 after regridHierarchies).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import api
+from ._lib import CENTERED4, LINEAR5
+
+RK_B = (1.0 / 6.0, 1.0 / 3.0, 1.0 / 3.0, 1.0 / 6.0)
+
+
+class AmrVlasov1D:
+    def __init__(self, ncells0: Sequence[int], lower: Sequence[float], dx0: Sequence[float], level_boxes,
+                 ratios, f0v_fn, recon: int = CENTERED4, interp: int = LINEAR5,
+                 stream: Optional[torch.cuda.Stream] = None):
+        """level_boxes[l]: boxes (lo, hi) in level-l index space; ratios[l]: ratio to level 0;
+        f0v_fn(ratio) -> unperturbed profile on the ghosted v range of a level (numpy)."""
+        self.stream = stream or torch.cuda.Stream()
+        self.ncells0 = tuple(ncells0)
+        self.lower = tuple(lower)
+        self.dx0 = tuple(dx0)
+        self.recon = recon
+        self.interp = interp
+        self.f0v_fn = f0v_fn
+        self.levels: List[api.Level] = []
+        self.bufs = []            # per level: dict A, B, C, U
+        self.E = []               # per level: [E_a, E_b] ghosted level fields
+        self.f0v = []
+        self.regs = []            # per level (None for level 0)
+        self.cur = 0              # which of E[l][0/1] holds E_bc
+        with torch.cuda.stream(self.stream):
+            for l, (bl, r) in enumerate(zip(level_boxes, ratios)):
+                self._append_level(bl, r)
+        self._make_field_plan()
+
+    # ------------------------------------------------------------------ construction
+    def _append_level(self, boxes, ratio):
+        coarser = self.levels[-1] if self.levels else None
+        L = api.Level(2, self.ncells0, self.lower, self.dx0, ratio, boxes, coarser=coarser, stream=self.stream)
+        self.levels.append(L)
+        self.bufs.append({k: L.field(0.0) for k in "ABCU"})
+        self.E.append([L.efield(), L.efield()])
+        self.f0v.append(torch.as_tensor(np.ascontiguousarray(self.f0v_fn(tuple(ratio))),
+                                        dtype=torch.float64).cuda())
+        n = L.info.fluxreg_doubles
+        self.regs.append(None if coarser is None else torch.zeros(max(1, n), dtype=torch.float64, device="cuda"))
+
+    def _make_field_plan(self):
+        self.nxf = self.levels[-1].info.domain_cells[0]
+        self.dxf = self.dx0[0] / self.levels[-1].ratio[0]
+        self.poisson = api.Poisson(self.nxf, self.dxf, self.stream)
+        self.rho = torch.zeros(self.nxf, dtype=torch.float64, device="cuda")
+        self.E_f = torch.zeros(self.nxf, dtype=torch.float64, device="cuda")
+
+    @property
+    def handles(self):
+        return [L.h for L in self.levels]
+
+    # ------------------------------------------------------------------ state
+    def set_state(self, level_arrays):
+        """level_arrays[l]: whole-level-domain array (only patch cells are read) or a list of
+        per-patch interior arrays."""
+        with torch.cuda.stream(self.stream):
+            for L, b, a in zip(self.levels, self.bufs, level_arrays):
+                if isinstance(a, (list, tuple)):
+                    L.set_patches(b["A"], a)
+                else:
+                    L.set_domain(b["A"], a)
+            for E in self.E:
+                E[0].zero_()
+                E[1].zero_()
+            self.cur = 0
+            self._initial_constraints()
+        self.stream.synchronize()
+
+    def _initial_constraints(self):
+        """Ghosts with the current E_bc, then E_bc := constraints(f_n) (Alg.5 start / after regrid)."""
+        A = [b["A"] for b in self.bufs]
+        self._fill(A, [E[self.cur] for E in self.E])
+        self._constraints(A, [E[self.cur] for E in self.E])
+
+    def get_state(self, ghost=0):
+        self.stream.synchronize()
+        return [L.get_patches(b["A"], ghost) for L, b in zip(self.levels, self.bufs)]
+
+    def field_state(self):
+        self.stream.synchronize()
+        return [E[self.cur][2:-2].cpu().numpy() for E in self.E]
+
+    # ------------------------------------------------------------------ pieces
+    def _fill(self, fs, E_bc):
+        for l, L in enumerate(self.levels):
+            cL = self.levels[l - 1].h if l else None
+            api.vlasov_fill_ghosts(L.h, fs[l], cL, fs[l - 1] if l else None, E_bc[l], self.f0v[l], self.interp)
+
+    def _constraints(self, fs, E_out):
+        api.vlasov_reduce_moment(self.handles, fs, self.rho)
+        self.poisson.solve(self.rho, None, self.E_f, 0)
+        for l, L in enumerate(self.levels):
+            api.vlasov_inject_field(L.h, self.E_f, (self.nxf,), E_out[l])
+
+    def _stage(self, s, dt):
+        order = {1: ("A", "B"), 2: ("B", "C"), 3: ("C", "B"), 4: ("B", "A")}[s]
+        fs = [b[order[0]] for b in self.bufs]
+        fnext = [b[order[1]] for b in self.bufs]
+        E_bc = [E[self.cur] for E in self.E]
+        E_cur = [E[1 - self.cur] for E in self.E]
+        self._fill(fs, E_bc)
+        self._constraints(fs, E_cur)
+        for l, L in enumerate(self.levels):
+            b = self.bufs[l]
+            api.vlasov_rk4_stage(L.h, s, dt, b["A"], fs[l], b["U"], fnext[l], E_cur[l], None, None, self.recon,
+                                 None)
+        for l in range(1, len(self.levels)):
+            api.vlasov_flux_register_accumulate(self.levels[l].h, fs[l], E_cur[l], fs[l - 1], E_cur[l - 1],
+                                                RK_B[s - 1], self.regs[l], self.recon)
+        self.cur = 1 - self.cur
+
+    def step(self, dt: float):
+        with torch.cuda.stream(self.stream):
+            for r in self.regs[1:]:
+                r.zero_()
+            for s in (1, 2, 3, 4):
+                self._stage(s, dt)
+            for l in range(len(self.levels) - 1, 0, -1):
+                api.vlasov_average_down(self.levels[l].h, self.bufs[l]["A"], self.bufs[l - 1]["A"], self.regs[l],
+                                        dt)
+
+    # ------------------------------------------------------------------ regrid (C3 rule)
+    def tags_level0(self, tol, buffer):
+        L0 = self.levels[0]
+        with torch.cuda.stream(self.stream):
+            self._fill([b["A"] for b in self.bufs], [E[self.cur] for E in self.E])
+            tags = torch.zeros(L0.info.tag_bytes, dtype=torch.uint8, device="cuda")
+            api.vlasov_tag_cells(L0.h, self.bufs[0]["A"], tol, buffer, tags)
+        self.stream.synchronize()
+        return tags.cpu().numpy().reshape(self.ncells0)
+
+    def regrid(self, tol, buffer, ratio, tile):
+        """Two-level regrid: returns the new fine boxes (possibly empty)."""
+        tags = self.tags_level0(tol, buffer)
+        new_boxes = api.vlasov_tags_to_boxes(tags, self.ncells0, ratio, tile)
+        old_boxes = self.levels[1].boxes if len(self.levels) > 1 else []
+        if [tuple(map(tuple, b)) for b in new_boxes] == [tuple(map(tuple, b)) for b in old_boxes] and \
+                (len(self.levels) == 1 or tuple(self.levels[1].ratio) == tuple(ratio)):
+            # same hierarchy: data unchanged; Alg.5 still re-evaluates the constraints
+            with torch.cuda.stream(self.stream):
+                self._initial_constraints()
+            return new_boxes
+        nlev_old = len(self.levels)
+        old_level = self.levels[1] if nlev_old > 1 else None
+        old_A = self.bufs[1]["A"] if nlev_old > 1 else None
+        old_E = [E[self.cur] for E in self.E]
+        with torch.cuda.stream(self.stream):
+            del self.levels[1:], self.bufs[1:], self.E[1:], self.f0v[1:], self.regs[1:]
+            if new_boxes:
+                self._append_level(new_boxes, ratio)
+                api.vlasov_level_fill_from(self.levels[1].h, self.bufs[1]["A"], old_level.h if old_level else None,
+                                           old_A, self.levels[0].h, self.bufs[0]["A"], self.interp)
+            # keep E_bc of the surviving levels, zero for new ones
+            self.E[0][self.cur].copy_(old_E[0])
+            if len(self.levels) > 1:
+                if nlev_old > 1:
+                    self.E[1][self.cur].copy_(old_E[1])
+                else:
+                    self.E[1][self.cur].zero_()
+            self._make_field_plan()
+            self._initial_constraints()
+        self.stream.synchronize()
+        del old_level
+        return new_boxes
+
+    def cells(self):
+        return sum(int(np.prod([hi[d] - lo[d] + 1 for d in range(2)])) for L in self.levels for lo, hi in L.boxes)

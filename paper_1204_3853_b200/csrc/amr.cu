@@ -1,0 +1,216 @@
+// AMR transfers of 1D+1V levels: Alg.8 sub-patch reduction, interface flux
+// registers + refluxing (Alg.4 flux substitution), average-down, tags
+// (P:1423-1437).  Task lists are built on the host at level creation (level.cpp).
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "scheme.cuh"
+
+namespace vk {
+
+// ------------------------------------------------------------------ Alg.8 sub-patch reduction
+struct LevelPtrs {
+    const double* f[MAXLEV];
+};
+
+// colsum[c] = sum over the sub-patch's velocity range of column c (one warp per grown column)
+__global__ void k_red_cols(const LevelPtrs P, const RedCol* __restrict__ cols, int64_t ncols,
+                           double* __restrict__ colsum) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (c >= ncols) return;
+    const RedCol C = cols[c];
+    const double* p = P.f[C.level] + C.addr;
+    double s = 0.0;
+    for (int j = lane; j < C.nv; j += 32) s += p[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) colsum[c] = s;
+}
+
+// rho[x] = 1 - sum over the contributions of x (level, patch, sub-patch order) of
+//          dv_l * sum_j b_j(s) colsum[c + j]          (linear5 refinement of the partial sums)
+__global__ void k_red_finest(const double* __restrict__ colsum, const RedContrib* __restrict__ con,
+                             const int32_t* __restrict__ xoff, int nxf, double* __restrict__ rho) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= nxf) return;
+    double acc = 0.0;
+    for (int k = xoff[x]; k < xoff[x + 1]; ++k) {
+        const RedContrib& C = con[k];
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) t += C.b[j] * colsum[C.cs + j];
+        acc += C.dv * t;
+    }
+    rho[x] = 1.0 - acc;
+}
+
+int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st) {
+    LevelPtrs lp;
+    for (int l = 0; l < MAXLEV; ++l) lp.f[l] = l < nlev ? f[l] : nullptr;
+    if (P->ncols > 0) {
+        k_red_cols<<<(unsigned)((P->ncols + 7) / 8), 256, 0, st>>>(lp, P->d_cols, P->ncols, P->d_colsum);
+        VK_LAUNCH("k_red_cols");
+    }
+    k_red_finest<<<(P->nxf + 127) / 128, 128, 0, st>>>(P->d_colsum, P->d_contrib, P->d_xoff, P->nxf, rho);
+    VK_LAUNCH("k_red_finest");
+    return VLASOV_OK;
+}
+
+// ------------------------------------------------------------------ face fluxes at one face
+// x-face flux F^x_{i+1/2,j} = vbar_j <f> + (dv/24)(<f>_{j+1} - <f>_{j-1})
+template <int RECON>
+__device__ double xface_flux(const double* f, const FaceRef& r, double v_lo, double dv) {
+    double fa[3];
+#pragma unroll
+    for (int t = -1; t <= 1; ++t) {
+        const double* p = f + r.s0 + t;
+        const double vb = v_lo + ((double)(r.g + t) + 0.5) * dv;
+        fa[t + 1] = face_avg<RECON>(p[0], p[r.pitch], p[2 * (int64_t)r.pitch], p[3 * (int64_t)r.pitch], vb);
+    }
+    const double vb0 = v_lo + ((double)r.g + 0.5) * dv;
+    return vb0 * fa[1] + (dv * (1.0 / 24.0)) * (fa[2] - fa[0]);
+}
+
+// v-face flux F^E_{i,j+1/2} = E_i <f> + (1/48)(E_{i+1} - E_{i-1})(<f>_{i+1} - <f>_{i-1})
+// (+1/48 reading #3); speed on each face a = -E of its column
+template <int RECON>
+__device__ double vface_flux(const double* f, const FaceRef& r, const double* E) {
+    double fa[3];
+#pragma unroll
+    for (int t = -1; t <= 1; ++t) {
+        const double* p = f + r.s0 + (int64_t)t * r.pitch;
+        fa[t + 1] = face_avg<RECON>(p[0], p[1], p[2], p[3], -E[r.g + t]);
+    }
+    const double c48 = (E[r.g + 1] - E[r.g - 1]) * (1.0 / 48.0);
+    return E[r.g] * fa[1] + c48 * (fa[2] - fa[0]);
+}
+
+// regs[t] += b_s (F_coarse - mean of the fine F) on every coarse face of the interface
+template <int RECON>
+__global__ void k_flux_registers(const RefluxTask* __restrict__ tasks, int64_t n, const double* __restrict__ ff,
+                                 const double* __restrict__ Ef, const double* __restrict__ fc,
+                                 const double* __restrict__ Ec, double vlo, double dvf, double dvc, double b_s,
+                                 double* __restrict__ regs) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const RefluxTask& T = tasks[t];
+    double Fc, Fs = 0.0;
+    if (T.dir == 0) {
+        Fc = xface_flux<RECON>(fc, T.cf, vlo, dvc);
+        for (int s = 0; s < T.nfine; ++s) Fs += xface_flux<RECON>(ff, T.ff[s], vlo, dvf);
+    } else {
+        Fc = vface_flux<RECON>(fc, T.cf, Ec);
+        for (int s = 0; s < T.nfine; ++s) Fs += vface_flux<RECON>(ff, T.ff[s], Ef);
+    }
+    regs[t] += b_s * (Fc - Fs / (double)T.nfine);
+}
+
+int launch_flux_registers(const vlasov_level* L, const double* f_fine, const double* E_fine, const double* f_coarse,
+                          const double* E_coarse, double b_s, double* regs, int recon) {
+    if (L->n_reflux == 0) return VLASOV_OK;
+    const vlasov_level* C = L->coarser;
+    const unsigned blocks = (unsigned)((L->n_reflux + 127) / 128);
+    if (recon == VLASOV_UPWIND)
+        k_flux_registers<VLASOV_UPWIND><<<blocks, 128, 0, L->stream>>>(L->d_reflux, L->n_reflux, f_fine, E_fine,
+                                                                        f_coarse, E_coarse, L->lower[1], L->h[1],
+                                                                        C->h[1], b_s, regs);
+    else
+        k_flux_registers<VLASOV_CENTERED4><<<blocks, 128, 0, L->stream>>>(L->d_reflux, L->n_reflux, f_fine, E_fine,
+                                                                           f_coarse, E_coarse, L->lower[1], L->h[1],
+                                                                           C->h[1], b_s, regs);
+    VK_LAUNCH("k_flux_registers");
+    return VLASOV_OK;
+}
+
+// ------------------------------------------------------------------ refluxing + average-down
+// Coarse cell next to the interface: f += dt * dk, where dk replaces the coarse face flux by the
+// mean fine one in k = -(Fx_hi - Fx_lo)/dx + (Fv_hi - Fv_lo)/dv and regs = F*_c - <F*_f>:
+//   x high face: +dt reg/dx, x low face: -dt reg/dx, v high face: -dt reg/dv, v low: +dt reg/dv.
+__global__ void k_reflux(const RefluxTask* __restrict__ tasks, const int64_t* __restrict__ cells,
+                         const int32_t* __restrict__ off, int64_t ncells, const double* __restrict__ regs,
+                         double dt, double dxc, double dvc, double* __restrict__ fc) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    double d = 0.0;
+    for (int k = off[c]; k < off[c + 1]; ++k) {
+        const RefluxTask& T = tasks[k];
+        const double r = regs[k];
+        if (T.dir == 0) d += (T.sign > 0 ? r : -r) / dxc;
+        else d += (T.sign > 0 ? -r : r) / dvc;
+    }
+    fc[cells[c]] += dt * d;
+}
+
+__global__ void k_average_down(const AvgTask* __restrict__ tasks, int64_t n, int Rx, int Rv,
+                               const double* __restrict__ ff, double* __restrict__ fc) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const AvgTask T = tasks[t];
+    double s = 0.0;
+    for (int a = 0; a < Rx; ++a)
+        for (int b = 0; b < Rv; ++b) s += ff[T.fcell0 + (int64_t)a * T.fpitch + b];
+    fc[T.ccell] = s / (double)(Rx * Rv);
+}
+
+int launch_average_down(const vlasov_level* L, const double* f_fine, double* f_coarse, const double* regs, double dt) {
+    const vlasov_level* C = L->coarser;
+    if (regs && L->n_reflux_cells > 0) {
+        k_reflux<<<(unsigned)((L->n_reflux_cells + 127) / 128), 128, 0, L->stream>>>(
+            L->d_reflux, L->d_reflux_cells, L->d_reflux_off, L->n_reflux_cells, regs, dt, C->h[0], C->h[1], f_coarse);
+        VK_LAUNCH("k_reflux");
+    }
+    if (L->n_avg > 0) {
+        k_average_down<<<(unsigned)((L->n_avg + 127) / 128), 128, 0, L->stream>>>(
+            L->d_avg, L->n_avg, L->coarse_ratio[0], L->coarse_ratio[1], f_fine, f_coarse);
+        VK_LAUNCH("k_average_down");
+    }
+    return VLASOV_OK;
+}
+
+// ------------------------------------------------------------------ tags (reading #18)
+// crit = sqrt(0.5 (hx (f_{i+1}-f_{i-1})^2 + hv (f_{j+1}-f_{j-1})^2))
+//      + 0.5 (hx^2 |f_{i+1} - 2f + f_{i-1}| + hv^2 |f_{j+1} - 2f + f_{j-1}|),  evaluated in this
+// order with round-to-nearest intrinsics (no FMA contraction), as the oracle does.
+__device__ __forceinline__ bool crit_exceeds(const double* f, int64_t c, int64_t pitch, double hx, double hv,
+                                             double tol) {
+    const double f0 = f[c], xp = f[c + pitch], xm = f[c - pitch], vp = f[c + 1], vm = f[c - 1];
+    const double dx1 = __dsub_rn(xp, xm), dv1 = __dsub_rn(vp, vm);
+    const double d1 = __dsqrt_rn(__dmul_rn(0.5, __dadd_rn(__dmul_rn(hx, __dmul_rn(dx1, dx1)),
+                                                          __dmul_rn(hv, __dmul_rn(dv1, dv1)))));
+    const double sx = __dadd_rn(__dsub_rn(xp, __dmul_rn(2.0, f0)), xm);
+    const double sv = __dadd_rn(__dsub_rn(vp, __dmul_rn(2.0, f0)), vm);
+    const double d2 = __dmul_rn(0.5, __dadd_rn(__dmul_rn(__dmul_rn(hx, hx), fabs(sx)),
+                                               __dmul_rn(__dmul_rn(hv, hv), fabs(sv))));
+    return __dadd_rn(d1, d2) > tol;
+}
+
+// tags[x * nv + j] = any crit > tol within the Chebyshev `buffer` (periodic in x, clipped in v)
+__global__ void k_tags(const double* __restrict__ f, int64_t off, int64_t pitch, int nx, int nv, double hx,
+                       double hv, double tol, int buffer, uint8_t* __restrict__ tags) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nx * nv) return;
+    const int x = (int)(t / nv), j = (int)(t % nv);
+    uint8_t hit = 0;
+    for (int a = -buffer; a <= buffer && !hit; ++a) {
+        int xx = x + a;
+        xx = (xx % nx + nx) % nx;
+        for (int b = -buffer; b <= buffer; ++b) {
+            const int jj = j + b;
+            if (jj < 0 || jj >= nv) continue;
+            if (crit_exceeds(f, off + (int64_t)(xx + G) * pitch + (jj + G), pitch, hx, hv, tol)) { hit = 1; break; }
+        }
+    }
+    tags[t] = hit;
+}
+
+int launch_tags(const vlasov_level* L, const double* f, double tol, int buffer, uint8_t* tags) {
+    const int nx = L->dom[0], nv = L->dom[1];
+    const int64_t n = (int64_t)nx * nv;
+    k_tags<<<(unsigned)((n + 255) / 256), 256, 0, L->stream>>>(f, L->block_off[0], L->block_str[0][0], nx, nv,
+                                                               L->h[0], L->h[1], tol, buffer, tags);
+    VK_LAUNCH("k_tags");
+    return VLASOV_OK;
+}
+
+}  // namespace vk

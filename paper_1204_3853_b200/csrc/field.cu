@@ -31,14 +31,21 @@ int launch_moment_direct(const vlasov_level* L, const double* f, double* rho) {
 }
 
 // out[i + ghost] = sum_k g[(i - k) mod n] (rho[k] - mean(rho)), plus periodic ghost copies.
-// One warp per output (OPW outputs per warp); every CTA stages the whole projected rho in
-// shared memory and reduces the mean itself in a fixed order, so the result is deterministic.
-constexpr int CIRC_THREADS = 256, CIRC_OPW = 2;
+// CTA = 16 x 16 threads for CIRC_OUT = 64 consecutive outputs: thread (tx, ty) accumulates outputs
+// o0 = 4 tx .. o0 + 3 over the k-chunk ty with a sliding 4-value window of the (periodically
+// extended) Green's function in shared memory; the 16 chunk partials are summed in chunk order.
+// Every CTA stages the whole projected rho and reduces the mean itself in a fixed order, so the
+// result is deterministic.  n <= CIRC_SMEM_MAX keeps g in shared memory (else read through L2).
+constexpr int CIRC_TX = 16, CIRC_TY = 16, CIRC_OUT = 4 * CIRC_TX, CIRC_SMEM_MAX = 4096;
 
-__global__ void __launch_bounds__(CIRC_THREADS) k_circulant(const double* __restrict__ rho,
-                                                             const double* __restrict__ g, int n, int ghost,
-                                                             double* __restrict__ out) {
-    extern __shared__ double s_rho[];
+template <bool G_SMEM>
+__global__ void __launch_bounds__(CIRC_TX * CIRC_TY) k_circulant(const double* __restrict__ rho,
+                                                                  const double* __restrict__ g, int n, int ghost,
+                                                                  double* __restrict__ out) {
+    extern __shared__ double sm[];
+    double* s_rho = sm;                                  // [n]
+    double* s_part = sm + n;                             // [CIRC_TY][CIRC_OUT]
+    double* s_g = s_part + CIRC_TY * CIRC_OUT;           // [2n + 4]: g[j mod n]
     __shared__ double s_red[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     double acc = 0.0;
@@ -47,6 +54,8 @@ __global__ void __launch_bounds__(CIRC_THREADS) k_circulant(const double* __rest
         s_rho[k] = v;
         acc += v;
     }
+    if (G_SMEM)
+        for (int j = tid; j < 2 * n + 4; j += blockDim.x) s_g[j] = __ldg(g + (j % n));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) s_red[warp] = acc;
@@ -60,20 +69,34 @@ __global__ void __launch_bounds__(CIRC_THREADS) k_circulant(const double* __rest
     const double mean = s_red[0];
     for (int k = tid; k < n; k += blockDim.x) s_rho[k] -= mean;      // projection
     __syncthreads();
-    const int per_block = nw * CIRC_OPW;
-#pragma unroll
-    for (int o = 0; o < CIRC_OPW; ++o) {
-        const int i = blockIdx.x * per_block + warp * CIRC_OPW + o;
-        if (i >= n) break;
-        double s = 0.0;
-        for (int k = lane; k < n; k += 32) {
-            int d = i - k;
-            d += (d < 0) ? n : 0;
-            s = fma(__ldg(g + d), s_rho[k], s);
+
+    const int tx = tid % CIRC_TX, ty = tid / CIRC_TX;
+    const int o0 = blockIdx.x * CIRC_OUT + 4 * tx;
+    const int kb = (int)((int64_t)n * ty / CIRC_TY), ke = (int)((int64_t)n * (ty + 1) / CIRC_TY);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (o0 < n && kb < ke) {
+        auto gv = [&](int j) -> double { return G_SMEM ? s_g[j] : __ldg(g + (j % n)); };
+        int j = n + o0 - kb;                             // g index of output o0 at k = kb
+        double w0 = gv(j), w1 = gv(j + 1), w2 = gv(j + 2), w3 = gv(j + 3);
+        for (int k = kb; k < ke; ++k) {
+            const double r = s_rho[k];
+            a0 = fma(w0, r, a0);
+            a1 = fma(w1, r, a1);
+            a2 = fma(w2, r, a2);
+            a3 = fma(w3, r, a3);
+            w3 = w2; w2 = w1; w1 = w0;
+            w0 = gv(--j);
         }
+    }
+    double* pp = s_part + ty * CIRC_OUT + 4 * tx;
+    pp[0] = a0; pp[1] = a1; pp[2] = a2; pp[3] = a3;
+    __syncthreads();
+    if (tid < CIRC_OUT) {
+        const int i = blockIdx.x * CIRC_OUT + tid;
+        if (i < n) {
+            double s = 0.0;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) {
+            for (int c = 0; c < CIRC_TY; ++c) s += s_part[c * CIRC_OUT + tid];
             out[i + ghost] = s;
             if (i < ghost) out[i + ghost + n] = s;
             if (i >= n - ghost) out[i + ghost - n] = s;
@@ -82,22 +105,23 @@ __global__ void __launch_bounds__(CIRC_THREADS) k_circulant(const double* __rest
 }
 
 int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E, int ghost) {
-    const int per_block = (CIRC_THREADS / 32) * CIRC_OPW;
-    const int blocks = (P->n + per_block - 1) / per_block;
-    const size_t smem = (size_t)P->n * sizeof(double);
-    if (smem > 48 * 1024) {
-        static bool conf = false;
-        if (!conf) {
-            VK_CUDA(cudaFuncSetAttribute(k_circulant, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            conf = true;
-        }
+    const int n = P->n;
+    const int blocks = (n + CIRC_OUT - 1) / CIRC_OUT;
+    const bool gs = n <= CIRC_SMEM_MAX;
+    const size_t smem = (size_t)(n + CIRC_TY * CIRC_OUT + (gs ? 2 * n + 4 : 0)) * sizeof(double);
+    static bool conf = false;
+    if (!conf) {
+        VK_CUDA(cudaFuncSetAttribute(k_circulant<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        VK_CUDA(cudaFuncSetAttribute(k_circulant<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        conf = true;
     }
+    auto kern = gs ? k_circulant<true> : k_circulant<false>;
     if (E) {
-        k_circulant<<<blocks, CIRC_THREADS, smem, P->stream>>>(rho, P->d_gE, P->n, ghost, E);
+        kern<<<blocks, CIRC_TX * CIRC_TY, smem, P->stream>>>(rho, P->d_gE, n, ghost, E);
         VK_LAUNCH("k_circulant(E)");
     }
     if (phi) {
-        k_circulant<<<blocks, CIRC_THREADS, smem, P->stream>>>(rho, P->d_gphi, P->n, ghost, phi);
+        kern<<<blocks, CIRC_TX * CIRC_TY, smem, P->stream>>>(rho, P->d_gphi, n, ghost, phi);
         VK_LAUNCH("k_circulant(phi)");
     }
     return VLASOV_OK;

@@ -61,30 +61,48 @@ struct PhysTask {             // characteristic v-BC of one column side (1D+1V)
     int32_t e_idx;            // index into the level E array (wrapped x + 2)
     int32_t side;             // 0 low, 1 high
 };
-struct RedEntry {             // one sub-patch of Alg.8
-    int64_t base;             // index of cell (x = s.lo_x - 2, v = s.lo_v) in its level array
-    int32_t level, pitch, ncols_g, nrows_v;  // ncols_g = nx_s + 4 (grown), nrows_v = v extent
-    int32_t R;                // x ratio to the finest level
-    int32_t xf0;              // finest x of the first fine cell (s.lo_x * R)
-    int32_t buf_off;          // offset of its refined values in the scratch buffer
-    double dv;                // velocity spacing of its level
+struct RedCol {               // one grown x-column of one Alg.8 sub-patch
+    int64_t addr;             // index of the column's first velocity cell in its level array
+    int32_t nv;               // velocity cells summed (the sub-patch's v extent)
+    int32_t level;            // index of the level in the hierarchy
 };
-struct RefluxTask {           // one coarse face on the coarse-fine interface
-    int64_t ccell;            // coarse cell (uncovered) whose face is corrected
-    int64_t cface_lo;         // coarse: index of the 4-cell stencil start along the face normal
+struct RedContrib {           // one refined partial sum landing on one finest x cell
+    int64_t cs;               // index of the first of the 5 stencil column sums (columns c-2..c+2)
+    double dv;                // velocity spacing of the sub-patch's level (reading #13)
+    double b[5];              // linear5 weights b_j(s), j = -2..2 (reading #12)
+};
+struct FaceRef {              // a face flux stencil in a level array
+    int64_t s0;               // first of the 4 cells along the face normal
+    int32_t pitch;            // x stride of the block holding the stencil
+    int32_t g;                // x-faces: global v index j (vbar_j); v-faces: E index of the column
+};
+struct RefluxTask {           // one coarse face on the coarse-fine interface (P:633-648)
+    int64_t ccell;            // uncovered coarse cell whose face is corrected
     int32_t dir;              // 0: x-face, 1: v-face
-    int32_t sign;             // +1: face is the cell's high face, -1: low face
-    int32_t c_e_idx;          // E index of the coarse column (x-faces: -1)
-    int32_t nfine;            // transverse fine faces (R_transverse)
-    int64_t fface_lo[MAXR];   // fine stencil starts (index of the first of 4 cells)
-    int32_t f_e_idx[MAXR];    // fine E indices of the fine faces' columns
+    int32_t sign;             // +1: the face is the cell's high face, -1: its low face
+    int32_t nfine;            // fine faces under the coarse face (transverse ratio)
+    int32_t pad;
+    FaceRef cf;               // coarse face stencil
+    FaceRef ff[MAXR];         // fine face stencils
 };
-struct AvgTask {              // one covered coarse cell
+struct AvgTask {              // one covered coarse cell (reading #14)
     int64_t ccell;
     int64_t fcell0;           // first fine cell
     int32_t fpitch;           // fine x stride
+    int32_t pad;
 };
 
+constexpr int MAXLEV = 8;     // levels of one hierarchy handled by the reduction
+struct RedPlan {              // Alg.8 sub-patch reduction plan (built on the host, level.cpp)
+    std::vector<uint64_t> uids;   // the hierarchy it was built for
+    int nxf = 0;                  // finest configuration cells
+    int64_t ncols = 0, ncontrib = 0;
+    RedCol* d_cols = nullptr;
+    double* d_colsum = nullptr;
+    RedContrib* d_contrib = nullptr;
+    int32_t* d_xoff = nullptr;    // CSR over finest x [nxf + 1]
+};
+void free_red_plan(RedPlan* p);
 }  // namespace vk
 
 // ------------------------------------------------------------------ opaque structs
@@ -114,7 +132,7 @@ struct vlasov_level {
     int n_strips = 0;
     double* d_partials = nullptr;         // moment scratch [n_vtiles][dom_x]
     unsigned* d_tickets = nullptr;        // per-strip arrival tickets
-    bool self_ghost_ok = false;           // single periodic block, even nv: in-kernel ghosts
+    bool self_ghost_ok = false;           // single periodic block, nv % 4 == 0: in-kernel ghosts
     // ghost fill
     int64_t n_copy = 0, n_cf = 0, n_phys = 0;
     int64_t* d_copy = nullptr;            // pairs (dst, src)
@@ -124,8 +142,13 @@ struct vlasov_level {
     // AMR transfers w.r.t. the coarser level
     int64_t n_reflux = 0, n_avg = 0;
     vk::RefluxTask* d_reflux = nullptr;
+    int64_t* d_reflux_cells = nullptr;    // CSR: distinct corrected coarse cells [n_reflux_cells]
+    int32_t* d_reflux_off = nullptr;      //      task range per cell [n_reflux_cells + 1]
+    int64_t n_reflux_cells = 0;
     vk::AvgTask* d_avg = nullptr;
     int avg_count = 1;                    // fine cells per coarse cell
+    // Alg.8 plan cached on the finest level of the hierarchy it was built for
+    mutable vk::RedPlan* red_plan = nullptr;
     // 2D+2V
     int64_t e_doubles = 0;
     // scratch (device): interpolation tables
@@ -146,6 +169,7 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
                       double* u, double* f_next, const double* E, const double* E_bc,
                       const double* f0v, int recon, double* rho);
 int stage_1d1v_ctas_per_sm(bool wide, int tile_rows);
+int stage_1d1v_tile_width(bool wide);   // cells per v-tile of the stage kernel
 int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double* E_bc,
                 const double* f0v, int interp);
 int launch_moment_direct(const vlasov_level* L, const double* f, double* rho);
@@ -154,4 +178,11 @@ int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest
 int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest,
                      double* E_lvl);
 int linear5_weights(int R, double* out /* R*5 */);
+int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
+int launch_flux_registers(const vlasov_level* L, const double* f_fine, const double* E_fine, const double* f_coarse,
+                          const double* E_coarse, double b_s, double* regs, int recon);
+int launch_average_down(const vlasov_level* L, const double* f_fine, double* f_coarse, const double* regs, double dt);
+int launch_tags(const vlasov_level* L, const double* f, double tol, int buffer, uint8_t* tags);
+int launch_fill_from(const vlasov_level* L, double* f, const double* f_old, const std::vector<int64_t>& copies,
+                     const double* f_coarse, const std::vector<CFTask>& cfs, int interp);
 }  // namespace vk

@@ -135,6 +135,14 @@ int linear5_weights(int R, double* out) {
     }
     return 0;
 }
+void free_red_plan(RedPlan* p) {
+    if (!p) return;
+    cudaFree(p->d_cols);
+    cudaFree(p->d_colsum);
+    cudaFree(p->d_contrib);
+    cudaFree(p->d_xoff);
+    delete p;
+}
 }  // namespace vk
 
 // ====================================================================== device helpers
@@ -571,6 +579,74 @@ int build_amr_tasks(const vlasov_level* L, const vlasov_level* C, std::vector<vk
     offs.push_back((int32_t)tasks.size());
     return VLASOV_OK;
 }
+
+// Alg.8 plan: grown columns of every sub-patch (level-major, patch-minor, Alg.7 order) and, per
+// finest x cell, its linear5-refined contributions in that order (readings #13, #16).
+int build_red_plan(const vlasov_level* const* levels, int nlev, vk::RedPlan** out) {
+    *out = nullptr;
+    const vlasov_level* Lf = levels[nlev - 1];
+    const int nxf = Lf->dom[0];
+    std::vector<vk::RedCol> cols;
+    std::vector<std::vector<vk::RedContrib>> per_x(nxf);
+    for (int l = 0; l < nlev; ++l) {
+        const vlasov_level* L = levels[l];
+        if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "sub-patch reduction: 1D+1V levels only");
+        if (nxf % L->dom[0]) return vk::fail(VLASOV_EINVAL, "finest x resolution not a multiple of a level's");
+        if (l > 0 && (L->coarser != levels[l - 1] || L->coarser_uid != levels[l - 1]->uid))
+            return vk::fail(VLASOV_ESTALE, "reduce_moment: levels are not a hierarchy (coarser mismatch)");
+        const int R = nxf / L->dom[0];
+        if (R > vk::MAXR * vk::MAXR) return vk::fail(VLASOV_EUNSUPPORTED, "x ratio to the finest level too large");
+        std::vector<double> b5((size_t)R * 5);
+        vk::linear5_weights(R, b5.data());
+        for (size_t p = 0; p < L->boxes.size(); ++p) {
+            const int blk = L->patch_block[p];
+            for (const Box& sp : subpatches_of(levels, nlev, l, (int)p)) {
+                const int64_t base = (int64_t)cols.size();
+                const int nxs = vk::box_ncells_dim(sp, 0);
+                for (int c = 0; c < nxs + 2 * vk::G; ++c) {
+                    int cc[4] = {sp.lo[0] - vk::G + c, sp.lo[1], 0, 0};
+                    vk::RedCol rc;
+                    rc.addr = cell_addr(L, blk, cc);
+                    rc.nv = vk::box_ncells_dim(sp, 1);
+                    rc.level = l;
+                    cols.push_back(rc);
+                }
+                for (int xc = sp.lo[0]; xc <= sp.hi[0]; ++xc)
+                    for (int s = 0; s < R; ++s) {
+                        vk::RedContrib k;
+                        k.cs = base + (xc - sp.lo[0]);            // grown column xc - 2
+                        k.dv = L->h[1];
+                        for (int j = 0; j < 5; ++j) k.b[j] = b5[(size_t)s * 5 + j];
+                        per_x[(size_t)xc * R + s].push_back(k);
+                    }
+            }
+        }
+    }
+    std::vector<vk::RedContrib> con;
+    std::vector<int32_t> xoff(nxf + 1, 0);
+    for (int x = 0; x < nxf; ++x) {
+        xoff[x] = (int32_t)con.size();
+        con.insert(con.end(), per_x[x].begin(), per_x[x].end());
+    }
+    xoff[nxf] = (int32_t)con.size();
+    vk::RedPlan* P = new vk::RedPlan();
+    for (int l = 0; l < nlev; ++l) P->uids.push_back(levels[l]->uid);
+    P->nxf = nxf;
+    P->ncols = (int64_t)cols.size();
+    P->ncontrib = (int64_t)con.size();
+    cudaStream_t st = Lf->stream;
+    int rc;
+    if ((rc = upload(&P->d_cols, cols, st)) || (rc = upload(&P->d_contrib, con, st)) ||
+        (rc = upload(&P->d_xoff, xoff, st))) {
+        vk::free_red_plan(P);
+        return rc;
+    }
+    if (!cols.empty()) VK_CUDA(cudaMalloc((void**)&P->d_colsum, sizeof(double) * cols.size()));
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { vk::free_red_plan(P); return vk::cuda_check(e, "reduction plan upload"); }
+    *out = P;
+    return VLASOV_OK;
+}
 }  // namespace
 
 // ====================================================================== C ABI
@@ -897,12 +973,23 @@ int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, con
 int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
                          double* rho_finest) {
     if (!levels || nlev < 1 || !rho_finest || !f) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (nlev > vk::MAXLEV) return vk::fail(VLASOV_EUNSUPPORTED, "more than 8 levels");
+    for (int l = 0; l < nlev; ++l)
+        if (!levels[l] || !f[l]) return vk::fail(VLASOV_EINVAL, "reduce_moment: level / field pointer required");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
-    if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 2) {
-        if (!f[0]) return vk::fail(VLASOV_EINVAL, "reduce_moment: field pointer required");
+    if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 2)
         return vk::launch_moment_direct(levels[0], f[0], rho_finest);
+    const vlasov_level* Lf = levels[nlev - 1];
+    bool fresh = Lf->red_plan != nullptr && (int)Lf->red_plan->uids.size() == nlev;
+    for (int l = 0; fresh && l < nlev; ++l) fresh = Lf->red_plan->uids[l] == levels[l]->uid;
+    if (!fresh) {                                   // observer: rebuild after a regrid
+        vk::free_red_plan(Lf->red_plan);
+        Lf->red_plan = nullptr;
+        vk::RedPlan* P = nullptr;
+        if (int rc = build_red_plan(levels, nlev, &P)) return rc;
+        Lf->red_plan = P;
     }
-    return vk::fail(VLASOV_EUNSUPPORTED, "sub-patch reduction: not in this build yet");
+    return vk::launch_reduce_subpatch(Lf->red_plan, f, nlev, rho_finest, Lf->stream);
 }
 
 int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisson** out) {
@@ -979,19 +1066,88 @@ int vlasov_inject_field(vlasov_level* L, const double* E_finest, const int32_t n
     return vk::launch_inject_2d(L, E_finest, n_finest, E_lvl);
 }
 
-int vlasov_flux_register_accumulate(vlasov_level*, const double*, const double*, const double*, const double*,
-                                    double, double*, int32_t) {
-    return vk::fail(VLASOV_EUNSUPPORTED, "flux registers: not in this build yet");
+int vlasov_flux_register_accumulate(vlasov_level* fine, const double* f_fine, const double* E_fine,
+                                    const double* f_coarse, const double* E_coarse, double b_s, double* regs,
+                                    int32_t recon) {
+    if (!fine || !f_fine || !E_fine || !f_coarse || !E_coarse) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!fine->coarser) return vk::fail(VLASOV_EINVAL, "flux registers: level has no coarser level");
+    if (fine->n_reflux > 0 && !regs) return vk::fail(VLASOV_EINVAL, "flux registers: regs required");
+    if (recon != VLASOV_CENTERED4 && recon != VLASOV_UPWIND) return vk::fail(VLASOV_EINVAL, "bad recon");
+    if (fine->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "flux registers: 1D+1V only");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_flux_registers(fine, f_fine, E_fine, f_coarse, E_coarse, b_s, regs, recon);
 }
-int vlasov_average_down(vlasov_level*, const double*, double*, const double*, double) {
-    return vk::fail(VLASOV_EUNSUPPORTED, "average_down: not in this build yet");
+
+int vlasov_average_down(vlasov_level* fine, const double* f_fine, double* f_coarse, const double* regs, double dt) {
+    if (!fine || !f_fine || !f_coarse) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!fine->coarser) return vk::fail(VLASOV_EINVAL, "average_down: level has no coarser level");
+    if (fine->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "average_down: 1D+1V only");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_average_down(fine, f_fine, f_coarse, regs, dt);
 }
-int vlasov_tag_cells(vlasov_level*, const double*, double, int32_t, uint8_t*) {
-    return vk::fail(VLASOV_EUNSUPPORTED, "tag_cells: not in this build yet");
+
+int vlasov_tag_cells(vlasov_level* L, const double* f, double tol, int32_t buffer, uint8_t* tags) {
+    if (!L || !f || !tags) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (buffer < 0) return vk::fail(VLASOV_EINVAL, "tag buffer < 0");
+    if (L->ndim != 2 || !L->single_block)
+        return vk::fail(VLASOV_EUNSUPPORTED, "tag_cells: 1D+1V level stored as one block covering its domain");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_tags(L, f, tol, buffer, tags);
 }
-int vlasov_level_fill_from(vlasov_level*, double*, const vlasov_level*, const double*, const vlasov_level*,
-                           const double*, int32_t) {
-    return vk::fail(VLASOV_EUNSUPPORTED, "level_fill_from: not in this build yet");
+
+int vlasov_level_fill_from(vlasov_level* L, double* f, const vlasov_level* old, const double* f_old,
+                           const vlasov_level* coarser, const double* f_coarse, int32_t interp) {
+    if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (old && !f_old) return vk::fail(VLASOV_EINVAL, "fill_from: f_old required with old");
+    if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "fill_from: 1D+1V only");
+    if (coarser && (coarser != L->coarser || coarser->uid != L->coarser_uid))
+        return vk::fail(VLASOV_ESTALE, "fill_from: coarser level does not match the one of level_create");
+    if (old) {
+        if (old->ndim != L->ndim) return vk::fail(VLASOV_EINVAL, "fill_from: old level ndim mismatch");
+        for (int d = 0; d < L->ndim; ++d)
+            if (old->ratio[d] != L->ratio[d]) return vk::fail(VLASOV_EINVAL, "fill_from: old level resolution differs");
+    }
+    // copy where an old patch holds the cell (same-level data wins), else interpolate
+    Owner oown;
+    if (old) oown = make_owner(old, old->blocks);
+    Owner cown;
+    const vlasov_level* C = L->coarser;
+    if (C) cown = make_owner(C, C->blocks);
+    std::vector<int64_t> copies;
+    std::vector<vk::CFTask> cfs;
+    int err = VLASOV_OK;
+    for (size_t p = 0; p < L->boxes.size(); ++p) {
+        const int blk = L->patch_block[p];
+        for_each_cell(L->boxes[p], L->ndim, [&](const int* c) {
+            if (err) return;
+            const int64_t dst = cell_addr(L, blk, c);
+            const int ob = old ? oown.find(c) : -1;
+            if (ob >= 0) {
+                copies.push_back(dst);
+                copies.push_back(cell_addr(old, ob, c));
+                return;
+            }
+            if (!C || !coarser || !f_coarse) {
+                err = vk::fail(VLASOV_EINVAL, "fill_from: cell without old data needs the coarser level");
+                return;
+            }
+            int cc[4] = {0, 0, 0, 0};
+            for (int d = 0; d < L->ndim; ++d) cc[d] = vk::floordiv(c[d], L->coarse_ratio[d]);
+            const int cq = cown.find(cc);
+            if (cq < 0) { err = vk::fail(VLASOV_ESTENCIL, "fill_from: coarse parent missing"); return; }
+            vk::CFTask t;
+            t.dst = dst;
+            t.csrc = cell_addr(C, cq, cc);
+            for (int d = 0; d < 4; ++d) {
+                t.cstride[d] = d < L->ndim ? (int32_t)C->block_str[cq][d] : 0;
+                t.sub[d] = d < L->ndim ? (int8_t)(c[d] - cc[d] * L->coarse_ratio[d]) : 0;
+            }
+            cfs.push_back(t);
+        });
+        if (err) return err;
+    }
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_fill_from(L, f, f_old, copies, f_coarse, cfs, interp);
 }
 
 }  // extern "C"

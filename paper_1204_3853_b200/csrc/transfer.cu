@@ -56,12 +56,12 @@ __device__ __forceinline__ double interp1(const double* u, const double* b5, int
 
 // ------------------------------------------------------------------ ghost fill kernels
 template <int INTERP>
-__global__ void k_fill_copy_cf(double* __restrict__ f, const int64_t* __restrict__ copies, int64_t ncopy,
-                               const double* __restrict__ fc, const CFTask* __restrict__ cf, int64_t ncf,
+__global__ void k_fill_copy_cf(double* __restrict__ f, const double* __restrict__ fsrc,
+                               const int64_t* __restrict__ copies, int64_t ncopy, const double* __restrict__ fc, const CFTask* __restrict__ cf, int64_t ncf,
                                const double* __restrict__ b5, int Rx, int Rv) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < ncopy) {
-        f[copies[2 * t]] = f[copies[2 * t + 1]];
+        f[copies[2 * t]] = fsrc[copies[2 * t + 1]];
         return;
     }
     const int64_t c = t - ncopy;
@@ -108,10 +108,10 @@ int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double
         const int64_t blocks = (n1 + 255) / 256;
         if (interp == VLASOV_WENO5)
             k_fill_copy_cf<VLASOV_WENO5><<<(unsigned)blocks, 256, 0, L->stream>>>(
-                f, L->d_copy, L->n_copy, f_coarse, L->d_cf, L->n_cf, L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
+                f, f, L->d_copy, L->n_copy, f_coarse, L->d_cf, L->n_cf, L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
         else
             k_fill_copy_cf<VLASOV_LINEAR5><<<(unsigned)blocks, 256, 0, L->stream>>>(
-                f, L->d_copy, L->n_copy, f_coarse, L->d_cf, L->n_cf, L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
+                f, f, L->d_copy, L->n_copy, f_coarse, L->d_cf, L->n_cf, L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
         VK_LAUNCH("k_fill_copy_cf");
     }
     if (L->n_phys > 0) {
@@ -120,6 +120,37 @@ int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double
                                                                              L->dom[1]);
         VK_LAUNCH("k_fill_phys");
     }
+    return VLASOV_OK;
+}
+
+// Regrid data motion (vlasov_level_fill_from): the task lists depend on the old level, so they
+// are built per call and staged through stream-ordered scratch; the call synchronises its stream
+// (a regrid is a host decision point anyway).
+int launch_fill_from(const vlasov_level* L, double* f, const double* f_old, const std::vector<int64_t>& copies,
+                     const double* f_coarse, const std::vector<CFTask>& cfs, int interp) {
+    const int64_t ncopy = (int64_t)copies.size() / 2, ncf = (int64_t)cfs.size();
+    if (ncopy + ncf == 0) return VLASOV_OK;
+    int64_t* d_copy = nullptr;
+    CFTask* d_cf = nullptr;
+    if (ncopy) {
+        VK_CUDA(cudaMallocAsync((void**)&d_copy, copies.size() * sizeof(int64_t), L->stream));
+        VK_CUDA(cudaMemcpyAsync(d_copy, copies.data(), copies.size() * sizeof(int64_t), cudaMemcpyHostToDevice, L->stream));
+    }
+    if (ncf) {
+        VK_CUDA(cudaMallocAsync((void**)&d_cf, cfs.size() * sizeof(CFTask), L->stream));
+        VK_CUDA(cudaMemcpyAsync(d_cf, cfs.data(), cfs.size() * sizeof(CFTask), cudaMemcpyHostToDevice, L->stream));
+    }
+    const unsigned blocks = (unsigned)((ncopy + ncf + 255) / 256);
+    if (interp == VLASOV_WENO5)
+        k_fill_copy_cf<VLASOV_WENO5><<<blocks, 256, 0, L->stream>>>(f, f_old, d_copy, ncopy, f_coarse, d_cf, ncf, L->d_b5,
+                                                                      L->coarse_ratio[0], L->coarse_ratio[1]);
+    else
+        k_fill_copy_cf<VLASOV_LINEAR5><<<blocks, 256, 0, L->stream>>>(f, f_old, d_copy, ncopy, f_coarse, d_cf, ncf,
+                                                                        L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
+    VK_LAUNCH("k_fill_copy_cf(fill_from)");
+    if (d_copy) cudaFreeAsync(d_copy, L->stream);
+    if (d_cf) cudaFreeAsync(d_cf, L->stream);
+    VK_CUDA(cudaStreamSynchronize(L->stream));
     return VLASOV_OK;
 }
 

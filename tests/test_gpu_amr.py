@@ -1,0 +1,208 @@
+"""GPU parity of the multi-level (AMR) path against the oracle, through the C ABI.
+
+* ghost fill (siblings, periodic, coarse-fine linear5 / WENO5, characteristic BC) on seeded
+  random hierarchies: element by element on the whole ghost frame;
+* Alg.8 sub-patch reduction on the same ghosted data;
+* full RK4 steps (fill, reduction, Poisson, injection, stage kernels, flux registers,
+  refluxing, average-down) on random 2- and 3-level hierarchies;
+* the fine level covering the domain reduces to the uniform fine run;
+* C3-style runs with tags / fixed-tile regrids: tags and box lists bit-exact, f within the
+  north-star tolerances (normwise per level, reading #25).
+"""
+import numpy as np
+import pytest
+
+import inputs
+from inputs.hierarchies import random_hierarchy
+from oracle import amr, interp, reduction, scheme, uniform
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import amr_drivers as drv  # noqa: E402
+from paper_1204_3853_b200 import _lib, api  # noqa: E402
+from paper_1204_3853_b200.amr_solver import AmrVlasov1D  # noqa: E402
+
+W = inputs.scaled(inputs.get("C3"), (16, 32), (8, 8))
+MODE = {interp.LINEAR5: _lib.LINEAR5, interp.WENO5: _lib.WENO5}
+RECON = {scheme.CENTERED4: _lib.CENTERED4, scheme.UPWIND: _lib.UPWIND}
+
+
+def relerr_levels(got, ref):
+    """max over levels of max|got - ref| / max|ref| (per-level normwise, reading #25)."""
+    worst = 0.0
+    for gl, rl in zip(got, ref):
+        g = np.concatenate([a.ravel() for a in gl])
+        r = np.concatenate([a.ravel() for a in rl])
+        worst = max(worst, np.max(np.abs(g - r)) / np.max(np.abs(r)))
+    return worst
+
+
+def _ic_data(H, w=W, noise_seed=None):
+    data = H.new_data()
+    rng = np.random.default_rng(noise_seed) if noise_seed is not None else None
+    for l, lvl in enumerate(H.levels):
+        for p, b in enumerate(lvl.boxes):
+            v = inputs.initial_cell_averages(w, lvl.ratio, b)
+            if rng is not None:
+                v = v * (1.0 + 0.05 * rng.standard_normal(v.shape))
+            data[l][p][2:-2, 2:-2] = v
+    return data
+
+
+def _gpu(rat, lb, w=W, recon=scheme.CENTERED4, mode=interp.LINEAR5):
+    return AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), lb, rat, lambda r: inputs.background_profile(w, r),
+                       RECON[recon], MODE[mode])
+
+
+def _interiors(data):
+    return [[a[2:-2, 2:-2] for a in lvl] for lvl in data]
+
+
+@pytest.mark.parametrize("mode", [interp.LINEAR5, interp.WENO5])
+@pytest.mark.parametrize("seed", range(8))
+def test_ghost_fill_parity_random_hierarchies(seed, mode):
+    rat, lb = random_hierarchy(seed)
+    H = drv.hierarchy(W, lb, rat, mode=mode)
+    data = _ic_data(H, noise_seed=seed)
+    rng = np.random.default_rng(100 + seed)
+    E_bc = [0.3 * rng.uniform(-1, 1, W.ncells[0] * r[0]) for r in rat]
+    G = _gpu(rat, lb, mode=mode)
+    with torch.cuda.stream(G.stream):
+        for L, b, lvl in zip(G.levels, G.bufs, data):
+            L.set_patches(b["A"], [a[2:-2, 2:-2] for a in lvl])
+        Eg = [torch.as_tensor(np.pad(e, 2, mode="wrap")).cuda() for e in E_bc]
+        G._fill([b["A"] for b in G.bufs], Eg)
+    got = G.get_state(ghost=2)
+    amr.fill_ghosts(H, data, E_bc)
+    for l in range(len(data)):
+        for p in range(len(data[l])):
+            np.testing.assert_allclose(got[l][p], data[l][p], rtol=0, atol=1e-13 * np.abs(data[l][p]).max(),
+                                       err_msg=f"level {l} patch {p}")
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_subpatch_reduction_parity(seed):
+    rat, lb = random_hierarchy(seed)
+    H = drv.hierarchy(W, lb, rat)
+    data = _ic_data(H, noise_seed=seed)
+    G = _gpu(rat, lb)
+    with torch.cuda.stream(G.stream):
+        for L, b, lvl in zip(G.levels, G.bufs, data):
+            L.set_patches(b["A"], [a[2:-2, 2:-2] for a in lvl])
+        Eg = [torch.zeros(L.info.e_doubles, dtype=torch.float64, device="cuda") for L in G.levels]
+        G._fill([b["A"] for b in G.bufs], Eg)
+        api.vlasov_reduce_moment(G.handles, [b["A"] for b in G.bufs], G.rho)
+    ghosted = G.get_state(ghost=2)                   # identical inputs for the oracle
+    rho = G.rho.cpu().numpy()
+    ref = reduction.subpatch_reduce(H.levels, ghosted, H.h0[1], H.ncells0[0])
+    np.testing.assert_allclose(rho, ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+    ref_mask = reduction.mask_reduce(H.levels, ghosted, H.h0[1], H.ncells0[0])
+    np.testing.assert_allclose(rho, ref_mask, rtol=0, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4, 5])
+def test_amr_steps_parity_random_hierarchies(seed, recon):
+    rat, lb = random_hierarchy(seed)
+    H = drv.hierarchy(W, lb, rat, recon=recon)
+    data = _ic_data(H)
+    dt = inputs.fixed_dt(W, H.levels[-1].ratio)
+    G = _gpu(rat, lb, recon=recon)
+    G.set_state([[a[2:-2, 2:-2] for a in lvl] for lvl in data])
+    E_bc = drv.start(H, data)
+    for n in range(3):
+        data, E_bc, _ = amr.step(H, data, E_bc, dt)
+        G.step(dt)
+        err = relerr_levels(G.get_state(), _interiors(data))
+        assert err < (1e-12 if n == 0 else 1e-11), (n, err)
+
+
+def test_fine_level_covering_domain_equals_uniform_fine_run():
+    R = (2, 2)
+    lb0 = inputs.level0_boxes(W)
+    fine = [((x, v), (x + 15, v + 31)) for x in (0, 16) for v in (0, 32)]
+    G = _gpu([(1, 1), R], [lb0, fine])
+    H = drv.hierarchy(W, [lb0, fine], [(1, 1), R])
+    data = _ic_data(H)
+    G.set_state([[a[2:-2, 2:-2] for a in lvl] for lvl in data])
+    wf = inputs.scaled(W, (32, 64))
+    prob = uniform.UniformProblem(W.lower, inputs.spacing(wf), (32, 64), inputs.background_profile(wf))
+    f = inputs.initial_cell_averages(wf)
+    Eu = prob.constraints(f)
+    dt = inputs.fixed_dt(W, R)
+    for _ in range(3):
+        G.step(dt)
+        f, Eu, _ = prob.step(f, Eu, dt)
+    got = G.levels[1].get_domain(G.bufs[1]["A"])
+    np.testing.assert_allclose(got, f, rtol=0, atol=1e-12 * np.abs(f).max())
+    coarse = G.levels[0].get_domain(G.bufs[0]["A"])
+    np.testing.assert_allclose(coarse, f.reshape(16, 2, 32, 2).mean(axis=(1, 3)), atol=1e-14)
+
+
+def test_c3_initial_tags_bitexact():
+    w = inputs.get("C3")
+    lb0 = inputs.level0_boxes(w)
+    H = drv.hierarchy(w, [lb0], [(1, 1)])
+    data = _ic_data(H, w)
+    amr.fill_ghosts(H, data, drv.zero_E(H))
+    G = AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), [lb0], [(1, 1)], lambda r: inputs.background_profile(w, r))
+    G.set_state([[a[2:-2, 2:-2] for a in data[0]]])
+    with torch.cuda.stream(G.stream):
+        for E in G.E:
+            E[G.cur].zero_()
+    for tol, buf in ((w.amr["tol"], 0), (w.amr["tol"], 1), (0.003, 2), (0.01, 1)):
+        got = G.tags_level0(tol, buf)
+        from oracle import boxes as obox
+        ref = obox.dilate_tags(amr.level0_tags(H, data, tol), buf, (True, False))
+        np.testing.assert_array_equal(got.astype(bool), ref)
+    assert G.tags_level0(w.amr["tol"], 0).sum() == 3304
+
+
+def _c3_small():
+    return inputs.scaled(inputs.get("C3"), (32, 64), (8, 16))
+
+
+@pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
+def test_c3_style_regrid_run_parity(recon):
+    w = _c3_small()
+    ratio, tile, tol, buf = (4, 4), 16, 0.05, 1
+    dt = inputs.fixed_dt(w, ratio)
+    log = []
+    H, data, _ = drv.c3_run(w, 6, 2, dt, tol, buf, ratio, tile, recon=recon, log=log)
+    assert any(len(b) for _, b, _ in log)
+    lb0 = inputs.level0_boxes(w)
+    G = AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), [lb0], [(1, 1)],
+                    lambda r: inputs.background_profile(w, r), RECON[recon])
+    G.set_state([inputs.initial_cell_averages(w)])
+    k = 0
+    for n in range(6):
+        if n % 2 == 0:
+            nb = G.regrid(tol, buf, ratio, tile)
+            assert [tuple(map(tuple, b)) for b in nb] == log[k][1], f"boxes differ at step {n}"
+            k += 1
+        G.step(dt)
+    err = relerr_levels(G.get_state(), _interiors(data))
+    assert err < 1e-11, err
+
+
+@pytest.mark.slow
+def test_c3_full_size_ten_steps_with_regrid():
+    w = inputs.get("C3")
+    a = w.amr
+    dt = inputs.fixed_dt(w, a["ratio"])
+    log = []
+    H, data, _ = drv.c3_run(w, 3, a["regrid"], dt, a["tol"], a["buffer"], a["ratio"], a["tile"], log=log)
+    lb0 = inputs.level0_boxes(w)
+    G = AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), [lb0], [(1, 1)],
+                    lambda r: inputs.background_profile(w, r))
+    G.set_state([inputs.initial_cell_averages(w)])
+    nb = G.regrid(a["tol"], a["buffer"], a["ratio"], a["tile"])
+    assert [tuple(map(tuple, b)) for b in nb] == log[0][1]
+    assert len(nb) == 124                                          # SURVEY 8(c) #18 (buffer 1)
+    for _ in range(3):
+        G.step(dt)
+    err = relerr_levels(G.get_state(), _interiors(data))
+    assert err < 1e-12, err
