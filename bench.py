@@ -149,7 +149,7 @@ def main():
 
     import inputs
     from paper_1204_3853_b200 import api
-    from paper_1204_3853_b200.solver import UniformVlasov1D
+    from paper_1204_3853_b200.solver import UniformVlasov1D, UniformVlasov2D
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -158,7 +158,11 @@ def main():
     h = inputs.spacing(w)
     dt = inputs.fixed_dt(w)
     f0 = inputs.initial_cell_averages(w)
-    S = UniformVlasov1D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w))
+    if w.ncfg == 1:
+        S = UniformVlasov1D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w))
+    else:
+        S = UniformVlasov2D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w),
+                            inputs.prescribed_field(w))
     S.set_state(f0)
     S.capture(dt, steps=1)                       # one warm-up step inside
     for _ in range(args.warmup - 1):
@@ -250,13 +254,13 @@ def main():
             "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "grid": list(w.ncells), "patches": "64x64 (merged single block)",
+            "config": {"workload": args.workload, "grid": list(w.ncells), "patches": "x".join(map(str, w.patch)) + " (merged single block)",
                        "cells": w.cells, "recon": "centered4", "dt": dt,
-                       "l2": "inputs larger than L2 (4 x 64 MiB fields per step > 126 MB)",
+                       "l2": f"inputs larger than L2 (4 fields of {S.A.numel() * 8 / 2**20:.0f} MiB per step > 126 MB L2)",
                        "parallelism": f"replicas x{world}", "graph": f"CUDA graph, 1 RK4 step ({S.launches_per_step()} launches)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_stage_1d1v (4 launches per step)",
+                         "kernel": ("k_stage_1d1v" if w.ncfg == 1 else "k_stage_2d2v") + " (4 launches per step)",
                          "algorithmic_bytes_per_cell_step": STEP_BYTES,
                          "stage_ms": [float(x) for x in per_stage_avg],
                          "share_of_step": kern_ms_step / ms_step},

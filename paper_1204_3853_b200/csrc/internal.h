@@ -151,6 +151,7 @@ struct vlasov_level {
     mutable vk::RedPlan* red_plan = nullptr;
     // 2D+2V
     int64_t e_doubles = 0;
+    int strips2 = 1;                      // x strips of the 2D+2V stage kernel
     // scratch (device): interpolation tables
     double* d_b5 = nullptr;               // linear5 weights for coarse_ratio, [dim][s][5]
 };
@@ -168,6 +169,10 @@ namespace vk {
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s,
                       double* u, double* f_next, const double* E, const double* E_bc,
                       const double* f0v, int recon, double* rho);
+int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
+                      double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
+                      double* rho);
+int launch_moment_2d2v(const vlasov_level* L, const double* f, double* rho);
 int stage_1d1v_ctas_per_sm(bool wide, int tile_rows);
 int stage_1d1v_tile_width(bool wide);   // cells per v-tile of the stage kernel
 int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double* E_bc,

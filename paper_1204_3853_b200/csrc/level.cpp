@@ -772,7 +772,19 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         if (!rc) rc = build_ghost_tasks(L, coarser, copies, cfs, phys);
         if (!rc && coarser) rc = build_amr_tasks(L, coarser, reflux, reflux_cells, reflux_off, avg);
     } else {
-        rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V levels: not in this build yet");
+        // 2D+2V: uniform levels stored as one block covering the periodic domain (in-kernel
+        // ghosts); the stage kernel marches along x in strips sized for about one wave
+        if (!L->single_block)
+            rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V: only levels whose boxes tile the whole domain");
+        else if (L->dom[3] % 2 || L->dom[2] < 4 || L->dom[3] < 4)
+            rc = vk::fail(VLASOV_EINVAL, "2D+2V: need nvy even and at least 4 cells per velocity dim");
+        else {
+            const int nmt = (L->dom[3] / 2 + 31) / 32, nlg = (L->dom[2] + 3) / 4;
+            const int64_t per = (int64_t)nmt * nlg * L->dom[1];
+            L->strips2 = (int)std::max<int64_t>(1, std::min<int64_t>(L->dom[0] / 8, (148 * 6 + per - 1) / per));
+            L->self_ghost_ok = true;
+            L->n_vtiles = L->dom[2] * nmt;                 // moment partial planes
+        }
     }
     if (rc) { free_level(L); return rc; }
     L->n_copy = (int64_t)copies.size() / 2;
@@ -789,6 +801,8 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         *out = L;
         return VLASOV_OK;
     }
+    if (L->single_block && L->ndim == 4)
+        VK_CUDA(cudaMalloc((void**)&L->d_partials, sizeof(double) * (size_t)L->n_vtiles * L->dom[0] * L->dom[1]));
     if (L->single_block && L->ndim == 2) {
         VK_CUDA(cudaMalloc((void**)&L->d_partials, sizeof(double) * (size_t)L->n_vtiles * L->dom[0]));
         VK_CUDA(cudaMalloc((void**)&L->d_tickets, sizeof(unsigned) * (size_t)std::max(1, L->n_strips)));
@@ -939,6 +953,8 @@ int vlasov_tags_to_boxes(const uint8_t* tags, const int32_t domain_cells[4], int
 int vlasov_fill_ghosts(vlasov_level* L, double* f, const vlasov_level* coarser, const double* f_coarse,
                        const double* E_bc, const double* f0v, int32_t interp) {
     if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim == 4)
+        return vk::fail(VLASOV_EUNSUPPORTED, "fill_ghosts: 2D+2V levels derive their ghosts inside the stage kernel");
     if (L->n_cf > 0 && (coarser != L->coarser || !coarser || coarser->uid != L->coarser_uid))
         return vk::fail(VLASOV_ESTALE, "fill_ghosts: coarser level does not match the one of level_create");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
@@ -965,7 +981,11 @@ int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, con
     if (E_bc && !L->self_ghost_ok)
         return vk::fail(VLASOV_EUNSUPPORTED, "in-kernel ghosts need one periodic block with nv a multiple of 4");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
-    if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage: 2D+2V not in this build yet");
+    if (L->ndim == 4) {
+        if (!E_bc) return vk::fail(VLASOV_EUNSUPPORTED, "2D+2V stage: in-kernel ghosts (E_bc, f0v) required");
+        return vk::launch_stage_2d2v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E,
+                                     E_bc, f0v, recon, rho_next);
+    }
     return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E,
                                  E_bc, f0v, recon, rho_next);
 }
@@ -979,6 +999,8 @@ int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const 
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 2)
         return vk::launch_moment_direct(levels[0], f[0], rho_finest);
+    if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 4)
+        return vk::launch_moment_2d2v(levels[0], f[0], rho_finest);
     const vlasov_level* Lf = levels[nlev - 1];
     bool fresh = Lf->red_plan != nullptr && (int)Lf->red_plan->uids.size() == nlev;
     for (int l = 0; fresh && l < nlev; ++l) fresh = Lf->red_plan->uids[l] == levels[l]->uid;

@@ -19,6 +19,9 @@
 #include "scheme.cuh"
 
 namespace vk {
+#ifndef STAGE2D_MINB
+#define STAGE2D_MINB 2
+#endif
 
 struct StageArgs2 {
     const double* f_s;
@@ -81,8 +84,72 @@ __device__ __forceinline__ double2 f2_at(const StageArgs2& A, int i, int k, int 
     return make_double2(f_at(A, i, k, l, m), f_at(A, i, k, l, m + 1));
 }
 
+// Unconditional 16-byte load of the pair (m, m+1) at clamped velocity indices (always a valid
+// interior address, so the loads of a row step issue back to back); `fix` tells whether the pair
+// holds ghost values that must be recomputed with f_at (rare: velocity-boundary threads only).
+__device__ __forceinline__ double2 ld2(const StageArgs2& A, int i, int k, int l, int m, bool& fix) {
+    fix = (l < 0) | (l >= A.nvx);            // vx ghosts: warp-uniform (whole vx line)
+    i += (i < 0) ? A.nx : 0;
+    i -= (i >= A.nx) ? A.nx : 0;
+    k += (k < 0) ? A.ny : 0;
+    k -= (k >= A.ny) ? A.ny : 0;
+    const int lc = min(max(l, 0), A.nvx - 1), mc = min(max(m, 0), A.nvy - 2);
+    return __ldg(reinterpret_cast<const double2*>(A.f_s + A.org + (int64_t)i * A.s0 + (int64_t)k * A.s1 +
+                                                  (int64_t)lc * A.s2 + mc));
+}
+
+// vx-ghost pair through the characteristic boundary condition: out of line (rare, warp-uniform
+// path) so that the unrolled row steps stay small enough for the instruction cache
+__device__ __noinline__ double2 fix_pair(const StageArgs2& A, int i, int k, int l, int m) {
+    return make_double2(f_at(A, i, k, l, m), f_at(A, i, k, l, m + 1));
+}
+
+// a batch of N pair loads (i, k[n], l[n], m[n]) followed by the ghost fix-up
+template <int N>
+__device__ __forceinline__ void ld2_batch(const StageArgs2& A, int i, const int (&k)[N], const int (&l)[N],
+                                          const int (&m)[N], double2 (&out)[N]) {
+    bool fix[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) out[n] = ld2(A, i, k[n], l[n], m[n], fix[n]);
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+        if (fix[n]) out[n] = fix_pair(A, i, k[n], l[n], m[n]);
+}
+
+// vy ghosts of a line triple (pl, pc, ph) = pairs at (m0-2, m0), (m0, m0+1), (m0+2, m0+3) of line
+// (i, k, l): the edge lanes replace pl (m0 == 0) or ph (m0 + 2 == nvy) by the characteristic
+// condition with a = -E_y(i, k) (warp-uniform), from the interior values they hold already.
+__device__ __forceinline__ void vy_fix(const StageArgs2& A, int i, int k, int l, int m0, double2& pl, const double2& pc,
+                                       double2& ph) {
+    const bool lo = (m0 == 0), hi = (m0 + 2 == A.nvy);
+    if (!(lo || hi)) return;
+    i += (i < 0) ? A.nx : 0;
+    i -= (i >= A.nx) ? A.nx : 0;
+    k += (k < 0) ? A.ny : 0;
+    k -= (k >= A.ny) ? A.ny : 0;
+    const int nyg = A.ny + 4;
+    const double a = -__ldg(A.E_bc + (int64_t)(A.nx + 4) * nyg + (int64_t)(i + 2) * nyg + (k + 2));
+    const double* prof = A.f0v + (int64_t)(l + 2) * (A.nvy + 4);
+    if (lo) {
+        if (a < 0.0) {
+            const double f0 = pc.x, f1 = pc.y, f2 = ph.x, f3 = ph.y;
+            pl = make_double2(10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3, 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3);
+        } else {
+            pl = make_double2(__ldg(prof + 0), __ldg(prof + 1));
+        }
+    }
+    if (hi) {
+        if (a > 0.0) {
+            const double f0 = pc.y, f1 = pc.x, f2 = pl.y, f3 = pl.x;
+            ph = make_double2(4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3, 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3);
+        } else {
+            ph = make_double2(__ldg(prof + A.nvy + 2), __ldg(prof + A.nvy + 3));
+        }
+    }
+}
+
 template <int STAGE, int RECON>
-__global__ void __launch_bounds__(128) k_stage_2d2v(const StageArgs2 A) {
+__global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArgs2 A) {
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int m0 = 2 * (blockIdx.x * 32 + tx);
     const int l = blockIdx.y * 4 + ty;
@@ -122,10 +189,16 @@ __global__ void __launch_bounds__(128) k_stage_2d2v(const StageArgs2 A) {
             if (q < Q) {
                 const int r = x0 - 2 + q;
                 // ---- row r: x-window, vx-faces, vy-faces
-                const double2 c01 = f2_at(A, r, k, lc, mc - 2), c23 = f2_at(A, r, k, lc, mc),
-                              c45 = f2_at(A, r, k, lc, mc + 2);
-                const double2 am1 = f2_at(A, r, k, lc - 1, mc), ap1 = f2_at(A, r, k, lc + 1, mc);
-                const double2 am2 = f2_at(A, r, k, lc - 2, mc), ap2 = f2_at(A, r, k, lc + 2, mc);
+                double2 rr[7];
+                {
+                    const int kk[7] = {k, k, k, k, k, k, k};
+                    const int ll[7] = {lc, lc, lc, lc - 1, lc + 1, lc - 2, lc + 2};
+                    const int mm[7] = {mc - 2, mc, mc + 2, mc, mc, mc, mc};
+                    ld2_batch<7>(A, r, kk, ll, mm, rr);
+                }
+                vy_fix(A, r, k, lc, mc, rr[0], rr[1], rr[2]);
+                const double2 c01 = rr[0], c23 = rr[1], c45 = rr[2], am1 = rr[3], ap1 = rr[4], am2 = rr[5],
+                              ap2 = rr[6];
                 W[K][0][0] = am1.x; W[K][0][1] = am1.y;
                 W[K][1][0] = c23.x; W[K][1][1] = c23.y;
                 W[K][2][0] = ap1.x; W[K][2][1] = ap1.y;
@@ -156,12 +229,25 @@ __global__ void __launch_bounds__(128) k_stage_2d2v(const StageArgs2 A) {
                     if (q >= 4) {
                         const int i = r - 2;
                         // ---- y-faces at (i, k -+ 1/2) for vy m0-1 .. m0+2
+                        // loads of row i: lines k-2..k+2 at (l, m0-2..m0+3), lines k-+1 at l-+1, l-+2
+                        double2 yy[23];
+                        {
+                            const int kk[23] = {k - 2, k - 2, k - 2, k - 1, k - 1, k - 1, k, k, k, k + 1, k + 1, k + 1,
+                                                k + 2, k + 2, k + 2, k - 1, k - 1, k - 1, k - 1, k + 1, k + 1, k + 1,
+                                                k + 1};
+                            const int ll[23] = {lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc,
+                                                lc - 1, lc + 1, lc - 2, lc + 2, lc - 1, lc + 1, lc - 2, lc + 2};
+                            const int mm[23] = {mc - 2, mc, mc + 2, mc - 2, mc, mc + 2, mc - 2, mc, mc + 2, mc - 2, mc,
+                                                mc + 2, mc - 2, mc, mc + 2, mc, mc, mc, mc, mc, mc, mc, mc};
+                            ld2_batch<23>(A, i, kk, ll, mm, yy);
+                        }
+#pragma unroll
+                        for (int d = 0; d < 5; ++d) vy_fix(A, i, k - 2 + d, lc, mc, yy[3 * d], yy[3 * d + 1], yy[3 * d + 2]);
                         double y[5][4];
 #pragma unroll
-                        for (int d = -2; d <= 2; ++d) {
-                            const double2 pl = f2_at(A, i, k + d, lc, mc - 2), pc = f2_at(A, i, k + d, lc, mc),
-                                          ph = f2_at(A, i, k + d, lc, mc + 2);
-                            y[d + 2][0] = pl.y; y[d + 2][1] = pc.x; y[d + 2][2] = pc.y; y[d + 2][3] = ph.x;
+                        for (int d = 0; d < 5; ++d) {
+                            const double2 pl = yy[3 * d], pc = yy[3 * d + 1], ph = yy[3 * d + 2];
+                            y[d][0] = pl.y; y[d][1] = pc.x; y[d][2] = pc.y; y[d][3] = ph.x;
                         }
                         double YL[4], YH[4];
 #pragma unroll
@@ -174,10 +260,9 @@ __global__ void __launch_bounds__(128) k_stage_2d2v(const StageArgs2 A) {
 #pragma unroll
                         for (int sgn = 0; sgn < 2; ++sgn) {
                             const int kk = k + (sgn ? 1 : -1);
-                            const double2 b01 = f2_at(A, i, kk, lc, mc - 2), b23 = f2_at(A, i, kk, lc, mc),
-                                          b45 = f2_at(A, i, kk, lc, mc + 2);
-                            const double2 bm1 = f2_at(A, i, kk, lc - 1, mc), bp1 = f2_at(A, i, kk, lc + 1, mc);
-                            const double2 bm2 = f2_at(A, i, kk, lc - 2, mc), bp2 = f2_at(A, i, kk, lc + 2, mc);
+                            const int yb = sgn ? 9 : 3, nb = sgn ? 19 : 15;
+                            const double2 b01 = yy[yb], b23 = yy[yb + 1], b45 = yy[yb + 2];
+                            const double2 bm1 = yy[nb], bp1 = yy[nb + 1], bm2 = yy[nb + 2], bp2 = yy[nb + 3];
                             const double ax = -Ex(i, kk), ay = -Ey(i, kk);
                             VXk[sgn][0][0] = face_avg<RECON>(bm2.x, bm1.x, b23.x, bp1.x, ax);
                             VXk[sgn][0][1] = face_avg<RECON>(bm2.y, bm1.y, b23.y, bp1.y, ax);

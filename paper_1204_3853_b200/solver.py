@@ -113,3 +113,82 @@ class UniformVlasov1D:
     def launches_per_step(self) -> int:
         # per stage: circulant (E with ghosts) + fused stage kernel  (+ 2 ghost-fill kernels)
         return 4 * (2 if self.self_ghost else 4)
+
+
+class UniformVlasov2D:
+    """Uniform 2D+2V level (BASELINE.json C5) with a prescribed configuration-space field
+    E(x, y) injected from a 2D mesh.  Per stage s = 1..4 one fused stage kernel
+    (in-kernel periodic x, y and characteristic vx, vy ghosts with E_bc = E, since a prescribed
+    field is its own previous constraint evaluation) whose epilogue writes per-(vx line, vy tile)
+    moment partials, and a tiny kernel summing them in a fixed order into rho(x, y)
+    (the 4D -> 2D reduction, P:295-297 / P:1061-1072)."""
+
+    def __init__(self, ncells, lower, dx, boxes, f0v: np.ndarray, E_mesh: np.ndarray, recon: int = CENTERED4,
+                 stream: Optional[torch.cuda.Stream] = None):
+        self.stream = stream or torch.cuda.Stream()
+        self.ncells = tuple(ncells)
+        self.recon = recon
+        with torch.cuda.stream(self.stream):
+            self.level = api.Level(4, ncells, lower, dx, (1, 1, 1, 1), boxes, stream=self.stream)
+            if self.level.info.nblocks != 1:
+                raise ValueError("UniformVlasov2D needs boxes that tile the domain")
+            self.A = self.level.field()
+            self.B = self.level.field()
+            self.C = self.level.field()
+            self.U = self.level.field()
+            self.E = self.level.efield()
+            Em = torch.as_tensor(np.ascontiguousarray(E_mesh), dtype=torch.float64).cuda()
+            api.vlasov_inject_field(self.level.h, Em, E_mesh.shape[1:], self.E)
+            self.rho = torch.zeros(ncells[0] * ncells[1], dtype=torch.float64, device="cuda")
+            self.f0v = torch.as_tensor(np.ascontiguousarray(f0v), dtype=torch.float64).cuda()
+        self.stream.synchronize()
+        self.graph = None
+
+    def set_state(self, f_full: np.ndarray):
+        with torch.cuda.stream(self.stream):
+            self.level.set_domain(self.A, f_full)
+            api.vlasov_reduce_moment([self.level.h], [self.A], self.rho)
+        self.stream.synchronize()
+
+    def get_state(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.level.get_domain(self.A)
+
+    def moment(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.rho.cpu().numpy().reshape(self.ncells[0], self.ncells[1])
+
+    def stage_launch(self, s, dt):
+        A, B, C = self.A, self.B, self.C
+        f_s, f_next = {1: (A, B), 2: (B, C), 3: (C, B), 4: (B, A)}[s]
+        api.vlasov_rk4_stage(self.level.h, s, dt, A, f_s, self.U, f_next, self.E, self.E, self.f0v, self.recon,
+                             self.rho)
+
+    def field_launch(self, s):
+        pass                      # prescribed field: nothing to solve
+
+    def _stage(self, s, dt):
+        self.stage_launch(s, dt)
+
+    def step(self, dt: float):
+        with torch.cuda.stream(self.stream):
+            for s in (1, 2, 3, 4):
+                self._stage(s, dt)
+
+    def capture(self, dt: float, steps: int = 1):
+        self.step(dt)
+        self.stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            for _ in range(steps):
+                for s in (1, 2, 3, 4):
+                    self._stage(s, dt)
+        self.graph, self.dt = g, dt
+        return g
+
+    def replay(self):
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
+
+    def launches_per_step(self) -> int:
+        return 4 * 2              # stage kernel + moment finish per stage

@@ -1,0 +1,101 @@
+"""GPU parity of the 2D+2V (BASELINE.json C5) path against the oracle, through the C ABI:
+one RK4 stage, one and several RK4 steps, CENTERED4 and UPWIND, ragged velocity tiles, and the
+fused 4D -> 2D moment against the oracle's moment and the closed form of the Maxwellian
+reduction.  Tolerances: 1e-12 after one step, 1e-11 / 1e-10 after more
+(north_star, reading #25)."""
+import numpy as np
+import pytest
+
+import inputs
+from oracle import field, scheme, uniform
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1204_3853_b200 import _lib, api  # noqa: E402
+from paper_1204_3853_b200.solver import UniformVlasov2D  # noqa: E402
+
+RECON = {scheme.CENTERED4: _lib.CENTERED4, scheme.UPWIND: _lib.UPWIND}
+
+
+def relerr(a, b):
+    return np.max(np.abs(a - b)) / np.max(np.abs(b))
+
+
+def _solver(w, recon=scheme.CENTERED4):
+    return UniformVlasov2D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w),
+                           inputs.background_profile(w), inputs.prescribed_field(w), RECON[recon])
+
+
+def _run(w, nsteps, recon=scheme.CENTERED4, noise=None):
+    f0 = inputs.initial_cell_averages(w)
+    if noise is not None:
+        f0 = f0 * (1.0 + 0.05 * inputs.random_field(f0.shape, noise))
+    dt = inputs.fixed_dt(w)
+    S = _solver(w, recon)
+    S.set_state(f0)
+    for _ in range(nsteps):
+        S.step(dt)
+    prob = uniform.problem_for(w, recon)
+    ref, _ = prob.run(f0, dt, nsteps)
+    return S, S.get_state(), ref
+
+
+SHAPES = [((8, 8, 12, 16), (8, 8, 12, 16)), ((10, 6, 9, 70), (5, 6, 9, 35)), ((6, 12, 16, 130), (6, 12, 16, 130))]
+
+
+@pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
+@pytest.mark.parametrize("shape,patch", SHAPES)
+def test_one_step(shape, patch, recon):
+    w = inputs.scaled(inputs.get("C5"), shape, patch)
+    _, got, ref = _run(w, 1, recon, noise=3)
+    assert relerr(got, ref) < 1e-12
+
+
+def test_one_stage_is_half_step_euler():
+    w = inputs.scaled(inputs.get("C5"), (8, 10, 12, 14))
+    f0 = inputs.initial_cell_averages(w) * (1.0 + 0.05 * inputs.random_field((8, 10, 12, 14), 5))
+    S = _solver(w)
+    S.set_state(f0)
+    dt = inputs.fixed_dt(w)
+    with torch.cuda.stream(S.stream):
+        S._stage(1, dt)
+    S.stream.synchronize()
+    got = S.level.get_domain(S.B)
+    prob = uniform.problem_for(w)
+    E = prob.constraints(f0)
+    k, _ = prob.rhs(f0, E, E)
+    np.testing.assert_allclose(got, f0 + 0.5 * dt * k, rtol=0, atol=1e-13 * np.abs(f0).max())
+
+
+def test_ten_steps_and_moment():
+    w = inputs.scaled(inputs.get("C5"), (16, 16, 16, 16))
+    S, got, ref = _run(w, 10)
+    assert relerr(got, ref) < 1e-11
+    rho_ref = field.moment_rho(ref, np.prod(inputs.spacing(w)[2:]))
+    np.testing.assert_allclose(S.moment(), rho_ref, rtol=0, atol=1e-13)
+    direct = torch.zeros_like(S.rho)
+    api.vlasov_reduce_moment([S.level.h], [S.A], direct)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(direct.cpu().numpy().reshape(16, 16), rho_ref, rtol=0, atol=1e-13)
+
+
+def test_moment_of_initial_state_closed_form():
+    # rho = 1 - (1 + 0.01 Sx Sy cos x_i cos y_k) erf(6/sqrt 2)^2 on cell averages
+    from scipy.special import erf
+    w = inputs.get("C5")
+    S = _solver(w)
+    S.set_state(inputs.initial_cell_averages(w))
+    hx, hy = inputs.spacing(w)[:2]
+    cx = (np.sin(np.arange(1, 65) * hx) - np.sin(np.arange(0, 64) * hx)) / hx
+    cy = (np.sin(np.arange(1, 65) * hy) - np.sin(np.arange(0, 64) * hy)) / hy
+    exact = 1.0 - (1.0 + 0.01 * cx[:, None] * cy[None, :]) * erf(6.0 / np.sqrt(2.0)) ** 2
+    np.testing.assert_allclose(S.moment(), exact, rtol=0, atol=1e-13)
+
+
+def test_c5_full_size_one_step():
+    w = inputs.get("C5")
+    _, got, ref = _run(w, 1)
+    assert relerr(got, ref) < 1e-12

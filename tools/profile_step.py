@@ -10,7 +10,7 @@ import torch  # noqa: E402
 
 import inputs  # noqa: E402
 from paper_1204_3853_b200 import _lib  # noqa: E402
-from paper_1204_3853_b200.solver import UniformVlasov1D  # noqa: E402
+from paper_1204_3853_b200.solver import UniformVlasov1D, UniformVlasov2D  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="C4")
@@ -18,8 +18,12 @@ ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--recon", default="centered4")
 a = ap.parse_args()
 w = inputs.get(a.workload)
-S = UniformVlasov1D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), inputs.background_profile(w),
-                    _lib.UPWIND if a.recon == "upwind" else _lib.CENTERED4)
+rc = _lib.UPWIND if a.recon == "upwind" else _lib.CENTERED4
+if w.ncfg == 1:
+    S = UniformVlasov1D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), inputs.background_profile(w), rc)
+else:
+    S = UniformVlasov2D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), inputs.background_profile(w),
+                        inputs.prescribed_field(w), rc)
 S.set_state(inputs.initial_cell_averages(w))
 dt = inputs.fixed_dt(w)
 for _ in range(a.steps):
