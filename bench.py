@@ -89,6 +89,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    """Max of a per-rank device time over all ranks (NCCL on the GPU path, gloo in the CPU
+    tests); identity for one rank."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_throughput(cells_per_rank: int, world: int, steps: int, ms_max: float) -> float:
+    """Replicas: every rank advances its own copy of the workload (weak scaling); the job's
+    throughput is all cells updated by all ranks over the slowest rank's device time."""
+    return cells_per_rank * world * steps / (ms_max / 1e3)
+
+
 def cpu_baseline(workload_name, budget_s=20.0):
     """Oracle (as it stands) on the host: full-size C4 RK4 steps until ~budget_s."""
     import inputs
@@ -186,12 +204,9 @@ def main():
     barrier()
     ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, "cuda")
     ms_step = ms / args.steps
-    value = w.cells * world * args.steps / (ms / 1e3)
+    value = whole_job_throughput(w.cells, world, args.steps, ms)
 
     # ---------------------------------------------------------------- dominant-kernel timing
     # eager replay of the same launches with events bracketing every stage kernel on its stream
@@ -239,11 +254,8 @@ def main():
         e1.record(S.stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / nE
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = w.cells * world / (e2e_ms / 1e3)
+    e2e_ms = max_over_ranks(e2e_ms, world, "cuda")
+    e2e_value = whole_job_throughput(w.cells, world, 1, e2e_ms)
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -154,6 +154,18 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
  * f_next, rho = 1 - dv sum_v f_next, fused into the stage: per-(row, v-tile) partial
  * sums combined in a fixed order by the last CTA of each row strip (deterministic).            */
 int vlasov_rhs(vlasov_level* level, const double* f, const double* E, double* k, int32_t recon);
+
+/* vlasov_rk4_stage_vp: the constraint evaluation of Alg.5 fused into the stage for a
+ * uniform 1D+1V level: E_s = -D4 phi(rho_s) (readings #1-#2; the same operator as
+ * vlasov_poisson_solve with `plan`) is computed inside the stage kernel from rho_s, the moment of
+ * f_s, and written to E_s (the level's ghosted E array), then the stage runs as vlasov_rk4_stage
+ * with E = E_s.  Requirements: the in-kernel ghost mode (E_bc, f0v non-NULL, one periodic block,
+ * nv % 4 == 0), plan->n == the level's x cells <= 4096, rho_next != rho_s (ping-pong buffers).
+ * One launch per stage instead of two.                                                          */
+int vlasov_rk4_stage_vp(vlasov_level* level, const vlasov_poisson* plan, int32_t stage, double dt,
+                        double* f_n, const double* f_s, double* u, double* f_next, const double* rho_s,
+                        double* E_s, const double* E_bc, const double* f0v, int32_t recon,
+                        double* rho_next);
 int vlasov_rk4_stage(vlasov_level* level, int32_t stage, double dt, double* f_n, const double* f_s,
                      double* u, double* f_next, const double* E, const double* E_bc,
                      const double* f0v, int32_t recon, double* rho_next);

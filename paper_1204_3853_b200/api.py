@@ -16,7 +16,7 @@ from ._lib import Box, Geom, LevelInfo, check, lib
 __all__ = [
     "Level", "Poisson", "make_geom", "vlasov_level_create", "vlasov_level_destroy",
     "vlasov_level_get_info", "vlasov_level_layout", "vlasov_level_ghost_map", "vlasov_subpatches",
-    "vlasov_fill_ghosts", "vlasov_rhs", "vlasov_rk4_stage", "vlasov_reduce_moment",
+    "vlasov_fill_ghosts", "vlasov_rhs", "vlasov_rk4_stage", "vlasov_rk4_stage_vp", "vlasov_reduce_moment",
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes",
     "vlasov_level_fill_from", "vlasov_device_ok", "vlasov_last_error",
@@ -116,6 +116,12 @@ def vlasov_rk4_stage(h, stage, dt, f_n, f_s, u, f_next, E, E_bc=None, f0v=None, 
                      rho_next=None):
     return check(lib.vlasov_rk4_stage(h, stage, float(dt), _ptr(f_n), _ptr(f_s), _ptr(u), _ptr(f_next), _ptr(E),
                                       _ptr(E_bc), _ptr(f0v), recon, _ptr(rho_next)))
+
+
+def vlasov_rk4_stage_vp(h, plan, stage, dt, f_n, f_s, u, f_next, rho_s, E_s, E_bc, f0v, recon=_lib.CENTERED4,
+                        rho_next=None):
+    return check(lib.vlasov_rk4_stage_vp(h, plan, stage, float(dt), _ptr(f_n), _ptr(f_s), _ptr(u), _ptr(f_next),
+                                         _ptr(rho_s), _ptr(E_s), _ptr(E_bc), _ptr(f0v), recon, _ptr(rho_next)))
 
 
 def vlasov_reduce_moment(levels, f_list, rho_finest):

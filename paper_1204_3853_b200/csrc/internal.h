@@ -130,6 +130,7 @@ struct vlasov_level {
     int tile_rows = 0;
     int n_vtiles = 0;                     // partial v-tiles (single-block only)
     int n_strips = 0;
+    int cluster_size = 1;                 // v-tiles per cluster of the fused-field stage launch
     double* d_partials = nullptr;         // moment scratch [n_vtiles][dom_x]
     unsigned* d_tickets = nullptr;        // per-strip arrival tickets
     bool self_ghost_ok = false;           // single periodic block, nv % 4 == 0: in-kernel ghosts
@@ -168,13 +169,15 @@ namespace vk {
 // ------------------------------------------------------------------ kernels (launchers)
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s,
                       double* u, double* f_next, const double* E, const double* E_bc,
-                      const double* f0v, int recon, double* rho);
+                      const double* f0v, int recon, double* rho, const double* rho_in = nullptr,
+                      const double* gE = nullptr, double* E_out = nullptr);
 int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
                       double* rho);
 int launch_moment_2d2v(const vlasov_level* L, const double* f, double* rho);
 int stage_1d1v_ctas_per_sm(bool wide, int tile_rows);
 int stage_1d1v_tile_width(bool wide);   // cells per v-tile of the stage kernel
+int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n);
 int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double* E_bc,
                 const double* f0v, int interp);
 int launch_moment_direct(const vlasov_level* L, const double* f, double* rho);

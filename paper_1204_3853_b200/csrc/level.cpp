@@ -317,7 +317,21 @@ int build_tiles_1d(vlasov_level* L, bool have_device) {
     if (L->blocks.size() == 1) {              // exact one-wave tiling of a single block
         const int nx = vk::box_ncells_dim(L->blocks[0], 0);
         const int nvt = (vk::box_ncells_dim(L->blocks[0], 1) + TV - 1) / TV;
-        const int64_t max_strips = std::max<int64_t>(1, slots / nvt);
+        int64_t max_strips = std::max<int64_t>(1, slots / nvt);
+        // the fused-field launch groups the v-tiles of a strip into one cluster: one wave of
+        // clusters (the unfused launch uses the same tiles)
+        L->cluster_size = 1;
+        if (have_device && L->single_block && nvt >= 2 && L->dom[0] <= 4096) {
+            // cluster size: the divisor of nvt (<= 8) that keeps the most strips in one wave
+            int64_t best = 0;
+            for (int cs = std::min(8, nvt); cs >= 2; --cs) {
+                if (nvt % cs) continue;
+                const int mc = vk::stage_1d1v_max_clusters(wide, 128, cs, L->dom[0]);
+                const int64_t strips = std::min<int64_t>(max_strips, (int64_t)mc * cs / nvt);
+                if (strips > best) { best = strips; L->cluster_size = cs; }
+            }
+            if (best > 0) max_strips = best;
+        }
         rows = (int)((nx + max_strips - 1) / max_strips);
     }
     rows = std::max(8, std::min(128, rows));
@@ -776,6 +790,8 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         // ghosts); the stage kernel marches along x in strips sized for about one wave
         if (!L->single_block)
             rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V: only levels whose boxes tile the whole domain");
+        else if (L->field_doubles >= ((int64_t)1 << 31))
+            rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V: level block larger than 2^31 doubles");
         else if (L->dom[3] % 2 || L->dom[2] < 4 || L->dom[3] < 4)
             rc = vk::fail(VLASOV_EINVAL, "2D+2V: need nvy even and at least 4 cells per velocity dim");
         else {
@@ -988,6 +1004,27 @@ int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, con
     }
     return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E,
                                  E_bc, f0v, recon, rho_next);
+}
+
+int vlasov_rk4_stage_vp(vlasov_level* L, const vlasov_poisson* plan, int32_t stage, double dt, double* f_n,
+                        const double* f_s, double* u, double* f_next, const double* rho_s, double* E_s,
+                        const double* E_bc, const double* f0v, int32_t recon, double* rho_next) {
+    if (!L || !plan || !f_s || !f_next || !rho_s || !E_s || !E_bc || !f0v)
+        return vk::fail(VLASOV_EINVAL, "null argument");
+    if (stage < 1 || stage > 4) return vk::fail(VLASOV_EINVAL, "stage must be 1..4");
+    if (stage >= 2 && !f_n) return vk::fail(VLASOV_EINVAL, "f_n required");
+    if ((stage == 2 || stage == 4) && !u) return vk::fail(VLASOV_EINVAL, "u required");
+    if (recon != VLASOV_CENTERED4 && recon != VLASOV_UPWIND) return vk::fail(VLASOV_EINVAL, "bad recon");
+    if (L->ndim != 2 || !L->self_ghost_ok)
+        return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage_vp: one periodic 1D+1V block with nv % 4 == 0");
+    if (plan->n != L->dom[0] || std::fabs(plan->dx - L->h[0]) > 1e-12 * L->h[0])
+        return vk::fail(VLASOV_EINVAL, "rk4_stage_vp: Poisson plan does not match the level's x mesh");
+    if (plan->n > 4096 || plan->n % 2)
+        return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage_vp: needs an even n <= 4096 (else use poisson_solve)");
+    if (rho_next == rho_s) return vk::fail(VLASOV_EINVAL, "rk4_stage_vp: rho_next must not alias rho_s");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E_s,
+                                 E_bc, f0v, recon, rho_next, rho_s, plan->d_gE, E_s);
 }
 
 int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,

@@ -42,7 +42,15 @@ struct StageArgs1 {
     const Block1* blocks;
     double dt, dx, dv, v_lo;   // v_lo: physical lower velocity of the level domain
     int dom_x, dom_v, n_vtiles, tile_rows;
+    // fused constraint evaluation (vlasov_rk4_stage_vp): E of the stage state from its moment
+    const double* rho_in;      // nullable: rho of f_s (dom_x values); then E is computed and written
+    const double* gE;          // Green's function of E = -D4 phi(rho) (Poisson plan, dom_x values)
+    double* E_out;             // ghosted level E array (owned rows + periodic ghosts)
+    int cluster;               // CTAs per cluster of the fused launch (the v-tiles of a strip)
 };
+
+// shared memory of the fused field prologue: rho [n], extended g [2n + 4], row results [<= 4 NT]
+static size_t field_smem_bytes(int n, int nt) { return (size_t)(3 * n + 4 + 4 * nt) * sizeof(double); }
 
 // CPT = 4 cells per consumer thread, TV = 4*NT cells per v-tile.
 constexpr int CPT = 4;
@@ -76,6 +84,8 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) uint64_t full_bar[NSLOT];
     __shared__ __align__(8) uint64_t empty_bar[NSLOT];
+    __shared__ __align__(8) uint64_t field_bar;
+    __shared__ __align__(8) uint64_t e_bar;      // fused field: all Q rows of E have landed
     __shared__ unsigned s_ticket;
     double* psum = smem + NSLOT * SLOT;          // [NW][tile_rows]
 
@@ -87,9 +97,10 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
     const int wpad = (T.ncols + 1) & ~1;
     double* sE = psum + NW * A.tile_rows;        // E of rows x0-2 .. x0+nrows+1
     double* sEbc = sE + (A.tile_rows + 4);       // E_bc of the same rows (SELF)
+    const bool field = SELF && (A.rho_in != nullptr);
     for (int t = tid; t < Q; t += blockDim.x) {
         const int gi = B.lo_x + T.x0 - 2 + t + G;  // index in the ghosted level E array
-        sE[t] = __ldg(A.E + gi);
+        if (!field) sE[t] = __ldg(A.E + gi);
         if (SELF) sEbc[t] = __ldg(A.E_bc + gi);
     }
     if (tid == 0) {
@@ -97,15 +108,32 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], NW);
         }
+        mbar_init(&field_bar, 1);
+        mbar_init(&e_bar, 1);
         fence_mbar_init();
     }
+    // fused field in a cluster (the v-tiles of one row strip): every CTA's barrier is initialised
+    // and armed before any CTA pushes E rows into its shared memory
+    const uint32_t crank = field ? cluster_ctarank() : 0u, csize = field ? cluster_nctarank() : 1u;
+    if (tid == 0 && csize > 1) mbar_arrive_expect_tx(&e_bar, (uint32_t)Q * 8u);
     __syncthreads();
+    if (field && csize > 1) cluster_sync_all();
 
     // row r (block-local interior index, may be -2..nx+1): interior column 0 of that row
     auto rowbase = [&](int r) -> int64_t { return B.off + (int64_t)(r + G) * B.pitch + G; };
 
+    // fused field: rho and the Green's function (twice: periodic extension) staged by the TMA engine
+    double* f_rho = sEbc + (A.tile_rows + 4);
+    double* f_g = f_rho + A.dom_x;
     if (warp == NW) {                            // ---------------- producer warp
         if (lane == 0) {
+            if (field) {
+                const uint32_t nb = (uint32_t)A.dom_x * 8u;
+                mbar_arrive_expect_tx(&field_bar, 3u * nb);
+                bulk_g2s(f_rho, A.rho_in, nb, &field_bar);
+                bulk_g2s(f_g, A.gE, nb, &field_bar);
+                bulk_g2s(f_g + A.dom_x, A.gE, nb, &field_bar);
+            }
             const uint32_t seg_bytes = (uint32_t)(wpad + 4) * 8u;
             const uint32_t row_bytes = (uint32_t)wpad * 8u;
             int slot = 0;
@@ -131,6 +159,78 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
     }
 
     // ---------------------------------------------------------------- consumers
+    if (field) {
+        // Constraint evaluation of the stage state (Alg.5) while the producer fills the
+        // ring: project rho to mean zero, E_i = sum_k gE[(i - k) mod n] rho_k for the rows of this
+        // tile, from rho and the periodically extended gE staged in shared memory by the TMA engine.
+        const int n = A.dom_x;
+        double* s_rho = f_rho;
+        double* s_g = f_g;                       // [2n + 4]
+        double* s_part = s_g + 2 * n + 4;        // [Q] E of the tile rows
+        if (tid < 4) s_g[2 * n + tid] = __ldg(A.gE + (tid % n));
+        mbar_wait(&field_bar, 0);
+        double acc = 0.0;
+        for (int k = tid; k < n; k += NT) acc += s_rho[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) psum[warp] = acc;
+        named_bar_sync(1, NT);
+        double mean = 0.0;
+        for (int w = 0; w < NW; ++w) mean += psum[w];
+        mean /= (double)n;
+        for (int k = tid; k < n; k += NT) s_rho[k] -= mean;          // projection
+        named_bar_sync(1, NT);
+        // The rows of the tile are split over the CTAs of the cluster (the strip's v-tiles compute
+        // disjoint row ranges); each row is pushed into every CTA's s_part with st.async, which
+        // completes on that CTA's e_bar.  One warp per group of 4 consecutive rows: lanes stride k
+        // (conflict-free shared-memory reads; rho[k] shared by the 4 rows), 8 accumulators, fixed
+        // butterflies -> deterministic.
+        const int tb = (int)((int64_t)Q * crank / csize), te = (int)((int64_t)Q * (crank + 1) / csize);
+        for (int t0 = tb + 4 * warp; t0 < te; t0 += 4 * NW) {
+            int gx = B.lo_x + T.x0 - 2 + t0;
+            gx += (gx < 0) ? n : 0;
+            gx -= (gx >= n) ? n : 0;
+            const double* gp = s_g + gx + n;                            // gp[j - k] = g[(gx + j - k) mod n]
+            double a[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+            int k = lane;
+            for (; k + 32 < n; k += 64) {
+                const double r0 = s_rho[k], r1 = s_rho[k + 32];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    a[0][j] = fma(gp[j - k], r0, a[0][j]);
+                    a[1][j] = fma(gp[j - k - 32], r1, a[1][j]);
+                }
+            }
+            if (k < n) {
+                const double r0 = s_rho[k];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a[0][j] = fma(gp[j - k], r0, a[0][j]);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                double e = a[0][j] + a[1][j];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+                const int t = t0 + j;
+                if (csize > 1) {
+                    if (t < te && lane < (int)csize)
+                        st_async_f64(map_shared_rank(s_part + t, lane), e, map_shared_rank(&e_bar, lane));
+                } else if (t < te && lane == 0) {
+                    s_part[t] = e;
+                }
+                if (t < te && lane == 0 && t >= 2 && t < Q - 2) {     // owned rows + periodic ghosts
+                    const int x = B.lo_x + T.x0 - 2 + t;
+                    A.E_out[x + G] = e;
+                    if (x < G) A.E_out[x + G + n] = e;
+                    if (x >= n - G) A.E_out[x + G - n] = e;
+                }
+            }
+        }
+        if (csize > 1) mbar_wait(&e_bar, 0);
+        else named_bar_sync(1, NT);
+        for (int t = tid; t < Q; t += NT) sE[t] = s_part[t];
+        named_bar_sync(1, NT);
+    }
     const int cl = CPT * tid;                    // tile-local column of my first cell
     const int c0 = T.j0 + cl;                    // block-local interior column
     const int nact = min(CPT, T.ncols - cl);     // active cells of this thread (may be <= 0)
@@ -162,6 +262,7 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
     int slot = 0;
     uint32_t phase = 0;
     for (int q0 = 0; q0 < Q; q0 += 4) {
+        double rs[4] = {0.0, 0.0, 0.0, 0.0};    // per-thread moment sums of the group's output rows
 #pragma unroll
         for (int K = 0; K < 4; ++K) {           // K == q mod 4 == row r mod 4 (shifted by 2)
             const int q = q0 + K;
@@ -264,12 +365,10 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
                             }
                     }
                     if (A.rho != nullptr) {
-                        double s = 0.0;
+                        double sr = 0.0;
 #pragma unroll
-                        for (int m = 0; m < CPT; ++m) s += (m < nact) ? o[m] : 0.0;
-#pragma unroll
-                        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-                        if (lane == 0) psum[warp * A.tile_rows + (i - T.x0)] = s;
+                        for (int m = 0; m < CPT; ++m) sr += (m < nact) ? o[m] : 0.0;
+                        rs[K] = sr;
                     }
                 } else if (q == 3) {             // x-fluxes at x0 - 1/2 (rows x0-2 .. x0+1)
                     const int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;
@@ -291,6 +390,23 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
                 if (lane == 0) mbar_arrive(&empty_bar[slot]);
                 if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
             }
+        }
+        if (A.rho != nullptr && q0 >= 4) {
+            // warp sums of the 4 rows of the group with one transposed butterfly (6 shuffles
+            // instead of 20): lane L ends with row 2*bit4(L) + bit3(L), lanes L % 8 == 0 write it
+            const bool b16 = lane & 16, b8 = lane & 8;
+            double v0 = b16 ? rs[2] : rs[0], v1 = b16 ? rs[3] : rs[1];
+            const double w0 = b16 ? rs[0] : rs[2], w1 = b16 ? rs[1] : rs[3];
+            v0 += __shfl_xor_sync(0xffffffffu, w0, 16);
+            v1 += __shfl_xor_sync(0xffffffffu, w1, 16);
+            double u = b8 ? v1 : v0;
+            const double xv = b8 ? v0 : v1;
+            u += __shfl_xor_sync(0xffffffffu, xv, 8);
+            u += __shfl_xor_sync(0xffffffffu, u, 4);
+            u += __shfl_xor_sync(0xffffffffu, u, 2);
+            u += __shfl_xor_sync(0xffffffffu, u, 1);
+            const int i = T.x0 - 4 + q0 + (b16 ? 2 : 0) + (b8 ? 1 : 0);      // output row of q = q0 + that
+            if ((lane & 7) == 0 && i >= T.x0 && i < T.x0 + T.nrows) psum[warp * A.tile_rows + (i - T.x0)] = u;
         }
     }
 
@@ -323,12 +439,28 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
 template <int STAGE, int RECON, int NT, bool SELF>
 static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
     using SG = StageGeom<STAGE, NT>;
-    const size_t smem = SG::smem_bytes(tile_rows);
+    const size_t smem = SG::smem_bytes(tile_rows) + (A.rho_in ? field_smem_bytes(A.dom_x, NT) : 0);
     auto kern = k_stage_1d1v<STAGE, RECON, NT, SELF>;
     static bool configured = false;   // per template instantiation
     if (!configured) {
         VK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
+    }
+    if (A.rho_in && A.cluster > 1) {   // fused field: the v-tiles of a row strip form one cluster
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ntiles);
+        cfg.blockDim = dim3(NT + 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)A.cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        VK_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
+        return VLASOV_OK;
     }
     kern<<<ntiles, NT + 32, smem, st>>>(A);
     VK_LAUNCH("k_stage_1d1v");
@@ -373,10 +505,43 @@ int stage_1d1v_ctas_per_sm(bool wide, int tile_rows) {
 
 int stage_1d1v_tile_width(bool wide) { return CPT * (wide ? NT_WIDE : NT_NARROW); }
 
+// co-resident clusters of `cs` CTAs of the fused stage-4 instance (field smem for n x cells)
+int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n) {
+    auto q = [&](auto kern, int nt, size_t smem) -> int {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cs * 64);
+        cfg.blockDim = dim3(nt + 32);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int m = 0;
+        if (cudaOccupancyMaxActiveClusters(&m, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        return m;
+    };
+    if (wide)
+        return q(k_stage_1d1v<4, VLASOV_CENTERED4, NT_WIDE, true>, NT_WIDE,
+                 StageGeom<4, NT_WIDE>::smem_bytes(tile_rows) + field_smem_bytes(n, NT_WIDE));
+    return q(k_stage_1d1v<4, VLASOV_CENTERED4, NT_NARROW, true>, NT_NARROW,
+             StageGeom<4, NT_NARROW>::smem_bytes(tile_rows) + field_smem_bytes(n, NT_NARROW));
+}
+
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
-                      double* rho) {
+                      double* rho, const double* rho_in, const double* gE, double* E_out) {
     StageArgs1 A;
+    A.rho_in = rho_in;
+    A.gE = gE;
+    A.E_out = E_out;
+    A.cluster = rho_in ? L->cluster_size : 1;
     A.f_s = f_s;
     A.f_n = f_n;
     A.u_in = u;

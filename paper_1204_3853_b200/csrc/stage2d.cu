@@ -163,6 +163,30 @@ __global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArg
     const int64_t ecomp = (int64_t)(A.nx + 4) * nyg;
     auto Ex = [&](int i, int kk) { return __ldg(A.E + (int64_t)(i + 2) * nyg + (kk + 2)); };
     auto Ey = [&](int i, int kk) { return __ldg(A.E + ecomp + (int64_t)(i + 2) * nyg + (kk + 2)); };
+    // per-thread constant load offsets (doubles): y lines k-2..k+2 (periodic), vx lines l-2..l+2
+    // (clamped: out-of-range lines are recomputed by the boundary condition), vy pairs
+    int ko[5];                       // 32-bit offsets: one block of a C5-sized level is < 2^31 doubles
+    int lo5[5];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        int kk = k - 2 + d;
+        kk += (kk < 0) ? A.ny : 0;
+        kk -= (kk >= A.ny) ? A.ny : 0;
+        ko[d] = kk * (int)A.s1;
+        lo5[d] = min(max(lc - 2 + d, 0), A.nvx - 1) * (int)A.s2;
+    }
+    const int mlo = max(mc - 2, 0), mhi = min(mc + 2, A.nvy - 2);
+    const bool l_edge = (lc < 2) || (lc + 2 >= A.nvx);            // warp-uniform
+    const bool m_edge = (mc == 0) || (mc + 2 == A.nvy);            // lanes at the vy boundary
+    const double* fbase = A.f_s + A.org;
+    auto P = [&](const double* rowp, int d, int e, int m) {
+        return __ldg(reinterpret_cast<const double2*>(rowp + (ko[d] + lo5[e] + m)));
+    };
+    auto rowptr = [&](int r) {
+        r += (r < 0) ? A.nx : 0;
+        r -= (r >= A.nx) ? A.nx : 0;
+        return fbase + (int64_t)r * A.s0;
+    };
     const double vbx = A.vx_lo + ((double)lc + 0.5) * A.hvx;
     const double vbxm = vbx - A.hvx, vbxp = vbx + A.hvx;
     double vby[4];                                     // m0-1 .. m0+2
@@ -189,16 +213,16 @@ __global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArg
             if (q < Q) {
                 const int r = x0 - 2 + q;
                 // ---- row r: x-window, vx-faces, vy-faces
-                double2 rr[7];
-                {
-                    const int kk[7] = {k, k, k, k, k, k, k};
-                    const int ll[7] = {lc, lc, lc, lc - 1, lc + 1, lc - 2, lc + 2};
-                    const int mm[7] = {mc - 2, mc, mc + 2, mc, mc, mc, mc};
-                    ld2_batch<7>(A, r, kk, ll, mm, rr);
+                const double* rp = rowptr(r);
+                double2 c01 = P(rp, 2, 2, mlo), c23 = P(rp, 2, 2, mc), c45 = P(rp, 2, 2, mhi);
+                double2 am1 = P(rp, 2, 1, mc), ap1 = P(rp, 2, 3, mc), am2 = P(rp, 2, 0, mc), ap2 = P(rp, 2, 4, mc);
+                if (l_edge) {
+                    if (lc - 2 < 0) am2 = fix_pair(A, r, k, lc - 2, mc);
+                    if (lc - 1 < 0) am1 = fix_pair(A, r, k, lc - 1, mc);
+                    if (lc + 1 >= A.nvx) ap1 = fix_pair(A, r, k, lc + 1, mc);
+                    if (lc + 2 >= A.nvx) ap2 = fix_pair(A, r, k, lc + 2, mc);
                 }
-                vy_fix(A, r, k, lc, mc, rr[0], rr[1], rr[2]);
-                const double2 c01 = rr[0], c23 = rr[1], c45 = rr[2], am1 = rr[3], ap1 = rr[4], am2 = rr[5],
-                              ap2 = rr[6];
+                if (m_edge) vy_fix(A, r, k, lc, mc, c01, c23, c45);
                 W[K][0][0] = am1.x; W[K][0][1] = am1.y;
                 W[K][1][0] = c23.x; W[K][1][1] = c23.y;
                 W[K][2][0] = ap1.x; W[K][2][1] = ap1.y;
@@ -230,19 +254,36 @@ __global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArg
                         const int i = r - 2;
                         // ---- y-faces at (i, k -+ 1/2) for vy m0-1 .. m0+2
                         // loads of row i: lines k-2..k+2 at (l, m0-2..m0+3), lines k-+1 at l-+1, l-+2
+                        const double* ip = rowptr(i);
                         double2 yy[23];
-                        {
-                            const int kk[23] = {k - 2, k - 2, k - 2, k - 1, k - 1, k - 1, k, k, k, k + 1, k + 1, k + 1,
-                                                k + 2, k + 2, k + 2, k - 1, k - 1, k - 1, k - 1, k + 1, k + 1, k + 1,
-                                                k + 1};
-                            const int ll[23] = {lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc, lc,
-                                                lc - 1, lc + 1, lc - 2, lc + 2, lc - 1, lc + 1, lc - 2, lc + 2};
-                            const int mm[23] = {mc - 2, mc, mc + 2, mc - 2, mc, mc + 2, mc - 2, mc, mc + 2, mc - 2, mc,
-                                                mc + 2, mc - 2, mc, mc + 2, mc, mc, mc, mc, mc, mc, mc, mc};
-                            ld2_batch<23>(A, i, kk, ll, mm, yy);
+#pragma unroll
+                        for (int d = 0; d < 5; ++d) {
+                            yy[3 * d] = P(ip, d, 2, mlo);
+                            yy[3 * d + 1] = P(ip, d, 2, mc);
+                            yy[3 * d + 2] = P(ip, d, 2, mhi);
                         }
 #pragma unroll
-                        for (int d = 0; d < 5; ++d) vy_fix(A, i, k - 2 + d, lc, mc, yy[3 * d], yy[3 * d + 1], yy[3 * d + 2]);
+                        for (int sg = 0; sg < 2; ++sg) {          // lines k-1 (sg 0), k+1 (sg 1) at l-1, l+1, l-2, l+2
+                            const int d = sg ? 3 : 1;
+                            yy[15 + 4 * sg] = P(ip, d, 1, mc);
+                            yy[16 + 4 * sg] = P(ip, d, 3, mc);
+                            yy[17 + 4 * sg] = P(ip, d, 0, mc);
+                            yy[18 + 4 * sg] = P(ip, d, 4, mc);
+                        }
+                        if (l_edge) {
+#pragma unroll
+                            for (int sg = 0; sg < 2; ++sg) {
+                                const int kk = k + (sg ? 1 : -1);
+                                if (lc - 1 < 0) yy[15 + 4 * sg] = fix_pair(A, i, kk, lc - 1, mc);
+                                if (lc + 1 >= A.nvx) yy[16 + 4 * sg] = fix_pair(A, i, kk, lc + 1, mc);
+                                if (lc - 2 < 0) yy[17 + 4 * sg] = fix_pair(A, i, kk, lc - 2, mc);
+                                if (lc + 2 >= A.nvx) yy[18 + 4 * sg] = fix_pair(A, i, kk, lc + 2, mc);
+                            }
+                        }
+                        if (m_edge) {
+#pragma unroll
+                            for (int d = 0; d < 5; ++d) vy_fix(A, i, k - 2 + d, lc, mc, yy[3 * d], yy[3 * d + 1], yy[3 * d + 2]);
+                        }
                         double y[5][4];
 #pragma unroll
                         for (int d = 0; d < 5; ++d) {

@@ -26,12 +26,15 @@ from ._lib import CENTERED4
 class UniformVlasov1D:
     def __init__(self, ncells: Sequence[int], lower: Sequence[float], dx: Sequence[float], boxes,
                  f0v: np.ndarray, recon: int = CENTERED4, stream: Optional[torch.cuda.Stream] = None,
-                 self_ghost: bool = True):
+                 self_ghost: bool = True, fused: Optional[bool] = None):
         self.stream = stream or torch.cuda.Stream()
         self.ncells = tuple(ncells)
         self.dx = tuple(dx)
         self.recon = recon
         self.self_ghost = self_ghost
+        # fused: constraint evaluation (Poisson + E) inside the stage kernel (vlasov_rk4_stage_vp)
+        self.fused = (self_ghost and ncells[0] <= 4096 and ncells[0] % 2 == 0 and ncells[1] % 4 == 0) \
+            if fused is None else fused
         with torch.cuda.stream(self.stream):
             self.level = api.Level(2, ncells, lower, dx, (1, 1), boxes, stream=self.stream)
             if self.level.info.nblocks != 1:
@@ -42,7 +45,8 @@ class UniformVlasov1D:
             self.C = self.level.field()
             self.U = self.level.field()
             self.E = [self.level.efield(), self.level.efield()]
-            self.rho = torch.zeros(ncells[0], dtype=torch.float64, device="cuda")
+            self.rhos = [torch.zeros(ncells[0], dtype=torch.float64, device="cuda") for _ in range(2)]
+            self.rho = self.rhos[0]
             self.f0v = torch.as_tensor(np.ascontiguousarray(f0v), dtype=torch.float64).cuda()
         self.graph = None
         self.dt = None
@@ -73,13 +77,20 @@ class UniformVlasov1D:
         return f_s, f_next, E_cur, E_bc
 
     def field_launch(self, s):
+        if self.fused:
+            return                                  # inside the stage kernel
         _, _, E_cur, _ = self.buffers(s)
         self.poisson.solve(self.rho, None, E_cur, 2)
 
     def stage_launch(self, s, dt):
         L = self.level.h
         f_s, f_next, E_cur, E_bc = self.buffers(s)
-        if self.self_ghost:
+        if self.fused:
+            # rho ping-pong: stage s reads the moment of f_s and writes the moment of f_next
+            rho_s, rho_n = (self.rhos[0], self.rhos[1]) if s % 2 == 1 else (self.rhos[1], self.rhos[0])
+            api.vlasov_rk4_stage_vp(L, self.poisson.h, s, dt, self.A, f_s, self.U, f_next, rho_s, E_cur, E_bc,
+                                    self.f0v, self.recon, rho_n)
+        elif self.self_ghost:
             api.vlasov_rk4_stage(L, s, dt, self.A, f_s, self.U, f_next, E_cur, E_bc, self.f0v, self.recon, self.rho)
         else:
             api.vlasov_fill_ghosts(L, f_s, None, None, E_bc, self.f0v)
@@ -111,7 +122,10 @@ class UniformVlasov1D:
             self.graph.replay()
 
     def launches_per_step(self) -> int:
-        # per stage: circulant (E with ghosts) + fused stage kernel  (+ 2 ghost-fill kernels)
+        # per stage: fused stage kernel (with the field solve when fused; else + circulant)
+        # (+ 2 ghost-fill kernels with stored ghosts)
+        if self.fused:
+            return 4
         return 4 * (2 if self.self_ghost else 4)
 
 

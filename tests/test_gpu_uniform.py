@@ -116,12 +116,12 @@ def test_fused_moment_equals_direct_moment(wname, shape):
     np.testing.assert_allclose(rho_direct.cpu().numpy(), ref, atol=1e-14)
 
 
-def _run_both(w, nsteps, recon=scheme.CENTERED4, boxes=None, graph=False, self_ghost=True):
+def _run_both(w, nsteps, recon=scheme.CENTERED4, boxes=None, graph=False, self_ghost=True, fused=None):
     h = inputs.spacing(w)
     dt = inputs.fixed_dt(w)
     f0 = inputs.initial_cell_averages(w)
     S = UniformVlasov1D(w.ncells, w.lower, h, boxes or inputs.level0_boxes(w), inputs.background_profile(w),
-                        RECON[recon], self_ghost=self_ghost)
+                        RECON[recon], self_ghost=self_ghost, fused=fused if self_ghost else False)
     S.set_state(f0)
     if graph:
         S.step(dt)
@@ -141,10 +141,14 @@ def _run_both(w, nsteps, recon=scheme.CENTERED4, boxes=None, graph=False, self_g
     return got, ref
 
 
-@pytest.mark.parametrize("self_ghost", [True, False])
+MODES = {"fused": dict(self_ghost=True, fused=True), "self": dict(self_ghost=True, fused=False),
+         "stored": dict(self_ghost=False)}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
-def test_c1_one_step(recon, self_ghost):
-    got, ref = _run_both(inputs.get("C1"), 1, recon, self_ghost=self_ghost)
+def test_c1_one_step(recon, mode):
+    got, ref = _run_both(inputs.get("C1"), 1, recon, **MODES[mode])
     assert relerr(got, ref) < 1e-12
 
 
@@ -158,17 +162,41 @@ def test_c1_fifty_steps_upwind_graph():
     assert relerr(got, ref) < 1e-10
 
 
-def test_c2_hundred_steps():
-    got, ref = _run_both(inputs.get("C2"), 100)
+@pytest.mark.parametrize("fused", [True, False])
+def test_c2_hundred_steps(fused):
+    got, ref = _run_both(inputs.get("C2"), 100, fused=fused)
     assert relerr(got, ref) < 1e-10
 
 
-@pytest.mark.parametrize("self_ghost", [True, False])
-def test_ragged_multi_tile_ten_steps(self_ghost):
+@pytest.mark.parametrize("mode", list(MODES))
+def test_ragged_multi_tile_ten_steps(mode):
     # 2 x 3 patches merged into one block, ragged tiles in both x (rows) and v (columns)
     w = inputs.scaled(inputs.get("C4"), (150, 600), (75, 200))
-    got, ref = _run_both(w, 10, self_ghost=self_ghost)
+    got, ref = _run_both(w, 10, **MODES[mode])
     assert relerr(got, ref) < 1e-11
+
+
+def test_fused_field_equals_poisson_solve():
+    """E written by the fused stage (vlasov_rk4_stage_vp) equals vlasov_poisson_solve of the same
+    moment, and the oracle's E of the stage state."""
+    w = inputs.scaled(inputs.get("C4"), (300, 1024), (300, 1024))
+    h = inputs.spacing(w)
+    S = UniformVlasov1D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w), fused=True)
+    f0 = inputs.initial_cell_averages(w)
+    S.set_state(f0)
+    with torch.cuda.stream(S.stream):
+        S._stage(1, inputs.fixed_dt(w))
+    S.stream.synchronize()
+    E_fused = S.E[1].cpu().numpy()
+    E_ref = torch.zeros_like(S.E[1])
+    S.poisson.solve(S.rhos[0], None, E_ref, 2)
+    torch.cuda.synchronize()
+    E_ref = E_ref.cpu().numpy()
+    np.testing.assert_allclose(E_fused, E_ref, rtol=0, atol=1e-13 * np.abs(E_ref).max())
+    E_or = field.efield_from_rho(field.moment_rho(f0, h[1]), h[0])
+    n = w.ncells[0]
+    cond = 64.0 / (30 - 32 * np.cos(2 * np.pi / n) + 2 * np.cos(4 * np.pi / n))   # as test_poisson_parity
+    np.testing.assert_allclose(E_fused[2:-2], E_or, rtol=0, atol=50 * np.finfo(float).eps * cond * np.abs(E_or).max())
 
 
 def test_c2_upwind_twenty_steps_stored_ghosts():
