@@ -1084,6 +1084,10 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
         gE[d] = (double)(aE / n);
         gphi[d] = (double)(aP / n);
     }
+    // gE is stored periodically extended (2n + 4 values, gE[j] = g[j mod n]) so that the fused
+    // stage kernel can read g[(i - k) mod n] = gE[i - k + n] without a modulo
+    gE.resize(2 * (size_t)n + 4);
+    for (size_t j = n; j < gE.size(); ++j) gE[j] = gE[j % n];
     vlasov_poisson* P = new vlasov_poisson();
     P->n = n;
     P->dx = dx;

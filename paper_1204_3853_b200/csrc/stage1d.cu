@@ -49,11 +49,20 @@ struct StageArgs1 {
     int cluster;               // CTAs per cluster of the fused launch (the v-tiles of a strip)
 };
 
-// shared memory of the fused field prologue: rho [n], extended g [2n + 4], row results [<= 4 NT]
-static size_t field_smem_bytes(int n, int nt) { return (size_t)(3 * n + 4 + 4 * nt) * sizeof(double); }
+// shared memory of the fused field prologue: rho [n], row results [<= 4 NT]
+static size_t field_smem_bytes(int n, int nt) { return (size_t)(n + 4 * nt) * sizeof(double); }
 
 // CPT = 4 cells per consumer thread, TV = 4*NT cells per v-tile.
-constexpr int CPT = 4;
+#ifndef STAGE1D_CPT
+#define STAGE1D_CPT 4
+#endif
+constexpr int CPT = STAGE1D_CPT;
+#ifndef STAGE1D_MINB
+#define STAGE1D_MINB 2
+#endif
+#ifndef RING_KB
+#define RING_KB 40
+#endif
 constexpr int NT_WIDE = 128, NT_NARROW = 32;   // consumer threads per CTA
 
 template <int STAGE, int NT>
@@ -62,8 +71,8 @@ struct StageGeom {
     static constexpr int SEG = TV + 4;                       // f_s row segment incl. 2+2 halo columns
     static constexpr int NFN = (STAGE >= 2 ? 1 : 0) + (STAGE == 4 ? 1 : 0);
     static constexpr int SLOT = SEG + NFN * TV;              // doubles per ring slot
-    // ring depth: ~40 KB of row data per CTA, 3..16 slots (a slot is consumed in one row step)
-    static constexpr int NSLOT_RAW = (40 * 1024) / (SLOT * 8);
+    // ring depth: ~RING_KB of row data per CTA, 3..16 slots (a slot is consumed in one row step)
+    static constexpr int NSLOT_RAW = (RING_KB * 1024) / (SLOT * 8);
     static constexpr int NSLOT = NSLOT_RAW < 3 ? 3 : (NSLOT_RAW > 16 ? 16 : NSLOT_RAW);
     static constexpr int NW = NT / 32;
     static size_t smem_bytes(int tile_rows) {
@@ -75,7 +84,7 @@ struct StageGeom {
 // the f_n / u rows are those of the output row i = r - 2 (q >= 4), so every slot is consumed
 // completely in its own row step and released at once.
 template <int STAGE, int RECON, int NT, bool SELF>
-__global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
+__global__ void __launch_bounds__(NT + 32, STAGE1D_MINB) k_stage_1d1v(const StageArgs1 A) {
     using SG = StageGeom<STAGE, NT>;
     constexpr int TV = SG::TV, SEG = SG::SEG, SLOT = SG::SLOT, NSLOT = SG::NSLOT, NW = SG::NW;
     constexpr bool NEED_FN = (STAGE >= 2);
@@ -124,15 +133,12 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
 
     // fused field: rho and the Green's function (twice: periodic extension) staged by the TMA engine
     double* f_rho = sEbc + (A.tile_rows + 4);
-    double* f_g = f_rho + A.dom_x;
     if (warp == NW) {                            // ---------------- producer warp
         if (lane == 0) {
             if (field) {
                 const uint32_t nb = (uint32_t)A.dom_x * 8u;
-                mbar_arrive_expect_tx(&field_bar, 3u * nb);
+                mbar_arrive_expect_tx(&field_bar, nb);
                 bulk_g2s(f_rho, A.rho_in, nb, &field_bar);
-                bulk_g2s(f_g, A.gE, nb, &field_bar);
-                bulk_g2s(f_g + A.dom_x, A.gE, nb, &field_bar);
             }
             const uint32_t seg_bytes = (uint32_t)(wpad + 4) * 8u;
             const uint32_t row_bytes = (uint32_t)wpad * 8u;
@@ -165,9 +171,7 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
         // tile, from rho and the periodically extended gE staged in shared memory by the TMA engine.
         const int n = A.dom_x;
         double* s_rho = f_rho;
-        double* s_g = f_g;                       // [2n + 4]
-        double* s_part = s_g + 2 * n + 4;        // [Q] E of the tile rows
-        if (tid < 4) s_g[2 * n + tid] = __ldg(A.gE + (tid % n));
+        double* s_part = s_rho + n;              // [Q] E of the tile rows
         mbar_wait(&field_bar, 0);
         double acc = 0.0;
         for (int k = tid; k < n; k += NT) acc += s_rho[k];
@@ -190,21 +194,21 @@ __global__ void __launch_bounds__(NT + 32, 2) k_stage_1d1v(const StageArgs1 A) {
             int gx = B.lo_x + T.x0 - 2 + t0;
             gx += (gx < 0) ? n : 0;
             gx -= (gx >= n) ? n : 0;
-            const double* gp = s_g + gx + n;                            // gp[j - k] = g[(gx + j - k) mod n]
+            const double* gp = A.gE + gx + n;                           // gp[j - k] = g[(gx + j - k) mod n] (L1)
             double a[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
             int k = lane;
             for (; k + 32 < n; k += 64) {
                 const double r0 = s_rho[k], r1 = s_rho[k + 32];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    a[0][j] = fma(gp[j - k], r0, a[0][j]);
-                    a[1][j] = fma(gp[j - k - 32], r1, a[1][j]);
+                    a[0][j] = fma(__ldg(gp + j - k), r0, a[0][j]);
+                    a[1][j] = fma(__ldg(gp + j - k - 32), r1, a[1][j]);
                 }
             }
             if (k < n) {
                 const double r0 = s_rho[k];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) a[0][j] = fma(gp[j - k], r0, a[0][j]);
+                for (int j = 0; j < 4; ++j) a[0][j] = fma(__ldg(gp + j - k), r0, a[0][j]);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
