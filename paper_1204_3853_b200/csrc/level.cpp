@@ -792,12 +792,13 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
             rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V: only levels whose boxes tile the whole domain");
         else if (L->field_doubles >= ((int64_t)1 << 31))
             rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V: level block larger than 2^31 doubles");
-        else if (L->dom[3] % 2 || L->dom[2] < 4 || L->dom[3] < 4)
-            rc = vk::fail(VLASOV_EINVAL, "2D+2V: need nvy even and at least 4 cells per velocity dim");
+        else if (L->dom[3] % 2 || L->dom[2] % 4 || L->dom[2] < 4 || L->dom[3] < 4)
+            rc = vk::fail(VLASOV_EINVAL, "2D+2V: need nvx % 4 == 0, nvy even and >= 4 cells per velocity dim");
         else {
-            const int nmt = (L->dom[3] / 2 + 31) / 32, nlg = (L->dom[2] + 3) / 4;
+            const int nmt = (L->dom[3] + 63) / 64, nlg = L->dom[2] / 4;   // CTA tile: 4 vx lines x 64 vy
             const int64_t per = (int64_t)nmt * nlg * L->dom[1];
-            L->strips2 = (int)std::max<int64_t>(1, std::min<int64_t>(L->dom[0] / 8, (148 * 6 + per - 1) / per));
+            // about one wave of 2 CTAs per SM, strips of at least 8 rows
+            L->strips2 = (int)std::max<int64_t>(1, std::min<int64_t>(L->dom[0] / 8, (148 * 2 + per - 1) / per));
             L->self_ghost_ok = true;
             L->n_vtiles = L->dom[2] * nmt;                 // moment partial planes
         }

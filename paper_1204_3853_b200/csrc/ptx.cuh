@@ -85,3 +85,14 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t 
                  ::"r"(raddr), "l"(__double_as_longlong(v)), "r"(rbar) : "memory");
 }
 }  // namespace vk
+
+namespace vk {
+// 4D tensor copy global -> shared::cta through the TMA unit (tensor map in param/const space);
+// coordinates innermost first; completion counted on `bar`.
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+        ::"r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)) : "memory");
+}
+}  // namespace vk

@@ -6,22 +6,52 @@
 // (dv_d/24); a velocity face along v_d carries one (1/48) product term per configuration dim.
 // Divergence of  f_t + div_x(v f) - div_v(E f) = 0  (reading #1).  Periodic x, y; the
 // characteristic condition on vx, vy (reading #6) is evaluated in the kernel, so the
-// level must be ONE block covering the periodic domain (SELF mode).
+// level must be ONE block covering the periodic domain (SELF mode) with nvx % 4 == 0.
 //
-// Layout: [x][y][vx][vy], vy contiguous, ghost frame 2 (never read).  Thread = (y = k, vx = l,
-// vy pair m0, m0+1); the CTA is 32 vy-pairs x 4 vx lines; every thread marches along x over a strip
-// of rows with register windows of the x-direction data (x-faces computed once per row) and of
-// the velocity-face averages of rows i-1, i, i+1 (x-transverse terms).  y-direction and vx +-2
-// neighbours are read through L1/L2 as 16-byte pairs.
+// Layout: [x][y][vx][vy], vy contiguous, ghost frame 2 (only addressed, never trusted).
+// CTA = one y line k, LT = 4 vx lines l0..l0+3 (one consumer warp each), a vy tile of TM = 64
+// cells (2 per lane), marching along x over a strip of rows, plus one producer warp.  Per row
+// step the producer streams into a 3-slot shared-memory ring with cp.async.bulk (TMA engine,
+// completion on mbarriers) every vy line segment (TM + 4 cells) the step needs:
+//   A  row r,  y = k,     vx lines l0-2 .. l0+5   (x window, velocity faces of row r)
+//   B  row i,  y = k -+ 1, vx lines l0-2 .. l0+5  (y-transverse velocity faces, y faces)
+//   C  row i,  y = k -+ 2, vx lines l0 .. l0+3    (y faces)
+//   D  row i,  y = k,     vx lines l0 .. l0+3     (y faces)
+//   F, U  f_n and u of the output row i = r - 2 (stages 2-4)
+// Consumers keep register windows along x (the x faces are computed once per row, the velocity
+// faces of rows i-1, i, i+1 are reused for the x-transverse terms) and read everything else from
+// shared memory.  Ghost values come from the characteristic condition: a ghost warp writes the
+// vy ghost columns into each landed slot (precomputed task descriptors), the consumers derive vx
+// ghost lines in registers on a warp-uniform path (CTAs at a vx boundary); E_bc and the profile
+// are staged in shared memory at kernel start.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "ptx.cuh"
 #include "scheme.cuh"
 
 namespace vk {
-#ifndef STAGE2D_MINB
-#define STAGE2D_MINB 2
+
+constexpr int S2_LT = 4;                  // vx lines (consumer warps) per CTA
+constexpr int S2_TM = 64;                 // vy cells per tile (2 per lane)
+constexpr int S2_LW = S2_TM + 4;          // doubles per line segment in a slot
+#ifndef S2_MAXNREG
+#define S2_MAXNREG 200
 #endif
+#ifndef S2_NSLOT_CFG
+#define S2_NSLOT_CFG 3
+#endif
+constexpr int S2_NSLOT = S2_NSLOT_CFG;
+constexpr int S2_NLINE = 8 + 16 + 8 + 4;  // A + B + C + D line segments per slot
+
+struct TMaps2 {                // TMA tensor maps over the ghosted level block [x][y][vx][vy]
+    CUtensorMap fs8;           // f_s, box (68 vy, 8 vx): parts A, B
+    CUtensorMap fs4;           // f_s, box (68 vy, 4 vx): parts C, D
+    CUtensorMap fn4;           // f_n, box (64 vy, 4 vx)
+    CUtensorMap u4;            // u,   box (64 vy, 4 vx)
+};
 
 struct StageArgs2 {
     const double* f_s;
@@ -35,165 +65,208 @@ struct StageArgs2 {
     double* partials;          // [nvx * n_mtiles][nx][ny] moment partials (nullable)
     int64_t s0, s1, s2;        // strides of x, y, vx (vy stride 1)
     int64_t org;               // index of interior cell (0,0,0,0)
-    int nx, ny, nvx, nvy, nrows, nstrips;
+    int nx, ny, nvx, nvy, nstrips;
     double dt, hx, hy, hvx, hvy, vx_lo, vy_lo;
 };
 
-// f at (i, k, l, m) with periodic x, y and the characteristic v-boundary condition
-__device__ __forceinline__ double f_at(const StageArgs2& A, int i, int k, int l, int m) {
-    i = (i < 0) ? i + A.nx : (i >= A.nx ? i - A.nx : i);
-    k = (k < 0) ? k + A.ny : (k >= A.ny ? k - A.ny : k);
-    const int64_t base = A.org + (int64_t)i * A.s0 + (int64_t)k * A.s1;
-    const int nyg = A.ny + 4;
-    if (l < 0 || l >= A.nvx) {               // vx ghost: a = -E_x(i, k)
-        const double a = -__ldg(A.E_bc + (int64_t)(i + 2) * nyg + (k + 2));
-        const bool lo = l < 0;
-        if (lo ? (a < 0.0) : (a > 0.0)) {
-            const int j0 = lo ? 0 : A.nvx - 1, dj = lo ? 1 : -1;
-            const double* p = A.f_s + base + m;
-            const double f0 = p[(int64_t)j0 * A.s2], f1 = p[(int64_t)(j0 + dj) * A.s2];
-            const double f2 = p[(int64_t)(j0 + 2 * dj) * A.s2], f3 = p[(int64_t)(j0 + 3 * dj) * A.s2];
-            const bool first = lo ? (l == -1) : (l == A.nvx);
-            return first ? 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3 : 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3;
-        }
-        return __ldg(A.f0v + (int64_t)(l + 2) * (A.nvy + 4) + (m + 2));
+template <int STAGE>
+struct Slot2 {
+    static constexpr int NFU = (STAGE >= 2 ? 1 : 0) + (STAGE == 4 ? 1 : 0);
+    static constexpr int SIZE = S2_NLINE * S2_LW + NFU * S2_LT * S2_TM;   // doubles (multiple of 16: 128-B parts)
+    static size_t smem_bytes(int qmax) {
+        return ((size_t)S2_NSLOT * SIZE + 10 * (size_t)qmax + 32 + 4 * S2_TM) * sizeof(double);  // ring + staging
     }
-    if (m < 0 || m >= A.nvy) {               // vy ghost: a = -E_y(i, k)
-        const double a = -__ldg(A.E_bc + (int64_t)(A.nx + 4) * nyg + (int64_t)(i + 2) * nyg + (k + 2));
-        const bool lo = m < 0;
-        if (lo ? (a < 0.0) : (a > 0.0)) {
-            const int j0 = lo ? 0 : A.nvy - 1, dj = lo ? 1 : -1;
-            const double* p = A.f_s + base + (int64_t)l * A.s2;
-            const double f0 = p[j0], f1 = p[j0 + dj], f2 = p[j0 + 2 * dj], f3 = p[j0 + 3 * dj];
-            const bool first = lo ? (m == -1) : (m == A.nvy);
-            return first ? 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3 : 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3;
-        }
-        return __ldg(A.f0v + (int64_t)(l + 2) * (A.nvy + 4) + (m + 2));
-    }
-    return __ldg(A.f_s + base + (int64_t)l * A.s2 + m);
-}
+};
 
-// pair (m, m+1), m even
-__device__ __forceinline__ double2 f2_at(const StageArgs2& A, int i, int k, int l, int m) {
-    if (l >= 0 && l < A.nvx && m >= 0 && m + 1 < A.nvy) {
-        i = (i < 0) ? i + A.nx : (i >= A.nx ? i - A.nx : i);
-        k = (k < 0) ? k + A.ny : (k >= A.ny ? k - A.ny : k);
-        return __ldg(reinterpret_cast<const double2*>(A.f_s + A.org + (int64_t)i * A.s0 + (int64_t)k * A.s1 +
-                                                      (int64_t)l * A.s2 + m));
-    }
-    return make_double2(f_at(A, i, k, l, m), f_at(A, i, k, l, m + 1));
-}
-
-// Unconditional 16-byte load of the pair (m, m+1) at clamped velocity indices (always a valid
-// interior address, so the loads of a row step issue back to back); `fix` tells whether the pair
-// holds ghost values that must be recomputed with f_at (rare: velocity-boundary threads only).
-__device__ __forceinline__ double2 ld2(const StageArgs2& A, int i, int k, int l, int m, bool& fix) {
-    fix = (l < 0) | (l >= A.nvx);            // vx ghosts: warp-uniform (whole vx line)
-    i += (i < 0) ? A.nx : 0;
-    i -= (i >= A.nx) ? A.nx : 0;
-    k += (k < 0) ? A.ny : 0;
-    k -= (k >= A.ny) ? A.ny : 0;
-    const int lc = min(max(l, 0), A.nvx - 1), mc = min(max(m, 0), A.nvy - 2);
-    return __ldg(reinterpret_cast<const double2*>(A.f_s + A.org + (int64_t)i * A.s0 + (int64_t)k * A.s1 +
-                                                  (int64_t)lc * A.s2 + mc));
-}
-
-// vx-ghost pair through the characteristic boundary condition: out of line (rare, warp-uniform
-// path) so that the unrolled row steps stay small enough for the instruction cache
-__device__ __noinline__ double2 fix_pair(const StageArgs2& A, int i, int k, int l, int m) {
-    return make_double2(f_at(A, i, k, l, m), f_at(A, i, k, l, m + 1));
-}
-
-// a batch of N pair loads (i, k[n], l[n], m[n]) followed by the ghost fix-up
-template <int N>
-__device__ __forceinline__ void ld2_batch(const StageArgs2& A, int i, const int (&k)[N], const int (&l)[N],
-                                          const int (&m)[N], double2 (&out)[N]) {
-    bool fix[N];
-#pragma unroll
-    for (int n = 0; n < N; ++n) out[n] = ld2(A, i, k[n], l[n], m[n], fix[n]);
-#pragma unroll
-    for (int n = 0; n < N; ++n)
-        if (fix[n]) out[n] = fix_pair(A, i, k[n], l[n], m[n]);
-}
-
-// vy ghosts of a line triple (pl, pc, ph) = pairs at (m0-2, m0), (m0, m0+1), (m0+2, m0+3) of line
-// (i, k, l): the edge lanes replace pl (m0 == 0) or ph (m0 + 2 == nvy) by the characteristic
-// condition with a = -E_y(i, k) (warp-uniform), from the interior values they hold already.
-__device__ __forceinline__ void vy_fix(const StageArgs2& A, int i, int k, int l, int m0, double2& pl, const double2& pc,
-                                       double2& ph) {
-    const bool lo = (m0 == 0), hi = (m0 + 2 == A.nvy);
-    if (!(lo || hi)) return;
-    i += (i < 0) ? A.nx : 0;
-    i -= (i >= A.nx) ? A.nx : 0;
-    k += (k < 0) ? A.ny : 0;
-    k -= (k >= A.ny) ? A.ny : 0;
-    const int nyg = A.ny + 4;
-    const double a = -__ldg(A.E_bc + (int64_t)(A.nx + 4) * nyg + (int64_t)(i + 2) * nyg + (k + 2));
-    const double* prof = A.f0v + (int64_t)(l + 2) * (A.nvy + 4);
-    if (lo) {
-        if (a < 0.0) {
-            const double f0 = pc.x, f1 = pc.y, f2 = ph.x, f3 = ph.y;
-            pl = make_double2(10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3, 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3);
-        } else {
-            pl = make_double2(__ldg(prof + 0), __ldg(prof + 1));
-        }
-    }
-    if (hi) {
-        if (a > 0.0) {
-            const double f0 = pc.y, f1 = pc.x, f2 = pl.y, f3 = pl.x;
-            ph = make_double2(4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3, 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3);
-        } else {
-            ph = make_double2(__ldg(prof + A.nvy + 2), __ldg(prof + A.nvy + 3));
-        }
-    }
+__device__ __forceinline__ int wrapi(int i, int n) {
+    i += (i < 0) ? n : 0;
+    i -= (i >= n) ? n : 0;
+    return i;
 }
 
 template <int STAGE, int RECON>
-__global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArgs2 A) {
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int m0 = 2 * (blockIdx.x * 32 + tx);
-    const int l = blockIdx.y * 4 + ty;
-    const int k = blockIdx.z % A.ny;
-    const int strip = blockIdx.z / A.ny;
+__global__ void __launch_bounds__(32 * (S2_LT + 2), 2) k_stage_2d2v(const StageArgs2 A, const __grid_constant__ TMaps2 M) {
+    using SL = Slot2<STAGE>;
+    constexpr int SIZE = SL::SIZE;
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) uint64_t full_bar[S2_NSLOT];    // TMA landed (producer -> ghost warp)
+    __shared__ __align__(8) uint64_t ready_bar[S2_NSLOT];   // vy ghosts derived (ghost warp -> consumers)
+    __shared__ __align__(8) uint64_t empty_bar[S2_NSLOT];   // slot consumed (consumers -> producer)
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int mt = blockIdx.x, l0 = blockIdx.y * S2_LT;
+    const int k = blockIdx.z % A.ny, strip = blockIdx.z / A.ny;
     const int x0 = (int)((int64_t)A.nx * strip / A.nstrips);
     const int x1 = (int)((int64_t)A.nx * (strip + 1) / A.nstrips);
-    const bool act = (m0 < A.nvy) && (l < A.nvx);
-    const int mc = act ? m0 : 0, lc = (l < A.nvx) ? l : 0;     // clamped for inactive threads
+    const int Q = (x1 - x0) + 4;
+    const int ncols = min(S2_TM, A.nvy - mt * S2_TM);           // vy cells of this tile
+    const int wpad = (ncols + 1) & ~1;
     const int nyg = A.ny + 4;
     const int64_t ecomp = (int64_t)(A.nx + 4) * nyg;
-    auto Ex = [&](int i, int kk) { return __ldg(A.E + (int64_t)(i + 2) * nyg + (kk + 2)); };
-    auto Ey = [&](int i, int kk) { return __ldg(A.E + ecomp + (int64_t)(i + 2) * nyg + (kk + 2)); };
-    // per-thread constant load offsets (doubles): y lines k-2..k+2 (periodic), vx lines l-2..l+2
-    // (clamped: out-of-range lines are recomputed by the boundary condition), vy pairs
-    int ko[5];                       // 32-bit offsets: one block of a C5-sized level is < 2^31 doubles
-    int lo5[5];
-#pragma unroll
-    for (int d = 0; d < 5; ++d) {
-        int kk = k - 2 + d;
-        kk += (kk < 0) ? A.ny : 0;
-        kk -= (kk >= A.ny) ? A.ny : 0;
-        ko[d] = kk * (int)A.s1;
-        lo5[d] = min(max(lc - 2 + d, 0), A.nvx - 1) * (int)A.s2;
+
+    if (tid == 0) {
+        for (int s = 0; s < S2_NSLOT; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&ready_bar[s], 32);
+            mbar_init(&empty_bar[s], S2_LT);
+        }
+        fence_mbar_init();
     }
-    const int mlo = max(mc - 2, 0), mhi = min(mc + 2, A.nvy - 2);
-    const bool l_edge = (lc < 2) || (lc + 2 >= A.nvx);            // warp-uniform
-    const bool m_edge = (mc == 0) || (mc + 2 == A.nvy);            // lanes at the vy boundary
-    const double* fbase = A.f_s + A.org;
-    auto P = [&](const double* rowp, int d, int e, int m) {
-        return __ldg(reinterpret_cast<const double2*>(rowp + (ko[d] + lo5[e] + m)));
-    };
-    auto rowptr = [&](int r) {
-        r += (r < 0) ? A.nx : 0;
-        r -= (r >= A.nx) ? A.nx : 0;
-        return fbase + (int64_t)r * A.s0;
-    };
+    // Stage what the ghost values need besides the slots: E_bc (x, y components) of the strip's
+    // rows at y = k-2 .. k+2, the unperturbed profile at the vy ghost cells of the CTA's vx lines
+    // and at the vx ghost lines (characteristic condition, reading #6).
+    double* gE = smem + S2_NSLOT * SIZE;                          // [Q][5][2]
+    double* gPv = gE + 10 * Q;                                    // [8 lines l0-2+L][4]: m = -2, -1, nvy, nvy+1
+    double* gPx = gPv + 32;                                       // [4][TM]: vx lines -2, -1, nvx, nvx+1
+    for (int t = tid; t < 5 * Q; t += blockDim.x) {
+        const int tq = t / 5, dy = t % 5;
+        const int xx = wrapi(x0 - 2 + tq, A.nx), yy = wrapi(k - 2 + dy, A.ny);
+        gE[2 * t] = __ldg(A.E_bc + (int64_t)(xx + 2) * nyg + (yy + 2));
+        gE[2 * t + 1] = __ldg(A.E_bc + ecomp + (int64_t)(xx + 2) * nyg + (yy + 2));
+    }
+    if (tid < 32) {
+        const int Lg = tid >> 2, which = tid & 3;
+        const int ll = min(max(l0 - 2 + Lg, 0), A.nvx - 1);
+        const int mm = which < 2 ? which : A.nvy + which;
+        gPv[tid] = __ldg(A.f0v + (int64_t)(ll + 2) * (A.nvy + 4) + mm);
+    }
+    for (int t = tid; t < 4 * S2_TM; t += blockDim.x) {
+        const int g = t / S2_TM, c = t % S2_TM;
+        const int lg = g < 2 ? g - 2 : A.nvx + (g - 2);
+        const int m = min(mt * S2_TM + c, A.nvy - 1);
+        gPx[t] = __ldg(A.f0v + (int64_t)(lg + 2) * (A.nvy + 4) + (m + 2));
+    }
+    __syncthreads();
+
+    if (warp == S2_LT) {                                          // ---------------- producer warp
+        // 6-8 tensor copies per row step (coordinates in the ghosted block: +2 per dim; x and y
+        // wrapped periodically; out-of-range vx / vy boxes are zero-filled by the TMA unit)
+        if (lane == 0) {
+            constexpr uint32_t BA = 8 * S2_LW * 8, BC = 4 * S2_LW * 8, BF = 4 * S2_TM * 8;
+            int slot = 0;
+            uint32_t phase = 0;
+            const int cm = mt * S2_TM;                                  // ghosted vy coord of m = mt*TM - 2
+            for (int q = 0; q < Q; ++q) {
+                if (q >= S2_NSLOT) mbar_wait(&empty_bar[slot], phase ^ 1u);
+                const bool out_row = q >= 4;
+                const int r = wrapi(x0 - 2 + q, A.nx), i = wrapi(x0 - 4 + q, A.nx);
+                double* dst = smem + slot * SIZE;
+                uint64_t* fb = &full_bar[slot];
+                mbar_arrive_expect_tx(fb, out_row ? 3 * BA + 3 * BC + SL::NFU * BF : BA);
+                tma_load_4d(dst, &M.fs8, cm, l0, k + 2, r + 2, fb);                              // A
+                if (out_row) {
+                    const int km = wrapi(k - 1, A.ny), kp = wrapi(k + 1, A.ny);
+                    const int kmm = wrapi(k - 2, A.ny), kpp = wrapi(k + 2, A.ny);
+                    tma_load_4d(dst + 8 * S2_LW, &M.fs8, cm, l0, km + 2, i + 2, fb);              // B0
+                    tma_load_4d(dst + 16 * S2_LW, &M.fs8, cm, l0, kp + 2, i + 2, fb);             // B1
+                    tma_load_4d(dst + 24 * S2_LW, &M.fs4, cm, l0 + 2, kmm + 2, i + 2, fb);        // C0
+                    tma_load_4d(dst + 28 * S2_LW, &M.fs4, cm, l0 + 2, kpp + 2, i + 2, fb);        // C1
+                    tma_load_4d(dst + 32 * S2_LW, &M.fs4, cm, l0 + 2, k + 2, i + 2, fb);          // D
+                    if (SL::NFU >= 1)
+                        tma_load_4d(dst + S2_NLINE * S2_LW, &M.fn4, cm + 2, l0 + 2, k + 2, i + 2, fb);   // F
+                    if (SL::NFU >= 2)
+                        tma_load_4d(dst + S2_NLINE * S2_LW + S2_LT * S2_TM, &M.u4, cm + 2, l0 + 2, k + 2, i + 2, fb);  // U
+                }
+                if (++slot == S2_NSLOT) { slot = 0; phase ^= 1u; }
+            }
+        }
+        return;
+    }
+
+    if (warp == S2_LT + 1) {                                      // ---------------- ghost warp
+        // vy ghost columns of the 24 line segments the consumers read as (m0-2 .. m0+3) triples
+        // (A, B lines 2..5; C, D lines 0..3), characteristic condition (reading #6) with E_bc of
+        // the segment's (x, y); task descriptors precomputed, <= 2 tasks per lane per slot.
+        const bool vlo = (mt == 0), vhi = (mt * S2_TM + ncols == A.nvy);
+        int seg[2], side[2], dq[2], dy[2];
+        bool valid[2];
+        double p0[2], p1[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int t = lane + 32 * j;                          // task: 24 segments x 2 sides
+            const int sidx = t >> 1, sd = t & 1;
+            int e, ddq, ddy, ll;
+            if (sidx < 4) { e = 2 + sidx; ddq = 0; ddy = 2; ll = l0 + sidx; }
+            else if (sidx < 8) { e = 10 + (sidx - 4); ddq = 2; ddy = 1; ll = l0 + sidx - 4; }
+            else if (sidx < 12) { e = 18 + (sidx - 8); ddq = 2; ddy = 3; ll = l0 + sidx - 8; }
+            else if (sidx < 16) { e = 24 + (sidx - 12); ddq = 2; ddy = 0; ll = l0 + sidx - 12; }
+            else if (sidx < 20) { e = 28 + (sidx - 16); ddq = 2; ddy = 4; ll = l0 + sidx - 16; }
+            else { e = 32 + (sidx - 20); ddq = 2; ddy = 2; ll = l0 + sidx - 20; }
+            seg[j] = e; side[j] = sd; dq[j] = ddq; dy[j] = ddy;
+            valid[j] = (t < 48) && (ll < A.nvx) && (sd == 0 ? vlo : vhi);
+            const int llc = min(ll, A.nvx - 1);
+            p0[j] = __ldg(A.f0v + (int64_t)(llc + 2) * (A.nvy + 4) + (sd == 0 ? 0 : A.nvy + 2));
+            p1[j] = __ldg(A.f0v + (int64_t)(llc + 2) * (A.nvy + 4) + (sd == 0 ? 1 : A.nvy + 3));
+        }
+        int slot = 0;
+        uint32_t phase = 0;
+        for (int q = 0; q < Q; ++q) {
+            mbar_wait(&full_bar[slot], phase);
+            double* S = smem + slot * SIZE;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (!valid[j] || (dq[j] && q < 4)) continue;
+                double* sg = S + seg[j] * S2_LW;
+                const double a = -gE[2 * (5 * (q - dq[j]) + dy[j]) + 1];
+                if (side[j] == 0) {                               // m = -2, -1 at columns 0, 1
+                    const double f0 = sg[2], f1 = sg[3], f2 = sg[4], f3 = sg[5];
+                    const bool out = a < 0.0;
+                    sg[1] = out ? 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3 : p1[j];
+                    sg[0] = out ? 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3 : p0[j];
+                } else {                                          // m = nvy, nvy+1
+                    const int c = ncols + 1;                      // column of m = nvy - 1
+                    const double f0 = sg[c], f1 = sg[c - 1], f2 = sg[c - 2], f3 = sg[c - 3];
+                    const bool out = a > 0.0;
+                    sg[c + 1] = out ? 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3 : p0[j];
+                    sg[c + 2] = out ? 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3 : p1[j];
+                }
+            }
+            mbar_arrive(&ready_bar[slot]);                        // release: this lane's writes
+            if (++slot == S2_NSLOT) { slot = 0; phase ^= 1u; }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int w = warp, l = l0 + w;
+    const bool lact = l < A.nvx;
+    const int lc = lact ? l : A.nvx - 1;
+    const int cl = 2 * lane + 2;                                  // slot column of my first cell
+    const int m0 = mt * S2_TM + 2 * lane;
+    const bool act = lact && (2 * lane < ncols);
+    auto Ex = [&](int ii, int kk) { return __ldg(A.E + (int64_t)(ii + 2) * nyg + (kk + 2)); };
+    auto Ey = [&](int ii, int kk) { return __ldg(A.E + ecomp + (int64_t)(ii + 2) * nyg + (kk + 2)); };
     const double vbx = A.vx_lo + ((double)lc + 0.5) * A.hvx;
     const double vbxm = vbx - A.hvx, vbxp = vbx + A.hvx;
-    double vby[4];                                     // m0-1 .. m0+2
+    double vby[4];                                                // m0-1 .. m0+2
 #pragma unroll
-    for (int a = 0; a < 4; ++a) vby[a] = A.vy_lo + ((double)(mc + a - 1) + 0.5) * A.hvy;
+    for (int a = 0; a < 4; ++a) vby[a] = A.vy_lo + ((double)(m0 + a - 1) + 0.5) * A.hvy;
     const double rdx = 1.0 / A.hx, rdy = 1.0 / A.hy, rdvx = 1.0 / A.hvx, rdvy = 1.0 / A.hvy;
     const double dvx24 = A.hvx * (1.0 / 24.0), dvy24 = A.hvy * (1.0 / 24.0);
+
+    const bool ledge = (l0 == 0) || (l0 + S2_LT >= A.nvx);            // CTA at a vx boundary (uniform)
+    // pair (col) of line L of a part; vx ghost lines (warp-uniform) by the characteristic
+    // condition from the part's interior lines, a = -E_x of the part's (x, y)
+    auto line_pair = [&](const double* part, int L, double a) -> double2 {
+        const int lg = l0 - 2 + L;
+        if (ledge && (lg < 0 || lg >= A.nvx)) {
+            const bool lo = lg < 0;
+            if (lo ? (a < 0.0) : (a > 0.0)) {
+                const int j0 = lo ? 0 : A.nvx - 1, dj = lo ? 1 : -1;
+                const double2 f0 = lds2(part + (j0 - l0 + 2) * S2_LW + cl), f1 = lds2(part + (j0 + dj - l0 + 2) * S2_LW + cl);
+                const double2 f2 = lds2(part + (j0 + 2 * dj - l0 + 2) * S2_LW + cl);
+                const double2 f3 = lds2(part + (j0 + 3 * dj - l0 + 2) * S2_LW + cl);
+                if (lo ? (lg == -1) : (lg == A.nvx))
+                    return make_double2(4.0 * f0.x - 6.0 * f1.x + 4.0 * f2.x - f3.x, 4.0 * f0.y - 6.0 * f1.y + 4.0 * f2.y - f3.y);
+                return make_double2(10.0 * f0.x - 20.0 * f1.x + 15.0 * f2.x - 4.0 * f3.x,
+                                    10.0 * f0.y - 20.0 * f1.y + 15.0 * f2.y - 4.0 * f3.y);
+            }
+            const double* px = gPx + (lo ? lg + 2 : 2 + lg - A.nvx) * S2_TM + 2 * lane;
+            return make_double2(px[0], px[1]);
+        }
+        return lds2(part + L * S2_LW + cl);
+    };
+    auto Ebx = [&](int tq, int dy) { return gE[2 * (5 * tq + dy)]; };
 
     double W[4][3][2];        // f rows (mod 4) at vx lines l-1, l, l+1, vy m0, m0+1
     double VX[4][2][2];       // vx-face averages (rows mod 4) at l-1/2, l+1/2
@@ -205,41 +278,42 @@ __global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArg
         for (int b = 0; b < 3; ++b) { W[a][b][0] = W[a][b][1] = 0.0; VY[a][b] = 0.0; }
         VX[a][0][0] = VX[a][0][1] = VX[a][1][0] = VX[a][1][1] = 0.0;
     }
-    const int Q = (x1 - x0) + 4;
+    int slot = 0;
+    uint32_t phase = 0;
     for (int q0 = 0; q0 < Q; q0 += 4) {
 #pragma unroll
         for (int K = 0; K < 4; ++K) {
             const int q = q0 + K;
             if (q < Q) {
-                const int r = x0 - 2 + q;
-                // ---- row r: x-window, vx-faces, vy-faces
-                const double* rp = rowptr(r);
-                double2 c01 = P(rp, 2, 2, mlo), c23 = P(rp, 2, 2, mc), c45 = P(rp, 2, 2, mhi);
-                double2 am1 = P(rp, 2, 1, mc), ap1 = P(rp, 2, 3, mc), am2 = P(rp, 2, 0, mc), ap2 = P(rp, 2, 4, mc);
-                if (l_edge) {
-                    if (lc - 2 < 0) am2 = fix_pair(A, r, k, lc - 2, mc);
-                    if (lc - 1 < 0) am1 = fix_pair(A, r, k, lc - 1, mc);
-                    if (lc + 1 >= A.nvx) ap1 = fix_pair(A, r, k, lc + 1, mc);
-                    if (lc + 2 >= A.nvx) ap2 = fix_pair(A, r, k, lc + 2, mc);
-                }
-                if (m_edge) vy_fix(A, r, k, lc, mc, c01, c23, c45);
+                const int r = wrapi(x0 - 2 + q, A.nx);
+                mbar_wait(&ready_bar[slot], phase);
+                const double* SA = smem + slot * SIZE;
+                const double* SB = SA + 8 * S2_LW;
+                const double* SC = SB + 16 * S2_LW;
+                const double* SD = SC + 8 * S2_LW;
+                const double* SF = SA + S2_NLINE * S2_LW;
+                const double* SU = SF + S2_LT * S2_TM;
+                // ---- row r: x window, vx faces, vy faces
+                const double axr = -Ebx(q, 2);
+                double2 c01 = lds2(SA + (w + 2) * S2_LW + cl - 2), c23 = lds2(SA + (w + 2) * S2_LW + cl),
+                        c45 = lds2(SA + (w + 2) * S2_LW + cl + 2);
+                const double2 am1 = line_pair(SA, w + 1, axr), ap1 = line_pair(SA, w + 3, axr);
+                const double2 am2 = line_pair(SA, w, axr), ap2 = line_pair(SA, w + 4, axr);
                 W[K][0][0] = am1.x; W[K][0][1] = am1.y;
                 W[K][1][0] = c23.x; W[K][1][1] = c23.y;
                 W[K][2][0] = ap1.x; W[K][2][1] = ap1.y;
                 {
-                    const double ax = -Ex(r, k);
+                    const double ax = -Ex(r, k), ay = -Ey(r, k);
                     VX[K][0][0] = face_avg<RECON>(am2.x, am1.x, c23.x, ap1.x, ax);
                     VX[K][0][1] = face_avg<RECON>(am2.y, am1.y, c23.y, ap1.y, ax);
                     VX[K][1][0] = face_avg<RECON>(am1.x, c23.x, ap1.x, ap2.x, ax);
                     VX[K][1][1] = face_avg<RECON>(am1.y, c23.y, ap1.y, ap2.y, ax);
-                    const double ay = -Ey(r, k);
                     VY[K][0] = face_avg<RECON>(c01.x, c01.y, c23.x, c23.y, ay);
                     VY[K][1] = face_avg<RECON>(c01.y, c23.x, c23.y, c45.x, ay);
                     VY[K][2] = face_avg<RECON>(c23.x, c23.y, c45.x, c45.y, ay);
                 }
                 const int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;   // rows r-3, r-2, r-1
                 if (q >= 3) {
-                    // x-faces at (r-2)+1/2 from rows r-3..r, lines l-1, l, l+1
                     double XF[3][2];
 #pragma unroll
                     for (int b = 0; b < 3; ++b)
@@ -251,85 +325,62 @@ __global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArg
 #pragma unroll
                     for (int mm = 0; mm < 2; ++mm) Fxn[mm] = vbx * XF[1][mm] + dvx24 * (XF[2][mm] - XF[0][mm]);
                     if (q >= 4) {
-                        const int i = r - 2;
-                        // ---- y-faces at (i, k -+ 1/2) for vy m0-1 .. m0+2
-                        // loads of row i: lines k-2..k+2 at (l, m0-2..m0+3), lines k-+1 at l-+1, l-+2
-                        const double* ip = rowptr(i);
-                        double2 yy[23];
+                        const int i = wrapi(x0 - 4 + q, A.nx);
+                        // ---- y faces at (i, k -+ 1/2) for vy m0-1 .. m0+2 (lines k-2 .. k+2)
+                        double2 t[5][3];
+                        const double* yl[5] = {SC + w * S2_LW, SB + (w + 2) * S2_LW, SD + w * S2_LW,
+                                               SB + (8 + w + 2) * S2_LW, SC + (4 + w) * S2_LW};
 #pragma unroll
                         for (int d = 0; d < 5; ++d) {
-                            yy[3 * d] = P(ip, d, 2, mlo);
-                            yy[3 * d + 1] = P(ip, d, 2, mc);
-                            yy[3 * d + 2] = P(ip, d, 2, mhi);
-                        }
-#pragma unroll
-                        for (int sg = 0; sg < 2; ++sg) {          // lines k-1 (sg 0), k+1 (sg 1) at l-1, l+1, l-2, l+2
-                            const int d = sg ? 3 : 1;
-                            yy[15 + 4 * sg] = P(ip, d, 1, mc);
-                            yy[16 + 4 * sg] = P(ip, d, 3, mc);
-                            yy[17 + 4 * sg] = P(ip, d, 0, mc);
-                            yy[18 + 4 * sg] = P(ip, d, 4, mc);
-                        }
-                        if (l_edge) {
-#pragma unroll
-                            for (int sg = 0; sg < 2; ++sg) {
-                                const int kk = k + (sg ? 1 : -1);
-                                if (lc - 1 < 0) yy[15 + 4 * sg] = fix_pair(A, i, kk, lc - 1, mc);
-                                if (lc + 1 >= A.nvx) yy[16 + 4 * sg] = fix_pair(A, i, kk, lc + 1, mc);
-                                if (lc - 2 < 0) yy[17 + 4 * sg] = fix_pair(A, i, kk, lc - 2, mc);
-                                if (lc + 2 >= A.nvx) yy[18 + 4 * sg] = fix_pair(A, i, kk, lc + 2, mc);
-                            }
-                        }
-                        if (m_edge) {
-#pragma unroll
-                            for (int d = 0; d < 5; ++d) vy_fix(A, i, k - 2 + d, lc, mc, yy[3 * d], yy[3 * d + 1], yy[3 * d + 2]);
-                        }
-                        double y[5][4];
-#pragma unroll
-                        for (int d = 0; d < 5; ++d) {
-                            const double2 pl = yy[3 * d], pc = yy[3 * d + 1], ph = yy[3 * d + 2];
-                            y[d][0] = pl.y; y[d][1] = pc.x; y[d][2] = pc.y; y[d][3] = ph.x;
+                            t[d][0] = lds2(yl[d] + cl - 2);
+                            t[d][1] = lds2(yl[d] + cl);
+                            t[d][2] = lds2(yl[d] + cl + 2);
                         }
                         double YL[4], YH[4];
 #pragma unroll
                         for (int a = 0; a < 4; ++a) {
-                            YL[a] = face_avg<RECON>(y[0][a], y[1][a], y[2][a], y[3][a], vby[a]);
-                            YH[a] = face_avg<RECON>(y[1][a], y[2][a], y[3][a], y[4][a], vby[a]);
+                            double y5[5];
+#pragma unroll
+                            for (int d = 0; d < 5; ++d)
+                                y5[d] = (a == 0) ? t[d][0].y : (a == 1) ? t[d][1].x : (a == 2) ? t[d][1].y : t[d][2].x;
+                            YL[a] = face_avg<RECON>(y5[0], y5[1], y5[2], y5[3], vby[a]);
+                            YH[a] = face_avg<RECON>(y5[1], y5[2], y5[3], y5[4], vby[a]);
                         }
                         // ---- y-transverse velocity-face averages at (i, k -+ 1)
                         double VXk[2][2][2], VYk[2][3];
 #pragma unroll
-                        for (int sgn = 0; sgn < 2; ++sgn) {
-                            const int kk = k + (sgn ? 1 : -1);
-                            const int yb = sgn ? 9 : 3, nb = sgn ? 19 : 15;
-                            const double2 b01 = yy[yb], b23 = yy[yb + 1], b45 = yy[yb + 2];
-                            const double2 bm1 = yy[nb], bp1 = yy[nb + 1], bm2 = yy[nb + 2], bp2 = yy[nb + 3];
+                        for (int sg = 0; sg < 2; ++sg) {
+                            const int kk = wrapi(k + (sg ? 1 : -1), A.ny);
+                            const double* P = SB + sg * 8 * S2_LW;
+                            const double axk = -Ebx(q - 2, sg ? 3 : 1);
+                            const double2 bm1 = line_pair(P, w + 1, axk), bp1 = line_pair(P, w + 3, axk);
+                            const double2 bm2 = line_pair(P, w, axk), bp2 = line_pair(P, w + 4, axk);
+                            const double2 b01 = t[sg ? 3 : 1][0], b23 = t[sg ? 3 : 1][1], b45 = t[sg ? 3 : 1][2];
                             const double ax = -Ex(i, kk), ay = -Ey(i, kk);
-                            VXk[sgn][0][0] = face_avg<RECON>(bm2.x, bm1.x, b23.x, bp1.x, ax);
-                            VXk[sgn][0][1] = face_avg<RECON>(bm2.y, bm1.y, b23.y, bp1.y, ax);
-                            VXk[sgn][1][0] = face_avg<RECON>(bm1.x, b23.x, bp1.x, bp2.x, ax);
-                            VXk[sgn][1][1] = face_avg<RECON>(bm1.y, b23.y, bp1.y, bp2.y, ax);
-                            VYk[sgn][0] = face_avg<RECON>(b01.x, b01.y, b23.x, b23.y, ay);
-                            VYk[sgn][1] = face_avg<RECON>(b01.y, b23.x, b23.y, b45.x, ay);
-                            VYk[sgn][2] = face_avg<RECON>(b23.x, b23.y, b45.x, b45.y, ay);
+                            VXk[sg][0][0] = face_avg<RECON>(bm2.x, bm1.x, b23.x, bp1.x, ax);
+                            VXk[sg][0][1] = face_avg<RECON>(bm2.y, bm1.y, b23.y, bp1.y, ax);
+                            VXk[sg][1][0] = face_avg<RECON>(bm1.x, b23.x, bp1.x, bp2.x, ax);
+                            VXk[sg][1][1] = face_avg<RECON>(bm1.y, b23.y, bp1.y, bp2.y, ax);
+                            VYk[sg][0] = face_avg<RECON>(b01.x, b01.y, b23.x, b23.y, ay);
+                            VYk[sg][1] = face_avg<RECON>(b01.y, b23.x, b23.y, b45.x, ay);
+                            VYk[sg][2] = face_avg<RECON>(b23.x, b23.y, b45.x, b45.y, ay);
                         }
+                        const int ip = wrapi(i + 1, A.nx), im = wrapi(i - 1, A.nx);
+                        const int kp = wrapi(k + 1, A.ny), km = wrapi(k - 1, A.ny);
                         const double exi = Ex(i, k), eyi = Ey(i, k);
-                        const double cxi = (Ex(i + 1, k) - Ex(i - 1, k)) * (1.0 / 48.0);
-                        const double cxk = (Ex(i, k + 1) - Ex(i, k - 1)) * (1.0 / 48.0);
-                        const double cyi = (Ey(i + 1, k) - Ey(i - 1, k)) * (1.0 / 48.0);
-                        const double cyk = (Ey(i, k + 1) - Ey(i, k - 1)) * (1.0 / 48.0);
+                        const double cxi = (Ex(ip, k) - Ex(im, k)) * (1.0 / 48.0);
+                        const double cxk = (Ex(i, kp) - Ex(i, km)) * (1.0 / 48.0);
+                        const double cyi = (Ey(ip, k) - Ey(im, k)) * (1.0 / 48.0);
+                        const double cyk = (Ey(i, kp) - Ey(i, km)) * (1.0 / 48.0);
                         double Fvy[3];
 #pragma unroll
                         for (int fc = 0; fc < 3; ++fc)
                             Fvy[fc] = eyi * VY[R1][fc] + cyi * (VY[R2][fc] - VY[R0][fc]) +
                                       cyk * (VYk[1][fc] - VYk[0][fc]);
-                        double o[2];
-                        const double* fnp = A.f_n + A.org + (int64_t)i * A.s0 + (int64_t)k * A.s1 + (int64_t)lc * A.s2 + mc;
                         double2 fn = make_double2(0.0, 0.0), uu = make_double2(0.0, 0.0);
-                        if (STAGE >= 2 && act) fn = *reinterpret_cast<const double2*>(fnp);
-                        if (STAGE == 4 && act)
-                            uu = *reinterpret_cast<const double2*>(A.u_in + (fnp - A.f_n));
-                        double un[2];
+                        if (STAGE >= 2) fn = lds2(SF + w * S2_TM + 2 * lane);
+                        if (STAGE == 4) uu = lds2(SU + w * S2_TM + 2 * lane);
+                        double o[2], un[2];
 #pragma unroll
                         for (int mm = 0; mm < 2; ++mm) {
                             const double Fvxl = exi * VX[R1][0][mm] + cxi * (VX[R2][0][mm] - VX[R0][0][mm]) +
@@ -358,7 +409,7 @@ __global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArg
                             }
                         }
                         if (act) {
-                            const int64_t off = fnp - A.f_n;
+                            const int64_t off = A.org + (int64_t)i * A.s0 + (int64_t)k * A.s1 + (int64_t)l * A.s2 + m0;
                             *reinterpret_cast<double2*>(A.f_next + off) = make_double2(o[0], o[1]);
                             if (STAGE == 2) *reinterpret_cast<double2*>(A.u_out + off) = make_double2(un[0], un[1]);
                         }
@@ -366,15 +417,17 @@ __global__ void __launch_bounds__(128, STAGE2D_MINB) k_stage_2d2v(const StageArg
                             double s = act ? (o[0] + o[1]) : 0.0;
 #pragma unroll
                             for (int of = 16; of > 0; of >>= 1) s += __shfl_xor_sync(0xffffffffu, s, of);
-                            if (tx == 0 && l < A.nvx) {
-                                const int nmt = gridDim.x;
-                                A.partials[((int64_t)l * nmt + blockIdx.x) * A.nx * A.ny + (int64_t)i * A.ny + k] = s;
-                            }
+                            if (lane == 0 && lact)
+                                A.partials[((int64_t)l * gridDim.x + mt) * A.nx * A.ny + (int64_t)i * A.ny + k] = s;
                         }
                     }
                     Fxp[0] = Fxn[0];
                     Fxp[1] = Fxn[1];
                 }
+                // release the slot: every value read from it has been consumed by this warp
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[slot]);
+                if (++slot == S2_NSLOT) { slot = 0; phase ^= 1u; }
             }
         }
     }
@@ -406,18 +459,54 @@ __global__ void k_moment_2d2v_direct(const double* __restrict__ f, int64_t org, 
     if (lane == 0) rho[c] = 1.0 - dvv * s;
 }
 
-template <int RECON>
-static int dispatch2(int stage, const StageArgs2& A, dim3 grid, cudaStream_t st) {
-    const dim3 block(32, 4);
-    switch (stage) {
-        case 0: k_stage_2d2v<0, RECON><<<grid, block, 0, st>>>(A); break;
-        case 1: k_stage_2d2v<1, RECON><<<grid, block, 0, st>>>(A); break;
-        case 2: k_stage_2d2v<2, RECON><<<grid, block, 0, st>>>(A); break;
-        case 3: k_stage_2d2v<3, RECON><<<grid, block, 0, st>>>(A); break;
-        case 4: k_stage_2d2v<4, RECON><<<grid, block, 0, st>>>(A); break;
-        default: return fail(VLASOV_EINVAL, "stage must be 0..4");
+template <int STAGE, int RECON>
+static int launch2_t(const StageArgs2& A, const TMaps2& M, dim3 grid, cudaStream_t st) {
+    auto kern = k_stage_2d2v<STAGE, RECON>;
+    const int qmax = (A.nx + A.nstrips - 1) / A.nstrips + 4;
+    const size_t smem = Slot2<STAGE>::smem_bytes(qmax);
+    static bool configured = false;
+    if (!configured) {
+        VK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
     }
+    kern<<<grid, 32 * (S2_LT + 2), smem, st>>>(A, M);
     VK_LAUNCH("k_stage_2d2v");
+    return VLASOV_OK;
+}
+
+template <int RECON>
+static int dispatch2(int stage, const StageArgs2& A, const TMaps2& M, dim3 grid, cudaStream_t st) {
+    switch (stage) {
+        case 0: return launch2_t<0, RECON>(A, M, grid, st);
+        case 1: return launch2_t<1, RECON>(A, M, grid, st);
+        case 2: return launch2_t<2, RECON>(A, M, grid, st);
+        case 3: return launch2_t<3, RECON>(A, M, grid, st);
+        case 4: return launch2_t<4, RECON>(A, M, grid, st);
+    }
+    return fail(VLASOV_EINVAL, "stage must be 0..4");
+}
+
+// tensor map of one field over the ghosted block of a single-block 2D+2V level
+static int encode_map(const vlasov_level* L, const double* f, unsigned box_vy, unsigned box_vx, CUtensorMap* out) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            cudaGetLastError();
+            return fail(VLASOV_ECUDA, "cuTensorMapEncodeTiled not available");
+        }
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint64_t dims[4] = {(cuuint64_t)L->block_str[0][2], (cuuint64_t)(L->dom[2] + 2 * G),
+                                (cuuint64_t)(L->dom[1] + 2 * G), (cuuint64_t)(L->dom[0] + 2 * G)};
+    const cuuint64_t strides[3] = {(cuuint64_t)L->block_str[0][2] * 8, (cuuint64_t)L->block_str[0][1] * 8,
+                                   (cuuint64_t)L->block_str[0][0] * 8};
+    const cuuint32_t box[4] = {box_vy, box_vx, 1, 1}, estr[4] = {1, 1, 1, 1};
+    CUresult rc = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)(f + L->block_off[0]), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) return fail(VLASOV_ECUDA, "cuTensorMapEncodeTiled failed");
     return VLASOV_OK;
 }
 
@@ -448,13 +537,17 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.hvy = L->h[3];
     A.vx_lo = L->lower[2];
     A.vy_lo = L->lower[3];
-    const int nmt = (A.nvy / 2 + 31) / 32, nlg = (A.nvx + 3) / 4;
+    const int nmt = (A.nvy + S2_TM - 1) / S2_TM, nlg = (A.nvx + S2_LT - 1) / S2_LT;
     A.nstrips = L->strips2;
-    A.nrows = (A.nx + A.nstrips - 1) / A.nstrips;
     A.partials = rho ? L->d_partials : nullptr;
     const dim3 grid(nmt, nlg, A.ny * A.nstrips);
-    int rc = recon == VLASOV_UPWIND ? dispatch2<VLASOV_UPWIND>(stage, A, grid, L->stream)
-                                    : dispatch2<VLASOV_CENTERED4>(stage, A, grid, L->stream);
+    TMaps2 M;
+    int rc;
+    if ((rc = encode_map(L, f_s, S2_LW, 8, &M.fs8)) || (rc = encode_map(L, f_s, S2_LW, 4, &M.fs4)) ||
+        (rc = encode_map(L, f_n ? f_n : f_s, S2_TM, 4, &M.fn4)) || (rc = encode_map(L, u ? u : f_s, S2_TM, 4, &M.u4)))
+        return rc;
+    rc = recon == VLASOV_UPWIND ? dispatch2<VLASOV_UPWIND>(stage, A, M, grid, L->stream)
+                                : dispatch2<VLASOV_CENTERED4>(stage, A, M, grid, L->stream);
     if (rc || !rho) return rc;
     const int ncfg = A.nx * A.ny;
     k_moment_2d2v_finish<<<(ncfg + 127) / 128, 128, 0, L->stream>>>(L->d_partials, A.nvx * nmt, ncfg,
