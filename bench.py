@@ -107,39 +107,77 @@ def whole_job_throughput(cells_per_rank: int, world: int, steps: int, ms_max: fl
     return cells_per_rank * world * steps / (ms_max / 1e3)
 
 
-def cpu_baseline(workload_name, budget_s=20.0):
-    """Oracle (as it stands) on the host: full-size C4 RK4 steps until ~budget_s."""
+def oracle_sample(w):
+    """Bounded sample of a workload for the CPU oracle: the same grid in velocity (and in y, v_y for
+    2D+2V) with the configuration x axis coarsened so that one oracle step takes ~0.5-2 s; the
+    per-cell arithmetic of the oracle is independent of the grid spacing, so cell-updates/s of the
+    sample is that of the workload."""
+    import inputs
+    nx = w.ncells[0]
+    target = 2 ** 20 if w.ncfg == 1 else 2 ** 21          # cells per sample step
+    while nx > 8 and (w.cells // w.ncells[0]) * nx > target:
+        nx //= 2
+    shape = (nx,) + tuple(w.ncells[1:])
+    return inputs.scaled(w, shape, name=f"{w.name}-sample")
+
+
+def oracle_steps(w, steps, warmup, budget_s=None):
+    """Time `steps` RK4 steps (after `warmup`) of the oracle, as it stands, on the bounded sample
+    of `w`; with budget_s, stop early once the timed steps exceed it (at least one step)."""
     import inputs
     from oracle import uniform
-    w = inputs.get(workload_name)
-    prob = uniform.problem_for(w)
-    f = inputs.initial_cell_averages(w)
-    dt = inputs.fixed_dt(w)
+    ws = oracle_sample(w)
+    prob = uniform.problem_for(ws)
+    f = inputs.initial_cell_averages(ws)
+    dt = inputs.fixed_dt(ws)
     E_bc = prob.constraints(f)
-    steps = 0
-    t0 = time.perf_counter()
-    while True:
+    for _ in range(warmup):
         f, E_bc, _ = prob.step(f, E_bc, dt)
-        steps += 1
-        if time.perf_counter() - t0 > budget_s or steps >= 3:
+    n = 0
+    t0 = time.perf_counter()
+    while n < steps:
+        f, E_bc, _ = prob.step(f, E_bc, dt)
+        n += 1
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
             break
     el = time.perf_counter() - t0
-    return {"value": w.cells * steps / el, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
-            "sample": f"{steps} full-size {workload_name} RK4 step(s) of the numpy fp64 oracle "
-                      f"({w.ncells[0]}x{w.ncells[1]}), {el:.1f} s, single thread"}
+    return {"value": ws.cells * n / el, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n} timed (+{warmup} warm-up) RK4 steps of the numpy fp64 oracle on a "
+                      f"{'x'.join(map(str, ws.ncells))} sample of {w.name} (x coarsened; per-cell work "
+                      f"identical), {el:.1f} s, single process"}, el / n
+
+
+def cpu_baseline(workload_name, budget_s=20.0):
+    """Oracle (as it stands) on the host cores, bounded sample of the workload, ~budget_s."""
+    import inputs
+    base, _ = oracle_steps(inputs.get(workload_name), 1000, 1, budget_s)
+    return base
+
+
+def workload_config(w, extra=None):
+    cfg = {"workload": w.name, "grid": list(w.ncells), "patches": "x".join(map(str, w.patch)) + " (merged single block)",
+           "cells": w.cells, "recon": "centered4", "dt": None}
+    import inputs
+    cfg["dt"] = inputs.fixed_dt(w)
+    if extra:
+        cfg.update(extra)
+    return cfg
 
 
 def run_reference(args, rank, world):
+    """Reference arm: there is no reference implementation (the paper ships no code), so the arm
+    is the oracle -- the plain CPU implementation of the same discretisation -- timed as it stands
+    on this host, W warm-up + K timed steps of a bounded sample of the workload."""
     if rank != 0:
         return
-    base = cpu_baseline(args.workload, budget_s=max(5.0, 60.0 / max(1, args.steps + args.warmup)))
     import inputs
     w = inputs.get(args.workload)
+    base, sec = oracle_steps(w, args.steps, args.warmup)
     line = {"impl": "reference", "metric": "fp64 phase-space cell-updates/s per RK4 step",
             "value": base["value"], "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * w.cells / base["value"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "cells": w.cells, "grid": list(w.ncells)},
+            "config": workload_config(w, {"parallelism": f"replicas x{world}"}),
             "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -266,10 +304,10 @@ def main():
             "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "grid": list(w.ncells), "patches": "x".join(map(str, w.patch)) + " (merged single block)",
-                       "cells": w.cells, "recon": "centered4", "dt": dt,
-                       "l2": f"inputs larger than L2 (4 fields of {S.A.numel() * 8 / 2**20:.0f} MiB per step > 126 MB L2)",
-                       "parallelism": f"replicas x{world}", "graph": f"CUDA graph, 1 RK4 step ({S.launches_per_step()} launches)"},
+            "config": workload_config(w, {
+                "l2": f"inputs larger than L2 (4 fields of {S.A.numel() * 8 / 2**20:.0f} MiB per step > 126 MB L2)",
+                "parallelism": f"replicas x{world}",
+                "graph": f"CUDA graph, 1 RK4 step ({S.launches_per_step()} launches)"}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": ("k_stage_1d1v" if w.ncfg == 1 else "k_stage_2d2v") + " (4 launches per step)",
