@@ -143,13 +143,37 @@ class AmrVlasov1D:
 
     def step(self, dt: float):
         with torch.cuda.stream(self.stream):
-            for r in self.regs[1:]:
-                r.zero_()
-            for s in (1, 2, 3, 4):
-                self._stage(s, dt)
-            for l in range(len(self.levels) - 1, 0, -1):
-                api.vlasov_average_down(self.levels[l].h, self.bufs[l]["A"], self.bufs[l - 1]["A"], self.regs[l],
-                                        dt)
+            self._step_launches(dt)
+
+    def _step_launches(self, dt):
+        for r in self.regs[1:]:
+            r.zero_()
+        for s in (1, 2, 3, 4):
+            self._stage(s, dt)
+        for l in range(len(self.levels) - 1, 0, -1):
+            api.vlasov_average_down(self.levels[l].h, self.bufs[l]["A"], self.bufs[l - 1]["A"], self.regs[l], dt)
+
+    def step_graph(self, dt: float):
+        """One step through a CUDA graph of the step's launches (captured on first use for the
+        current hierarchy and dt; an eager step first builds the lazily created reduction plan).
+        The E_bc ping-pong index returns to its value after 4 stages, so the graph is reusable."""
+        key = (tuple(L.h.value for L in self.levels), float(dt))
+        if getattr(self, "_graph_key", None) != key:
+            self.step(dt)
+            self.stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self._step_launches(dt)
+            self._graph, self._graph_key = g, key
+            return
+        with torch.cuda.stream(self.stream):
+            self._graph.replay()
+
+    def launches_per_step(self) -> int:
+        nl = len(self.levels)
+        # per stage: fill (copy/CF + phys) per level, reduction (2), Poisson (1), inject per level,
+        # stage kernel per level, flux registers per fine level; then refluxing + average-down
+        return 4 * (2 * nl + 2 + 1 + nl + nl + (nl - 1)) + 2 * (nl - 1)
 
     # ------------------------------------------------------------------ regrid (C3 rule)
     def tags_level0(self, tol, buffer):
