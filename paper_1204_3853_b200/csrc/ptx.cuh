@@ -25,14 +25,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Wait for the phase with the given parity.  try_wait with a suspend-time hint: a waiting thread
+// is parked (woken when the phase completes or the hint elapses) instead of re-issuing the test,
+// so waiting producer / consumer warps do not burn issue slots of the warps that have work.
+#ifndef VK_MBAR_SUSPEND_NS
+#define VK_MBAR_SUSPEND_NS 20000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+        "}\n" ::"r"(smem_u32(bar)), "r"(parity), "n"(VK_MBAR_SUSPEND_NS) : "memory");
 }
 
 // 1D bulk copy global -> shared::cta through the async (TMA) engine; completion counted on `bar`.

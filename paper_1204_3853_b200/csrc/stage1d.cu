@@ -369,9 +369,14 @@ __global__ void __launch_bounds__(NT + 32, STAGE1D_MINB) k_stage_1d1v(const Stag
                             }
                     }
                     if (A.rho != nullptr) {
-                        double sr = 0.0;
+                        double sr;
+                        if (nact == CPT) {
+                            sr = (o[0] + o[1]) + (o[2] + o[3]);
+                        } else {
+                            sr = 0.0;
 #pragma unroll
-                        for (int m = 0; m < CPT; ++m) sr += (m < nact) ? o[m] : 0.0;
+                            for (int m = 0; m < CPT; ++m) sr += (m < nact) ? o[m] : 0.0;
+                        }
                         rs[K] = sr;
                     }
                 } else if (q == 3) {             // x-fluxes at x0 - 1/2 (rows x0-2 .. x0+1)
