@@ -227,6 +227,17 @@ int vlasov_tag_cells(vlasov_level* level, const double* f, double tol, int32_t b
 int vlasov_tags_to_boxes(const uint8_t* tags_host, const int32_t domain_cells[4], int32_t ndim,
                          const int32_t ratio[4], int32_t tile, vlasov_box* out, int32_t cap,
                          int32_t* n);
+/* Host: tag clustering into rectangular patches ("grouped and expanded minimally";
+ * reading #28 in DESIGN.md): signature-based recursive bisection (cut at a hole of the tag
+ * signature closest to the centre, else at the strongest inflection of its Laplacian, else at the
+ * midpoint of the longest side) until the fill efficiency |tags|/|box| >= `efficiency` and every
+ * side is <= largest (P:1495-1515 largest_patch_size); cuts keep >= smallest cells per side
+ * (smallest_patch_size).  tags: row-major [shape[0]][shape[1]] (velocity fastest), index (0,0) =
+ * level cell `lo`.  Boxes in level index space, disjoint, sorted lexicographically; *n receives
+ * the count, at most `cap` are written.  1D+1V only.                                            */
+int vlasov_cluster_tags(const uint8_t* tags, const int32_t shape[2], const int32_t lo[2],
+                        const int32_t smallest[2], const int32_t largest[2], double efficiency,
+                        vlasov_box* out, int32_t cap, int32_t* n);
 /* Regrid data motion: interior of every patch of `level` (new) from `old` (same resolution,
  * may be NULL) where the old patches overlap, else by conservative interpolation from
  * `coarser` (ghosts of f_coarse current).                                                         */

@@ -966,6 +966,126 @@ int vlasov_tags_to_boxes(const uint8_t* tags, const int32_t domain_cells[4], int
     return VLASOV_OK;
 }
 
+// Tag clustering into rectangular patches (reading #28, same rules and tie-breaks as the
+// oracle): signature-based recursive bisection -- holes, then Laplacian inflection, then midpoint --
+// until the fill efficiency is reached and every side is <= largest; cuts keep >= smallest cells.
+namespace {
+struct Clusterer {
+    const uint8_t* t;
+    int nx, nv, lo0, lo1;
+    int smallest[2], largest[2];
+    double eff;
+    std::vector<Box> out;
+    bool tag(int i, int j) const { return t[(int64_t)i * nv + j] != 0; }
+    void tile_large(const Box& b) {
+        std::vector<std::pair<int, int>> r[2];
+        for (int d = 0; d < 2; ++d) {
+            const int n = b.hi[d] - b.lo[d] + 1, k = (n + largest[d] - 1) / largest[d];
+            for (int j = 0; j < k; ++j)
+                r[d].push_back({b.lo[d] + (int)((int64_t)n * j / k), b.lo[d] + (int)((int64_t)n * (j + 1) / k) - 1});
+        }
+        for (auto& a : r[0])
+            for (auto& c : r[1]) {
+                Box o;
+                o.lo[0] = a.first; o.hi[0] = a.second; o.lo[1] = c.first; o.hi[1] = c.second;
+                out.push_back(o);
+            }
+    }
+    // region in local tag indices [a0, b0] x [a1, b1]
+    void rec(int a0, int b0, int a1, int b1) {
+        int lo[2] = {INT32_MAX, INT32_MAX}, hi[2] = {-1, -1};
+        for (int i = a0; i <= b0; ++i)
+            for (int j = a1; j <= b1; ++j)
+                if (tag(i, j)) {
+                    lo[0] = std::min(lo[0], i); hi[0] = std::max(hi[0], i);
+                    lo[1] = std::min(lo[1], j); hi[1] = std::max(hi[1], j);
+                }
+        if (hi[0] < 0) return;
+        const int n[2] = {hi[0] - lo[0] + 1, hi[1] - lo[1] + 1};
+        std::vector<int64_t> sig[2] = {std::vector<int64_t>(n[0], 0), std::vector<int64_t>(n[1], 0)};
+        int64_t cnt = 0;
+        for (int i = lo[0]; i <= hi[0]; ++i)
+            for (int j = lo[1]; j <= hi[1]; ++j)
+                if (tag(i, j)) { ++sig[0][i - lo[0]]; ++sig[1][j - lo[1]]; ++cnt; }
+        const bool too_big = n[0] > largest[0] || n[1] > largest[1];
+        const double e = (double)cnt / (double)((int64_t)n[0] * n[1]);
+        Box B;
+        B.lo[0] = lo[0] + lo0; B.hi[0] = hi[0] + lo0; B.lo[1] = lo[1] + lo1; B.hi[1] = hi[1] + lo1;
+        if (e >= eff && !too_big) { out.push_back(B); return; }
+        int order[2] = {0, 1};
+        if (n[1] > n[0]) { order[0] = 1; order[1] = 0; }
+        auto adm = [&](int d, int c) { return c >= smallest[d] && n[d] - c >= smallest[d]; };
+        int cd = -1, cc = -1;
+        for (int oi = 0; oi < 2 && cd < 0; ++oi) {                     // a. holes
+            const int d = order[oi];
+            int64_t best = -1;
+            for (int c = 1; c < n[d]; ++c)
+                if ((sig[d][c - 1] == 0 || sig[d][c] == 0) && adm(d, c)) {
+                    const int64_t key = std::llabs(2LL * c - n[d]);
+                    if (best < 0 || key < best) { best = key; cc = c; cd = d; }
+                }
+        }
+        for (int oi = 0; oi < 2 && cd < 0; ++oi) {                     // b. inflection
+            const int d = order[oi];
+            if (n[d] < 3) continue;
+            std::vector<int64_t> lap(n[d] - 2);
+            for (int j = 0; j + 2 < n[d]; ++j) lap[j] = sig[d][j] - 2 * sig[d][j + 1] + sig[d][j + 2];
+            int64_t bj = 0, bcent = 0;
+            int bc = -1;
+            for (int j = 1; j < (int)lap.size(); ++j)
+                if ((lap[j - 1] < 0 && lap[j] > 0) || (lap[j - 1] > 0 && lap[j] < 0)) {
+                    const int c = j + 1;
+                    if (!adm(d, c)) continue;
+                    const int64_t jump = std::llabs(lap[j] - lap[j - 1]), cent = std::llabs(2LL * c - n[d]);
+                    if (bc < 0 || jump > bj || (jump == bj && (cent < bcent || (cent == bcent && c < bc)))) {
+                        bj = jump; bcent = cent; bc = c;
+                    }
+                }
+            if (bc >= 0) { cd = d; cc = bc; }
+        }
+        for (int oi = 0; oi < 2 && cd < 0; ++oi) {                     // c. bisection
+            const int d = order[oi], c = n[d] / 2;
+            if (adm(d, c)) { cd = d; cc = c; }
+        }
+        if (cd < 0) {
+            if (too_big) tile_large(B);
+            else out.push_back(B);
+            return;
+        }
+        if (cd == 0) {
+            rec(lo[0], lo[0] + cc - 1, lo[1], hi[1]);
+            rec(lo[0] + cc, hi[0], lo[1], hi[1]);
+        } else {
+            rec(lo[0], hi[0], lo[1], lo[1] + cc - 1);
+            rec(lo[0], hi[0], lo[1] + cc, hi[1]);
+        }
+    }
+};
+}  // namespace
+
+int vlasov_cluster_tags(const uint8_t* tags, const int32_t shape[2], const int32_t lo[2],
+                        const int32_t smallest[2], const int32_t largest[2], double efficiency,
+                        vlasov_box* out, int32_t cap, int32_t* n) {
+    if (!tags || !shape || !lo || !smallest || !largest || !n) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (shape[0] < 0 || shape[1] < 0 || !(efficiency > 0.0) || efficiency > 1.0)
+        return vk::fail(VLASOV_EINVAL, "cluster_tags: bad shape or efficiency");
+    for (int d = 0; d < 2; ++d)
+        if (smallest[d] < 1 || largest[d] < smallest[d])
+            return vk::fail(VLASOV_EINVAL, "cluster_tags: need 1 <= smallest <= largest");
+    Clusterer C;
+    C.t = tags; C.nx = shape[0]; C.nv = shape[1]; C.lo0 = lo[0]; C.lo1 = lo[1];
+    for (int d = 0; d < 2; ++d) { C.smallest[d] = smallest[d]; C.largest[d] = largest[d]; }
+    C.eff = efficiency;
+    if (shape[0] > 0 && shape[1] > 0) C.rec(0, shape[0] - 1, 0, shape[1] - 1);
+    std::sort(C.out.begin(), C.out.end(), [](const Box& a, const Box& b) { return vk::box_less(a, b, 2); });
+    *n = (int32_t)C.out.size();
+    for (int i = 0; i < (int)C.out.size() && i < cap; ++i) {
+        std::memset(&out[i], 0, sizeof(vlasov_box));
+        for (int d = 0; d < 2; ++d) { out[i].lo[d] = C.out[i].lo[d]; out[i].hi[d] = C.out[i].hi[d]; }
+    }
+    return VLASOV_OK;
+}
+
 // ---------------------------------------------------------------- compute entry points
 int vlasov_fill_ghosts(vlasov_level* L, double* f, const vlasov_level* coarser, const double* f_coarse,
                        const double* E_bc, const double* f0v, int32_t interp) {
