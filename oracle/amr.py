@@ -258,6 +258,25 @@ def regrid_two_level(H, data, E_bc, tol, buffer, ratio, tile):
     Returns (new data, new level-1 boxes)."""
     tags = boxes.dilate_tags(level0_tags(H, data, tol), buffer, (True, False))
     new_boxes = boxes.tiles_from_tags(tags, ratio, tile)
+    return regrid_to(H, data, new_boxes, ratio), new_boxes
+
+
+def regrid_two_level_clustered(H, data, E_bc, tol, buffer, ratio, smallest, largest, efficiency=0.7):
+    """As regrid_two_level, with the level-1 boxes grouped from the dilated level-0 tags by
+    clustering.cluster_tags (P:468-475, reading #28); smallest / largest are level-1 patch sizes
+     in level-1 cells, converted to level-0 cells (ceil / floor by the ratio)."""
+    from . import clustering
+    tags = boxes.dilate_tags(level0_tags(H, data, tol), buffer, (True, False))
+    sm = [-(-smallest[d] // ratio[d]) for d in range(2)]
+    lg = [max(sm[d], largest[d] // ratio[d]) for d in range(2)]
+    coarse = clustering.cluster_tags(tags, sm, lg, efficiency)
+    new_boxes = boxes.sort_boxes([boxes.refine(b, ratio) for b in coarse])
+    return regrid_to(H, data, new_boxes, ratio), new_boxes
+
+
+def regrid_to(H, data, new_boxes, ratio):
+    """Data motion of a two-level regrid to the level-1 boxes `new_boxes`: new fine
+    patches copy old fine data where they overlap it, else are interpolated from level 0."""
     old_levels = H.levels
     old_data = data
     lb = [old_levels[0].boxes] + ([new_boxes] if new_boxes else [])
@@ -289,4 +308,4 @@ def regrid_two_level(H, data, E_bc, tol, buffer, ratio, tile):
                     fine[ov[0][0] - nb[0][0]: ov[1][0] - nb[0][0] + 1, ov[0][1] - nb[0][1]: ov[1][1] - nb[0][1] + 1] = \
                         _interior(old_data[1][op])[ov[0][0] - ob[0][0]: ov[1][0] - ob[0][0] + 1,
                                                    ov[0][1] - ob[0][1]: ov[1][1] - ob[0][1] + 1]
-    return new, new_boxes
+    return new

@@ -186,9 +186,25 @@ class AmrVlasov1D:
         return tags.cpu().numpy().reshape(self.ncells0)
 
     def regrid(self, tol, buffer, ratio, tile):
-        """Two-level regrid: returns the new fine boxes (possibly empty)."""
+        """Two-level regrid, C3 fixed-tile rule (reading #18): returns the new fine boxes."""
         tags = self.tags_level0(tol, buffer)
-        new_boxes = api.vlasov_tags_to_boxes(tags, self.ncells0, ratio, tile)
+        return self.regrid_to(api.vlasov_tags_to_boxes(tags, self.ncells0, ratio, tile), ratio)
+
+    def regrid_clustered(self, tol, buffer, ratio, smallest, largest, efficiency=0.7):
+        """Two-level regrid with the level-1 boxes grouped from the dilated level-0 tags by
+        vlasov_cluster_tags (reading #28); smallest / largest are level-1 patch sizes
+         in level-1 cells, converted to level-0 cells (ceil / floor by the ratio)."""
+        tags = self.tags_level0(tol, buffer)
+        sm = [-(-smallest[d] // ratio[d]) for d in range(2)]
+        lg = [max(sm[d], largest[d] // ratio[d]) for d in range(2)]
+        coarse = api.vlasov_cluster_tags(tags, sm, lg, efficiency)
+        fine = sorted(((lo[0] * ratio[0], lo[1] * ratio[1]), ((hi[0] + 1) * ratio[0] - 1, (hi[1] + 1) * ratio[1] - 1))
+                      for lo, hi in coarse)
+        return self.regrid_to(fine, ratio)
+
+    def regrid_to(self, new_boxes, ratio):
+        """Replace level 1 by `new_boxes` (data: copy old fine where it overlaps, else interpolate
+        from level 0; then the constraints of the new hierarchy)."""
         old_boxes = self.levels[1].boxes if len(self.levels) > 1 else []
         if [tuple(map(tuple, b)) for b in new_boxes] == [tuple(map(tuple, b)) for b in old_boxes] and \
                 (len(self.levels) == 1 or tuple(self.levels[1].ratio) == tuple(ratio)):

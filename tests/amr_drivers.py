@@ -32,11 +32,15 @@ def start(H, data):
     return E_bc
 
 
-def regrid(H, data, E_bc, tol, buffer, ratio, tile):
+def regrid(H, data, E_bc, tol, buffer, ratio, tile, clustered=None):
+    """clustered: None (C3 fixed tiles) or (smallest, largest, efficiency) in level-1 cells."""
     amr.fill_ghosts(H, data, E_bc)
     nlev_old = len(H.levels)
     tags = amr.level0_tags(H, data, tol)
-    new, new_boxes = amr.regrid_two_level(H, data, E_bc, tol, buffer, ratio, tile)
+    if clustered is None:
+        new, new_boxes = amr.regrid_two_level(H, data, E_bc, tol, buffer, ratio, tile)
+    else:
+        new, new_boxes = amr.regrid_two_level_clustered(H, data, E_bc, tol, buffer, ratio, *clustered)
     E_fill = [E_bc[0]]
     if new_boxes:
         E_fill.append(E_bc[1] if nlev_old > 1 else np.zeros(H.ncells0[0] * ratio[0]))
@@ -46,7 +50,7 @@ def regrid(H, data, E_bc, tol, buffer, ratio, tile):
 
 
 def c3_run(w, nsteps, regrid_every, dt, tol, buffer, ratio, tile, recon=scheme.CENTERED4, mode=interp.LINEAR5,
-           log=None):
+           log=None, clustered=None):
     """Two-level run from level 0 only: regrid at step 0 and every `regrid_every` steps."""
     lb0 = inputs.level0_boxes(w)
     H = hierarchy(w, [lb0], [(1, 1)], recon, mode)
@@ -56,7 +60,7 @@ def c3_run(w, nsteps, regrid_every, dt, tol, buffer, ratio, tile, recon=scheme.C
     E_bc = start(H, data)
     for n in range(nsteps):
         if n % regrid_every == 0:
-            data, E_bc, nb, tags = regrid(H, data, E_bc, tol, buffer, ratio, tile)
+            data, E_bc, nb, tags = regrid(H, data, E_bc, tol, buffer, ratio, tile, clustered)
             if log is not None:
                 log.append((n, [tuple(map(tuple, b)) for b in nb], tags))
         data, E_bc, _ = amr.step(H, data, E_bc, dt)

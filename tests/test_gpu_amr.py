@@ -224,3 +224,30 @@ def test_step_graph_equals_eager_steps():
     for a, b in zip(G1.get_state(), G2.get_state()):
         for x, y in zip(a, b):
             np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("params", [((4, 4), (32, 32), 0.7, (4, 4), 1, 0.05, interp.LINEAR5),
+                                    ((8, 8), (32, 64), 0.85, (2, 4), 2, 0.04, interp.WENO5)])
+def test_clustered_regrid_run_parity(params):
+    """N1: regrids with clustered boxes (paper's smallest / largest patch sizes, tag buffer),
+    anisotropic ratio, linear5 / WENO5 fill of new patches: boxes bit-exact, f within tolerance."""
+    smallest, largest, eff, ratio, buf, tol, mode = params
+    w = _c3_small()
+    dt = inputs.fixed_dt(w, ratio)
+    log = []
+    H, data, _ = drv.c3_run(w, 4, 2, dt, tol, buf, ratio, None, mode=mode, log=log,
+                            clustered=(smallest, largest, eff))
+    assert any(len(b) for _, b, _ in log)
+    lb0 = inputs.level0_boxes(w)
+    G = AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), [lb0], [(1, 1)],
+                    lambda r: inputs.background_profile(w, r), interp=MODE[mode])
+    G.set_state([inputs.initial_cell_averages(w)])
+    k = 0
+    for n in range(4):
+        if n % 2 == 0:
+            nb = G.regrid_clustered(tol, buf, ratio, smallest, largest, eff)
+            assert [tuple(map(tuple, b)) for b in nb] == log[k][1], f"boxes differ at step {n}"
+            k += 1
+        G.step_graph(dt)
+    err = relerr_levels(G.get_state(), _interiors(data))
+    assert err < 1e-11, err
