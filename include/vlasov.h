@@ -245,6 +245,11 @@ int vlasov_level_fill_from(vlasov_level* level, double* f, const vlasov_level* o
                            const double* f_old, const vlasov_level* coarser,
                            const double* f_coarse, int32_t interp);
 
+/* ---- adaptive time step ("50% of the stability limit"; reading #17) -------------- *
+ * out[0] (device) = max_i |x_i| over n doubles, on `cuda_stream`; deterministic.  The drivers form
+ * dt = min(cfl / max_l(max|vbar|/dx_l + max|E_l|/dv_l), growth * dt_prev) from it.              */
+int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream);
+
 /* ---- misc ------------------------------------------------------------------------------------ */
 const char* vlasov_last_error(void);
 int vlasov_device_ok(void);         /* 1 if a compute-capability 10.x device is current, else 0 */

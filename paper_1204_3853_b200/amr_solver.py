@@ -169,6 +169,25 @@ class AmrVlasov1D:
         with torch.cuda.stream(self.stream):
             self._graph.replay()
 
+    def next_dt(self, dt_prev, cfl=0.5, growth=1.1, vmax=None):
+        """Adaptive step (reading #17): dt = min(cfl / rate, growth * dt_prev) with
+        rate = max over levels of (max|vbar|/dx_l + max|E_l|/dv_l), E_l the last constraint
+        evaluation; max|E_l| by vlasov_absmax on the device (one 8-byte read per level)."""
+        if vmax is None:
+            L = self.levels[-1]
+            dv = self.dx0[1] / L.ratio[1]
+            nv = L.info.domain_cells[1]
+            vmax = max(abs(self.lower[1] + 0.5 * dv), abs(self.lower[1] + (nv - 0.5) * dv))
+        out = torch.zeros(len(self.levels), dtype=torch.float64, device="cuda")
+        with torch.cuda.stream(self.stream):
+            for l, E in enumerate(self.E):
+                api.vlasov_absmax(E[self.cur], out[l:l + 1], self.stream)
+        self.stream.synchronize()
+        em = out.cpu().numpy()
+        rate = max(vmax / (self.dx0[0] / L.ratio[0]) + em[l] / (self.dx0[1] / L.ratio[1])
+                   for l, L in enumerate(self.levels))
+        return min(cfl / rate, growth * dt_prev)
+
     def launches_per_step(self) -> int:
         nl = len(self.levels)
         # per stage: fill (copy/CF + phys) per level, reduction (2), Poisson (1), inject per level,

@@ -174,4 +174,27 @@ int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_
     return VLASOV_OK;
 }
 
+// out[0] = max_i |x_i| (one CTA, fixed-order tree: deterministic); used by the adaptive time step
+__global__ void k_absmax(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+    __shared__ double s[32];
+    double m = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(x[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = (threadIdx.x < (blockDim.x >> 5)) ? s[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) out[0] = m;
+    }
+}
+
+int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st) {
+    k_absmax<<<1, 1024, 0, st>>>(x, n, out);
+    VK_LAUNCH("k_absmax");
+    return VLASOV_OK;
+}
+
 }  // namespace vk

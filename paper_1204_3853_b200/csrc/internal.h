@@ -186,6 +186,7 @@ int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest
 int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest,
                      double* E_lvl);
 int linear5_weights(int R, double* out /* R*5 */);
+int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st);
 int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
 int launch_flux_registers(const vlasov_level* L, const double* f_fine, const double* E_fine, const double* f_coarse,
                           const double* E_coarse, double b_s, double* regs, int recon);

@@ -1172,6 +1172,12 @@ int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const 
     return vk::launch_reduce_subpatch(Lf->red_plan, f, nlev, rho_finest, Lf->stream);
 }
 
+int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream) {
+    if (!x || !out || n < 0) return vk::fail(VLASOV_EINVAL, "null argument or n < 0");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_absmax(x, n, out, (cudaStream_t)cuda_stream);
+}
+
 int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisson** out) {
     if (!out) return vk::fail(VLASOV_EINVAL, "null argument");
     *out = nullptr;

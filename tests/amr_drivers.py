@@ -49,8 +49,18 @@ def regrid(H, data, E_bc, tol, buffer, ratio, tile, clustered=None):
     return new, E_new, new_boxes, tags
 
 
+def next_dt(H, E_bc, dt_prev, cfl=0.5, growth=1.1):
+    """Adaptive step (reading #17): min(cfl / max_l(max|vbar|/dx_l + max|E_l|/dv_l),
+    growth * dt_prev), vbar over the finest level's whole velocity range."""
+    hf = H.h(len(H.levels) - 1)
+    nv = H.ncells0[1] * H.levels[-1].ratio[1]
+    vmax = max(abs(H.lower[1] + 0.5 * hf[1]), abs(H.lower[1] + (nv - 0.5) * hf[1]))
+    rate = max(vmax / H.h(l)[0] + np.max(np.abs(E_bc[l])) / H.h(l)[1] for l in range(len(H.levels)))
+    return min(cfl / rate, growth * dt_prev)
+
+
 def c3_run(w, nsteps, regrid_every, dt, tol, buffer, ratio, tile, recon=scheme.CENTERED4, mode=interp.LINEAR5,
-           log=None, clustered=None):
+           log=None, clustered=None, adaptive=False):
     """Two-level run from level 0 only: regrid at step 0 and every `regrid_every` steps."""
     lb0 = inputs.level0_boxes(w)
     H = hierarchy(w, [lb0], [(1, 1)], recon, mode)
@@ -64,4 +74,8 @@ def c3_run(w, nsteps, regrid_every, dt, tol, buffer, ratio, tile, recon=scheme.C
             if log is not None:
                 log.append((n, [tuple(map(tuple, b)) for b in nb], tags))
         data, E_bc, _ = amr.step(H, data, E_bc, dt)
+        if adaptive:
+            dt = next_dt(H, E_bc, dt)
+            if log is not None:
+                log.append(("dt", dt))
     return H, data, E_bc

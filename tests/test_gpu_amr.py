@@ -251,3 +251,30 @@ def test_clustered_regrid_run_parity(params):
         G.step_graph(dt)
     err = relerr_levels(G.get_state(), _interiors(data))
     assert err < 1e-11, err
+
+
+def test_adaptive_dt_clustered_run_parity():
+    """N1: adaptive time step (<= 10 % growth, 50 % of the stability bound) with clustered regrids."""
+    w = _c3_small()
+    ratio, tol, buf, sm, lg, eff = (2, 2), 0.05, 1, (4, 4), (32, 32), 0.7
+    dt0 = 0.5 * inputs.fixed_dt(w, ratio)
+    log = []
+    H, data, _ = drv.c3_run(w, 4, 2, dt0, tol, buf, ratio, None, log=log, clustered=(sm, lg, eff), adaptive=True)
+    dts = [e[1] for e in log if e[0] == "dt"]
+    boxes_log = [e[1] for e in log if e[0] != "dt"]
+    lb0 = inputs.level0_boxes(w)
+    G = AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), [lb0], [(1, 1)], lambda r: inputs.background_profile(w, r))
+    G.set_state([inputs.initial_cell_averages(w)])
+    dt, k, gdts = dt0, 0, []
+    for n in range(4):
+        if n % 2 == 0:
+            nb = G.regrid_clustered(tol, buf, ratio, sm, lg, eff)
+            assert [tuple(map(tuple, b)) for b in nb] == boxes_log[k]
+            k += 1
+        G.step(dt)
+        dt = G.next_dt(dt)
+        gdts.append(dt)
+    np.testing.assert_allclose(gdts, dts, rtol=1e-12)
+    assert dts[0] == pytest.approx(1.1 * dt0)                       # growth-limited first
+    err = relerr_levels(G.get_state(), _interiors(data))
+    assert err < 1e-11, err
