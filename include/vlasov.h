@@ -216,9 +216,9 @@ int vlasov_average_down(vlasov_level* fine, const double* f_fine, double* f_coar
                         const double* regs, double dt);
 
 /* ---- tagging and regrid -------------------------------------------- *
- * tags[cell of the level domain] = (delta1 f + delta2 f > tol), dilated by `buffer` cells
- * (Chebyshev, periodic in configuration dims, clipped in velocity); f ghosts must be filled;
- * the level must tile its domain.  Evaluated without FMA contraction in the fixed order stated in
+ * tags[cell of the level domain] = (delta1 f + delta2 f > tol) on the level's patches (0 off
+ * them), dilated by `buffer` cells (Chebyshev, periodic in configuration dims, clipped in
+ * velocity); f ghosts must be filled.  Evaluated without FMA contraction in the fixed order stated in
  * DESIGN.md so that tags are bit-identical to the oracle's.                                      */
 int vlasov_tag_cells(vlasov_level* level, const double* f, double tol, int32_t buffer,
                      uint8_t* tags);
@@ -238,6 +238,16 @@ int vlasov_tags_to_boxes(const uint8_t* tags_host, const int32_t domain_cells[4]
 int vlasov_cluster_tags(const uint8_t* tags, const int32_t shape[2], const int32_t lo[2],
                         const int32_t smallest[2], const int32_t largest[2], double efficiency,
                         vlasov_box* out, int32_t cap, int32_t* n);
+/* Host: boxes of the next finer level (level index space of the finer level, sorted) from the
+ * dilated tags of `level` (row-major over the level domain): tags restricted to the nesting region
+ * of `level` (cells whose Chebyshev `nest`-neighbourhood lies in its patches, configuration dims
+ * periodic, cells beyond the velocity domain count as covered; Fig.1 caption proper nesting),
+ * clustered as vlasov_cluster_tags with smallest / largest given in FINER-level cells (converted
+ * by `ratio`, ceil / floor), each cluster intersected with the nesting region (row-run
+ * decomposition), refined by `ratio` (reading #28).                                           */
+int vlasov_regrid_boxes(const vlasov_level* level, const uint8_t* tags, const int32_t ratio[2],
+                        const int32_t smallest[2], const int32_t largest[2], double efficiency,
+                        int32_t nest, vlasov_box* out, int32_t cap, int32_t* n);
 /* Regrid data motion: interior of every patch of `level` (new) from `old` (same resolution,
  * may be NULL) where the old patches overlap, else by conservative interpolation from
  * `coarser` (ghosts of f_coarse current).                                                         */

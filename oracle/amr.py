@@ -252,6 +252,85 @@ def level0_tags(H, data, tol):
     return t
 
 
+def level_tags(H, data, l, tol):
+    """Tags (P:1428-1436) of level l's patches on its whole level domain (False off the patches);
+    the level's ghosts must be filled."""
+    lvl = H.levels[l]
+    t = np.zeros(boxes.size(lvl.domain), dtype=bool)
+    hx, hv = H.h(l)
+    for p, b in enumerate(lvl.boxes):
+        t[b[0][0]: b[1][0] + 1, b[0][1]: b[1][1] + 1] = tag_cells(data[l][p], hx, hv, tol)
+    return t
+
+
+def new_level_boxes(level, tags, ratio, smallest, largest, efficiency, nest=1):
+    """Boxes of the next finer level from the (dilated) tags of `level` (reading #28): tags kept
+    inside the nesting region of `level` (boxes.nesting_mask), clustered (clustering.cluster_tags
+    in level cells; smallest / largest are finer-level patch sizes converted by the ratio), each
+    cluster intersected with the nesting region (boxes.mask_to_boxes), refined by `ratio`."""
+    from . import clustering
+    nm = boxes.nesting_mask(level, nest)
+    t = np.asarray(tags, bool) & nm
+    sm = [-(-smallest[d] // ratio[d]) for d in range(2)]
+    lg = [max(sm[d], largest[d] // ratio[d]) for d in range(2)]
+    out = []
+    for b in clustering.cluster_tags(t, sm, lg, efficiency):
+        sub = nm[b[0][0]: b[1][0] + 1, b[0][1]: b[1][1] + 1]
+        out.extend(boxes.mask_to_boxes(sub, b[0]))
+    return boxes.sort_boxes([boxes.refine(b, ratio) for b in out])
+
+
+def regrid_hierarchy(H, data, E_bc, tol, buffers, ratios, smallest, largest, efficiency=0.7):
+    """Multi-level regrid: for k = 0, 1, ...: fill the ghosts of the new
+    levels 0..k (E_bc kept for existing level indices, 0 for new ones), tag level k (buffer[k]),
+    build level k+1 by new_level_boxes(ratio[k], smallest[k], largest[k]); its data copies the old
+    level k+1 where they overlap, else is interpolated from the new level k.  Stops
+    when a level has no tags or len(ratios) fine levels exist.  ratios[k]: ratio of level k+1 to k.
+    Returns (new data, list of new boxes per fine level)."""
+    old_levels, old_data = H.levels, data
+    lb = [old_levels[0].boxes]
+    rs = [old_levels[0].ratio]
+    H.set_levels(lb, rs)
+    new = [[a.copy() for a in old_data[0]]]
+    out_boxes = []
+    for k in range(len(ratios)):
+        E_fill = [E_bc[l] if (l < len(old_levels) and old_levels[l].ratio == H.levels[l].ratio)
+                  else np.zeros(H.ncells0[0] * H.levels[l].ratio[0]) for l in range(len(H.levels))]
+        fill_ghosts(H, new, E_fill)
+        tags = boxes.dilate_tags(level_tags(H, new, k, tol), buffers[k], (True, False))
+        nb = new_level_boxes(H.levels[k], tags, ratios[k], smallest[k], largest[k], efficiency)
+        if not nb:
+            break
+        r_next = tuple(a * b for a, b in zip(H.levels[k].ratio, ratios[k]))
+        H.set_levels(lb + [nb], rs + [r_next])
+        lb, rs = lb + [nb], rs + [r_next]
+        fine_new = [np.full(tuple(n + 2 * G for n in boxes.size(b)), np.nan) for b in nb]
+        rr = tuple(ratios[k])
+        for q, b in enumerate(nb):
+            fine = _interior(fine_new[q])
+            for p, cb in enumerate(H.levels[k].boxes):          # interpolate from the new level k
+                cbox = boxes.intersect(boxes.coarsen(b, rr), cb)
+                if boxes.is_empty(cbox):
+                    continue
+                cg = new[k][p]
+                sub = cg[cbox[0][0] - cb[0][0]: cbox[1][0] - cb[0][0] + 2 * G + 1,
+                         cbox[0][1] - cb[0][1]: cbox[1][1] - cb[0][1] + 2 * G + 1]
+                ref = interp.refine_patch_2d(sub, rr[0], rr[1], H.interp_mode)
+                fb = boxes.refine(cbox, rr)
+                fine[fb[0][0] - b[0][0]: fb[1][0] - b[0][0] + 1, fb[0][1] - b[0][1]: fb[1][1] - b[0][1] + 1] = ref
+            if k + 1 < len(old_levels) and old_levels[k + 1].ratio == r_next:   # copy old level k+1
+                for op, ob in enumerate(old_levels[k + 1].boxes):
+                    ov = boxes.intersect(ob, b)
+                    if boxes.is_empty(ov):
+                        continue
+                    fine[ov[0][0] - b[0][0]: ov[1][0] - b[0][0] + 1, ov[0][1] - b[0][1]: ov[1][1] - b[0][1] + 1] = \
+                        _interior(old_data[k + 1][op])[ov[0][0] - ob[0][0]: ov[1][0] - ob[0][0] + 1,
+                                                       ov[0][1] - ob[0][1]: ov[1][1] - ob[0][1] + 1]
+        new.append(fine_new)
+        out_boxes.append(nb)
+    return new, out_boxes
+
+
 def regrid_two_level(H, data, E_bc, tol, buffer, ratio, tile):
     """Tag level 0, dilate, tile -> new level-1 boxes; move data (copy old fine where the new
     patch overlaps it, else interpolate from level 0).  Level 0 ghosts must be filled.

@@ -273,3 +273,68 @@ def tiles_from_tags(tags, ratio, tile):
         if t[sl].any():
             out.append(box([i * tile for i in idx], [(i + 1) * tile - 1 for i in idx]))
     return sort_boxes(out)
+
+
+# --------------------------------------------------------------------------- nesting (multi-level regrid)
+def nesting_mask(level, buffer=1):
+    """Cells of `level` (whole level domain) around which every cell within Chebyshev distance
+    `buffer` lies in a patch of the level (configuration dims periodic; cells beyond the velocity
+    domain count as covered): where a finer level may be placed so that it is properly nested
+    (Fig.1 caption) with room for the coarse-fine stencils."""
+    shape = size(level.domain)
+    cov = np.zeros(shape, bool)
+    for b in level.boxes:
+        cov[tuple(slice(b[0][d], b[1][d] + 1) for d in range(level.ndim))] = True
+    out = cov.copy()
+    for offs in itertools.product(range(-buffer, buffer + 1), repeat=level.ndim):
+        sh = cov
+        for ax, o in enumerate(offs):
+            if o == 0:
+                continue
+            if level.periodic[ax]:
+                sh = np.roll(sh, -o, axis=ax)            # sh[c] = cov[c + o]
+            else:
+                z = np.ones_like(sh)                     # outside the velocity domain: covered
+                src = [slice(None)] * level.ndim
+                dst = [slice(None)] * level.ndim
+                n = sh.shape[ax]
+                if o > 0:
+                    dst[ax] = slice(0, n - o); src[ax] = slice(o, n)
+                else:
+                    dst[ax] = slice(-o, n); src[ax] = slice(0, n + o)
+                z[tuple(dst)] = sh[tuple(src)]
+                sh = z
+        out &= sh
+    return out
+
+
+def mask_to_boxes(mask, lo=(0, 0)):
+    """Deterministic decomposition of a 2D boolean mask into disjoint boxes: maximal runs of True
+    along the last dim in every row; a run continues its box while the next row has the identical
+    run.  Boxes offset by `lo`, sorted lexicographically."""
+    m = np.asarray(mask, bool)
+    nx = m.shape[0]
+    active = {}
+    out = []
+
+    def runs(row):
+        r, j, n = [], 0, row.size
+        while j < n:
+            if row[j]:
+                k = j
+                while k + 1 < n and row[k + 1]:
+                    k += 1
+                r.append((j, k))
+                j = k + 1
+            else:
+                j += 1
+        return r
+    for x in range(nx + 1):
+        cur = runs(m[x]) if x < nx else []
+        for run in sorted(list(active)):
+            if run not in cur:
+                out.append(box((lo[0] + active.pop(run), lo[1] + run[0]), (lo[0] + x - 1, lo[1] + run[1])))
+        for run in cur:
+            if run not in active:
+                active[run] = x
+    return sort_boxes(out)

@@ -74,6 +74,7 @@ _SIGS = {
     "vlasov_tag_cells": (I32, [P, P, D, I32, P]),
     "vlasov_tags_to_boxes": (I32, [P, PI32, I32, PI32, I32, C.POINTER(Box), I32, PI32]),
     "vlasov_cluster_tags": (I32, [P, PI32, PI32, PI32, PI32, D, C.POINTER(Box), I32, PI32]),
+    "vlasov_regrid_boxes": (I32, [P, P, PI32, PI32, PI32, D, I32, C.POINTER(Box), I32, PI32]),
     "vlasov_level_fill_from": (I32, [P, P, P, P, P, P, I32]),
     "vlasov_last_error": (C.c_char_p, []),
     "vlasov_device_ok": (I32, []),

@@ -221,6 +221,51 @@ class AmrVlasov1D:
                       for lo, hi in coarse)
         return self.regrid_to(fine, ratio)
 
+    def tags_level(self, k, tol, buffer):
+        """Dilated tags of level k on its level domain (ghosts of levels 0..k filled first)."""
+        L = self.levels[k]
+        with torch.cuda.stream(self.stream):
+            self._fill([b["A"] for b in self.bufs], [E[self.cur] for E in self.E])
+            tags = torch.zeros(L.info.tag_bytes, dtype=torch.uint8, device="cuda")
+            api.vlasov_tag_cells(L.h, self.bufs[k]["A"], tol, buffer, tags)
+        self.stream.synchronize()
+        return tags.cpu().numpy().reshape(tuple(L.info.domain_cells[d] for d in range(2)))
+
+    def regrid_hierarchy(self, tol, buffers, ratios, smallest, largest, efficiency=0.7):
+        """Multi-level regrid: for k = 0, 1, ...: ghosts of the new levels 0..k, tags of
+        level k (buffers[k]), next-level boxes by vlasov_regrid_boxes (nesting in level k, clustering
+        with the level-(k+1) patch sizes smallest[k] / largest[k], ratio ratios[k]); the new level
+        k+1 copies the old level k+1 where they overlap, else interpolates from the new level k
+        (vlasov_level_fill_from).  E_bc kept for surviving level indices, 0 for new ones; then the
+        constraints of the new hierarchy.  Returns the list of new fine-level box lists."""
+        old_levels, old_bufs, old_E = self.levels[1:], self.bufs[1:], [E[self.cur] for E in self.E[1:]]
+        with torch.cuda.stream(self.stream):
+            del self.levels[1:], self.bufs[1:], self.E[1:], self.f0v[1:], self.regs[1:]
+        out = []
+        for k in range(len(ratios)):
+            tags = self.tags_level(k, tol, buffers[k])
+            nb = api.vlasov_regrid_boxes(self.levels[k].h, tags, ratios[k], smallest[k], largest[k], efficiency)
+            if not nb:
+                break
+            r_next = tuple(a * b for a, b in zip(self.levels[k].ratio, ratios[k]))
+            with torch.cuda.stream(self.stream):
+                self._append_level(nb, r_next)
+                old = old_levels[k] if k < len(old_levels) and tuple(old_levels[k].ratio) == r_next else None
+                api.vlasov_level_fill_from(self.levels[k + 1].h, self.bufs[k + 1]["A"], old.h if old else None,
+                                           old_bufs[k]["A"] if old else None, self.levels[k].h, self.bufs[k]["A"],
+                                           self.interp)
+                if k < len(old_E) and old is not None:
+                    self.E[k + 1][self.cur].copy_(old_E[k])
+                else:
+                    self.E[k + 1][self.cur].zero_()
+            out.append(nb)
+        with torch.cuda.stream(self.stream):
+            self._make_field_plan()
+            self._initial_constraints()
+        self.stream.synchronize()
+        del old_levels, old_bufs, old_E
+        return out
+
     def regrid_to(self, new_boxes, ratio):
         """Replace level 1 by `new_boxes` (data: copy old fine where it overlaps, else interpolate
         from level 0; then the constraints of the new hierarchy)."""

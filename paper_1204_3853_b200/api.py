@@ -18,7 +18,7 @@ __all__ = [
     "vlasov_level_get_info", "vlasov_level_layout", "vlasov_level_ghost_map", "vlasov_subpatches",
     "vlasov_fill_ghosts", "vlasov_rhs", "vlasov_rk4_stage", "vlasov_rk4_stage_vp", "vlasov_reduce_moment",
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
-    "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags",
+    "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
     "vlasov_level_fill_from", "vlasov_absmax", "vlasov_device_ok", "vlasov_last_error",
 ]
 
@@ -186,6 +186,18 @@ def vlasov_cluster_tags(tags_host: np.ndarray, smallest, largest, efficiency=0.7
     out = (Box * cap)()
     n = C.c_int32()
     check(lib.vlasov_cluster_tags(t.ctypes.data_as(C.c_void_p), sh, l, sm, lg, float(efficiency), out, cap,
+                                  C.byref(n)))
+    return [(tuple(out[i].lo[:2]), tuple(out[i].hi[:2])) for i in range(min(n.value, cap))]
+
+
+def vlasov_regrid_boxes(h, tags_host: np.ndarray, ratio, smallest, largest, efficiency=0.7, nest=1, cap=65536):
+    t = np.ascontiguousarray(tags_host, dtype=np.uint8)
+    r = (C.c_int32 * 2)(*ratio)
+    sm = (C.c_int32 * 2)(*smallest)
+    lg = (C.c_int32 * 2)(*largest)
+    out = (Box * cap)()
+    n = C.c_int32()
+    check(lib.vlasov_regrid_boxes(h, t.ctypes.data_as(C.c_void_p), r, sm, lg, float(efficiency), int(nest), out, cap,
                                   C.byref(n)))
     return [(tuple(out[i].lo[:2]), tuple(out[i].hi[:2])) for i in range(min(n.value, cap))]
 

@@ -3,6 +3,8 @@
 // (P:1423-1437).  Task lists are built on the host at level creation (level.cpp).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "internal.h"
 #include "scheme.cuh"
 
@@ -204,12 +206,51 @@ __global__ void k_tags(const double* __restrict__ f, int64_t off, int64_t pitch,
     tags[t] = hit;
 }
 
+// Multi-patch levels: raw tags per block interior (the crit of a cell uses its block's ghost
+// frame), into a level-domain scratch that is zero off the patches; then the dilation.
+__global__ void k_tags_raw(const double* __restrict__ f, const Block1* __restrict__ blocks, int maxcells, int nv,
+                           double hx, double hv, double tol, uint8_t* __restrict__ raw) {
+    const Block1 B = blocks[blockIdx.y];
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= B.nx * B.nv || t >= maxcells) return;
+    const int i = t / B.nv, j = t % B.nv;
+    const int64_t c = B.off + (int64_t)(i + G) * B.pitch + (j + G);
+    raw[(int64_t)(B.lo_x + i) * nv + (B.lo_v + j)] = crit_exceeds(f, c, B.pitch, hx, hv, tol) ? 1 : 0;
+}
+
+__global__ void k_tags_dilate(const uint8_t* __restrict__ raw, int nx, int nv, int buffer, uint8_t* __restrict__ tags) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nx * nv) return;
+    const int x = (int)(t / nv), j = (int)(t % nv);
+    uint8_t hit = 0;
+    for (int a = -buffer; a <= buffer && !hit; ++a) {
+        const int xx = ((x + a) % nx + nx) % nx;
+        for (int b = -buffer; b <= buffer; ++b) {
+            const int jj = j + b;
+            if (jj < 0 || jj >= nv) continue;
+            if (raw[(int64_t)xx * nv + jj]) { hit = 1; break; }
+        }
+    }
+    tags[t] = hit;
+}
+
 int launch_tags(const vlasov_level* L, const double* f, double tol, int buffer, uint8_t* tags) {
     const int nx = L->dom[0], nv = L->dom[1];
     const int64_t n = (int64_t)nx * nv;
-    k_tags<<<(unsigned)((n + 255) / 256), 256, 0, L->stream>>>(f, L->block_off[0], L->block_str[0][0], nx, nv,
-                                                               L->h[0], L->h[1], tol, buffer, tags);
-    VK_LAUNCH("k_tags");
+    if (L->single_block) {                               // fused: crit + dilation in one pass
+        k_tags<<<(unsigned)((n + 255) / 256), 256, 0, L->stream>>>(f, L->block_off[0], L->block_str[0][0], nx, nv,
+                                                                   L->h[0], L->h[1], tol, buffer, tags);
+        VK_LAUNCH("k_tags");
+        return VLASOV_OK;
+    }
+    VK_CUDA(cudaMemsetAsync(L->d_rawtags, 0, (size_t)n, L->stream));
+    int maxcells = 0;
+    for (const Block1& B : L->h_blocks1) maxcells = std::max(maxcells, B.nx * B.nv);
+    const dim3 grid((unsigned)((maxcells + 255) / 256), (unsigned)L->h_blocks1.size());
+    k_tags_raw<<<grid, 256, 0, L->stream>>>(f, L->d_blocks1, maxcells, nv, L->h[0], L->h[1], tol, L->d_rawtags);
+    VK_LAUNCH("k_tags_raw");
+    k_tags_dilate<<<(unsigned)((n + 255) / 256), 256, 0, L->stream>>>(L->d_rawtags, nx, nv, buffer, tags);
+    VK_LAUNCH("k_tags_dilate");
     return VLASOV_OK;
 }
 

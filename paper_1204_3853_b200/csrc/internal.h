@@ -132,6 +132,7 @@ struct vlasov_level {
     int n_strips = 0;
     int cluster_size = 1;                 // v-tiles per cluster of the fused-field stage launch
     double* d_partials = nullptr;         // moment scratch [n_vtiles][dom_x]
+    uint8_t* d_rawtags = nullptr;         // raw tags of a multi-patch level (level domain)
     unsigned* d_tickets = nullptr;        // per-strip arrival tickets
     bool self_ghost_ok = false;           // single periodic block, nv % 4 == 0: in-kernel ghosts
     // ghost fill

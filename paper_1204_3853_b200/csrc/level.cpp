@@ -174,6 +174,7 @@ void free_level(vlasov_level* L) {
     cudaFree(L->d_b5);
     cudaFree(L->d_partials);
     cudaFree(L->d_tickets);
+    cudaFree(L->d_rawtags);
     delete L;
 }
 
@@ -818,6 +819,10 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         *out = L;
         return VLASOV_OK;
     }
+    if (!L->single_block && L->ndim == 2) {      // tag scratch of multi-patch levels (regrid)
+        int64_t tb = (int64_t)L->dom[0] * L->dom[1];
+        VK_CUDA(cudaMalloc((void**)&L->d_rawtags, (size_t)tb));
+    }
     if (L->single_block && L->ndim == 4)
         VK_CUDA(cudaMalloc((void**)&L->d_partials, sizeof(double) * (size_t)L->n_vtiles * L->dom[0] * L->dom[1]));
     if (L->single_block && L->ndim == 2) {
@@ -1086,6 +1091,87 @@ int vlasov_cluster_tags(const uint8_t* tags, const int32_t shape[2], const int32
     return VLASOV_OK;
 }
 
+// Boxes of the next finer level from the dilated tags of `level` (reading #28): tags restricted to
+// the nesting region (cells whose Chebyshev `nest`-neighbourhood lies in the level's patches; x
+// periodic, beyond the velocity domain counts as covered), clustered, each cluster intersected with
+// the nesting region (row-run decomposition), refined by `ratio`.  Same rules as the oracle.
+int vlasov_regrid_boxes(const vlasov_level* L, const uint8_t* tags, const int32_t ratio[2],
+                        const int32_t smallest[2], const int32_t largest[2], double efficiency, int32_t nest,
+                        vlasov_box* out, int32_t cap, int32_t* n) {
+    if (!L || !tags || !ratio || !smallest || !largest || !n) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "regrid_boxes: 1D+1V levels only");
+    if (nest < 0 || ratio[0] < 1 || ratio[1] < 1) return vk::fail(VLASOV_EINVAL, "regrid_boxes: bad nest or ratio");
+    const int nx = L->dom[0], nv = L->dom[1];
+    std::vector<uint8_t> cov((size_t)nx * nv, 0), nm((size_t)nx * nv, 0);
+    for (const Box& b : L->boxes)
+        for (int x = b.lo[0]; x <= b.hi[0]; ++x)
+            for (int v = b.lo[1]; v <= b.hi[1]; ++v) cov[(size_t)x * nv + v] = 1;
+    for (int x = 0; x < nx; ++x)
+        for (int v = 0; v < nv; ++v) {
+            bool ok = true;
+            for (int a = -nest; a <= nest && ok; ++a)
+                for (int c = -nest; c <= nest && ok; ++c) {
+                    const int vv = v + c;
+                    if (vv < 0 || vv >= nv) continue;
+                    ok = cov[(size_t)wrap(x + a, nx) * nv + vv] != 0;
+                }
+            nm[(size_t)x * nv + v] = ok ? 1 : 0;
+        }
+    std::vector<uint8_t> t((size_t)nx * nv);
+    for (size_t i = 0; i < t.size(); ++i) t[i] = (tags[i] && nm[i]) ? 1 : 0;
+    int sm[2], lg[2];
+    for (int d = 0; d < 2; ++d) {
+        sm[d] = (smallest[d] + ratio[d] - 1) / ratio[d];
+        lg[d] = std::max(sm[d], largest[d] / ratio[d]);
+    }
+    Clusterer C;
+    C.t = t.data(); C.nx = nx; C.nv = nv; C.lo0 = 0; C.lo1 = 0;
+    for (int d = 0; d < 2; ++d) { C.smallest[d] = sm[d]; C.largest[d] = lg[d]; }
+    C.eff = efficiency;
+    if (nx > 0 && nv > 0) C.rec(0, nx - 1, 0, nv - 1);
+    std::vector<Box> res;
+    for (const Box& b : C.out) {               // cluster box  x  nesting region, row runs
+        std::map<std::pair<int, int>, int> active;
+        for (int x = b.lo[0]; x <= b.hi[0] + 1; ++x) {
+            std::vector<std::pair<int, int>> cur;
+            if (x <= b.hi[0]) {
+                int j = b.lo[1];
+                while (j <= b.hi[1]) {
+                    if (nm[(size_t)x * nv + j]) {
+                        int k = j;
+                        while (k + 1 <= b.hi[1] && nm[(size_t)x * nv + k + 1]) ++k;
+                        cur.push_back({j, k});
+                        j = k + 1;
+                    } else {
+                        ++j;
+                    }
+                }
+            }
+            for (auto it = active.begin(); it != active.end();) {
+                if (std::find(cur.begin(), cur.end(), it->first) == cur.end()) {
+                    Box o;
+                    o.lo[0] = it->second; o.hi[0] = x - 1; o.lo[1] = it->first.first; o.hi[1] = it->first.second;
+                    res.push_back(o);
+                    it = active.erase(it);
+                } else {
+                    ++it;
+                }
+            }
+            for (auto& r : cur)
+                if (!active.count(r)) active[r] = x;
+        }
+    }
+    std::vector<Box> fine;
+    for (const Box& b : res) fine.push_back(vk::box_refine(b, ratio, 2));
+    std::sort(fine.begin(), fine.end(), [](const Box& a, const Box& b) { return vk::box_less(a, b, 2); });
+    *n = (int32_t)fine.size();
+    for (int i = 0; i < (int)fine.size() && i < cap; ++i) {
+        std::memset(&out[i], 0, sizeof(vlasov_box));
+        for (int d = 0; d < 2; ++d) { out[i].lo[d] = fine[i].lo[d]; out[i].hi[d] = fine[i].hi[d]; }
+    }
+    return VLASOV_OK;
+}
+
 // ---------------------------------------------------------------- compute entry points
 int vlasov_fill_ghosts(vlasov_level* L, double* f, const vlasov_level* coarser, const double* f_coarse,
                        const double* E_bc, const double* f0v, int32_t interp) {
@@ -1279,8 +1365,7 @@ int vlasov_average_down(vlasov_level* fine, const double* f_fine, double* f_coar
 int vlasov_tag_cells(vlasov_level* L, const double* f, double tol, int32_t buffer, uint8_t* tags) {
     if (!L || !f || !tags) return vk::fail(VLASOV_EINVAL, "null argument");
     if (buffer < 0) return vk::fail(VLASOV_EINVAL, "tag buffer < 0");
-    if (L->ndim != 2 || !L->single_block)
-        return vk::fail(VLASOV_EUNSUPPORTED, "tag_cells: 1D+1V level stored as one block covering its domain");
+    if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "tag_cells: 1D+1V levels only");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     return vk::launch_tags(L, f, tol, buffer, tags);
 }

@@ -79,3 +79,15 @@ def c3_run(w, nsteps, regrid_every, dt, tol, buffer, ratio, tile, recon=scheme.C
             if log is not None:
                 log.append(("dt", dt))
     return H, data, E_bc
+
+
+def regrid_multilevel(H, data, E_bc, tol, buffers, ratios, smallest, largest, efficiency=0.7):
+    """Oracle side of AmrVlasov1D.regrid_hierarchy: multi-level regrid, then ghosts (E_bc kept for
+    surviving level indices with the same ratio, 0 for new ones) and the constraints."""
+    old_ratios = [l.ratio for l in H.levels]
+    new, nbs = amr.regrid_hierarchy(H, data, E_bc, tol, buffers, ratios, smallest, largest, efficiency)
+    E_fill = [E_bc[l] if (l < len(E_bc) and l < len(old_ratios) and old_ratios[l] == H.levels[l].ratio)
+              else np.zeros(H.ncells0[0] * H.levels[l].ratio[0]) for l in range(len(H.levels))]
+    amr.fill_ghosts(H, new, E_fill)
+    E_new, _ = amr.constraints(H, new)
+    return new, E_new, nbs

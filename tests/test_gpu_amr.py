@@ -278,3 +278,28 @@ def test_adaptive_dt_clustered_run_parity():
     assert dts[0] == pytest.approx(1.1 * dt0)                       # growth-limited first
     err = relerr_levels(G.get_state(), _interiors(data))
     assert err < 1e-11, err
+
+
+def test_three_level_regrid_run_parity():
+    """N1: >= 3 levels with the paper's anisotropic ratios [2,4], [4,2], multi-level regrid
+    (tags on every level, proper nesting, clustering with the AMR1 patch sizes P:1495-1503),
+    every 2 steps: boxes of every level bit-exact, f within 1e-11."""
+    w = inputs.scaled(inputs.get("C3"), (16, 32), (8, 8))
+    args = (0.02, [1, 1], [(2, 4), (4, 2)], [(4, 4), (4, 4)], [(32, 32), (64, 64)], 0.7)
+    dt = inputs.fixed_dt(w, (8, 8))
+    H = drv.hierarchy(w, [inputs.level0_boxes(w)], [(1, 1)])
+    data = _ic_data(H, w)
+    E_bc = drv.start(H, data)
+    G = AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), [inputs.level0_boxes(w)], [(1, 1)],
+                    lambda r: inputs.background_profile(w, r))
+    G.set_state([inputs.initial_cell_averages(w)])
+    for n in range(4):
+        if n % 2 == 0:
+            data, E_bc, nbs = drv.regrid_multilevel(H, data, E_bc, *args)
+            got = G.regrid_hierarchy(*args)
+            assert len(nbs) == 2
+            assert [[tuple(map(tuple, b)) for b in lvl] for lvl in got] == [[tuple(map(tuple, b)) for b in lvl] for lvl in nbs]
+        data, E_bc, _ = amr.step(H, data, E_bc, dt)
+        G.step_graph(dt)
+        err = relerr_levels(G.get_state(), _interiors(data))
+        assert err < 1e-11, (n, err)

@@ -113,3 +113,42 @@ def test_cabi_cluster_c3_tags_amr_params():
         got = api.vlasov_cluster_tags(t.astype(np.uint8), smallest, largest, 0.7)
         assert got == [(tuple(b[0]), tuple(b[1])) for b in exp]
         assert 0 < len(got) < 200
+
+
+def test_mask_to_boxes_exact_cover():
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        m = rng.random((int(rng.integers(1, 20)), int(rng.integers(1, 20)))) < 0.6
+        bx = boxes.mask_to_boxes(m, (3, -2))
+        cov = np.zeros(m.shape, int)
+        for (a, b) in bx:
+            cov[a[0] - 3: b[0] - 3 + 1, a[1] + 2: b[1] + 2 + 1] += 1
+        assert np.array_equal(cov, m.astype(int))
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_cabi_regrid_boxes_bitexact_vs_oracle(seed):
+    """Next-level boxes from tags under the proper-nesting constraint (reading #28): C ABI == oracle,
+    and the result is properly nested (Fig.1 caption) with a one-cell buffer."""
+    import inputs
+    from inputs.hierarchies import random_hierarchy
+    from oracle import amr
+    rng = np.random.default_rng(2000 + seed)
+    rat, lb = random_hierarchy(seed)
+    w = inputs.scaled(inputs.get("C3"), (16, 32), (8, 8))
+    levels = []
+    for r, bl in zip(rat, lb):
+        levels.append(api.Level(2, w.ncells, w.lower, inputs.spacing(w), r, bl, coarser=levels[-1] if levels else None))
+    dom = boxes.box((0, 0), (15, 31))
+    metas = [boxes.LevelMeta(dom, r, [boxes.box(*b) for b in bl], (True, False)) for r, bl in zip(rat, lb)]
+    k = len(levels) - 1
+    shape = boxes.size(metas[k].domain)
+    t = rng.random(shape) < 0.05
+    ratio = (int(rng.choice([2, 4])), int(rng.choice([2, 4])))
+    sm, lg, eff = (4, 4), (32, 64), float(rng.choice([0.5, 0.7]))
+    exp = amr.new_level_boxes(metas[k], t, ratio, sm, lg, eff)
+    got = api.vlasov_regrid_boxes(levels[k].h, t.astype(np.uint8), ratio, sm, lg, eff)
+    assert got == [(tuple(b[0]), tuple(b[1])) for b in exp]
+    if exp:
+        fine = boxes.LevelMeta(dom, tuple(a * b for a, b in zip(rat[k], ratio)), exp, (True, False))
+        assert boxes.properly_nested(fine, metas[k])
