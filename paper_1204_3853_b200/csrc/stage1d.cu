@@ -63,6 +63,12 @@ constexpr int CPT = STAGE1D_CPT;
 #ifndef RING_KB
 #define RING_KB 40
 #endif
+// 1: a dedicated producer warp issues the TMA ring; 0: thread 0 of the consumers issues it (no
+// extra warp: 4 warps x 168 registers lets 3 CTAs share an SM instead of 2)
+#ifndef STAGE1D_PRODUCER
+#define STAGE1D_PRODUCER 1
+#endif
+constexpr int PWARPS = STAGE1D_PRODUCER;
 constexpr int NT_WIDE = 128, NT_NARROW = 32;   // consumer threads per CTA
 
 template <int STAGE, int NT>
@@ -84,7 +90,7 @@ struct StageGeom {
 // the f_n / u rows are those of the output row i = r - 2 (q >= 4), so every slot is consumed
 // completely in its own row step and released at once.
 template <int STAGE, int RECON, int NT, bool SELF>
-__global__ void __launch_bounds__(NT + 32, STAGE1D_MINB) k_stage_1d1v(const StageArgs1 A) {
+__global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(const StageArgs1 A) {
     using SG = StageGeom<STAGE, NT>;
     constexpr int TV = SG::TV, SEG = SG::SEG, SLOT = SG::SLOT, NSLOT = SG::NSLOT, NW = SG::NW;
     constexpr bool NEED_FN = (STAGE >= 2);
@@ -133,35 +139,46 @@ __global__ void __launch_bounds__(NT + 32, STAGE1D_MINB) k_stage_1d1v(const Stag
 
     // fused field: rho and the Green's function (twice: periodic extension) staged by the TMA engine
     double* f_rho = sEbc + (A.tile_rows + 4);
-    if (warp == NW) {                            // ---------------- producer warp
+    const uint32_t seg_bytes = (uint32_t)(wpad + 4) * 8u;
+    const uint32_t row_bytes = (uint32_t)wpad * 8u;
+    // TMA loads of row step q into ring slot `sl`
+    auto issue = [&](int q, int sl) {
+        const int r = T.x0 - 2 + q;
+        int rs = r;
+        if (SELF) rs = (r < 0) ? r + B.nx : (r >= B.nx ? r - B.nx : r);
+        const bool out_row = (q >= 4);
+        uint32_t bytes = seg_bytes;
+        if (NEED_FN && out_row) bytes += row_bytes;
+        if (NEED_U && out_row) bytes += row_bytes;
+        double* dst = smem + sl * SLOT;
+        mbar_arrive_expect_tx(&full_bar[sl], bytes);
+        bulk_g2s(dst, A.f_s + rowbase(rs) + T.j0 - 2, seg_bytes, &full_bar[sl]);
+        if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(r - 2) + T.j0, row_bytes, &full_bar[sl]);
+        if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(r - 2) + T.j0, row_bytes, &full_bar[sl]);
+    };
+    auto issue_field = [&]() {
+        if (field) {
+            const uint32_t nb = (uint32_t)A.dom_x * 8u;
+            mbar_arrive_expect_tx(&field_bar, nb);
+            bulk_g2s(f_rho, A.rho_in, nb, &field_bar);
+        }
+    };
+    if (PWARPS && warp == NW) {                  // ---------------- producer warp
         if (lane == 0) {
-            if (field) {
-                const uint32_t nb = (uint32_t)A.dom_x * 8u;
-                mbar_arrive_expect_tx(&field_bar, nb);
-                bulk_g2s(f_rho, A.rho_in, nb, &field_bar);
-            }
-            const uint32_t seg_bytes = (uint32_t)(wpad + 4) * 8u;
-            const uint32_t row_bytes = (uint32_t)wpad * 8u;
+            issue_field();
             int slot = 0;
             uint32_t phase = 0;
             for (int q = 0; q < Q; ++q) {
                 if (q >= NSLOT) mbar_wait(&empty_bar[slot], phase ^ 1u);
-                const int r = T.x0 - 2 + q;
-                int rs = r;
-                if (SELF) rs = (r < 0) ? r + B.nx : (r >= B.nx ? r - B.nx : r);
-                const bool out_row = (q >= 4);
-                uint32_t bytes = seg_bytes;
-                if (NEED_FN && out_row) bytes += row_bytes;
-                if (NEED_U && out_row) bytes += row_bytes;
-                double* dst = smem + slot * SLOT;
-                mbar_arrive_expect_tx(&full_bar[slot], bytes);
-                bulk_g2s(dst, A.f_s + rowbase(rs) + T.j0 - 2, seg_bytes, &full_bar[slot]);
-                if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(r - 2) + T.j0, row_bytes, &full_bar[slot]);
-                if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(r - 2) + T.j0, row_bytes, &full_bar[slot]);
+                issue(q, slot);
                 if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
             }
         }
         return;
+    }
+    if (!PWARPS && tid == 0) {                   // consumer thread 0 primes the ring
+        issue_field();
+        for (int q = 0; q < min(Q, NSLOT); ++q) issue(q, q);
     }
 
     // ---------------------------------------------------------------- consumers
@@ -397,6 +414,10 @@ __global__ void __launch_bounds__(NT + 32, STAGE1D_MINB) k_stage_1d1v(const Stag
                 // still in flight when the producer overwrites it
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[slot]);
+                if (!PWARPS && tid == 0 && q + NSLOT < Q) {   // refill the slot once every warp released it
+                    mbar_wait(&empty_bar[slot], phase);
+                    issue(q + NSLOT, slot);
+                }
                 if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
             }
         }
@@ -458,7 +479,7 @@ static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t
     if (A.rho_in && A.cluster > 1) {   // fused field: the v-tiles of a row strip form one cluster
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(ntiles);
-        cfg.blockDim = dim3(NT + 32);
+        cfg.blockDim = dim3(NT + 32 * PWARPS);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute at[1];
@@ -471,7 +492,7 @@ static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t
         VK_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
         return VLASOV_OK;
     }
-    kern<<<ntiles, NT + 32, smem, st>>>(A);
+    kern<<<ntiles, NT + 32 * PWARPS, smem, st>>>(A);
     VK_LAUNCH("k_stage_1d1v");
     return VLASOV_OK;
 }
@@ -501,7 +522,7 @@ static int ctas_per_sm_t(int tile_rows) {
     using SG = StageGeom<4, NT>;
     auto k = k_stage_1d1v<4, VLASOV_CENTERED4, NT, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT + 32, SG::smem_bytes(tile_rows)) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT + 32 * PWARPS, SG::smem_bytes(tile_rows)) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -520,7 +541,7 @@ int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(cs * 64);
-        cfg.blockDim = dim3(nt + 32);
+        cfg.blockDim = dim3(nt + 32 * PWARPS);
         cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
