@@ -180,6 +180,13 @@ int vlasov_rk4_stage(vlasov_level* level, int32_t stage, double dt, double* f_n,
 int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
                          double* rho_finest);
 
+/* Alg.6 Mask Reduction: the same rho by refining every patch in x (linear5 with 2
+ * ghost columns), masking the cells covered by the next finer level and summing over v -- the
+ * paper's comparator of Alg.8 (sub-patch reduction = 64% of mask-reduction time).
+ * Same arguments and plan caching as vlasov_reduce_moment; equal to it up to rounding.          */
+int vlasov_reduce_moment_mask(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
+                              double* rho_finest);
+
 /* ---- periodic Poisson + E -------------------------------------------------------- *
  * Plan for n >= 5 periodic cells of width dx (1D configuration space).  solve: projects rho to
  * mean zero, solves 30 phi_i - 16(phi_{i+1}+phi_{i-1}) + (phi_{i+2}+phi_{i-2}) = 12 dx^2 rho_i

@@ -64,6 +64,7 @@ _SIGS = {
     "vlasov_rk4_stage": (I32, [P, I32, D, P, P, P, P, P, P, P, I32, P]),
     "vlasov_rk4_stage_vp": (I32, [P, P, I32, D, P, P, P, P, P, P, P, P, I32, P]),
     "vlasov_reduce_moment": (I32, [C.POINTER(P), I32, C.POINTER(P), P]),
+    "vlasov_reduce_moment_mask": (I32, [C.POINTER(P), I32, C.POINTER(P), P]),
     "vlasov_absmax": (I32, [P, I64, P, P]),
     "vlasov_poisson_create": (I32, [I32, D, P, C.POINTER(P)]),
     "vlasov_poisson_solve": (I32, [P, P, P, P, I32]),

@@ -59,6 +59,67 @@ int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, d
     return VLASOV_OK;
 }
 
+// ------------------------------------------------------------------ Alg.6 Mask Reduction
+// one warp per (patch, coarse x column): over the patch's v range, the R linear5-refined values
+// of the column (from columns x_c-2 .. x_c+2), masked by mu(x_c, v), summed
+__global__ void k_red_mask(const LevelPtrs P, const MaskCol* __restrict__ cols, int64_t ncols,
+                           const uint8_t* __restrict__ mask, const double* __restrict__ w, double* __restrict__ part) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (c >= ncols) return;
+    const MaskCol C = cols[c];
+    const double* f = P.f[C.level] + C.addr;
+    const double* b = w + C.woff;
+    double acc[MAXR];
+#pragma unroll
+    for (int s = 0; s < MAXR; ++s) acc[s] = 0.0;
+    for (int j = lane; j < C.nv; j += 32) {
+        if (!mask[C.mask + j]) continue;
+        double u[5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) u[a] = f[(int64_t)a * C.pitch + j];
+#pragma unroll
+        for (int s = 0; s < MAXR; ++s) {
+            if (s >= C.R) break;
+            double v = 0.0;
+#pragma unroll
+            for (int a = 0; a < 5; ++a) v += b[5 * s + a] * u[a];
+            acc[s] += v;
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < MAXR; ++s) {
+        if (s >= C.R) break;
+        double v = acc[s];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) part[C.out + s] = v;
+    }
+}
+
+__global__ void k_red_mask_finest(const double* __restrict__ part, const int32_t* __restrict__ xoff,
+                                  const int32_t* __restrict__ idx, const double* __restrict__ dv, int nxf,
+                                  double* __restrict__ rho) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= nxf) return;
+    double acc = 0.0;
+    for (int k = xoff[x]; k < xoff[x + 1]; ++k) acc += dv[k] * part[idx[k]];
+    rho[x] = 1.0 - acc;
+}
+
+int launch_reduce_mask(const MaskPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st) {
+    LevelPtrs lp;
+    for (int l = 0; l < MAXLEV; ++l) lp.f[l] = l < nlev ? f[l] : nullptr;
+    if (P->ncols > 0) {
+        k_red_mask<<<(unsigned)((P->ncols + 7) / 8), 256, 0, st>>>(lp, P->d_cols, P->ncols, P->d_mask, P->d_w,
+                                                                   P->d_part);
+        VK_LAUNCH("k_red_mask");
+    }
+    k_red_mask_finest<<<(P->nxf + 127) / 128, 128, 0, st>>>(P->d_part, P->d_xoff, P->d_idx, P->d_dv, P->nxf, rho);
+    VK_LAUNCH("k_red_mask_finest");
+    return VLASOV_OK;
+}
+
 // ------------------------------------------------------------------ face fluxes at one face
 // x-face flux F^x_{i+1/2,j} = vbar_j <f> + (dv/24)(<f>_{j+1} - <f>_{j-1})
 template <int RECON>

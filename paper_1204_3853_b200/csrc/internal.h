@@ -103,6 +103,28 @@ struct RedPlan {              // Alg.8 sub-patch reduction plan (built on the ho
     int32_t* d_xoff = nullptr;    // CSR over finest x [nxf + 1]
 };
 void free_red_plan(RedPlan* p);
+
+struct MaskCol {              // Alg.6: one coarse x column of one patch, refined by R in x
+    int64_t addr;             // index of cell (x_c - 2, lo_v) of the patch in its level array
+    int64_t mask;             // index of (x_c, lo_v) in the hierarchy mask buffer
+    int32_t pitch, nv, level, R;
+    int32_t out;              // first of the R partial sums of this column
+    int32_t woff;             // offset of the R x 5 linear5 weights in the weight table
+};
+struct MaskPlan {             // Alg.6 Mask Reduction plan (comparator of Alg.8)
+    std::vector<uint64_t> uids;
+    int nxf = 0;
+    int64_t ncols = 0, npart = 0;
+    MaskCol* d_cols = nullptr;
+    uint8_t* d_mask = nullptr;    // mu per level (1: not covered by the next finer level)
+    double* d_w = nullptr;        // linear5 weights per distinct R
+    double* d_part = nullptr;     // partial sums
+    int32_t* d_xoff = nullptr;    // CSR over finest x
+    int32_t* d_idx = nullptr;     // partial index per contribution
+    double* d_dv = nullptr;       // dv of the contribution's level
+};
+void free_mask_plan(MaskPlan* p);
+int launch_reduce_mask(const MaskPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
 }  // namespace vk
 
 // ------------------------------------------------------------------ opaque structs
@@ -151,6 +173,7 @@ struct vlasov_level {
     int avg_count = 1;                    // fine cells per coarse cell
     // Alg.8 plan cached on the finest level of the hierarchy it was built for
     mutable vk::RedPlan* red_plan = nullptr;
+    mutable vk::MaskPlan* mask_plan = nullptr;
     // 2D+2V
     int64_t e_doubles = 0;
     int strips2 = 1;                      // x strips of the 2D+2V stage kernel

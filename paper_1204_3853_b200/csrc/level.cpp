@@ -135,6 +135,18 @@ int linear5_weights(int R, double* out) {
     }
     return 0;
 }
+void free_mask_plan(MaskPlan* p) {
+    if (!p) return;
+    cudaFree(p->d_cols);
+    cudaFree(p->d_mask);
+    cudaFree(p->d_w);
+    cudaFree(p->d_part);
+    cudaFree(p->d_xoff);
+    cudaFree(p->d_idx);
+    cudaFree(p->d_dv);
+    delete p;
+}
+
 void free_red_plan(RedPlan* p) {
     if (!p) return;
     cudaFree(p->d_cols);
@@ -171,6 +183,7 @@ void free_level(vlasov_level* L) {
     cudaFree(L->d_reflux_off);
     cudaFree(L->d_avg);
     vk::free_red_plan(L->red_plan);
+    vk::free_mask_plan(L->mask_plan);
     cudaFree(L->d_b5);
     cudaFree(L->d_partials);
     cudaFree(L->d_tickets);
@@ -1262,6 +1275,111 @@ int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream) {
     if (!x || !out || n < 0) return vk::fail(VLASOV_EINVAL, "null argument or n < 0");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     return vk::launch_absmax(x, n, out, (cudaStream_t)cuda_stream);
+}
+
+// Alg.6 Mask Reduction: every patch refined in x (linear5, ghost columns current),
+// covered cells masked, summed over v; the comparator of Alg.8.
+static int build_mask_plan(const vlasov_level* const* levels, int nlev, vk::MaskPlan** out) {
+    *out = nullptr;
+    const vlasov_level* Lf = levels[nlev - 1];
+    const int nxf = Lf->dom[0];
+    std::vector<vk::MaskCol> cols;
+    std::vector<uint8_t> mask;
+    std::vector<double> w;
+    std::map<int, int> woff;
+    std::vector<std::vector<std::pair<int32_t, double>>> per_x(nxf);
+    int32_t npart = 0;
+    for (int l = 0; l < nlev; ++l) {
+        const vlasov_level* L = levels[l];
+        if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "mask reduction: 1D+1V levels only");
+        if (nxf % L->dom[0]) return vk::fail(VLASOV_EINVAL, "finest x resolution not a multiple of a level's");
+        if (l > 0 && (L->coarser != levels[l - 1] || L->coarser_uid != levels[l - 1]->uid))
+            return vk::fail(VLASOV_ESTALE, "reduce_moment_mask: levels are not a hierarchy (coarser mismatch)");
+        const int R = nxf / L->dom[0];
+        if (R > vk::MAXR) return vk::fail(VLASOV_EUNSUPPORTED, "mask reduction: x ratio to the finest level > 16");
+        if (!woff.count(R)) {
+            woff[R] = (int)w.size();
+            std::vector<double> b((size_t)R * 5);
+            vk::linear5_weights(R, b.data());
+            w.insert(w.end(), b.begin(), b.end());
+        }
+        const int64_t moff = (int64_t)mask.size();
+        std::vector<uint8_t> mu((size_t)L->dom[0] * L->dom[1], 1);
+        if (l + 1 < nlev) {
+            const vlasov_level* F = levels[l + 1];
+            int rr[4];
+            for (int d = 0; d < 2; ++d) rr[d] = F->ratio[d] / L->ratio[d];
+            for (const Box& fb : F->boxes) {
+                const Box cb = vk::box_coarsen(fb, rr, 2);
+                for (int x = cb.lo[0]; x <= cb.hi[0]; ++x)
+                    for (int v = cb.lo[1]; v <= cb.hi[1]; ++v) mu[(size_t)x * L->dom[1] + v] = 0;
+            }
+        }
+        mask.insert(mask.end(), mu.begin(), mu.end());
+        for (size_t p = 0; p < L->boxes.size(); ++p) {
+            const Box& b = L->boxes[p];
+            const int blk = L->patch_block[p];
+            for (int xc = b.lo[0]; xc <= b.hi[0]; ++xc) {
+                vk::MaskCol c;
+                int cc[4] = {xc - 2, b.lo[1], 0, 0};
+                c.addr = cell_addr(L, blk, cc);
+                c.mask = moff + (int64_t)xc * L->dom[1] + b.lo[1];
+                c.pitch = (int32_t)L->block_str[blk][0];
+                c.nv = vk::box_ncells_dim(b, 1);
+                c.level = l;
+                c.R = R;
+                c.out = npart;
+                c.woff = woff[R];
+                cols.push_back(c);
+                for (int s = 0; s < R; ++s) per_x[(size_t)xc * R + s].push_back({npart + s, L->h[1]});
+                npart += R;
+            }
+        }
+    }
+    std::vector<int32_t> xoff(nxf + 1, 0), idx;
+    std::vector<double> dv;
+    for (int x = 0; x < nxf; ++x) {
+        xoff[x] = (int32_t)idx.size();
+        for (auto& e : per_x[x]) { idx.push_back(e.first); dv.push_back(e.second); }
+    }
+    xoff[nxf] = (int32_t)idx.size();
+    vk::MaskPlan* P = new vk::MaskPlan();
+    for (int l = 0; l < nlev; ++l) P->uids.push_back(levels[l]->uid);
+    P->nxf = nxf;
+    P->ncols = (int64_t)cols.size();
+    P->npart = npart;
+    cudaStream_t st = Lf->stream;
+    int rc;
+    if ((rc = upload(&P->d_cols, cols, st)) || (rc = upload(&P->d_mask, mask, st)) || (rc = upload(&P->d_w, w, st)) ||
+        (rc = upload(&P->d_xoff, xoff, st)) || (rc = upload(&P->d_idx, idx, st)) || (rc = upload(&P->d_dv, dv, st))) {
+        vk::free_mask_plan(P);
+        return rc;
+    }
+    if (npart) VK_CUDA(cudaMalloc((void**)&P->d_part, sizeof(double) * (size_t)npart));
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { vk::free_mask_plan(P); return vk::cuda_check(e, "mask plan upload"); }
+    *out = P;
+    return VLASOV_OK;
+}
+
+int vlasov_reduce_moment_mask(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
+                              double* rho_finest) {
+    if (!levels || nlev < 1 || !rho_finest || !f) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (nlev > vk::MAXLEV) return vk::fail(VLASOV_EUNSUPPORTED, "more than 8 levels");
+    for (int l = 0; l < nlev; ++l)
+        if (!levels[l] || !f[l]) return vk::fail(VLASOV_EINVAL, "reduce_moment_mask: level / field pointer required");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    const vlasov_level* Lf = levels[nlev - 1];
+    bool fresh = Lf->mask_plan != nullptr && (int)Lf->mask_plan->uids.size() == nlev;
+    for (int l = 0; fresh && l < nlev; ++l) fresh = Lf->mask_plan->uids[l] == levels[l]->uid;
+    if (!fresh) {
+        vk::free_mask_plan(Lf->mask_plan);
+        Lf->mask_plan = nullptr;
+        vk::MaskPlan* P = nullptr;
+        if (int rc = build_mask_plan(levels, nlev, &P)) return rc;
+        Lf->mask_plan = P;
+    }
+    return vk::launch_reduce_mask(Lf->mask_plan, f, nlev, rho_finest, Lf->stream);
 }
 
 int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisson** out) {

@@ -103,6 +103,28 @@ def test_subpatch_reduction_parity(seed):
     np.testing.assert_allclose(rho, ref_mask, rtol=0, atol=1e-12 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("seed", range(10))
+def test_mask_reduction_parity(seed):
+    """Alg.6 Mask Reduction on the GPU (the paper's comparator) against the oracle's
+    mask_reduce on the same ghosted data, and against the GPU sub-patch reduction."""
+    rat, lb = random_hierarchy(seed)
+    H = drv.hierarchy(W, lb, rat)
+    data = _ic_data(H, noise_seed=seed)
+    G = _gpu(rat, lb)
+    rho_m = torch.zeros_like(G.rho)
+    with torch.cuda.stream(G.stream):
+        for L, b, lvl in zip(G.levels, G.bufs, data):
+            L.set_patches(b["A"], [a[2:-2, 2:-2] for a in lvl])
+        Eg = [torch.zeros(L.info.e_doubles, dtype=torch.float64, device="cuda") for L in G.levels]
+        G._fill([b["A"] for b in G.bufs], Eg)
+        api.vlasov_reduce_moment(G.handles, [b["A"] for b in G.bufs], G.rho)
+        api.vlasov_reduce_moment_mask(G.handles, [b["A"] for b in G.bufs], rho_m)
+    ghosted = G.get_state(ghost=2)
+    ref = reduction.mask_reduce(H.levels, ghosted, H.h0[1], H.ncells0[0])
+    np.testing.assert_allclose(rho_m.cpu().numpy(), ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+    np.testing.assert_allclose(rho_m.cpu().numpy(), G.rho.cpu().numpy(), rtol=0, atol=1e-12 * np.abs(ref).max())
+
+
 @pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
 @pytest.mark.parametrize("seed", [0, 1, 2, 3, 4, 5])
 def test_amr_steps_parity_random_hierarchies(seed, recon):
