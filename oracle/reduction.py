@@ -77,7 +77,13 @@ def mask_reduce(levels, data, dv0, nx0):
 
 
 def subpatch_reduce(levels, data, dv0, nx0):
-    """Alg.8.  Returns rho on the finest configuration mesh."""
+    """Alg.8.  Returns rho = 1 - n on the finest configuration mesh (electrons over the immobile
+    neutralising background)."""
+    return 1.0 - subpatch_moment(levels, data, dv0, nx0)
+
+
+def subpatch_moment(levels, data, dv0, nx0):
+    """Alg.8 velocity moment n = sum_l dv_l sum_v f (reading #13) on the finest configuration mesh."""
     rxf = _finest_rx(levels)
     total = np.zeros(nx0 * rxf)
     partials = []
@@ -98,7 +104,7 @@ def subpatch_reduce(levels, data, dv0, nx0):
             partials.append((b[0][0] * R, pp))
     for x0, pp in partials:
         total[x0: x0 + pp.size] += pp
-    return 1.0 - total
+    return total
 
 
 def inject(E_finest, rx_finest_over_level):
