@@ -179,6 +179,12 @@ int vlasov_rk4_stage(vlasov_level* level, int32_t stage, double dt, double* f_n,
  * patch, sub-patch).  The sub-patch plan is rebuilt lazily when any level changed.*/
 int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
                          double* rho_finest);
+/* Several species (one hierarchy each): rho[x] = (accumulate ? rho[x] : base)
+ * + q * n[x], n = sum_l dv_l sum_v f the same moment (direct or Alg.8); vlasov_reduce_moment is
+ * (q, base, accumulate) = (-1, 1, 0).  Call once per species, the first with accumulate = 0 and
+ * base = the background charge.                                                              */
+int vlasov_reduce_charge(const vlasov_level* const* levels, int32_t nlev, const double* const* f, double q,
+                         double base, int32_t accumulate, double* rho_finest);
 
 /* Alg.6 Mask Reduction: the same rho by refining every patch in x (linear5 with 2
  * ghost columns), masking the cells covered by the next finer level and summing over v -- the
@@ -207,6 +213,10 @@ int vlasov_poisson_destroy(vlasov_poisson* plan);
  * n_finest[1] cells.                                                                          */
 int vlasov_inject_field(vlasov_level* level, const double* E_finest, const int32_t n_finest[2],
                         double* E_lvl);
+/* As vlasov_inject_field (1D+1V) times `scale`: for species s the field entering its update is
+ * A_s = -(q_s/m_s) E (electrons: scale 1).                                         */
+int vlasov_inject_field_scaled(vlasov_level* level, const double* E_finest, const int32_t n_finest[2],
+                               double scale, double* E_lvl);
 
 /* ---- AMR transfers -------------------------------------------------------------- *
  * Flux registers of `fine` with respect to its coarser level: for every coarse face on the

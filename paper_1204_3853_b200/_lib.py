@@ -65,6 +65,8 @@ _SIGS = {
     "vlasov_rk4_stage_vp": (I32, [P, P, I32, D, P, P, P, P, P, P, P, P, I32, P]),
     "vlasov_reduce_moment": (I32, [C.POINTER(P), I32, C.POINTER(P), P]),
     "vlasov_reduce_moment_mask": (I32, [C.POINTER(P), I32, C.POINTER(P), P]),
+    "vlasov_reduce_charge": (I32, [C.POINTER(P), I32, C.POINTER(P), D, D, I32, P]),
+    "vlasov_inject_field_scaled": (I32, [P, P, PI32, D, P]),
     "vlasov_absmax": (I32, [P, I64, P, P]),
     "vlasov_poisson_create": (I32, [I32, D, P, C.POINTER(P)]),
     "vlasov_poisson_solve": (I32, [P, P, P, P, I32]),

@@ -82,9 +82,10 @@ class AmrVlasov1D:
         return [L.h for L in self.levels]
 
     # ------------------------------------------------------------------ state
-    def set_state(self, level_arrays):
+    def set_state(self, level_arrays, constraints: bool = True):
         """level_arrays[l]: whole-level-domain array (only patch cells are read) or a list of
-        per-patch interior arrays."""
+        per-patch interior arrays.  constraints=False: only load f (a multi-species driver then
+        evaluates the joint constraints)."""
         with torch.cuda.stream(self.stream):
             for L, b, a in zip(self.levels, self.bufs, level_arrays):
                 if isinstance(a, (list, tuple)):
@@ -95,7 +96,8 @@ class AmrVlasov1D:
                 E[0].zero_()
                 E[1].zero_()
             self.cur = 0
-            self._initial_constraints()
+            if constraints:
+                self._initial_constraints()
         self.stream.synchronize()
 
     def _initial_constraints(self):
@@ -301,3 +303,77 @@ class AmrVlasov1D:
 
     def cells(self):
         return sum(int(np.prod([hi[d] - lo[d] + 1 for d in range(2)])) for L in self.levels for lo, hi in L.boxes)
+
+
+class MultiSpeciesVlasov1D:
+    """Several species, one 1D+1V hierarchy (AmrVlasov1D) each, coupled only through the
+    configuration-space field and advanced synchronously (Alg.5).  Per
+    stage: the ghosts of every species (with its own previous field), the charge density
+    rho = rho_bg + sum_s q_s n_s (vlasov_reduce_charge, accumulated over species), one Poisson
+    solve on the common finest x mesh, and A_s = -(q_s/m_s) E injected into every level of species
+    s (vlasov_inject_field_scaled; electrons A = E), then the stage kernels and flux registers of
+    every species; after stage 4 the refluxing / average-down of every hierarchy."""
+
+    def __init__(self, hierarchies, charges, masses, rho_bg=0.0):
+        self.sp = list(hierarchies)
+        self.q = [float(q) for q in charges]
+        self.m = [float(m) for m in masses]
+        self.rho_bg = float(rho_bg)
+        nxf = {h.nxf for h in self.sp}
+        if len(nxf) != 1:
+            raise ValueError("species hierarchies must share the finest configuration mesh")
+        self.stream = self.sp[0].stream
+        h0 = self.sp[0]
+        self.nxf, self.dxf = h0.nxf, h0.dxf
+        self.poisson = api.Poisson(self.nxf, self.dxf, self.stream)
+        self.rho = torch.zeros(self.nxf, dtype=torch.float64, device="cuda")
+        self.E_f = torch.zeros(self.nxf, dtype=torch.float64, device="cuda")
+
+    def _constraints(self, fs_all, E_out_all):
+        for i, (h, fs) in enumerate(zip(self.sp, fs_all)):
+            api.vlasov_reduce_charge(h.handles, fs, self.q[i], self.rho_bg, i > 0, self.rho)
+        self.poisson.solve(self.rho, None, self.E_f, 0)
+        for i, h in enumerate(self.sp):
+            for l, L in enumerate(h.levels):
+                api.vlasov_inject_field_scaled(L.h, self.E_f, (self.nxf,), -self.q[i] / self.m[i], E_out_all[i][l])
+
+    def set_state(self, states):
+        """states[s]: level arrays of species s (as AmrVlasov1D.set_state)."""
+        for h, st in zip(self.sp, states):
+            h.set_state(st, constraints=False)
+        with torch.cuda.stream(self.stream):
+            A = [[b["A"] for b in h.bufs] for h in self.sp]
+            for h, fs in zip(self.sp, A):
+                h._fill(fs, [E[h.cur] for E in h.E])
+            self._constraints(A, [[E[h.cur] for E in h.E] for h in self.sp])
+        self.stream.synchronize()
+
+    def step(self, dt):
+        order = {1: ("A", "B"), 2: ("B", "C"), 3: ("C", "B"), 4: ("B", "A")}
+        with torch.cuda.stream(self.stream):
+            for h in self.sp:
+                for r in h.regs[1:]:
+                    r.zero_()
+            for s in (1, 2, 3, 4):
+                fs_all = [[b[order[s][0]] for b in h.bufs] for h in self.sp]
+                for h, fs in zip(self.sp, fs_all):
+                    h._fill(fs, [E[h.cur] for E in h.E])
+                E_cur = [[E[1 - h.cur] for E in h.E] for h in self.sp]
+                self._constraints(fs_all, E_cur)
+                for i, h in enumerate(self.sp):
+                    fnext = [b[order[s][1]] for b in h.bufs]
+                    for l, L in enumerate(h.levels):
+                        b = h.bufs[l]
+                        api.vlasov_rk4_stage(L.h, s, dt, b["A"], fs_all[i][l], b["U"], fnext[l], E_cur[i][l], None,
+                                             None, h.recon, None)
+                    for l in range(1, len(h.levels)):
+                        api.vlasov_flux_register_accumulate(h.levels[l].h, fs_all[i][l], E_cur[i][l],
+                                                            fs_all[i][l - 1], E_cur[i][l - 1], RK_B[s - 1],
+                                                            h.regs[l], h.recon)
+                    h.cur = 1 - h.cur
+            for h in self.sp:
+                for l in range(len(h.levels) - 1, 0, -1):
+                    api.vlasov_average_down(h.levels[l].h, h.bufs[l]["A"], h.bufs[l - 1]["A"], h.regs[l], dt)
+
+    def get_state(self):
+        return [h.get_state() for h in self.sp]

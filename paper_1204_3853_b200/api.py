@@ -16,7 +16,7 @@ from ._lib import Box, Geom, LevelInfo, check, lib
 __all__ = [
     "Level", "Poisson", "make_geom", "vlasov_level_create", "vlasov_level_destroy",
     "vlasov_level_get_info", "vlasov_level_layout", "vlasov_level_ghost_map", "vlasov_subpatches",
-    "vlasov_fill_ghosts", "vlasov_rhs", "vlasov_rk4_stage", "vlasov_rk4_stage_vp", "vlasov_reduce_moment", "vlasov_reduce_moment_mask",
+    "vlasov_fill_ghosts", "vlasov_rhs", "vlasov_rk4_stage", "vlasov_rk4_stage_vp", "vlasov_reduce_moment", "vlasov_reduce_moment_mask", "vlasov_reduce_charge", "vlasov_inject_field_scaled",
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
     "vlasov_level_fill_from", "vlasov_absmax", "vlasov_device_ok", "vlasov_last_error",
@@ -132,6 +132,18 @@ def vlasov_reduce_moment(levels, f_list, rho_finest):
 
 def vlasov_absmax(x, out, stream=None):
     return check(lib.vlasov_absmax(_ptr(x), x.numel(), _ptr(out), _stream_ptr(stream)))
+
+
+def vlasov_reduce_charge(levels, f_list, q, base, accumulate, rho_finest):
+    arr = (C.c_void_p * len(levels))(*[l.value if isinstance(l, C.c_void_p) else l for l in levels])
+    fp = (C.c_void_p * len(levels))(*[(t.data_ptr() if t is not None else None) for t in f_list])
+    return check(lib.vlasov_reduce_charge(arr, len(levels), fp, float(q), float(base), int(accumulate),
+                                          _ptr(rho_finest)))
+
+
+def vlasov_inject_field_scaled(h, E_finest, n_finest, scale, E_lvl):
+    n = (C.c_int32 * 2)(*(list(n_finest) + [1] * (2 - len(n_finest))))
+    return check(lib.vlasov_inject_field_scaled(h, _ptr(E_finest), n, float(scale), _ptr(E_lvl)))
 
 
 def vlasov_reduce_moment_mask(levels, f_list, rho_finest):

@@ -33,7 +33,8 @@ __global__ void k_red_cols(const LevelPtrs P, const RedCol* __restrict__ cols, i
 // rho[x] = 1 - sum over the contributions of x (level, patch, sub-patch order) of
 //          dv_l * sum_j b_j(s) colsum[c + j]          (linear5 refinement of the partial sums)
 __global__ void k_red_finest(const double* __restrict__ colsum, const RedContrib* __restrict__ con,
-                             const int32_t* __restrict__ xoff, int nxf, double* __restrict__ rho) {
+                             const int32_t* __restrict__ xoff, int nxf, double q, double base, int accumulate,
+                             double* __restrict__ rho) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= nxf) return;
     double acc = 0.0;
@@ -44,17 +45,19 @@ __global__ void k_red_finest(const double* __restrict__ colsum, const RedContrib
         for (int j = 0; j < 5; ++j) t += C.b[j] * colsum[C.cs + j];
         acc += C.dv * t;
     }
-    rho[x] = 1.0 - acc;
+    rho[x] = (accumulate ? rho[x] : base) + q * acc;
 }
 
-int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st) {
+int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st,
+                           double q, double base, int accumulate) {
     LevelPtrs lp;
     for (int l = 0; l < MAXLEV; ++l) lp.f[l] = l < nlev ? f[l] : nullptr;
     if (P->ncols > 0) {
         k_red_cols<<<(unsigned)((P->ncols + 7) / 8), 256, 0, st>>>(lp, P->d_cols, P->ncols, P->d_colsum);
         VK_LAUNCH("k_red_cols");
     }
-    k_red_finest<<<(P->nxf + 127) / 128, 128, 0, st>>>(P->d_colsum, P->d_contrib, P->d_xoff, P->nxf, rho);
+    k_red_finest<<<(P->nxf + 127) / 128, 128, 0, st>>>(P->d_colsum, P->d_contrib, P->d_xoff, P->nxf, q, base,
+                                                        accumulate, rho);
     VK_LAUNCH("k_red_finest");
     return VLASOV_OK;
 }

@@ -10,7 +10,7 @@ namespace vk {
 // rho[x] = 1 - dv * sum_v f[x][v] on a single block covering the domain (one warp per x row;
 // lane-strided sums combined by a fixed butterfly: deterministic)
 __global__ void k_moment_direct(const double* __restrict__ f, int64_t off, int pitch, int nx, int nv, double dv,
-                                double* __restrict__ rho) {
+                                double q, double base, int accumulate, double* __restrict__ rho) {
     const int lane = threadIdx.x & 31;
     const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (x >= nx) return;
@@ -19,13 +19,13 @@ __global__ void k_moment_direct(const double* __restrict__ f, int64_t off, int p
     for (int j = lane; j < nv; j += 32) s += row[j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) rho[x] = 1.0 - dv * s;
+    if (lane == 0) rho[x] = (accumulate ? rho[x] : base) + q * (dv * s);
 }
 
-int launch_moment_direct(const vlasov_level* L, const double* f, double* rho) {
+int launch_moment_direct(const vlasov_level* L, const double* f, double* rho, double q, double base, int accumulate) {
     const int nx = L->dom[0], nv = L->dom[1];
     k_moment_direct<<<(nx + 7) / 8, 256, 0, L->stream>>>(f, L->block_off[0], (int)L->block_str[0][0], nx, nv,
-                                                          L->h[1], rho);
+                                                          L->h[1], q, base, accumulate, rho);
     VK_LAUNCH("k_moment_direct");
     return VLASOV_OK;
 }
@@ -127,22 +127,22 @@ int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E,
     return VLASOV_OK;
 }
 
-// E_lvl[i + 2] = mean_{s<R} E_f[R i + s]; periodic ghosts i = -2, -1, n, n+1.
-__global__ void k_inject_1d(const double* __restrict__ Ef, int nf, int R, int n, double* __restrict__ El) {
+// E_lvl[i + 2] = scale * mean_{s<R} E_f[R i + s]; periodic ghosts i = -2, -1, n, n+1.
+__global__ void k_inject_1d(const double* __restrict__ Ef, int nf, int R, int n, double scale, double* __restrict__ El) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n + 4) return;
     int i = t - 2;
     i = (i < 0) ? i + n : (i >= n ? i - n : i);
     double s = 0.0;
     for (int q = 0; q < R; ++q) s += Ef[(int64_t)i * R + q];
-    El[t] = (R == 1) ? s : s / (double)R;
+    El[t] = scale * ((R == 1) ? s : s / (double)R);
 }
 
-int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest, double* E_lvl) {
+int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest, double* E_lvl, double scale) {
     const int n = L->dom[0];
     if (n_finest % n) return fail(VLASOV_EINVAL, "inject: finest size not a multiple of the level size");
     const int R = n_finest / n;
-    k_inject_1d<<<(n + 4 + 127) / 128, 128, 0, L->stream>>>(E_finest, n_finest, R, n, E_lvl);
+    k_inject_1d<<<(n + 4 + 127) / 128, 128, 0, L->stream>>>(E_finest, n_finest, R, n, scale, E_lvl);
     VK_LAUNCH("k_inject_1d");
     return VLASOV_OK;
 }

@@ -204,14 +204,16 @@ int stage_1d1v_tile_width(bool wide);   // cells per v-tile of the stage kernel
 int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n);
 int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double* E_bc,
                 const double* f0v, int interp);
-int launch_moment_direct(const vlasov_level* L, const double* f, double* rho);
+int launch_moment_direct(const vlasov_level* L, const double* f, double* rho, double q = -1.0, double base = 1.0,
+                         int accumulate = 0);
 int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E, int ghost);
-int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest, double* E_lvl);
+int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest, double* E_lvl, double scale = 1.0);
 int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest,
                      double* E_lvl);
 int linear5_weights(int R, double* out /* R*5 */);
 int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st);
-int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
+int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st,
+                           double q = -1.0, double base = 1.0, int accumulate = 0);
 int launch_flux_registers(const vlasov_level* L, const double* f_fine, const double* E_fine, const double* f_coarse,
                           const double* E_coarse, double b_s, double* regs, int recon);
 int launch_average_down(const vlasov_level* L, const double* f_fine, double* f_coarse, const double* regs, double dt);

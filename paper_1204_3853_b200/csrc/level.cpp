@@ -1247,17 +1247,20 @@ int vlasov_rk4_stage_vp(vlasov_level* L, const vlasov_poisson* plan, int32_t sta
                                  E_bc, f0v, recon, rho_next, rho_s, plan->d_gE, E_s);
 }
 
-int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
-                         double* rho_finest) {
+int vlasov_reduce_charge(const vlasov_level* const* levels, int32_t nlev, const double* const* f, double q,
+                         double base, int32_t accumulate, double* rho_finest) {
     if (!levels || nlev < 1 || !rho_finest || !f) return vk::fail(VLASOV_EINVAL, "null argument");
     if (nlev > vk::MAXLEV) return vk::fail(VLASOV_EUNSUPPORTED, "more than 8 levels");
     for (int l = 0; l < nlev; ++l)
         if (!levels[l] || !f[l]) return vk::fail(VLASOV_EINVAL, "reduce_moment: level / field pointer required");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 2)
-        return vk::launch_moment_direct(levels[0], f[0], rho_finest);
-    if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 4)
+        return vk::launch_moment_direct(levels[0], f[0], rho_finest, q, base, accumulate);
+    if (nlev == 1 && levels[0]->single_block && levels[0]->ndim == 4) {
+        if (q != -1.0 || base != 1.0 || accumulate)
+            return vk::fail(VLASOV_EUNSUPPORTED, "reduce_charge: 2D+2V levels compute the electron density 1 - n only");
         return vk::launch_moment_2d2v(levels[0], f[0], rho_finest);
+    }
     const vlasov_level* Lf = levels[nlev - 1];
     bool fresh = Lf->red_plan != nullptr && (int)Lf->red_plan->uids.size() == nlev;
     for (int l = 0; fresh && l < nlev; ++l) fresh = Lf->red_plan->uids[l] == levels[l]->uid;
@@ -1268,7 +1271,12 @@ int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const 
         if (int rc = build_red_plan(levels, nlev, &P)) return rc;
         Lf->red_plan = P;
     }
-    return vk::launch_reduce_subpatch(Lf->red_plan, f, nlev, rho_finest, Lf->stream);
+    return vk::launch_reduce_subpatch(Lf->red_plan, f, nlev, rho_finest, Lf->stream, q, base, accumulate);
+}
+
+int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
+                         double* rho_finest) {
+    return vlasov_reduce_charge(levels, nlev, f, -1.0, 1.0, 0, rho_finest);
 }
 
 int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream) {
@@ -1458,6 +1466,14 @@ int vlasov_inject_field(vlasov_level* L, const double* E_finest, const int32_t n
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (L->ndim == 2) return vk::launch_inject_1d(L, E_finest, n_finest[0], E_lvl);
     return vk::launch_inject_2d(L, E_finest, n_finest, E_lvl);
+}
+
+int vlasov_inject_field_scaled(vlasov_level* L, const double* E_finest, const int32_t n_finest[2], double scale,
+                               double* E_lvl) {
+    if (!L || !E_finest || !n_finest || !E_lvl) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "inject_field_scaled: 1D+1V levels only");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_inject_1d(L, E_finest, n_finest[0], E_lvl, scale);
 }
 
 int vlasov_flux_register_accumulate(vlasov_level* fine, const double* f_fine, const double* E_fine,
