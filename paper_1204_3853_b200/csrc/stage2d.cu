@@ -44,6 +44,13 @@ constexpr int S2_LW = S2_TM + 4;          // doubles per line segment in a slot
 #define S2_NSLOT_CFG 3
 #endif
 constexpr int S2_NSLOT = S2_NSLOT_CFG;
+// 1: the velocity ghost frame of f_s is derived in global memory by k_vghost_2d2v before the stage
+// (TMA then loads ghost values like interior ones; no ghost warp, branch-free consumers);
+// 0: a ghost warp derives them in every landed slot
+#ifndef S2_GLOBAL_GHOSTS
+#define S2_GLOBAL_GHOSTS 1
+#endif
+constexpr int S2_GWARP = S2_GLOBAL_GHOSTS ? 0 : 1;
 constexpr int S2_NLINE = 8 + 16 + 8 + 4;  // A + B + C + D line segments per slot
 
 struct TMaps2 {                // TMA tensor maps over the ghosted level block [x][y][vx][vy]
@@ -85,7 +92,7 @@ __device__ __forceinline__ int wrapi(int i, int n) {
 }
 
 template <int STAGE, int RECON>
-__global__ void __launch_bounds__(32 * (S2_LT + 2), 2) k_stage_2d2v(const StageArgs2 A, const __grid_constant__ TMaps2 M) {
+__global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(const StageArgs2 A, const __grid_constant__ TMaps2 M) {
     using SL = Slot2<STAGE>;
     constexpr int SIZE = SL::SIZE;
     extern __shared__ __align__(128) double smem[];
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(32 * (S2_LT + 2), 2) k_stage_2d2v(const StageA
         return;
     }
 
-    if (warp == S2_LT + 1) {                                      // ---------------- ghost warp
+    if (S2_GWARP && warp == S2_LT + 1) {                          // ---------------- ghost warp
         // vy ghost columns of the 24 line segments the consumers read as (m0-2 .. m0+3) triples
         // (A, B lines 2..5; C, D lines 0..3), characteristic condition (reading #6) with E_bc of
         // the segment's (x, y); task descriptors precomputed, <= 2 tasks per lane per slot.
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(32 * (S2_LT + 2), 2) k_stage_2d2v(const StageA
     // condition from the part's interior lines, a = -E_x of the part's (x, y)
     auto line_pair = [&](const double* part, int L, double a) -> double2 {
         const int lg = l0 - 2 + L;
-        if (ledge && (lg < 0 || lg >= A.nvx)) {
+        if (S2_GWARP && ledge && (lg < 0 || lg >= A.nvx)) {
             const bool lo = lg < 0;
             if (lo ? (a < 0.0) : (a > 0.0)) {
                 const int j0 = lo ? 0 : A.nvx - 1, dj = lo ? 1 : -1;
@@ -286,7 +293,7 @@ __global__ void __launch_bounds__(32 * (S2_LT + 2), 2) k_stage_2d2v(const StageA
             const int q = q0 + K;
             if (q < Q) {
                 const int r = wrapi(x0 - 2 + q, A.nx);
-                mbar_wait(&ready_bar[slot], phase);
+                mbar_wait(S2_GWARP ? &ready_bar[slot] : &full_bar[slot], phase);
                 const double* SA = smem + slot * SIZE;
                 const double* SB = SA + 8 * S2_LW;
                 const double* SC = SB + 16 * S2_LW;
@@ -433,6 +440,46 @@ __global__ void __launch_bounds__(32 * (S2_LT + 2), 2) k_stage_2d2v(const StageA
     }
 }
 
+// Velocity ghost frame of f (characteristic condition, reading #6, a = -E_bc of the (x, y) column):
+// threads [0, nx ny nvx): the vy ghosts m = -2, -1, nvy, nvy+1 of one (x, y, vx) line;
+// threads [nx ny nvx, nx ny (nvx + nvy)): the vx ghosts l = -2, -1, nvx, nvx+1 at one (x, y, vy).
+// Only the ghosts the stage stencils read are derived (vx ghosts at interior vy and vice versa).
+__global__ void k_vghost_2d2v(double* __restrict__ f, int64_t org, int64_t s0, int64_t s1, int64_t s2, int nx, int ny,
+                              int nvx, int nvy, const double* __restrict__ E_bc, const double* __restrict__ f0v) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n1 = (int64_t)nx * ny * nvx, n2 = (int64_t)nx * ny * nvy;
+    if (t >= n1 + n2) return;
+    const int nyg = ny + 4;
+    const bool vy = t < n1;
+    const int64_t u = vy ? t : t - n1;
+    const int inner = vy ? nvx : nvy;
+    const int li = (int)(u % inner);
+    const int64_t xy = u / inner;
+    const int i = (int)(xy / ny), k = (int)(xy % ny);
+    const int64_t col = (int64_t)(i + 2) * nyg + (k + 2);
+    const double a = -__ldg(E_bc + (vy ? (int64_t)(nx + 4) * nyg : 0) + col);
+    double* base = f + org + (int64_t)i * s0 + (int64_t)k * s1;
+    const int64_t st = vy ? 1 : s2;                               // stride along the ghosted dim
+    double* line = vy ? base + (int64_t)li * s2 : base + li;     // element 0 of the ghosted dim
+    const int n = vy ? nvy : nvx;
+    auto prof = [&](int g) {                                      // profile at ghosted index g of the dim
+        return vy ? __ldg(f0v + (int64_t)(li + 2) * (nvy + 4) + (g + 2)) : __ldg(f0v + (int64_t)(g + 2) * (nvy + 4) + (li + 2));
+    };
+    {   // low side
+        const double f0 = line[0], f1 = line[st], f2 = line[2 * st], f3 = line[3 * st];
+        const bool out = a < 0.0;
+        line[-st] = out ? 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3 : prof(-1);
+        line[-2 * st] = out ? 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3 : prof(-2);
+    }
+    {   // high side
+        double* e = line + (int64_t)(n - 1) * st;
+        const double f0 = e[0], f1 = e[-st], f2 = e[-2 * st], f3 = e[-3 * st];
+        const bool out = a > 0.0;
+        e[st] = out ? 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3 : prof(n);
+        e[2 * st] = out ? 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3 : prof(n + 1);
+    }
+}
+
 // rho[i][k] = 1 - dvx dvy sum_p partials[p][i][k]  (fixed order: deterministic)
 __global__ void k_moment_2d2v_finish(const double* __restrict__ partials, int np, int ncfg, double dvv,
                                      double* __restrict__ rho) {
@@ -469,7 +516,7 @@ static int launch2_t(const StageArgs2& A, const TMaps2& M, dim3 grid, cudaStream
         VK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    kern<<<grid, 32 * (S2_LT + 2), smem, st>>>(A, M);
+    kern<<<grid, 32 * (S2_LT + 1 + S2_GWARP), smem, st>>>(A, M);
     VK_LAUNCH("k_stage_2d2v");
     return VLASOV_OK;
 }
@@ -546,6 +593,12 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
     if ((rc = encode_map(L, f_s, S2_LW, 8, &M.fs8)) || (rc = encode_map(L, f_s, S2_LW, 4, &M.fs4)) ||
         (rc = encode_map(L, f_n ? f_n : f_s, S2_TM, 4, &M.fn4)) || (rc = encode_map(L, u ? u : f_s, S2_TM, 4, &M.u4)))
         return rc;
+    if (S2_GLOBAL_GHOSTS) {
+        const int64_t nt = (int64_t)A.nx * A.ny * (A.nvx + A.nvy);
+        k_vghost_2d2v<<<(unsigned)((nt + 255) / 256), 256, 0, L->stream>>>(const_cast<double*>(f_s), A.org, A.s0, A.s1,
+                                                                           A.s2, A.nx, A.ny, A.nvx, A.nvy, E_bc, f0v);
+        VK_LAUNCH("k_vghost_2d2v");
+    }
     rc = recon == VLASOV_UPWIND ? dispatch2<VLASOV_UPWIND>(stage, A, M, grid, L->stream)
                                 : dispatch2<VLASOV_CENTERED4>(stage, A, M, grid, L->stream);
     if (rc || !rho) return rc;
