@@ -40,6 +40,9 @@ constexpr int S2_LW = S2_TM + 4;          // doubles per line segment in a slot
 #ifndef S2_MAXNREG
 #define S2_MAXNREG 200
 #endif
+#ifndef S2_MAXNREG_ON
+#define S2_MAXNREG_ON 0
+#endif
 #ifndef S2_NSLOT_CFG
 #define S2_NSLOT_CFG 3
 #endif
@@ -92,7 +95,12 @@ __device__ __forceinline__ int wrapi(int i, int n) {
 }
 
 template <int STAGE, int RECON>
-__global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(const StageArgs2 A, const __grid_constant__ TMaps2 M) {
+#if S2_MAXNREG_ON
+__global__ void __maxnreg__(S2_MAXNREG) k_stage_2d2v(
+#else
+__global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
+#endif
+    const StageArgs2 A, const __grid_constant__ TMaps2 M) {
     using SL = Slot2<STAGE>;
     constexpr int SIZE = SL::SIZE;
     extern __shared__ __align__(128) double smem[];
