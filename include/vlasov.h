@@ -145,11 +145,16 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
  *   stage 2: u = f_n + (f_s - f_n)/3 + dt/3 k(f_s);  f_next = f_n + dt/2 k(f_s)
  *   stage 3: f_next = f_n + dt k(f_s)
  *   stage 4: f_next = u + (f_s - f_n)/3 + dt/6 k(f_s)           (f_next may alias f_n)
- * Ghosts of f_s: if E_bc and f0v are both non-NULL the level must be ONE block covering the
- * (periodic) domain with a number of velocity cells divisible by 4; the kernel then derives the ghost
- * values itself (periodic wrap in x, characteristic v-boundary condition with E_bc, exactly as
- * vlasov_fill_ghosts(E_bc, f0v) would) and never reads the ghost frame.  Otherwise (NULL) the
- * ghost frame of f_s must have been filled by vlasov_fill_ghosts.
+ * Ghosts of f_s: if f0v is non-NULL the level must be ONE block covering the (periodic) domain
+ * with a number of velocity cells divisible by 4; x is wrapped periodically in-kernel (the ghost
+ * rows are never read), and the velocity ghosts of f_s follow the characteristic v-boundary
+ * condition (reading #6) either derived in-kernel from E_bc (E_bc non-NULL, exactly as
+ * vlasov_fill_ghosts(E_bc, f0v) would) or, with E_bc == NULL ("carried ghosts"), read from f_s's
+ * velocity ghost columns.  With f0v non-NULL the stage also writes f_next's velocity ghost columns
+ * (interior rows) for the field E of this stage -- the E_bc of the next stage (reading #6b) -- so a
+ * chain of stages with E_bc == NULL needs one vlasov_fill_ghosts of the initial state only.
+ * With f0v == NULL (E_bc must be NULL too) the ghost frame of f_s must have been filled by
+ * vlasov_fill_ghosts.
  * rho_next (nullable; single block covering the domain only): receives the velocity moment of
  * f_next, rho = 1 - dv sum_v f_next, fused into the stage: per-(row, v-tile) partial
  * sums combined in a fixed order by the last CTA of each row strip (deterministic).            */
@@ -159,9 +164,9 @@ int vlasov_rhs(vlasov_level* level, const double* f, const double* E, double* k,
  * uniform 1D+1V level: E_s = -D4 phi(rho_s) (readings #1-#2; the same operator as
  * vlasov_poisson_solve with `plan`) is computed inside the stage kernel from rho_s, the moment of
  * f_s, and written to E_s (the level's ghosted E array), then the stage runs as vlasov_rk4_stage
- * with E = E_s.  Requirements: the in-kernel ghost mode (E_bc, f0v non-NULL, one periodic block,
- * nv % 4 == 0), plan->n == the level's x cells <= 4096, rho_next != rho_s (ping-pong buffers).
- * One launch per stage instead of two.                                                          */
+ * with E = E_s.  Requirements: f0v non-NULL (one periodic block, nv % 4 == 0; E_bc non-NULL or
+ * carried ghosts as in vlasov_rk4_stage), plan->n == the level's x cells <= 4096, even,
+ * rho_next != rho_s (ping-pong buffers).  One launch per stage instead of two.                  */
 int vlasov_rk4_stage_vp(vlasov_level* level, const vlasov_poisson* plan, int32_t stage, double dt,
                         double* f_n, const double* f_s, double* u, double* f_next, const double* rho_s,
                         double* E_s, const double* E_bc, const double* f0v, int32_t recon,

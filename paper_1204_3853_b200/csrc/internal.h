@@ -14,6 +14,7 @@
 namespace vk {
 
 constexpr int G = 2;              // ghost width (reading #7)
+constexpr int GX_PAD = 16;        // padding of the periodically extended Green's function gX
 constexpr int MAXR = 16;          // largest refinement ratio per dim supported by the transfers
 
 // ------------------------------------------------------------------ errors
@@ -187,6 +188,7 @@ struct vlasov_poisson {
     cudaStream_t stream = nullptr;
     double* d_gE = nullptr;
     double* d_gphi = nullptr;
+    double* d_gX = nullptr;               // gX[m] = gE[(m - GX_PAD) mod n], m < 2n + 2 GX_PAD
 };
 
 namespace vk {
@@ -194,7 +196,7 @@ namespace vk {
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s,
                       double* u, double* f_next, const double* E, const double* E_bc,
                       const double* f0v, int recon, double* rho, const double* rho_in = nullptr,
-                      const double* gE = nullptr, double* E_out = nullptr);
+                      const double* gE = nullptr, double* E_out = nullptr, const double* gX = nullptr);
 int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
                       double* rho);

@@ -1213,8 +1213,8 @@ int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, con
     if ((stage == 2 || stage == 4) && !u) return vk::fail(VLASOV_EINVAL, "u required");
     if (recon != VLASOV_CENTERED4 && recon != VLASOV_UPWIND) return vk::fail(VLASOV_EINVAL, "bad recon");
     if (rho_next && !L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "fused moment needs a single-block level");
-    if ((E_bc == nullptr) != (f0v == nullptr)) return vk::fail(VLASOV_EINVAL, "E_bc and f0v go together");
-    if (E_bc && !L->self_ghost_ok)
+    if (E_bc && !f0v) return vk::fail(VLASOV_EINVAL, "E_bc needs f0v");
+    if (f0v && !L->self_ghost_ok)
         return vk::fail(VLASOV_EUNSUPPORTED, "in-kernel ghosts need one periodic block with nv a multiple of 4");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (L->ndim == 4) {
@@ -1229,7 +1229,7 @@ int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, con
 int vlasov_rk4_stage_vp(vlasov_level* L, const vlasov_poisson* plan, int32_t stage, double dt, double* f_n,
                         const double* f_s, double* u, double* f_next, const double* rho_s, double* E_s,
                         const double* E_bc, const double* f0v, int32_t recon, double* rho_next) {
-    if (!L || !plan || !f_s || !f_next || !rho_s || !E_s || !E_bc || !f0v)
+    if (!L || !plan || !f_s || !f_next || !rho_s || !E_s || !f0v)
         return vk::fail(VLASOV_EINVAL, "null argument");
     if (stage < 1 || stage > 4) return vk::fail(VLASOV_EINVAL, "stage must be 1..4");
     if (stage >= 2 && !f_n) return vk::fail(VLASOV_EINVAL, "f_n required");
@@ -1244,7 +1244,7 @@ int vlasov_rk4_stage_vp(vlasov_level* L, const vlasov_poisson* plan, int32_t sta
     if (rho_next == rho_s) return vk::fail(VLASOV_EINVAL, "rk4_stage_vp: rho_next must not alias rho_s");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E_s,
-                                 E_bc, f0v, recon, rho_next, rho_s, plan->d_gE, E_s);
+                                 E_bc, f0v, recon, rho_next, rho_s, plan->d_gE, E_s, plan->d_gX);
 }
 
 int vlasov_reduce_charge(const vlasov_level* const* levels, int32_t nlev, const double* const* f, double q,
@@ -1423,8 +1423,11 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
         gE[d] = (double)(aE / n);
         gphi[d] = (double)(aP / n);
     }
-    // gE is stored periodically extended (2n + 4 values, gE[j] = g[j mod n]) so that the fused
-    // stage kernel can read g[(i - k) mod n] = gE[i - k + n] without a modulo
+    // gE is stored periodically extended (2n + 4 values, gE[j] = g[j mod n]); gX (fused stage
+    // kernel) is the same with GX_PAD values of padding on both sides, gX[m] = g[(m - GX_PAD) mod n],
+    // so that the prologue reads g[(i - k) mod n] = gX[GX_PAD + n + i - k] without a modulo
+    std::vector<double> gX(2 * (size_t)n + 2 * vk::GX_PAD);
+    for (size_t m = 0; m < gX.size(); ++m) gX[m] = gE[((int64_t)m - vk::GX_PAD + 2 * (int64_t)n) % n];
     gE.resize(2 * (size_t)n + 4);
     for (size_t j = n; j < gE.size(); ++j) gE[j] = gE[j % n];
     vlasov_poisson* P = new vlasov_poisson();
@@ -1432,14 +1435,20 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
     P->dx = dx;
     P->stream = (cudaStream_t)cuda_stream;
     int rc;
-    if ((rc = upload(&P->d_gE, gE, P->stream)) || (rc = upload(&P->d_gphi, gphi, P->stream))) {
+    if ((rc = upload(&P->d_gE, gE, P->stream)) || (rc = upload(&P->d_gphi, gphi, P->stream)) ||
+        (rc = upload(&P->d_gX, gX, P->stream))) {
         cudaFree(P->d_gE);
         cudaFree(P->d_gphi);
+        cudaFree(P->d_gX);
         delete P;
         return rc;
     }
     cudaError_t e = cudaStreamSynchronize(P->stream);
-    if (e != cudaSuccess) { cudaFree(P->d_gE); cudaFree(P->d_gphi); delete P; return vk::cuda_check(e, "poisson upload"); }
+    if (e != cudaSuccess) {
+        cudaFree(P->d_gE); cudaFree(P->d_gphi); cudaFree(P->d_gX);
+        delete P;
+        return vk::cuda_check(e, "poisson upload");
+    }
     *out = P;
     return VLASOV_OK;
 }
@@ -1456,6 +1465,7 @@ int vlasov_poisson_destroy(vlasov_poisson* P) {
         cudaStreamSynchronize(P->stream);
         cudaFree(P->d_gE);
         cudaFree(P->d_gphi);
+        cudaFree(P->d_gX);
         delete P;
     }
     return VLASOV_OK;

@@ -26,6 +26,20 @@
 
 namespace vk {
 
+// STAGE1D_TRACE (experiments only): per-CTA %globaltimer stamps of the kernel's phases, read back
+// with vlasov_debug_stage_trace (not part of the C ABI of include/vlasov.h)
+#ifdef STAGE1D_TRACE
+__device__ unsigned long long g_trace[2048][10];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(i) do { if (threadIdx.x == 0) g_trace[blockIdx.x][i] = gtimer(); } while (0)
+#else
+#define TRACE(i) do { } while (0)
+#endif
+
 struct StageArgs1 {
     const double* f_s;
     const double* f_n;
@@ -47,10 +61,23 @@ struct StageArgs1 {
     const double* gE;          // Green's function of E = -D4 phi(rho) (Poisson plan, dom_x values)
     double* E_out;             // ghosted level E array (owned rows + periodic ghosts)
     int cluster;               // CTAs per cluster of the fused launch (the v-tiles of a strip)
+    int g_smem;                // fused field: gX staged in shared memory too
+    const double* gX;          // gX[m] = g[(m - GX_PAD) mod n], m in [0, 2n + 2 GX_PAD)
+    int nstrip1;               // > 0: single block, tiles computed from blockIdx (no table load)
+    Block1 blk0;               // that block
 };
 
-// shared memory of the fused field prologue: rho [n], row results [<= 4 NT]
-static size_t field_smem_bytes(int n, int nt) { return (size_t)(n + 4 * nt) * sizeof(double); }
+// the fused prologue stages the whole (periodically extended) Green's function in shared memory
+// for n <= G_SMEM_MAX_N (two CTAs per SM still fit); larger n reads it through L1
+constexpr int G_SMEM_MAX_N = 2048;
+static bool g_in_smem(int n) { return n <= G_SMEM_MAX_N; }
+// shared memory of the fused field prologue: rho [n], row results [PART_MAX >= tile_rows + 4],
+// gX [2n + 2 GX_PAD]
+constexpr int PART_MAX = 136;
+static size_t field_smem_bytes(int n) {
+    return (size_t)(n + PART_MAX + (g_in_smem(n) ? 2 * n + 2 * GX_PAD : 0)) * sizeof(double);
+}
+constexpr int EROWS = 8;   // rows of E per warp group in the fused prologue (Toeplitz blocking)
 
 // CPT = 4 cells per consumer thread, TV = 4*NT cells per v-tile.
 #ifndef STAGE1D_CPT
@@ -82,7 +109,7 @@ struct StageGeom {
     static constexpr int NSLOT = NSLOT_RAW < 3 ? 3 : (NSLOT_RAW > 16 ? 16 : NSLOT_RAW);
     static constexpr int NW = NT / 32;
     static size_t smem_bytes(int tile_rows) {
-        return (size_t)(NSLOT * SLOT + NW * tile_rows + 2 * (tile_rows + 4)) * sizeof(double);
+        return (size_t)(NSLOT * SLOT + NW * tile_rows + 2 * (tile_rows + 4) + 2 * CPT * tile_rows) * sizeof(double);
     }
 };
 
@@ -102,10 +129,29 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
     __shared__ __align__(8) uint64_t field_bar;
     __shared__ __align__(8) uint64_t e_bar;      // fused field: all Q rows of E have landed
     __shared__ unsigned s_ticket;
+    __shared__ double s_f0[4];                   // f0v at v-ghost columns -2, -1, nv, nv + 1 (SELF)
     double* psum = smem + NSLOT * SLOT;          // [NW][tile_rows]
 
-    const Tile1 T = A.tiles[blockIdx.x];
-    const Block1 B = A.blocks[T.block];
+    TRACE(0);
+#ifdef STAGE1D_TRACE
+    if (threadIdx.x == 0) { unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); g_trace[blockIdx.x][8] = sm; }
+#endif
+    Tile1 T;
+    Block1 B;
+    if (A.nstrip1 > 0) {                         // single block: the tiling of build_tiles_1d
+        B = A.blk0;
+        const int st = blockIdx.x / A.n_vtiles, vt = blockIdx.x - st * A.n_vtiles;
+        T.block = 0;
+        T.x0 = (int)((int64_t)B.nx * st / A.nstrip1);
+        T.nrows = (int)((int64_t)B.nx * (st + 1) / A.nstrip1) - T.x0;
+        T.j0 = vt * TV;
+        T.ncols = min(TV, B.nv - T.j0);
+        T.pvt = vt;
+        T.strip = st;
+    } else {
+        T = A.tiles[blockIdx.x];
+        B = A.blocks[T.block];
+    }
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int Q = T.nrows + 4;
@@ -116,8 +162,9 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
     for (int t = tid; t < Q; t += blockDim.x) {
         const int gi = B.lo_x + T.x0 - 2 + t + G;  // index in the ghosted level E array
         if (!field) sE[t] = __ldg(A.E + gi);
-        if (SELF) sEbc[t] = __ldg(A.E_bc + gi);
+        if (SELF && A.E_bc) sEbc[t] = __ldg(A.E_bc + gi);
     }
+    if (SELF && tid < 4) s_f0[tid] = __ldg(A.f0v + (tid < 2 ? tid : A.dom_v + tid));
     if (tid == 0) {
         for (int s = 0; s < NSLOT; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -132,13 +179,19 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
     const uint32_t crank = field ? cluster_ctarank() : 0u, csize = field ? cluster_nctarank() : 1u;
     if (tid == 0 && csize > 1) mbar_arrive_expect_tx(&e_bar, (uint32_t)Q * 8u);
     __syncthreads();
-    if (field && csize > 1) cluster_sync_all();
+    // consumers arrive now and wait only before their first remote store; the producer waits at once
+    if (field && csize > 1) {
+        if (PWARPS && warp == NW) cluster_sync_all();
+        else cluster_arrive();
+    }
+    TRACE(1);
 
     // row r (block-local interior index, may be -2..nx+1): interior column 0 of that row
     auto rowbase = [&](int r) -> int64_t { return B.off + (int64_t)(r + G) * B.pitch + G; };
 
     // fused field: rho and the Green's function (twice: periodic extension) staged by the TMA engine
-    double* f_rho = sEbc + (A.tile_rows + 4);
+    double* s_edge = sEbc + (A.tile_rows + 4);   // [tile_rows][2 sides][CPT] boundary cells of f_next
+    double* f_rho = s_edge + 2 * CPT * A.tile_rows;
     const uint32_t seg_bytes = (uint32_t)(wpad + 4) * 8u;
     const uint32_t row_bytes = (uint32_t)wpad * 8u;
     // TMA loads of row step q into ring slot `sl`
@@ -156,11 +209,14 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
         if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(r - 2) + T.j0, row_bytes, &full_bar[sl]);
         if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(r - 2) + T.j0, row_bytes, &full_bar[sl]);
     };
+    double* f_g = f_rho + A.dom_x + PART_MAX;      // gX staged (A.g_smem)
     auto issue_field = [&]() {
         if (field) {
             const uint32_t nb = (uint32_t)A.dom_x * 8u;
-            mbar_arrive_expect_tx(&field_bar, nb);
+            const uint32_t ng = A.g_smem ? (uint32_t)(2 * A.dom_x + 2 * GX_PAD) * 8u : 0u;
+            mbar_arrive_expect_tx(&field_bar, nb + ng);
             bulk_g2s(f_rho, A.rho_in, nb, &field_bar);
+            if (ng) bulk_g2s(f_g, A.gX, ng, &field_bar);
         }
     };
     if (PWARPS && warp == NW) {                  // ---------------- producer warp
@@ -184,62 +240,100 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
     // ---------------------------------------------------------------- consumers
     if (field) {
         // Constraint evaluation of the stage state (Alg.5) while the producer fills the
-        // ring: project rho to mean zero, E_i = sum_k gE[(i - k) mod n] rho_k for the rows of this
-        // tile, from rho and the periodically extended gE staged in shared memory by the TMA engine.
+        // ring: E_i = sum_k g[(i - k) mod n] (rho_k - mean) for the rows of this tile (projection to
+        // mean zero, applied on the fly), from rho and the periodically extended g staged
+        // in shared memory by the TMA engine (through L1 for n > G_SMEM_MAX_N).
         const int n = A.dom_x;
-        double* s_rho = f_rho;
-        double* s_part = s_rho + n;              // [Q] E of the tile rows
+        const double* s_rho = f_rho;
+        double* s_part = f_rho + n;              // [Q] E of the tile rows
         mbar_wait(&field_bar, 0);
-        double acc = 0.0;
-        for (int k = tid; k < n; k += NT) acc += s_rho[k];
+        TRACE(2);
+        {   // mean: warp w sums the w-th quarter of rho (lanes strided), warp partials in warp order
+            const int kb = (int)((int64_t)n * warp / NW), ke = (int)((int64_t)n * (warp + 1) / NW);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int k = kb + lane;
+            for (; k + 96 < ke; k += 128) {
+                a0 += s_rho[k]; a1 += s_rho[k + 32]; a2 += s_rho[k + 64]; a3 += s_rho[k + 96];
+            }
+            for (; k < ke; k += 32) a0 += s_rho[k];
+            double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) psum[warp] = acc;
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) psum[warp] = acc;
+        }
         named_bar_sync(1, NT);
         double mean = 0.0;
+#pragma unroll
         for (int w = 0; w < NW; ++w) mean += psum[w];
         mean /= (double)n;
-        for (int k = tid; k < n; k += NT) s_rho[k] -= mean;          // projection
-        named_bar_sync(1, NT);
-        // The rows of the tile are split over the CTAs of the cluster (the strip's v-tiles compute
+        TRACE(3);
+        // Rows [tb, te) of the tile are this CTA's share (the strip's v-tiles of a cluster compute
         // disjoint row ranges); each row is pushed into every CTA's s_part with st.async, which
-        // completes on that CTA's e_bar.  One warp per group of 4 consecutive rows: lanes stride k
-        // (conflict-free shared-memory reads; rho[k] shared by the 4 rows), 8 accumulators, fixed
-        // butterflies -> deterministic.
+        // completes on that CTA's e_bar.  Toeplitz blocking: a warp computes EROWS consecutive
+        // rows; lane l sums over its own contiguous k-chunk [C l, C l + C) (C odd: conflict-free
+        // shared-memory banks) with a sliding window of g, so each g value loaded serves EROWS
+        // rows; fixed chunk order and transposed butterflies -> deterministic.
         const int tb = (int)((int64_t)Q * crank / csize), te = (int)((int64_t)Q * (crank + 1) / csize);
-        for (int t0 = tb + 4 * warp; t0 < te; t0 += 4 * NW) {
+#ifdef STAGE1D_TRACE
+        if (tid == 0) { g_trace[blockIdx.x][9] = te - tb; }
+#endif
+        const int C = ((n + 31) / 32) | 1;
+        const int kc0 = min(n, C * lane), kc1 = min(n, kc0 + C);
+        bool waited = false;
+        auto erows = [&](const double* gsrc, auto ld) {   // gX[m] = g[(m - GX_PAD) mod n]
+        for (int t0 = tb + EROWS * warp; t0 < te; t0 += EROWS * NW) {
             int gx = B.lo_x + T.x0 - 2 + t0;
             gx += (gx < 0) ? n : 0;
             gx -= (gx >= n) ? n : 0;
-            const double* gp = A.gE + gx + n;                           // gp[j - k] = g[(gx + j - k) mod n] (L1)
-            double a[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-            int k = lane;
-            for (; k + 32 < n; k += 64) {
-                const double r0 = s_rho[k], r1 = s_rho[k + 32];
+            // row r, step k: g[(gx + r - k) mod n] = gX[GX_PAD + n + gx + r - k];
+            // block of 8 steps from kb: H[m] = gX[GX_PAD + n + gx - kb - 7 + m], row r at step u uses H[r - u + 7]
+            const double* gq = gsrc + GX_PAD + n + gx - 7 - kc0;
+            double acc[EROWS];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    a[0][j] = fma(__ldg(gp + j - k), r0, a[0][j]);
-                    a[1][j] = fma(__ldg(gp + j - k - 32), r1, a[1][j]);
-                }
+            for (int r = 0; r < EROWS; ++r) acc[r] = 0.0;
+            double H[15];
+#pragma unroll
+            for (int m = 0; m < 15; ++m) H[m] = ld(gq + m);
+            for (int kb = kc0; kb < kc1; kb += 8) {
+                double rr[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) rr[u] = (kb + u < kc1) ? s_rho[kb + u] - mean : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int r = 0; r < EROWS; ++r) acc[r] = fma(H[r - u + 7], rr[u], acc[r]);
+                gq -= 8;
+#pragma unroll
+                for (int m = 14; m >= 8; --m) H[m] = H[m - 8];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) H[m] = ld(gq + m);
             }
-            if (k < n) {
-                const double r0 = s_rho[k];
+            // transposed butterfly: lane ends with row 4 b16 + 2 b8 + b4 (bits of the lane index)
+            const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+            double s4[4], s2[2];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) a[0][j] = fma(__ldg(gp + j - k), r0, a[0][j]);
+            for (int m = 0; m < 4; ++m) {
+                const double mine = b16 ? acc[4 + m] : acc[m], oth = b16 ? acc[m] : acc[4 + m];
+                s4[m] = mine + __shfl_xor_sync(0xffffffffu, oth, 16);
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                double e = a[0][j] + a[1][j];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-                const int t = t0 + j;
+            for (int m = 0; m < 2; ++m) {
+                const double mine = b8 ? s4[2 + m] : s4[m], oth = b8 ? s4[m] : s4[2 + m];
+                s2[m] = mine + __shfl_xor_sync(0xffffffffu, oth, 8);
+            }
+            double e = (b4 ? s2[1] : s2[0]) + __shfl_xor_sync(0xffffffffu, b4 ? s2[0] : s2[1], 4);
+            e += __shfl_xor_sync(0xffffffffu, e, 2);
+            e += __shfl_xor_sync(0xffffffffu, e, 1);
+            const int t = t0 + (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+            if (csize > 1 && !waited) { cluster_wait(); waited = true; }
+            if ((lane & 3) == 0 && t < te) {
                 if (csize > 1) {
-                    if (t < te && lane < (int)csize)
-                        st_async_f64(map_shared_rank(s_part + t, lane), e, map_shared_rank(&e_bar, lane));
-                } else if (t < te && lane == 0) {
+                    for (uint32_t c = 0; c < csize; ++c)
+                        st_async_f64(map_shared_rank(s_part + t, c), e, map_shared_rank(&e_bar, c));
+                } else {
                     s_part[t] = e;
                 }
-                if (t < te && lane == 0 && t >= 2 && t < Q - 2) {     // owned rows + periodic ghosts
+                if (t >= 2 && t < Q - 2) {       // owned rows + periodic ghosts
                     const int x = B.lo_x + T.x0 - 2 + t;
                     A.E_out[x + G] = e;
                     if (x < G) A.E_out[x + G + n] = e;
@@ -247,25 +341,43 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
                 }
             }
         }
+        };
+        if (A.g_smem) erows(f_g, [](const double* p) { return *p; });
+        else erows(A.gX, [](const double* p) { return __ldg(p); });
+        if (csize > 1 && !waited) cluster_wait();   // warps without rows still complete the barrier
+        TRACE(4);
         if (csize > 1) mbar_wait(&e_bar, 0);
         else named_bar_sync(1, NT);
         for (int t = tid; t < Q; t += NT) sE[t] = s_part[t];
         named_bar_sync(1, NT);
     }
+    TRACE(5);
     const int cl = CPT * tid;                    // tile-local column of my first cell
     const int c0 = T.j0 + cl;                    // block-local interior column
     const int nact = min(CPT, T.ncols - cl);     // active cells of this thread (may be <= 0)
-    double vb[CPT + 2];                          // exact cell-average velocities of c0-1 .. c0+4
-#pragma unroll
-    for (int n = 0; n < CPT + 2; ++n) vb[n] = A.v_lo + ((double)(B.lo_v + c0 + n - 1) + 0.5) * A.dv;
+    // exact cell-average velocity of column c0 - 1 + n (recomputed where used: no registers held)
+    const int jb = B.lo_v + c0 - 1;
+    auto vbar = [&](int n) -> double { return A.v_lo + ((double)(jb + n) + 0.5) * A.dv; };
     const double dv24 = A.dv * (1.0 / 24.0);
     const double rdx = 1.0 / A.dx, rdv = 1.0 / A.dv;
     const double* E = sE + 2 - T.x0;             // E[i] for block-local row i (x0-2 <= i <= x0+nrows+1)
     const double* Ebc = sEbc + 2 - T.x0;
     // SELF: the thread holding domain cells 0..3 computes the low v-ghosts, the one holding
     // nv-4 .. nv-1 the high ones (level nv % 4 == 0)
-    const bool lo_edge = SELF && (B.lo_v + c0 == 0);
-    const bool hi_edge = SELF && (B.lo_v + c0 + CPT == A.dom_v);
+    const bool edge_lo = SELF && (B.lo_v + c0 == 0);
+    const bool edge_hi = SELF && (B.lo_v + c0 + CPT == A.dom_v);
+    // input ghosts derived in-kernel from E_bc (else read from f_s's ghost columns, written by the
+    // stage that produced f_s); output ghosts: the edge threads write f_next's velocity ghost
+    // columns for this stage's field E, off the critical path of the row march
+    const bool ghost_in = SELF && (A.E_bc != nullptr);
+    const bool lo_edge = ghost_in && edge_lo, hi_edge = ghost_in && edge_hi;
+#ifdef STAGE1D_NOGHOSTOUT   // experiments only (carried ghosts then go stale)
+    constexpr bool GHOST_OUT = false;
+#else
+    constexpr bool GHOST_OUT = SELF && STAGE >= 1;
+#endif
+    // unperturbed-profile ghost values (s_f0, staged at the start): read by the edge threads only
+    // when needed, so that they hold no registers across the row march
 
     double W[4][CPT + 2];                        // f_s rows (mod 4) at columns c0-1 .. c0+4
     double VF[4][CPT + 1];                       // v-faces (mod 4) at c0-1/2 .. c0+CPT-1/2
@@ -290,6 +402,9 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
             if (q < Q) {
                 const int r = T.x0 - 2 + q;
                 mbar_wait(&full_bar[slot], phase);
+#ifdef STAGE1D_TRACE
+                if (q == 0) TRACE(6);
+#endif
                 const double* seg = smem + slot * SLOT;
                 double v[CPT + 4];               // columns c0-2 .. c0+5
 #pragma unroll
@@ -315,8 +430,8 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
                             v[1] = 4.0 * v[2] - 6.0 * v[3] + 4.0 * v[4] - v[5];
                             v[0] = 10.0 * v[2] - 20.0 * v[3] + 15.0 * v[4] - 4.0 * v[5];
                         } else {
-                            v[1] = __ldg(A.f0v + 1);
-                            v[0] = __ldg(A.f0v + 0);
+                            v[1] = s_f0[1];
+                            v[0] = s_f0[0];
                         }
                     }
                     if (hi_edge) {
@@ -325,8 +440,8 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
                             v[L + 1] = 4.0 * v[L] - 6.0 * v[L - 1] + 4.0 * v[L - 2] - v[L - 3];
                             v[L + 2] = 10.0 * v[L] - 20.0 * v[L - 1] + 15.0 * v[L - 2] - 4.0 * v[L - 3];
                         } else {
-                            v[L + 1] = __ldg(A.f0v + A.dom_v + 2);
-                            v[L + 2] = __ldg(A.f0v + A.dom_v + 3);
+                            v[L + 1] = s_f0[2];
+                            v[L + 2] = s_f0[3];
                         }
                     }
                 }
@@ -341,7 +456,7 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
                     double XF[CPT + 2];
 #pragma unroll
                     for (int n = 0; n < CPT + 2; ++n)
-                        XF[n] = face_avg<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vb[n]);
+                        XF[n] = face_avg<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vbar(n));
                     const double Ei = E[i], Em = E[i - 1], Ep = E[i + 1];
                     const double c48 = (Ep - Em) * (1.0 / 48.0);
                     // v-fluxes of row i from the v-faces of rows i-1 (R... see below), i, i+1
@@ -352,7 +467,7 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
                     double o[CPT];
 #pragma unroll
                     for (int n = 0; n < CPT; ++n) {
-                        const double Fxn = vb[n + 1] * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
+                        const double Fxn = vbar(n + 1) * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
                         const double k = (Fv[n + 1] - Fv[n]) * rdv - (Fxn - Fxp[n]) * rdx;
                         Fxp[n] = Fxn;
                         const double fs = W[R1][n + 1];
@@ -385,6 +500,18 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
                                 if (STAGE == 2) up[m] = uu[m];
                             }
                     }
+                    if (GHOST_OUT && (edge_lo || edge_hi)) {   // boundary cells of f_next, for the
+                        // characteristic v-ghosts written after the march (off the critical path)
+                        double* se = s_edge + (i - T.x0) * 2 * CPT;
+                        if (edge_lo) {
+                            *reinterpret_cast<double2*>(se) = make_double2(o[0], o[1]);
+                            *reinterpret_cast<double2*>(se + 2) = make_double2(o[2], o[3]);
+                        }
+                        if (edge_hi) {
+                            *reinterpret_cast<double2*>(se + CPT) = make_double2(o[0], o[1]);
+                            *reinterpret_cast<double2*>(se + CPT + 2) = make_double2(o[2], o[3]);
+                        }
+                    }
                     if (A.rho != nullptr) {
                         double sr;
                         if (nact == CPT) {
@@ -401,9 +528,9 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
                     double XF[CPT + 2];
 #pragma unroll
                     for (int n = 0; n < CPT + 2; ++n)
-                        XF[n] = face_avg<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vb[n]);
+                        XF[n] = face_avg<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vbar(n));
 #pragma unroll
-                    for (int n = 0; n < CPT; ++n) Fxp[n] = vb[n + 1] * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
+                    for (int n = 0; n < CPT; ++n) Fxp[n] = vbar(n + 1) * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
                 }
                 // v-faces of row r (c0-1/2 .. c0+CPT-1/2); speed a = -E_r; stored in VF[K]
                 const double ar = -E[r];
@@ -440,6 +567,31 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
         }
     }
 
+    if (GHOST_OUT && (T.j0 == 0 || T.j0 + T.ncols == B.nv)) {
+        // velocity ghost columns of f_next (characteristic BC, reading #6, for this stage's field:
+        // the E_bc of the next stage, reading #6b) from the boundary cells staged during the march
+        named_bar_sync(1, NT);
+        const bool has_lo = (T.j0 == 0), has_hi = (T.j0 + T.ncols == B.nv);
+        for (int idx = tid; idx < 2 * T.nrows; idx += NT) {
+            const int rr = idx >> 1, side = idx & 1;
+            if (side == 0 ? !has_lo : !has_hi) continue;
+            const int i = T.x0 + rr;
+            const double* se = s_edge + (rr * 2 + side) * CPT;
+            const double a = -E[i];
+            double2 g;
+            if (side == 0) {
+                g = a < 0.0 ? make_double2(10.0 * se[0] - 20.0 * se[1] + 15.0 * se[2] - 4.0 * se[3],
+                                           4.0 * se[0] - 6.0 * se[1] + 4.0 * se[2] - se[3])
+                            : make_double2(s_f0[0], s_f0[1]);
+                *reinterpret_cast<double2*>(A.f_next + rowbase(i) - 2) = g;
+            } else {
+                g = a > 0.0 ? make_double2(4.0 * se[3] - 6.0 * se[2] + 4.0 * se[1] - se[0],
+                                           10.0 * se[3] - 20.0 * se[2] + 15.0 * se[1] - 4.0 * se[0])
+                            : make_double2(s_f0[2], s_f0[3]);
+                *reinterpret_cast<double2*>(A.f_next + rowbase(i) + B.nv) = g;
+            }
+        }
+    }
     if (A.rho != nullptr) {
         named_bar_sync(1, NT);
         for (int rr = tid; rr < T.nrows; rr += NT) {
@@ -464,12 +616,13 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
             if (tid == 0) A.tickets[T.strip] = 0u;     // reset for the next launch
         }
     }
+    TRACE(7);
 }
 
 template <int STAGE, int RECON, int NT, bool SELF>
 static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
     using SG = StageGeom<STAGE, NT>;
-    const size_t smem = SG::smem_bytes(tile_rows) + (A.rho_in ? field_smem_bytes(A.dom_x, NT) : 0);
+    const size_t smem = SG::smem_bytes(tile_rows) + (A.rho_in ? field_smem_bytes(A.dom_x) : 0);
     auto kern = k_stage_1d1v<STAGE, RECON, NT, SELF>;
     static bool configured = false;   // per template instantiation
     if (!configured) {
@@ -559,19 +712,23 @@ int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n) {
     };
     if (wide)
         return q(k_stage_1d1v<4, VLASOV_CENTERED4, NT_WIDE, true>, NT_WIDE,
-                 StageGeom<4, NT_WIDE>::smem_bytes(tile_rows) + field_smem_bytes(n, NT_WIDE));
+                 StageGeom<4, NT_WIDE>::smem_bytes(tile_rows) + field_smem_bytes(n));
     return q(k_stage_1d1v<4, VLASOV_CENTERED4, NT_NARROW, true>, NT_NARROW,
-             StageGeom<4, NT_NARROW>::smem_bytes(tile_rows) + field_smem_bytes(n, NT_NARROW));
+             StageGeom<4, NT_NARROW>::smem_bytes(tile_rows) + field_smem_bytes(n));
 }
 
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
-                      double* rho, const double* rho_in, const double* gE, double* E_out) {
+                      double* rho, const double* rho_in, const double* gE, double* E_out, const double* gX) {
     StageArgs1 A;
     A.rho_in = rho_in;
     A.gE = gE;
     A.E_out = E_out;
     A.cluster = rho_in ? L->cluster_size : 1;
+    A.g_smem = (rho_in && g_in_smem(L->dom[0])) ? 1 : 0;
+    A.gX = gX;
+    A.nstrip1 = L->single_block ? L->n_strips : 0;
+    if (!L->h_blocks1.empty()) A.blk0 = L->h_blocks1[0];
     A.f_s = f_s;
     A.f_n = f_n;
     A.u_in = u;
@@ -592,7 +749,7 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.dom_v = L->dom[1];
     A.n_vtiles = L->n_vtiles;
     A.tile_rows = L->tile_rows;
-    const bool self = (E_bc != nullptr && f0v != nullptr);
+    const bool self = (f0v != nullptr);     // periodic single block: E_bc (in-kernel input ghosts) or carried ghosts
     const bool wide = !L->h_tiles_wide.empty();
     A.tiles = wide ? L->d_tiles_wide : L->d_tiles_narrow;
     const int nt = (int)(wide ? L->h_tiles_wide.size() : L->h_tiles_narrow.size());
@@ -607,3 +764,9 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
 }
 
 }  // namespace vk
+
+#ifdef STAGE1D_TRACE
+extern "C" int vlasov_debug_stage_trace(unsigned long long* out, int nblocks) {
+    return cudaMemcpyFromSymbol(out, vk::g_trace, (size_t)nblocks * 10 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -3;
+}
+#endif

@@ -26,7 +26,7 @@ from ._lib import CENTERED4
 class UniformVlasov1D:
     def __init__(self, ncells: Sequence[int], lower: Sequence[float], dx: Sequence[float], boxes,
                  f0v: np.ndarray, recon: int = CENTERED4, stream: Optional[torch.cuda.Stream] = None,
-                 self_ghost: bool = True, fused: Optional[bool] = None):
+                 self_ghost: bool = True, fused: Optional[bool] = None, carry_ghosts: bool = True):
         self.stream = stream or torch.cuda.Stream()
         self.ncells = tuple(ncells)
         self.dx = tuple(dx)
@@ -35,6 +35,10 @@ class UniformVlasov1D:
         # fused: constraint evaluation (Poisson + E) inside the stage kernel (vlasov_rk4_stage_vp)
         self.fused = (self_ghost and ncells[0] <= 4096 and ncells[0] % 2 == 0 and ncells[1] % 4 == 0) \
             if fused is None else fused
+        # carry_ghosts (in-kernel ghost modes): every stage writes the velocity ghost columns of its
+        # output for its own field (the next stage's E_bc), so stages read them instead of deriving
+        # them from E_bc; set_state fills them once
+        self.carry = self_ghost and carry_ghosts
         with torch.cuda.stream(self.stream):
             self.level = api.Level(2, ncells, lower, dx, (1, 1), boxes, stream=self.stream)
             if self.level.info.nblocks != 1:
@@ -58,6 +62,8 @@ class UniformVlasov1D:
             # first constraint evaluation (t = 0): moment of f_n, field -> E_bc of stage 1
             api.vlasov_reduce_moment([self.level.h], [self.A], self.rho)
             self.poisson.solve(self.rho, None, self.E[0], 2)
+            if self.carry:    # velocity ghosts of f_n for E_bc = E[0] (stage 1 reads them)
+                api.vlasov_fill_ghosts(self.level.h, self.A, None, None, self.E[0], self.f0v)
         self.stream.synchronize()
 
     def get_state(self) -> np.ndarray:
@@ -88,10 +94,11 @@ class UniformVlasov1D:
         if self.fused:
             # rho ping-pong: stage s reads the moment of f_s and writes the moment of f_next
             rho_s, rho_n = (self.rhos[0], self.rhos[1]) if s % 2 == 1 else (self.rhos[1], self.rhos[0])
-            api.vlasov_rk4_stage_vp(L, self.poisson.h, s, dt, self.A, f_s, self.U, f_next, rho_s, E_cur, E_bc,
-                                    self.f0v, self.recon, rho_n)
+            api.vlasov_rk4_stage_vp(L, self.poisson.h, s, dt, self.A, f_s, self.U, f_next, rho_s, E_cur,
+                                    None if self.carry else E_bc, self.f0v, self.recon, rho_n)
         elif self.self_ghost:
-            api.vlasov_rk4_stage(L, s, dt, self.A, f_s, self.U, f_next, E_cur, E_bc, self.f0v, self.recon, self.rho)
+            api.vlasov_rk4_stage(L, s, dt, self.A, f_s, self.U, f_next, E_cur, None if self.carry else E_bc,
+                                 self.f0v, self.recon, self.rho)
         else:
             api.vlasov_fill_ghosts(L, f_s, None, None, E_bc, self.f0v)
             api.vlasov_rk4_stage(L, s, dt, self.A, f_s, self.U, f_next, E_cur, None, None, self.recon, self.rho)

@@ -116,12 +116,14 @@ def test_fused_moment_equals_direct_moment(wname, shape):
     np.testing.assert_allclose(rho_direct.cpu().numpy(), ref, atol=1e-14)
 
 
-def _run_both(w, nsteps, recon=scheme.CENTERED4, boxes=None, graph=False, self_ghost=True, fused=None):
+def _run_both(w, nsteps, recon=scheme.CENTERED4, boxes=None, graph=False, self_ghost=True, fused=None,
+              carry_ghosts=True):
     h = inputs.spacing(w)
     dt = inputs.fixed_dt(w)
     f0 = inputs.initial_cell_averages(w)
     S = UniformVlasov1D(w.ncells, w.lower, h, boxes or inputs.level0_boxes(w), inputs.background_profile(w),
-                        RECON[recon], self_ghost=self_ghost, fused=fused if self_ghost else False)
+                        RECON[recon], self_ghost=self_ghost, fused=fused if self_ghost else False,
+                        carry_ghosts=carry_ghosts)
     S.set_state(f0)
     if graph:
         S.step(dt)
@@ -141,7 +143,11 @@ def _run_both(w, nsteps, recon=scheme.CENTERED4, boxes=None, graph=False, self_g
     return got, ref
 
 
+# fused / self: carried velocity ghosts (each stage writes its output's); *_ebc: velocity ghosts
+# derived in-kernel from E_bc; stored: ghost frame filled by vlasov_fill_ghosts every stage
 MODES = {"fused": dict(self_ghost=True, fused=True), "self": dict(self_ghost=True, fused=False),
+         "fused_ebc": dict(self_ghost=True, fused=True, carry_ghosts=False),
+         "self_ebc": dict(self_ghost=True, fused=False, carry_ghosts=False),
          "stored": dict(self_ghost=False)}
 
 
@@ -174,6 +180,34 @@ def test_ragged_multi_tile_ten_steps(mode):
     w = inputs.scaled(inputs.get("C4"), (150, 600), (75, 200))
     got, ref = _run_both(w, 10, **MODES[mode])
     assert relerr(got, ref) < 1e-11
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_carried_velocity_ghosts_equal_fill_ghosts(fused):
+    """With f0v given, a stage writes f_next's velocity ghost columns for its own field E (reading
+    #6b: the next stage's E_bc); they equal vlasov_fill_ghosts(E, f0v) of f_next on every row, for
+    both signs of E (outgoing: cubic extrapolation, incoming: the unperturbed profile)."""
+    w = inputs.scaled(inputs.get("C4"), (96, 512), (96, 512))
+    h = inputs.spacing(w)
+    S = UniformVlasov1D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w), fused=fused)
+    S.set_state(inputs.initial_cell_averages(w))
+    dt = inputs.fixed_dt(w)
+    nv = w.ncells[1]
+    with torch.cuda.stream(S.stream):
+        for s in (1, 2, 3):
+            S._stage(s, dt)
+            f_s, f_next, E_cur, _ = S.buffers(s)
+            S.stream.synchronize()
+            got = S.level.patch_view(f_next, 0, 2)[2:-2].cpu().numpy()
+            ref_t = f_next.clone()
+            api.vlasov_fill_ghosts(S.level.h, ref_t, None, None, E_cur, S.f0v)
+            S.stream.synchronize()
+            ref = S.level.patch_view(ref_t, 0, 2)[2:-2].cpu().numpy()
+            E = E_cur.cpu().numpy()[2:-2]
+            assert (E > 0).any() and (E < 0).any()
+            for cols in (slice(0, 2), slice(nv + 2, nv + 4)):
+                np.testing.assert_allclose(got[:, cols], ref[:, cols], rtol=4e-15, atol=1e-300)
+            np.testing.assert_array_equal(got[:, 2:nv + 2], ref[:, 2:nv + 2])
 
 
 def test_fused_field_equals_poisson_solve():
