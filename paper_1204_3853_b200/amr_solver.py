@@ -323,6 +323,10 @@ class MultiSpeciesVlasov1D:
         if len(nxf) != 1:
             raise ValueError("species hierarchies must share the finest configuration mesh")
         self.stream = self.sp[0].stream
+        # every C-ABI call enqueues on its level's stream: the species exchange rho and E every
+        # stage, so their hierarchies must be built on one stream (else the stages race)
+        if any(h.stream != self.stream for h in self.sp):
+            raise ValueError("species hierarchies must share one CUDA stream (AmrVlasov1D(..., stream=s))")
         h0 = self.sp[0]
         self.nxf, self.dxf = h0.nxf, h0.dxf
         self.poisson = api.Poisson(self.nxf, self.dxf, self.stream)

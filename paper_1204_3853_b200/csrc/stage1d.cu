@@ -20,6 +20,8 @@
 // (atomic ticket) adds the v-tiles in tile order -> rho = 1 - dv sum (deterministic).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "internal.h"
 #include "ptx.cuh"
 #include "scheme.cuh"
@@ -95,7 +97,19 @@ constexpr int CPT = STAGE1D_CPT;
 #ifndef STAGE1D_PRODUCER
 #define STAGE1D_PRODUCER 1
 #endif
-constexpr int PWARPS = STAGE1D_PRODUCER;
+// STAGE1D_PWG 1: for the wide tiles the producer is a whole warpgroup (4 warps, one of which issues
+// the ring) that hands its registers to the consumer warpgroup with setmaxnreg (launch: 256 x 128
+// registers; producer 24, consumers 232 -- no spills in the row march)
+#ifndef STAGE1D_PWG
+#define STAGE1D_PWG 1
+#endif
+template <int NT>
+struct Roles {
+    static constexpr bool PWG = STAGE1D_PWG && NT == 128;
+    static constexpr int PWARPS = PWG ? 4 : STAGE1D_PRODUCER;
+    static constexpr int THREADS = NT + 32 * PWARPS;
+};
+constexpr int PWG_PRODUCER_REGS = 24, PWG_CONSUMER_REGS = 232;
 constexpr int NT_WIDE = 128, NT_NARROW = 32;   // consumer threads per CTA
 
 template <int STAGE, int NT>
@@ -106,7 +120,7 @@ struct StageGeom {
     static constexpr int SLOT = SEG + NFN * TV;              // doubles per ring slot
     // ring depth: ~RING_KB of row data per CTA, 3..16 slots (a slot is consumed in one row step)
     static constexpr int NSLOT_RAW = (RING_KB * 1024) / (SLOT * 8);
-    static constexpr int NSLOT = NSLOT_RAW < 3 ? 3 : (NSLOT_RAW > 16 ? 16 : NSLOT_RAW);
+    static constexpr int NSLOT = NSLOT_RAW < 4 ? 4 : (NSLOT_RAW > 16 ? 16 : NSLOT_RAW);
     static constexpr int NW = NT / 32;
     static size_t smem_bytes(int tile_rows) {
         return (size_t)(NSLOT * SLOT + NW * tile_rows + 2 * (tile_rows + 4) + 2 * CPT * tile_rows) * sizeof(double);
@@ -116,10 +130,16 @@ struct StageGeom {
 // Ring slot of row step q (row r = x0 - 2 + q): [ f_s(r, j0-2 .. j0+TV+1) | f_n(r-2, j0..) | u(r-2, j0..) ];
 // the f_n / u rows are those of the output row i = r - 2 (q >= 4), so every slot is consumed
 // completely in its own row step and released at once.
-template <int STAGE, int RECON, int NT, bool SELF>
-__global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(const StageArgs1 A) {
+// GM (ghost mode of f_s): 0 = ghost frame read from memory (any level); 1 = one periodic block,
+// x wrapped in-kernel, velocity ghosts derived from E_bc; 2 = one periodic block, velocity ghosts
+// carried in memory (written by the stage that produced f_s)
+template <int STAGE, int RECON, int NT, int GM>
+__global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v(const StageArgs1 A) {
+    constexpr int PWARPS = Roles<NT>::PWARPS;
+    constexpr bool PWG = Roles<NT>::PWG;
     using SG = StageGeom<STAGE, NT>;
     constexpr int TV = SG::TV, SEG = SG::SEG, SLOT = SG::SLOT, NSLOT = SG::NSLOT, NW = SG::NW;
+    constexpr bool SELF = (GM != 0);
     constexpr bool NEED_FN = (STAGE >= 2);
     constexpr bool NEED_U = (STAGE == 4);
 
@@ -130,6 +150,7 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
     __shared__ __align__(8) uint64_t e_bar;      // fused field: all Q rows of E have landed
     __shared__ unsigned s_ticket;
     __shared__ double s_f0[4];                   // f0v at v-ghost columns -2, -1, nv, nv + 1 (SELF)
+    __shared__ uint32_t s_dep[NT];               // slot-release dependency sink (see the row step)
     double* psum = smem + NSLOT * SLOT;          // [NW][tile_rows]
 
     TRACE(0);
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
     __syncthreads();
     // consumers arrive now and wait only before their first remote store; the producer waits at once
     if (field && csize > 1) {
-        if (PWARPS && warp == NW) cluster_sync_all();
+        if (PWARPS && warp >= NW) cluster_sync_all();
         else cluster_arrive();
     }
     TRACE(1);
@@ -219,8 +240,9 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
             if (ng) bulk_g2s(f_g, A.gX, ng, &field_bar);
         }
     };
-    if (PWARPS && warp == NW) {                  // ---------------- producer warp
-        if (lane == 0) {
+    if (PWARPS && warp >= NW) {                  // ---------------- producer warp(group)
+        if (PWG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PWG_PRODUCER_REGS));
+        if (warp == NW && lane == 0) {
             issue_field();
             int slot = 0;
             uint32_t phase = 0;
@@ -232,6 +254,7 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
         }
         return;
     }
+    if (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PWG_CONSUMER_REGS));
     if (!PWARPS && tid == 0) {                   // consumer thread 0 primes the ring
         issue_field();
         for (int q = 0; q < min(Q, NSLOT); ++q) issue(q, q);
@@ -355,200 +378,219 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
     const int cl = CPT * tid;                    // tile-local column of my first cell
     const int c0 = T.j0 + cl;                    // block-local interior column
     const int nact = min(CPT, T.ncols - cl);     // active cells of this thread (may be <= 0)
-    // exact cell-average velocity of column c0 - 1 + n (recomputed where used: no registers held)
+    // SELF levels have nv % 4 == 0: a thread is either fully active or idle
+    const bool act = SELF ? (nact > 0) : (nact == CPT);
+    // exact cell-average velocity of column c0 - 1 + n
     const int jb = B.lo_v + c0 - 1;
     auto vbar = [&](int n) -> double { return A.v_lo + ((double)(jb + n) + 0.5) * A.dv; };
+    const double vb1 = vbar(1);                  // centered: vbar(n + 1) = vb1 + n dv
+    auto vbx = [&](int n) -> double { return RECON == VLASOV_CENTERED4 ? vb1 + (double)(n - 1) * A.dv : vbar(n); };
     const double dv24 = A.dv * (1.0 / 24.0);
-    const double rdx = 1.0 / A.dx, rdv = 1.0 / A.dv;
+    // face values are carried times 12 (face12), fluxes too; 1/12 folds into these factors
+    const double rdx12 = 1.0 / (12.0 * A.dx), rdv12 = 1.0 / (12.0 * A.dv);
     const double* E = sE + 2 - T.x0;             // E[i] for block-local row i (x0-2 <= i <= x0+nrows+1)
     const double* Ebc = sEbc + 2 - T.x0;
-    // SELF: the thread holding domain cells 0..3 computes the low v-ghosts, the one holding
-    // nv-4 .. nv-1 the high ones (level nv % 4 == 0)
+    // the thread holding domain cells 0..3 / nv-4 .. nv-1 (SELF: level nv % 4 == 0)
     const bool edge_lo = SELF && (B.lo_v + c0 == 0);
     const bool edge_hi = SELF && (B.lo_v + c0 + CPT == A.dom_v);
-    // input ghosts derived in-kernel from E_bc (else read from f_s's ghost columns, written by the
-    // stage that produced f_s); output ghosts: the edge threads write f_next's velocity ghost
-    // columns for this stage's field E, off the critical path of the row march
-    const bool ghost_in = SELF && (A.E_bc != nullptr);
-    const bool lo_edge = ghost_in && edge_lo, hi_edge = ghost_in && edge_hi;
+    // GM 1: input v-ghosts derived in-kernel from E_bc; GM 2: read from f_s's ghost columns.
+    // SELF: the edge threads stage f_next's boundary cells; its velocity ghost columns for this
+    // stage's field E are written after the march, off the critical path
+    const bool lo_edge = (GM == 1) && edge_lo, hi_edge = (GM == 1) && edge_hi;
 #ifdef STAGE1D_NOGHOSTOUT   // experiments only (carried ghosts then go stale)
     constexpr bool GHOST_OUT = false;
 #else
     constexpr bool GHOST_OUT = SELF && STAGE >= 1;
 #endif
-    // unperturbed-profile ghost values (s_f0, staged at the start): read by the edge threads only
-    // when needed, so that they hold no registers across the row march
 
     double W[4][CPT + 2];                        // f_s rows (mod 4) at columns c0-1 .. c0+4
-    double VF[4][CPT + 1];                       // v-faces (mod 4) at c0-1/2 .. c0+CPT-1/2
-    double Fxp[CPT];                             // x-fluxes at i-1/2
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-#pragma unroll
-        for (int b = 0; b < CPT + 2; ++b) W[a][b] = 0.0;
-#pragma unroll
-        for (int b = 0; b < CPT + 1; ++b) VF[a][b] = 0.0;
-    }
-#pragma unroll
-    for (int n = 0; n < CPT; ++n) Fxp[n] = 0.0;
+    double VF[4][CPT + 1];                       // 12 x v-faces (mod 4) at c0-1/2 .. c0+CPT-1/2
+    double Fxp[CPT];                             // 12 x x-fluxes at i-1/2
 
     int slot = 0;
     uint32_t phase = 0;
-    for (int q0 = 0; q0 < Q; q0 += 4) {
-        double rs[4] = {0.0, 0.0, 0.0, 0.0};    // per-thread moment sums of the group's output rows
-#pragma unroll
-        for (int K = 0; K < 4; ++K) {           // K == q mod 4 == row r mod 4 (shifted by 2)
-            const int q = q0 + K;
-            if (q < Q) {
-                const int r = T.x0 - 2 + q;
-                mbar_wait(&full_bar[slot], phase);
+    // The slot of row q is released at the end of row q + 1 (see below): pending slot and the
+    // dependency word of its fn / u loads
+    int pend_slot = 0;
+    uint32_t pend_phase = 0, pend_dep = 0;
+    // one row step q (row r = x0 - 2 + q, W slot K = q mod 4): OUT rows (q >= 4) produce output
+    // row i = r - 2; `live` == false only in the last group (rows past the tile: no wait, no
+    // stores, no slot release; their arithmetic is discarded)
+    auto row = [&](auto Kc, auto OUTc, int q, bool live, double& rsK) {
+        constexpr int K = decltype(Kc)::value;
+        constexpr bool OUT = decltype(OUTc)::value;
+        const int r = T.x0 - 2 + q;
+        if (live) mbar_wait(&full_bar[slot], phase);
 #ifdef STAGE1D_TRACE
-                if (q == 0) TRACE(6);
+        if (q == 0) TRACE(6);
 #endif
-                const double* seg = smem + slot * SLOT;
-                double v[CPT + 4];               // columns c0-2 .. c0+5
+        const double* seg = smem + slot * SLOT;
+        double v[CPT + 4];                       // columns c0-2 .. c0+5
 #pragma unroll
-                for (int m = 0; m < CPT + 4; m += 2) {
-                    const double2 p = lds2(seg + cl + m);
-                    v[m] = p.x; v[m + 1] = p.y;
+        for (int m = 0; m < CPT + 4; m += 2) {
+            const double2 p = lds2(seg + cl + m);
+            v[m] = p.x; v[m + 1] = p.y;
+        }
+        double fn[CPT], uu[CPT];
+        uint32_t fnuu = 0u;                      // dependency word of the fn / u loads
+        if (OUT && NEED_FN) {
+#pragma unroll
+            for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + cl + m); fn[m] = p.x; fn[m + 1] = p.y; }
+        }
+        if (OUT && NEED_U) {
+#pragma unroll
+            for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + TV + cl + m); uu[m] = p.x; uu[m + 1] = p.y; }
+        }
+        if (GM == 1 && (lo_edge || hi_edge)) {   // characteristic BC (reading #6), a = -E_bc
+            const double a = -Ebc[r];
+            if (lo_edge) {
+                if (a < 0.0) {
+                    v[1] = 4.0 * v[2] - 6.0 * v[3] + 4.0 * v[4] - v[5];
+                    v[0] = 10.0 * v[2] - 20.0 * v[3] + 15.0 * v[4] - 4.0 * v[5];
+                } else {
+                    v[1] = s_f0[1];
+                    v[0] = s_f0[0];
                 }
-                double fn[CPT], uu[CPT];
-                if (q >= 4) {
-                    if (NEED_FN) {
-#pragma unroll
-                        for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + cl + m); fn[m] = p.x; fn[m + 1] = p.y; }
-                    }
-                    if (NEED_U) {
-#pragma unroll
-                        for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + TV + cl + m); uu[m] = p.x; uu[m + 1] = p.y; }
-                    }
+            }
+            if (hi_edge) {
+                constexpr int L = CPT + 1;       // last interior column of the thread
+                if (a > 0.0) {
+                    v[L + 1] = 4.0 * v[L] - 6.0 * v[L - 1] + 4.0 * v[L - 2] - v[L - 3];
+                    v[L + 2] = 10.0 * v[L] - 20.0 * v[L - 1] + 15.0 * v[L - 2] - 4.0 * v[L - 3];
+                } else {
+                    v[L + 1] = s_f0[2];
+                    v[L + 2] = s_f0[3];
                 }
-                if (SELF && (lo_edge || hi_edge)) {   // characteristic BC (reading #6), a = -E_bc
-                    const double a = -Ebc[r];
-                    if (lo_edge) {
-                        if (a < 0.0) {
-                            v[1] = 4.0 * v[2] - 6.0 * v[3] + 4.0 * v[4] - v[5];
-                            v[0] = 10.0 * v[2] - 20.0 * v[3] + 15.0 * v[4] - 4.0 * v[5];
-                        } else {
-                            v[1] = s_f0[1];
-                            v[0] = s_f0[0];
-                        }
-                    }
-                    if (hi_edge) {
-                        constexpr int L = CPT + 1;   // last interior column of the thread
-                        if (a > 0.0) {
-                            v[L + 1] = 4.0 * v[L] - 6.0 * v[L - 1] + 4.0 * v[L - 2] - v[L - 3];
-                            v[L + 2] = 10.0 * v[L] - 20.0 * v[L - 1] + 15.0 * v[L - 2] - 4.0 * v[L - 3];
-                        } else {
-                            v[L + 1] = s_f0[2];
-                            v[L + 2] = s_f0[3];
-                        }
-                    }
-                }
-                // register window: row r -> W[K]
-#pragma unroll
-                for (int b = 0; b < CPT + 2; ++b) W[K][b] = v[b + 1];
-
-                if (q >= 4) {                    // output row i = r - 2
-                    const int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;   // rows r-3, r-2, r-1
-                    const int i = r - 2;
-                    // x-faces at i + 1/2 (rows i-1 .. i+2 = r-3 .. r) for columns c0-1 .. c0+4
-                    double XF[CPT + 2];
-#pragma unroll
-                    for (int n = 0; n < CPT + 2; ++n)
-                        XF[n] = face_avg<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vbar(n));
-                    const double Ei = E[i], Em = E[i - 1], Ep = E[i + 1];
-                    const double c48 = (Ep - Em) * (1.0 / 48.0);
-                    // v-fluxes of row i from the v-faces of rows i-1 (R... see below), i, i+1
-                    const int VM = (K + 1) & 3, V0 = (K + 2) & 3, VP = (K + 3) & 3;  // rows r-3, r-2, r-1
-                    double Fv[CPT + 1];
-#pragma unroll
-                    for (int m = 0; m < CPT + 1; ++m) Fv[m] = Ei * VF[V0][m] + c48 * (VF[VP][m] - VF[VM][m]);
-                    double o[CPT];
-#pragma unroll
-                    for (int n = 0; n < CPT; ++n) {
-                        const double Fxn = vbar(n + 1) * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
-                        const double k = (Fv[n + 1] - Fv[n]) * rdv - (Fxn - Fxp[n]) * rdx;
-                        Fxp[n] = Fxn;
-                        const double fs = W[R1][n + 1];
-                        if (STAGE == 0) {
-                            o[n] = k;
-                        } else if (STAGE == 1) {
-                            o[n] = fs + (0.5 * A.dt) * k;
-                        } else if (STAGE == 2) {
-                            uu[n] = fn[n] + (fs - fn[n]) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * k;
-                            o[n] = fn[n] + (0.5 * A.dt) * k;
-                        } else if (STAGE == 3) {
-                            o[n] = fn[n] + A.dt * k;
-                        } else {
-                            o[n] = uu[n] + (fs - fn[n]) * (1.0 / 3.0) + (A.dt * (1.0 / 6.0)) * k;
-                        }
-                    }
-                    double* op = A.f_next + rowbase(i) + c0;
-                    double* up = A.u_out + rowbase(i) + c0;
-                    if (nact == CPT) {
-#pragma unroll
-                        for (int m = 0; m < CPT; m += 2) {
-                            *reinterpret_cast<double2*>(op + m) = make_double2(o[m], o[m + 1]);
-                            if (STAGE == 2) *reinterpret_cast<double2*>(up + m) = make_double2(uu[m], uu[m + 1]);
-                        }
-                    } else {
-#pragma unroll
-                        for (int m = 0; m < CPT; ++m)
-                            if (m < nact) {
-                                op[m] = o[m];
-                                if (STAGE == 2) up[m] = uu[m];
-                            }
-                    }
-                    if (GHOST_OUT && (edge_lo || edge_hi)) {   // boundary cells of f_next, for the
-                        // characteristic v-ghosts written after the march (off the critical path)
-                        double* se = s_edge + (i - T.x0) * 2 * CPT;
-                        if (edge_lo) {
-                            *reinterpret_cast<double2*>(se) = make_double2(o[0], o[1]);
-                            *reinterpret_cast<double2*>(se + 2) = make_double2(o[2], o[3]);
-                        }
-                        if (edge_hi) {
-                            *reinterpret_cast<double2*>(se + CPT) = make_double2(o[0], o[1]);
-                            *reinterpret_cast<double2*>(se + CPT + 2) = make_double2(o[2], o[3]);
-                        }
-                    }
-                    if (A.rho != nullptr) {
-                        double sr;
-                        if (nact == CPT) {
-                            sr = (o[0] + o[1]) + (o[2] + o[3]);
-                        } else {
-                            sr = 0.0;
-#pragma unroll
-                            for (int m = 0; m < CPT; ++m) sr += (m < nact) ? o[m] : 0.0;
-                        }
-                        rs[K] = sr;
-                    }
-                } else if (q == 3) {             // x-fluxes at x0 - 1/2 (rows x0-2 .. x0+1)
-                    const int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;
-                    double XF[CPT + 2];
-#pragma unroll
-                    for (int n = 0; n < CPT + 2; ++n)
-                        XF[n] = face_avg<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vbar(n));
-#pragma unroll
-                    for (int n = 0; n < CPT; ++n) Fxp[n] = vbar(n + 1) * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
-                }
-                // v-faces of row r (c0-1/2 .. c0+CPT-1/2); speed a = -E_r; stored in VF[K]
-                const double ar = -E[r];
-#pragma unroll
-                for (int m = 0; m < CPT + 1; ++m) VF[K][m] = face_avg<RECON>(v[m], v[m + 1], v[m + 2], v[m + 3], ar);
-                // release the slot only now: every value loaded from it has been consumed by an
-                // instruction of this (converged) warp, so no shared-memory read of the slot is
-                // still in flight when the producer overwrites it
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[slot]);
-                if (!PWARPS && tid == 0 && q + NSLOT < Q) {   // refill the slot once every warp released it
-                    mbar_wait(&empty_bar[slot], phase);
-                    issue(q + NSLOT, slot);
-                }
-                if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
             }
         }
-        if (A.rho != nullptr && q0 >= 4) {
+#pragma unroll
+        for (int b = 0; b < CPT + 2; ++b) W[K][b] = v[b + 1];   // register window: row r -> W[K]
+        constexpr int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;   // rows r-3, r-2, r-1
+        if (OUT) {
+            const int i = r - 2;
+            // x-faces at i + 1/2 (rows i-1 .. i+2 = r-3 .. r) for columns c0-1 .. c0+4
+            double XF[CPT + 2];
+#pragma unroll
+            for (int n = 0; n < CPT + 2; ++n) XF[n] = face12<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vbx(n));
+            const double Ei = E[i], Em = E[i - 1], Ep = E[i + 1];
+            const double c48 = (Ep - Em) * (1.0 / 48.0);
+            // v-fluxes of row i from the v-faces of rows i-1, i, i+1 (= r-3, r-2, r-1)
+            double Fv[CPT + 1];
+#pragma unroll
+            for (int m = 0; m < CPT + 1; ++m) Fv[m] = Ei * VF[R1][m] + c48 * (VF[R2][m] - VF[R0][m]);
+            double o[CPT];
+#pragma unroll
+            for (int n = 0; n < CPT; ++n) {
+                const double Fxn = vbx(n + 1) * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
+                const double dFv = Fv[n + 1] - Fv[n], dFx = Fxn - Fxp[n];
+                Fxp[n] = Fxn;
+                const double fs = W[R1][n + 1];
+                if (STAGE == 0) {
+                    o[n] = dFv * rdv12 - dFx * rdx12;
+                } else if (STAGE == 1) {
+                    o[n] = fma((0.5 * A.dt) * rdv12, dFv, fma(-(0.5 * A.dt) * rdx12, dFx, fs));
+                } else if (STAGE == 2) {
+                    const double k = dFv * rdv12 - dFx * rdx12;
+                    uu[n] = fn[n] + (fs - fn[n]) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * k;
+                    o[n] = fn[n] + (0.5 * A.dt) * k;
+                } else if (STAGE == 3) {
+                    o[n] = fma(A.dt * rdv12, dFv, fma(-A.dt * rdx12, dFx, fn[n]));
+                } else {
+                    o[n] = fma((A.dt * (1.0 / 6.0)) * rdv12, dFv,
+                               fma(-(A.dt * (1.0 / 6.0)) * rdx12, dFx, fma(fs - fn[n], 1.0 / 3.0, uu[n])));
+                }
+            }
+            if (NEED_FN) fnuu ^= __double2hiint(fn[0]) ^ __double2hiint(fn[2]);
+            if (NEED_U) fnuu ^= __double2hiint(uu[0]) ^ __double2hiint(uu[2]);
+            double* op = A.f_next + rowbase(i) + c0;
+            double* up = A.u_out + rowbase(i) + c0;
+            if (SELF || nact == CPT) {
+                if (live && act) {
+#pragma unroll
+                    for (int m = 0; m < CPT; m += 2) {
+                        *reinterpret_cast<double2*>(op + m) = make_double2(o[m], o[m + 1]);
+                        if (STAGE == 2) *reinterpret_cast<double2*>(up + m) = make_double2(uu[m], uu[m + 1]);
+                    }
+                }
+            } else if (live) {
+#pragma unroll
+                for (int m = 0; m < CPT; ++m)
+                    if (m < nact) {
+                        op[m] = o[m];
+                        if (STAGE == 2) up[m] = uu[m];
+                    }
+            }
+            if (GHOST_OUT && live && (edge_lo || edge_hi)) {   // boundary cells of f_next
+                double* se = s_edge + (i - T.x0) * 2 * CPT + (edge_lo ? 0 : CPT);
+                *reinterpret_cast<double2*>(se) = make_double2(o[0], o[1]);
+                *reinterpret_cast<double2*>(se + 2) = make_double2(o[2], o[3]);
+                if (edge_lo && edge_hi) {        // nv == 4: one thread holds both boundaries
+                    *reinterpret_cast<double2*>(se + CPT) = make_double2(o[0], o[1]);
+                    *reinterpret_cast<double2*>(se + CPT + 2) = make_double2(o[2], o[3]);
+                }
+            }
+            double sr = 0.0;
+            if (SELF || nact == CPT) {
+                sr = (o[0] + o[1]) + (o[2] + o[3]);
+            } else {
+#pragma unroll
+                for (int m = 0; m < CPT; ++m) sr += (m < nact) ? o[m] : 0.0;
+            }
+            rsK = (live && (act || !SELF)) ? sr : 0.0;
+        } else if (K == 3) {                     // x-fluxes at x0 - 1/2 (rows x0-2 .. x0+1)
+            double XF[CPT + 2];
+#pragma unroll
+            for (int n = 0; n < CPT + 2; ++n) XF[n] = face12<RECON>(W[R0][n], W[R1][n], W[R2][n], W[K][n], vbx(n));
+#pragma unroll
+            for (int n = 0; n < CPT; ++n) Fxp[n] = vbx(n + 1) * XF[n + 1] + dv24 * (XF[n + 2] - XF[n]);
+        }
+        // v-faces of row r (c0-1/2 .. c0+CPT-1/2); speed a = -E_r; stored in VF[K]
+        const double ar = -E[r];
+#pragma unroll
+        for (int m = 0; m < CPT + 1; ++m) VF[K][m] = face12<RECON>(v[m], v[m + 1], v[m + 2], v[m + 3], ar);
+        if (live) {
+            // Release the slot of the previous row.  Shared-memory loads are asynchronous and the
+            // compiler may schedule their consumers after the arrive, so an integer xor of one
+            // word of every load of that row (its window W[R2] = v[1..6], fn / u via pend_dep) is
+            // stored (volatile) first: in-order issue holds the arrive until they have landed,
+            // which by now costs no stall.  (Row 0 has no previous row.)
+            if (OUT || K > 0) {
+                const uint32_t dep = pend_dep ^ __double2hiint(W[R2][0]) ^ __double2hiint(W[R2][2]) ^
+                                     __double2hiint(W[R2][4]) ^ __double2hiint(W[R2][5]);
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_dep[tid])), "r"(dep) : "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[pend_slot]);
+                if (!PWARPS && tid == 0 && q - 1 + NSLOT < Q) {   // refill it once every warp released it
+                    mbar_wait(&empty_bar[pend_slot], pend_phase);
+                    issue(q - 1 + NSLOT, pend_slot);
+                }
+            }
+            pend_slot = slot;
+            pend_phase = phase;
+            pend_dep = fnuu;
+            if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
+        }
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>;
+    using NO = std::false_type;
+    using YES = std::true_type;
+    {   // rows q = 0..3 (Q >= 5): window and v-faces only, x-fluxes at x0 - 1/2 at q = 3
+        double dummy;
+        row(I0{}, NO{}, 0, true, dummy);
+        row(I1{}, NO{}, 1, true, dummy);
+        row(I2{}, NO{}, 2, true, dummy);
+        row(I3{}, NO{}, 3, true, dummy);
+    }
+    for (int q0 = 4; q0 < Q; q0 += 4) {
+        double rs[4];                            // per-thread moment sums of the group's output rows
+        row(I0{}, YES{}, q0, true, rs[0]);
+        row(I1{}, YES{}, q0 + 1, q0 + 1 < Q, rs[1]);
+        row(I2{}, YES{}, q0 + 2, q0 + 2 < Q, rs[2]);
+        row(I3{}, YES{}, q0 + 3, q0 + 3 < Q, rs[3]);
+        if (A.rho != nullptr) {
             // warp sums of the 4 rows of the group with one transposed butterfly (6 shuffles
             // instead of 20): lane L ends with row 2*bit4(L) + bit3(L), lanes L % 8 == 0 write it
             const bool b16 = lane & 16, b8 = lane & 8;
@@ -619,11 +661,11 @@ __global__ void __launch_bounds__(NT + 32 * PWARPS, STAGE1D_MINB) k_stage_1d1v(c
     TRACE(7);
 }
 
-template <int STAGE, int RECON, int NT, bool SELF>
+template <int STAGE, int RECON, int NT, int GM>
 static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
     using SG = StageGeom<STAGE, NT>;
     const size_t smem = SG::smem_bytes(tile_rows) + (A.rho_in ? field_smem_bytes(A.dom_x) : 0);
-    auto kern = k_stage_1d1v<STAGE, RECON, NT, SELF>;
+    auto kern = k_stage_1d1v<STAGE, RECON, NT, GM>;
     static bool configured = false;   // per template instantiation
     if (!configured) {
         VK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -632,7 +674,7 @@ static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t
     if (A.rho_in && A.cluster > 1) {   // fused field: the v-tiles of a row strip form one cluster
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(ntiles);
-        cfg.blockDim = dim3(NT + 32 * PWARPS);
+        cfg.blockDim = dim3(Roles<NT>::THREADS);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute at[1];
@@ -645,27 +687,27 @@ static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t
         VK_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
         return VLASOV_OK;
     }
-    kern<<<ntiles, NT + 32 * PWARPS, smem, st>>>(A);
+    kern<<<ntiles, Roles<NT>::THREADS, smem, st>>>(A);
     VK_LAUNCH("k_stage_1d1v");
     return VLASOV_OK;
 }
 
-template <int RECON, int NT, bool SELF>
+template <int RECON, int NT, int GM>
 static int dispatch_stage(int stage, const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
     switch (stage) {
-        case 0: return launch_t<0, RECON, NT, SELF>(A, ntiles, tile_rows, st);
-        case 1: return launch_t<1, RECON, NT, SELF>(A, ntiles, tile_rows, st);
-        case 2: return launch_t<2, RECON, NT, SELF>(A, ntiles, tile_rows, st);
-        case 3: return launch_t<3, RECON, NT, SELF>(A, ntiles, tile_rows, st);
-        case 4: return launch_t<4, RECON, NT, SELF>(A, ntiles, tile_rows, st);
+        case 0: return launch_t<0, RECON, NT, GM>(A, ntiles, tile_rows, st);
+        case 1: return launch_t<1, RECON, NT, GM>(A, ntiles, tile_rows, st);
+        case 2: return launch_t<2, RECON, NT, GM>(A, ntiles, tile_rows, st);
+        case 3: return launch_t<3, RECON, NT, GM>(A, ntiles, tile_rows, st);
+        case 4: return launch_t<4, RECON, NT, GM>(A, ntiles, tile_rows, st);
     }
     return fail(VLASOV_EINVAL, "stage must be 1..4");
 }
 
-template <int NT, bool SELF>
+template <int NT, int GM>
 static int dispatch_recon(int recon, int stage, const StageArgs1& A, int nt, int rows, cudaStream_t st) {
-    return recon == VLASOV_UPWIND ? dispatch_stage<VLASOV_UPWIND, NT, SELF>(stage, A, nt, rows, st)
-                                  : dispatch_stage<VLASOV_CENTERED4, NT, SELF>(stage, A, nt, rows, st);
+    return recon == VLASOV_UPWIND ? dispatch_stage<VLASOV_UPWIND, NT, GM>(stage, A, nt, rows, st)
+                                  : dispatch_stage<VLASOV_CENTERED4, NT, GM>(stage, A, nt, rows, st);
 }
 
 // CTAs per SM of the most demanding stage instance (stage 4), for one-wave tiling.
@@ -673,9 +715,9 @@ template <int NT>
 static int ctas_per_sm_t(int tile_rows) {
     int n = 0;
     using SG = StageGeom<4, NT>;
-    auto k = k_stage_1d1v<4, VLASOV_CENTERED4, NT, true>;
+    auto k = k_stage_1d1v<4, VLASOV_CENTERED4, NT, 2>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, NT + 32 * PWARPS, SG::smem_bytes(tile_rows)) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, Roles<NT>::THREADS, SG::smem_bytes(tile_rows)) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -694,7 +736,7 @@ int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(cs * 64);
-        cfg.blockDim = dim3(nt + 32 * PWARPS);
+        cfg.blockDim = dim3(nt == NT_WIDE ? Roles<NT_WIDE>::THREADS : Roles<NT_NARROW>::THREADS);
         cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -711,9 +753,9 @@ int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n) {
         return m;
     };
     if (wide)
-        return q(k_stage_1d1v<4, VLASOV_CENTERED4, NT_WIDE, true>, NT_WIDE,
+        return q(k_stage_1d1v<4, VLASOV_CENTERED4, NT_WIDE, 2>, NT_WIDE,
                  StageGeom<4, NT_WIDE>::smem_bytes(tile_rows) + field_smem_bytes(n));
-    return q(k_stage_1d1v<4, VLASOV_CENTERED4, NT_NARROW, true>, NT_NARROW,
+    return q(k_stage_1d1v<4, VLASOV_CENTERED4, NT_NARROW, 2>, NT_NARROW,
              StageGeom<4, NT_NARROW>::smem_bytes(tile_rows) + field_smem_bytes(n));
 }
 
@@ -755,12 +797,15 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     const int nt = (int)(wide ? L->h_tiles_wide.size() : L->h_tiles_narrow.size());
     if (nt == 0) return VLASOV_OK;
     const int rows = L->tile_rows;
+    const int gm = self ? (E_bc ? 1 : 2) : 0;
     if (wide) {
-        return self ? dispatch_recon<NT_WIDE, true>(recon, stage, A, nt, rows, L->stream)
-                    : dispatch_recon<NT_WIDE, false>(recon, stage, A, nt, rows, L->stream);
+        return gm == 2 ? dispatch_recon<NT_WIDE, 2>(recon, stage, A, nt, rows, L->stream)
+             : gm == 1 ? dispatch_recon<NT_WIDE, 1>(recon, stage, A, nt, rows, L->stream)
+                       : dispatch_recon<NT_WIDE, 0>(recon, stage, A, nt, rows, L->stream);
     }
-    return self ? dispatch_recon<NT_NARROW, true>(recon, stage, A, nt, rows, L->stream)
-                : dispatch_recon<NT_NARROW, false>(recon, stage, A, nt, rows, L->stream);
+    return gm == 2 ? dispatch_recon<NT_NARROW, 2>(recon, stage, A, nt, rows, L->stream)
+         : gm == 1 ? dispatch_recon<NT_NARROW, 1>(recon, stage, A, nt, rows, L->stream)
+                   : dispatch_recon<NT_NARROW, 0>(recon, stage, A, nt, rows, L->stream);
 }
 
 }  // namespace vk

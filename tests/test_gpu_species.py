@@ -24,8 +24,12 @@ def _oh(rat, lb, scale=1.0):
                          lambda r: scale * inputs.background_profile(W, r), scheme.CENTERED4, interp.LINEAR5)
 
 
-def _gh(rat, lb, scale=1.0):
-    return AmrVlasov1D(W.ncells, W.lower, inputs.spacing(W), lb, rat, lambda r: scale * inputs.background_profile(W, r))
+_STREAM = torch.cuda.Stream()   # species coupled by MultiSpeciesVlasov1D share one stream
+
+
+def _gh(rat, lb, scale=1.0, stream=None):
+    return AmrVlasov1D(W.ncells, W.lower, inputs.spacing(W), lb, rat, lambda r: scale * inputs.background_profile(W, r),
+                       stream=stream)
 
 
 def _init(rat, lb, scale=1.0):
@@ -61,7 +65,7 @@ def test_electrons_and_ions_parity(seeds):
     sp = [species.Species(He, q[0], m[0]), species.Species(Hi, q[1], m[1])]
     datas = [_odata(He, ie), _odata(Hi, ii)]
     A = species.start(sp, datas, rho_bg)
-    G = MultiSpeciesVlasov1D([_gh(rat_e, lb_e), _gh(rat_i, lb_i)], q, m, rho_bg)
+    G = MultiSpeciesVlasov1D([_gh(rat_e, lb_e, stream=_STREAM), _gh(rat_i, lb_i, stream=_STREAM)], q, m, rho_bg)
     G.set_state([ie, ii])
     dt = inputs.fixed_dt(W, rat_e[-1])
     for n in range(3):
@@ -73,11 +77,17 @@ def test_electrons_and_ions_parity(seeds):
             assert err < (1e-12 if n == 0 else 1e-11), (n, err)
 
 
+def test_species_on_different_streams_rejected():
+    rat, lb = random_hierarchy(4)
+    with pytest.raises(ValueError):
+        MultiSpeciesVlasov1D([_gh(rat, lb), _gh(rat, lb)], (-1.0, -1.0), (1.0, 1.0), 1.0)
+
+
 def test_split_electrons_superpose_on_gpu():
     rat, lb = random_hierarchy(4)
     one = _gh(rat, lb)
     one.set_state(_init(rat, lb))
-    G = MultiSpeciesVlasov1D([_gh(rat, lb, 0.3), _gh(rat, lb, 0.7)], (-1.0, -1.0), (1.0, 1.0), 1.0)
+    G = MultiSpeciesVlasov1D([_gh(rat, lb, 0.3, _STREAM), _gh(rat, lb, 0.7, _STREAM)], (-1.0, -1.0), (1.0, 1.0), 1.0)
     G.set_state([_init(rat, lb, 0.3), _init(rat, lb, 0.7)])
     dt = inputs.fixed_dt(W, rat[-1])
     for _ in range(3):
