@@ -15,6 +15,7 @@ namespace vk {
 
 constexpr int G = 2;              // ghost width (reading #7)
 constexpr int GX_PAD = 16;        // padding of the periodically extended Green's function gX
+constexpr int GX_TAIL = 176;      // gX continues periodically past 2n + GX_PAD for unwrapped rows
 constexpr int MAXR = 16;          // largest refinement ratio per dim supported by the transfers
 
 // ------------------------------------------------------------------ errors
@@ -188,7 +189,7 @@ struct vlasov_poisson {
     cudaStream_t stream = nullptr;
     double* d_gE = nullptr;
     double* d_gphi = nullptr;
-    double* d_gX = nullptr;               // gX[m] = gE[(m - GX_PAD) mod n], m < 2n + 2 GX_PAD
+    double* d_gX = nullptr;               // gX[m] = gE[(m - GX_PAD) mod n], m < 2n + GX_PAD + GX_TAIL
 };
 
 namespace vk {

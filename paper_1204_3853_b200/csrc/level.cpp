@@ -344,6 +344,13 @@ int build_tiles_1d(vlasov_level* L, bool have_device) {
                 const int64_t strips = std::min<int64_t>(max_strips, (int64_t)mc * cs / nvt);
                 if (strips > best) { best = strips; L->cluster_size = cs; }
             }
+            if (const char* e = std::getenv("VLASOV_CLUSTER")) {   // experiments: force the cluster size
+                const int cs = atoi(e);
+                if (cs >= 1 && cs <= 8 && nvt % cs == 0) {
+                    L->cluster_size = cs;
+                    best = cs > 1 ? std::min<int64_t>(max_strips, (int64_t)vk::stage_1d1v_max_clusters(wide, 128, cs, L->dom[0]) * cs / nvt) : max_strips;
+                }
+            }
             if (best > 0) max_strips = best;
         }
         rows = (int)((nx + max_strips - 1) / max_strips);
@@ -1424,10 +1431,10 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
         gphi[d] = (double)(aP / n);
     }
     // gE is stored periodically extended (2n + 4 values, gE[j] = g[j mod n]); gX (fused stage
-    // kernel) is the same with GX_PAD values of padding on both sides, gX[m] = g[(m - GX_PAD) mod n],
+    // kernel) is the same with GX_PAD / GX_TAIL values of padding, gX[m] = g[(m - GX_PAD) mod n],
     // so that the prologue reads g[(i - k) mod n] = gX[GX_PAD + n + i - k] without a modulo
-    std::vector<double> gX(2 * (size_t)n + 2 * vk::GX_PAD);
-    for (size_t m = 0; m < gX.size(); ++m) gX[m] = gE[((int64_t)m - vk::GX_PAD + 2 * (int64_t)n) % n];
+    std::vector<double> gX(2 * (size_t)n + vk::GX_PAD + vk::GX_TAIL);
+    for (size_t m = 0; m < gX.size(); ++m) gX[m] = gE[((int64_t)m - vk::GX_PAD + 4 * (int64_t)n) % n];
     gE.resize(2 * (size_t)n + 4);
     for (size_t j = n; j < gE.size(); ++j) gE[j] = gE[j % n];
     vlasov_poisson* P = new vlasov_poisson();

@@ -64,7 +64,7 @@ struct StageArgs1 {
     double* E_out;             // ghosted level E array (owned rows + periodic ghosts)
     int cluster;               // CTAs per cluster of the fused launch (the v-tiles of a strip)
     int g_smem;                // fused field: gX staged in shared memory too
-    const double* gX;          // gX[m] = g[(m - GX_PAD) mod n], m in [0, 2n + 2 GX_PAD)
+    const double* gX;          // gX[m] = g[(m - GX_PAD) mod n], m in [0, 2n + GX_PAD + GX_TAIL)
     int nstrip1;               // > 0: single block, tiles computed from blockIdx (no table load)
     Block1 blk0;               // that block
 };
@@ -74,10 +74,10 @@ struct StageArgs1 {
 constexpr int G_SMEM_MAX_N = 2048;
 static bool g_in_smem(int n) { return n <= G_SMEM_MAX_N; }
 // shared memory of the fused field prologue: rho [n], row results [PART_MAX >= tile_rows + 4],
-// gX [2n + 2 GX_PAD]
+// the window of gX the CTA's rows need [<= n + PART_MAX + 32]
 constexpr int PART_MAX = 136;
 static size_t field_smem_bytes(int n) {
-    return (size_t)(n + PART_MAX + (g_in_smem(n) ? 2 * n + 2 * GX_PAD : 0)) * sizeof(double);
+    return (size_t)(n + PART_MAX + (g_in_smem(n) ? n + PART_MAX + 32 : 0)) * sizeof(double);
 }
 constexpr int EROWS = 8;   // rows of E per warp group in the fused prologue (Toeplitz blocking)
 
@@ -90,7 +90,12 @@ constexpr int CPT = STAGE1D_CPT;
 #define STAGE1D_MINB 2
 #endif
 #ifndef RING_KB
-#define RING_KB 40
+#define RING_KB 48
+#endif
+// programmatic dependent launch of the stage kernels: measured slower in the CUDA-graph step
+// (C4: 195 vs 185 us), so off; the kernel is PDL-safe (constants only before griddep_wait)
+#ifndef STAGE1D_PDL
+#define STAGE1D_PDL 0
 #endif
 // 1: a dedicated producer warp issues the TMA ring; 0: thread 0 of the consumers issues it (no
 // extra warp: 4 warps x 168 registers lets 3 CTAs share an SM instead of 2)
@@ -154,6 +159,9 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     double* psum = smem + NSLOT * SLOT;          // [NW][tile_rows]
 
     TRACE(0);
+    // programmatic dependent launch: the next stage may be scheduled as this grid's CTAs retire;
+    // everything before griddep_wait() below touches only constants (tiles, f0v, gX)
+    griddep_launch_dependents();
 #ifdef STAGE1D_TRACE
     if (threadIdx.x == 0) { unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); g_trace[blockIdx.x][8] = sm; }
 #endif
@@ -180,11 +188,6 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     double* sE = psum + NW * A.tile_rows;        // E of rows x0-2 .. x0+nrows+1
     double* sEbc = sE + (A.tile_rows + 4);       // E_bc of the same rows (SELF)
     const bool field = SELF && (A.rho_in != nullptr);
-    for (int t = tid; t < Q; t += blockDim.x) {
-        const int gi = B.lo_x + T.x0 - 2 + t + G;  // index in the ghosted level E array
-        if (!field) sE[t] = __ldg(A.E + gi);
-        if (SELF && A.E_bc) sEbc[t] = __ldg(A.E_bc + gi);
-    }
     if (SELF && tid < 4) s_f0[tid] = __ldg(A.f0v + (tid < 2 ? tid : A.dom_v + tid));
     if (tid == 0) {
         for (int s = 0; s < NSLOT; ++s) {
@@ -230,19 +233,33 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(r - 2) + T.j0, row_bytes, &full_bar[sl]);
         if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(r - 2) + T.j0, row_bytes, &full_bar[sl]);
     };
-    double* f_g = f_rho + A.dom_x + PART_MAX;      // gX staged (A.g_smem)
-    auto issue_field = [&]() {
+    // fused field: this CTA computes rows [tb, te) of the tile's Q rows of E (the strip's v-tiles
+    // of a cluster split them); row tb + t is x = gxu0 + t (unwrapped, gxu0 in [0, n)); they read
+    // gX[ws, ws + wl) only (see the Toeplitz loop), staged in shared memory at f_g
+    const int tb = (int)((int64_t)Q * crank / csize), te = (int)((int64_t)Q * (crank + 1) / csize);
+    int gxu0 = B.lo_x + T.x0 - 2 + tb;
+    gxu0 += (gxu0 < 0) ? A.dom_x : 0;
+    gxu0 -= (gxu0 >= A.dom_x) ? A.dom_x : 0;
+    const int ws = (GX_PAD + gxu0 - 14) & ~1;
+    const int wl = ((GX_PAD + A.dom_x + gxu0 + (te - tb) + 8 - ws) + 1) & ~1;
+    double* f_g = f_rho + A.dom_x + PART_MAX;      // gX[ws ..] staged (A.g_smem)
+    // the producing thread: gX (a constant) before the grid dependency wait, rho after it
+    auto issue_field_const = [&]() {
         if (field) {
             const uint32_t nb = (uint32_t)A.dom_x * 8u;
-            const uint32_t ng = A.g_smem ? (uint32_t)(2 * A.dom_x + 2 * GX_PAD) * 8u : 0u;
+            const uint32_t ng = A.g_smem ? (uint32_t)wl * 8u : 0u;
             mbar_arrive_expect_tx(&field_bar, nb + ng);
-            bulk_g2s(f_rho, A.rho_in, nb, &field_bar);
-            if (ng) bulk_g2s(f_g, A.gX, ng, &field_bar);
+            if (ng) bulk_g2s(f_g, A.gX + ws, ng, &field_bar);
         }
+    };
+    auto issue_field = [&]() {
+        if (field) bulk_g2s(f_rho, A.rho_in, (uint32_t)A.dom_x * 8u, &field_bar);
     };
     if (PWARPS && warp >= NW) {                  // ---------------- producer warp(group)
         if (PWG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PWG_PRODUCER_REGS));
         if (warp == NW && lane == 0) {
+            issue_field_const();
+            griddep_wait();                      // f_s, f_n, u, rho of the previous stages
             issue_field();
             int slot = 0;
             uint32_t phase = 0;
@@ -255,6 +272,14 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         return;
     }
     if (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PWG_CONSUMER_REGS));
+    if (!PWARPS && tid == 0) issue_field_const();
+    griddep_wait();                              // E, E_bc, f_s, f_n, u, rho of the previous stages
+    for (int t = tid; t < Q; t += NT) {
+        const int gi = B.lo_x + T.x0 - 2 + t + G;  // index in the ghosted level E array
+        if (!field) sE[t] = __ldg(A.E + gi);
+        if (SELF && A.E_bc) sEbc[t] = __ldg(A.E_bc + gi);
+    }
+    named_bar_sync(1, NT);
     if (!PWARPS && tid == 0) {                   // consumer thread 0 primes the ring
         issue_field();
         for (int q = 0; q < min(Q, NSLOT); ++q) issue(q, q);
@@ -296,7 +321,6 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         // rows; lane l sums over its own contiguous k-chunk [C l, C l + C) (C odd: conflict-free
         // shared-memory banks) with a sliding window of g, so each g value loaded serves EROWS
         // rows; fixed chunk order and transposed butterflies -> deterministic.
-        const int tb = (int)((int64_t)Q * crank / csize), te = (int)((int64_t)Q * (crank + 1) / csize);
 #ifdef STAGE1D_TRACE
         if (tid == 0) { g_trace[blockIdx.x][9] = te - tb; }
 #endif
@@ -305,9 +329,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         bool waited = false;
         auto erows = [&](const double* gsrc, auto ld) {   // gX[m] = g[(m - GX_PAD) mod n]
         for (int t0 = tb + EROWS * warp; t0 < te; t0 += EROWS * NW) {
-            int gx = B.lo_x + T.x0 - 2 + t0;
-            gx += (gx < 0) ? n : 0;
-            gx -= (gx >= n) ? n : 0;
+            const int gx = gxu0 + (t0 - tb);     // unwrapped (gX is periodic past 2n)
             // row r, step k: g[(gx + r - k) mod n] = gX[GX_PAD + n + gx + r - k];
             // block of 8 steps from kb: H[m] = gX[GX_PAD + n + gx - kb - 7 + m], row r at step u uses H[r - u + 7]
             const double* gq = gsrc + GX_PAD + n + gx - 7 - kc0;
@@ -365,7 +387,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
             }
         }
         };
-        if (A.g_smem) erows(f_g, [](const double* p) { return *p; });
+        if (A.g_smem) erows(f_g - ws, [](const double* p) { return *p; });
         else erows(A.gX, [](const double* p) { return __ldg(p); });
         if (csize > 1 && !waited) cluster_wait();   // warps without rows still complete the barrier
         TRACE(4);
@@ -671,24 +693,28 @@ static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t
         VK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles);
+    cfg.blockDim = dim3(Roles<NT>::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    // programmatic dependent launch: this grid may start while the previous kernel on the stream
+    // retires; the kernel waits (griddepcontrol.wait) before reading what earlier kernels wrote
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = STAGE1D_PDL;
+    ++na;
     if (A.rho_in && A.cluster > 1) {   // fused field: the v-tiles of a row strip form one cluster
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(ntiles);
-        cfg.blockDim = dim3(Roles<NT>::THREADS);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)A.cluster;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        VK_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
-        return VLASOV_OK;
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = (unsigned)A.cluster;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        ++na;
     }
-    kern<<<ntiles, Roles<NT>::THREADS, smem, st>>>(A);
-    VK_LAUNCH("k_stage_1d1v");
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    VK_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     return VLASOV_OK;
 }
 
