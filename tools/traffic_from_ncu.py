@@ -1,0 +1,41 @@
+"""Write profiles/stage_traffic.json (DRAM bytes per RK4 step of the 1D+1V stage kernels, read by
+bench.py's roofline.traffic) from an `ncu --set full` capture of the 4 stage launches of one step."""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+rep = sys.argv[1]
+cells = int(sys.argv[2]) if len(sys.argv) > 2 else 2048 * 4096
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr, units = rows[0], rows[1]
+kn = hdr.index("Kernel Name")
+scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1.0, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+
+
+def val(r, key, table):
+    i = hdr.index(key)
+    return float(r[i]) * table[units[i]]
+
+
+per = []
+for r in rows[2:]:
+    if "k_stage_1d1v" not in r[kn]:
+        continue
+    per.append({"kernel": r[kn][:60], "dram_read_bytes": val(r, "dram__bytes_read.sum", scale),
+                "dram_write_bytes": val(r, "dram__bytes_write.sum", scale),
+                "duration_us": val(r, "gpu__time_duration.sum", tscale)})
+per = per[:4]
+tot = sum(p["dram_read_bytes"] + p["dram_write_bytes"] for p in per)
+res = {"source": f"ncu --set full --clock-control none, {len(per)} stage launches of one C4 RK4 step ({rep})",
+       "bytes_per_step": tot, "bytes_per_step_per_cell": tot / cells, "algorithmic_bytes_per_step_per_cell": 104,
+       "note": "ncu counts DRAM writes that leave L2 during the kernel; part of the last rows' writes are flushed "
+               "after it, and rows still resident in L2 from the previous launch are not re-read",
+       "per_launch": per}
+dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "stage_traffic.json")
+json.dump(res, open(dst, "w"), indent=1)
+print(json.dumps(res, indent=1))
