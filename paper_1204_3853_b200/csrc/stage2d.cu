@@ -84,7 +84,7 @@ struct Slot2 {
     static constexpr int NFU = (STAGE >= 2 ? 1 : 0) + (STAGE == 4 ? 1 : 0);
     static constexpr int SIZE = S2_NLINE * S2_LW + NFU * S2_LT * S2_TM;   // doubles (multiple of 16: 128-B parts)
     static size_t smem_bytes(int qmax) {
-        return ((size_t)S2_NSLOT * SIZE + 10 * (size_t)qmax + 32 + 4 * S2_TM) * sizeof(double);  // ring + staging
+        return ((size_t)S2_NSLOT * SIZE + 20 * (size_t)qmax + 32 + 4 * S2_TM) * sizeof(double);  // ring + staging
     }
 };
 
@@ -94,11 +94,20 @@ __device__ __forceinline__ int wrapi(int i, int n) {
     return i;
 }
 
+// S2_PWG 1 (needs the global ghost frame): the producer is a whole warpgroup (one lane issues the
+// TMA copies) that hands its registers to the consumer warpgroup with setmaxnreg (launch 256 x 128
+// registers; producer 24, consumers 232)
+#ifndef S2_PWG
+#define S2_PWG 1
+#endif
+constexpr bool S2_PWG_ON = S2_PWG && S2_GWARP == 0;
+constexpr int S2_THREADS = S2_PWG_ON ? 32 * (S2_LT + 4) : 32 * (S2_LT + 1 + S2_GWARP);
+
 template <int STAGE, int RECON>
 #if S2_MAXNREG_ON
 __global__ void __maxnreg__(S2_MAXNREG) k_stage_2d2v(
 #else
-__global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
+__global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(
 #endif
     const StageArgs2 A, const __grid_constant__ TMaps2 M) {
     using SL = Slot2<STAGE>;
@@ -107,6 +116,7 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
     __shared__ __align__(8) uint64_t full_bar[S2_NSLOT];    // TMA landed (producer -> ghost warp)
     __shared__ __align__(8) uint64_t ready_bar[S2_NSLOT];   // vy ghosts derived (ghost warp -> consumers)
     __shared__ __align__(8) uint64_t empty_bar[S2_NSLOT];   // slot consumed (consumers -> producer)
+    __shared__ uint32_t s_dep[32 * S2_LT];                   // slot-release dependency sink
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int mt = blockIdx.x, l0 = blockIdx.y * S2_LT;
@@ -130,14 +140,17 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
     // Stage what the ghost values need besides the slots: E_bc (x, y components) of the strip's
     // rows at y = k-2 .. k+2, the unperturbed profile at the vy ghost cells of the CTA's vx lines
     // and at the vx ghost lines (characteristic condition, reading #6).
-    double* gE = smem + S2_NSLOT * SIZE;                          // [Q][5][2]
-    double* gPv = gE + 10 * Q;                                    // [8 lines l0-2+L][4]: m = -2, -1, nvy, nvy+1
+    double* gE = smem + S2_NSLOT * SIZE;                          // [Q][5][2] E_bc
+    double* gEf = gE + 10 * Q;                                    // [Q][5][2] E (the stage's field)
+    double* gPv = gEf + 10 * Q;                                   // [8 lines l0-2+L][4]: m = -2, -1, nvy, nvy+1
     double* gPx = gPv + 32;                                       // [4][TM]: vx lines -2, -1, nvx, nvx+1
     for (int t = tid; t < 5 * Q; t += blockDim.x) {
         const int tq = t / 5, dy = t % 5;
         const int xx = wrapi(x0 - 2 + tq, A.nx), yy = wrapi(k - 2 + dy, A.ny);
         gE[2 * t] = __ldg(A.E_bc + (int64_t)(xx + 2) * nyg + (yy + 2));
         gE[2 * t + 1] = __ldg(A.E_bc + ecomp + (int64_t)(xx + 2) * nyg + (yy + 2));
+        gEf[2 * t] = __ldg(A.E + (int64_t)(xx + 2) * nyg + (yy + 2));
+        gEf[2 * t + 1] = __ldg(A.E + ecomp + (int64_t)(xx + 2) * nyg + (yy + 2));
     }
     if (tid < 32) {
         const int Lg = tid >> 2, which = tid & 3;
@@ -153,10 +166,11 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
     }
     __syncthreads();
 
-    if (warp == S2_LT) {                                          // ---------------- producer warp
+    if (S2_PWG_ON ? warp >= S2_LT : warp == S2_LT) {              // ---------------- producer warp(group)
         // 6-8 tensor copies per row step (coordinates in the ghosted block: +2 per dim; x and y
         // wrapped periodically; out-of-range vx / vy boxes are zero-filled by the TMA unit)
-        if (lane == 0) {
+        if (S2_PWG_ON) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(24));
+        if (warp == S2_LT && lane == 0) {
             constexpr uint32_t BA = 8 * S2_LW * 8, BC = 4 * S2_LW * 8, BF = 4 * S2_TM * 8;
             int slot = 0;
             uint32_t phase = 0;
@@ -243,20 +257,24 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
     }
 
     // ---------------------------------------------------------------- consumers
+    if (S2_PWG_ON) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(232));
     const int w = warp, l = l0 + w;
     const bool lact = l < A.nvx;
     const int lc = lact ? l : A.nvx - 1;
     const int cl = 2 * lane + 2;                                  // slot column of my first cell
     const int m0 = mt * S2_TM + 2 * lane;
     const bool act = lact && (2 * lane < ncols);
-    auto Ex = [&](int ii, int kk) { return __ldg(A.E + (int64_t)(ii + 2) * nyg + (kk + 2)); };
-    auto Ey = [&](int ii, int kk) { return __ldg(A.E + ecomp + (int64_t)(ii + 2) * nyg + (kk + 2)); };
+    // E of row step tq (row x0 - 2 + tq) at y = k - 2 + dy, staged in shared memory
+    auto Efx = [&](int tq, int dy) { return gEf[2 * (5 * tq + dy)]; };
+    auto Efy = [&](int tq, int dy) { return gEf[2 * (5 * tq + dy) + 1]; };
     const double vbx = A.vx_lo + ((double)lc + 0.5) * A.hvx;
     const double vbxm = vbx - A.hvx, vbxp = vbx + A.hvx;
     double vby[4];                                                // m0-1 .. m0+2
 #pragma unroll
     for (int a = 0; a < 4; ++a) vby[a] = A.vy_lo + ((double)(m0 + a - 1) + 0.5) * A.hvy;
-    const double rdx = 1.0 / A.hx, rdy = 1.0 / A.hy, rdvx = 1.0 / A.hvx, rdvy = 1.0 / A.hvy;
+    // face values and fluxes are carried x12 (face12); 1/12 folds into the divergence factors
+    const double rdx = 1.0 / (12.0 * A.hx), rdy = 1.0 / (12.0 * A.hy), rdvx = 1.0 / (12.0 * A.hvx),
+                 rdvy = 1.0 / (12.0 * A.hvy);
     const double dvx24 = A.hvx * (1.0 / 24.0), dvy24 = A.hvy * (1.0 / 24.0);
 
     const bool ledge = (l0 == 0) || (l0 + S2_LT >= A.nvx);            // CTA at a vx boundary (uniform)
@@ -318,23 +336,27 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
                 W[K][1][0] = c23.x; W[K][1][1] = c23.y;
                 W[K][2][0] = ap1.x; W[K][2][1] = ap1.y;
                 {
-                    const double ax = -Ex(r, k), ay = -Ey(r, k);
-                    VX[K][0][0] = face_avg<RECON>(am2.x, am1.x, c23.x, ap1.x, ax);
-                    VX[K][0][1] = face_avg<RECON>(am2.y, am1.y, c23.y, ap1.y, ax);
-                    VX[K][1][0] = face_avg<RECON>(am1.x, c23.x, ap1.x, ap2.x, ax);
-                    VX[K][1][1] = face_avg<RECON>(am1.y, c23.y, ap1.y, ap2.y, ax);
-                    VY[K][0] = face_avg<RECON>(c01.x, c01.y, c23.x, c23.y, ay);
-                    VY[K][1] = face_avg<RECON>(c01.y, c23.x, c23.y, c45.x, ay);
-                    VY[K][2] = face_avg<RECON>(c23.x, c23.y, c45.x, c45.y, ay);
+                    const double ax = -Efx(q, 2), ay = -Efy(q, 2);
+                    VX[K][0][0] = face12<RECON>(am2.x, am1.x, c23.x, ap1.x, ax);
+                    VX[K][0][1] = face12<RECON>(am2.y, am1.y, c23.y, ap1.y, ax);
+                    VX[K][1][0] = face12<RECON>(am1.x, c23.x, ap1.x, ap2.x, ax);
+                    VX[K][1][1] = face12<RECON>(am1.y, c23.y, ap1.y, ap2.y, ax);
+                    VY[K][0] = face12<RECON>(c01.x, c01.y, c23.x, c23.y, ay);
+                    VY[K][1] = face12<RECON>(c01.y, c23.x, c23.y, c45.x, ay);
+                    VY[K][2] = face12<RECON>(c23.x, c23.y, c45.x, c45.y, ay);
                 }
                 const int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;   // rows r-3, r-2, r-1
+                // one word of every shared-memory load of the row (slot-release dependency, below)
+                uint32_t dep = __double2hiint(c01.x) ^ __double2hiint(c23.x) ^ __double2hiint(c45.x) ^
+                               __double2hiint(am1.x) ^ __double2hiint(ap1.x) ^ __double2hiint(am2.x) ^
+                               __double2hiint(ap2.x);
                 if (q >= 3) {
                     double XF[3][2];
 #pragma unroll
                     for (int b = 0; b < 3; ++b)
 #pragma unroll
                         for (int mm = 0; mm < 2; ++mm)
-                            XF[b][mm] = face_avg<RECON>(W[R0][b][mm], W[R1][b][mm], W[R2][b][mm], W[K][b][mm],
+                            XF[b][mm] = face12<RECON>(W[R0][b][mm], W[R1][b][mm], W[R2][b][mm], W[K][b][mm],
                                                         b == 0 ? vbxm : (b == 1 ? vbx : vbxp));
                     double Fxn[2];
 #pragma unroll
@@ -351,6 +373,9 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
                             t[d][1] = lds2(yl[d] + cl);
                             t[d][2] = lds2(yl[d] + cl + 2);
                         }
+#pragma unroll
+                        for (int d = 0; d < 5; ++d)
+                            dep ^= __double2hiint(t[d][0].x) ^ __double2hiint(t[d][1].x) ^ __double2hiint(t[d][2].x);
                         double YL[4], YH[4];
 #pragma unroll
                         for (int a = 0; a < 4; ++a) {
@@ -358,8 +383,8 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
 #pragma unroll
                             for (int d = 0; d < 5; ++d)
                                 y5[d] = (a == 0) ? t[d][0].y : (a == 1) ? t[d][1].x : (a == 2) ? t[d][1].y : t[d][2].x;
-                            YL[a] = face_avg<RECON>(y5[0], y5[1], y5[2], y5[3], vby[a]);
-                            YH[a] = face_avg<RECON>(y5[1], y5[2], y5[3], y5[4], vby[a]);
+                            YL[a] = face12<RECON>(y5[0], y5[1], y5[2], y5[3], vby[a]);
+                            YH[a] = face12<RECON>(y5[1], y5[2], y5[3], y5[4], vby[a]);
                         }
                         // ---- y-transverse velocity-face averages at (i, k -+ 1)
                         double VXk[2][2][2], VYk[2][3];
@@ -370,23 +395,23 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
                             const double axk = -Ebx(q - 2, sg ? 3 : 1);
                             const double2 bm1 = line_pair(P, w + 1, axk), bp1 = line_pair(P, w + 3, axk);
                             const double2 bm2 = line_pair(P, w, axk), bp2 = line_pair(P, w + 4, axk);
+                            dep ^= __double2hiint(bm1.x) ^ __double2hiint(bp1.x) ^ __double2hiint(bm2.x) ^
+                                   __double2hiint(bp2.x);
                             const double2 b01 = t[sg ? 3 : 1][0], b23 = t[sg ? 3 : 1][1], b45 = t[sg ? 3 : 1][2];
-                            const double ax = -Ex(i, kk), ay = -Ey(i, kk);
-                            VXk[sg][0][0] = face_avg<RECON>(bm2.x, bm1.x, b23.x, bp1.x, ax);
-                            VXk[sg][0][1] = face_avg<RECON>(bm2.y, bm1.y, b23.y, bp1.y, ax);
-                            VXk[sg][1][0] = face_avg<RECON>(bm1.x, b23.x, bp1.x, bp2.x, ax);
-                            VXk[sg][1][1] = face_avg<RECON>(bm1.y, b23.y, bp1.y, bp2.y, ax);
-                            VYk[sg][0] = face_avg<RECON>(b01.x, b01.y, b23.x, b23.y, ay);
-                            VYk[sg][1] = face_avg<RECON>(b01.y, b23.x, b23.y, b45.x, ay);
-                            VYk[sg][2] = face_avg<RECON>(b23.x, b23.y, b45.x, b45.y, ay);
+                            const double ax = -Efx(q - 2, sg ? 3 : 1), ay = -Efy(q - 2, sg ? 3 : 1);
+                            VXk[sg][0][0] = face12<RECON>(bm2.x, bm1.x, b23.x, bp1.x, ax);
+                            VXk[sg][0][1] = face12<RECON>(bm2.y, bm1.y, b23.y, bp1.y, ax);
+                            VXk[sg][1][0] = face12<RECON>(bm1.x, b23.x, bp1.x, bp2.x, ax);
+                            VXk[sg][1][1] = face12<RECON>(bm1.y, b23.y, bp1.y, bp2.y, ax);
+                            VYk[sg][0] = face12<RECON>(b01.x, b01.y, b23.x, b23.y, ay);
+                            VYk[sg][1] = face12<RECON>(b01.y, b23.x, b23.y, b45.x, ay);
+                            VYk[sg][2] = face12<RECON>(b23.x, b23.y, b45.x, b45.y, ay);
                         }
-                        const int ip = wrapi(i + 1, A.nx), im = wrapi(i - 1, A.nx);
-                        const int kp = wrapi(k + 1, A.ny), km = wrapi(k - 1, A.ny);
-                        const double exi = Ex(i, k), eyi = Ey(i, k);
-                        const double cxi = (Ex(ip, k) - Ex(im, k)) * (1.0 / 48.0);
-                        const double cxk = (Ex(i, kp) - Ex(i, km)) * (1.0 / 48.0);
-                        const double cyi = (Ey(ip, k) - Ey(im, k)) * (1.0 / 48.0);
-                        const double cyk = (Ey(i, kp) - Ey(i, km)) * (1.0 / 48.0);
+                        const double exi = Efx(q - 2, 2), eyi = Efy(q - 2, 2);
+                        const double cxi = (Efx(q - 1, 2) - Efx(q - 3, 2)) * (1.0 / 48.0);
+                        const double cxk = (Efx(q - 2, 3) - Efx(q - 2, 1)) * (1.0 / 48.0);
+                        const double cyi = (Efy(q - 1, 2) - Efy(q - 3, 2)) * (1.0 / 48.0);
+                        const double cyk = (Efy(q - 2, 3) - Efy(q - 2, 1)) * (1.0 / 48.0);
                         double Fvy[3];
 #pragma unroll
                         for (int fc = 0; fc < 3; ++fc)
@@ -395,6 +420,7 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
                         double2 fn = make_double2(0.0, 0.0), uu = make_double2(0.0, 0.0);
                         if (STAGE >= 2) fn = lds2(SF + w * S2_TM + 2 * lane);
                         if (STAGE == 4) uu = lds2(SU + w * S2_TM + 2 * lane);
+                        dep ^= __double2hiint(fn.x) ^ __double2hiint(uu.x);
                         double o[2], un[2];
 #pragma unroll
                         for (int mm = 0; mm < 2; ++mm) {
@@ -439,7 +465,10 @@ __global__ void __launch_bounds__(32 * (S2_LT + 1 + S2_GWARP), 2) k_stage_2d2v(
                     Fxp[0] = Fxn[0];
                     Fxp[1] = Fxn[1];
                 }
-                // release the slot: every value read from it has been consumed by this warp
+                // Release the slot.  Shared loads are asynchronous and the compiler may schedule their
+                // consumers after the arrive: a volatile store of a value depending on every load of
+                // the row precedes it, so in-order issue holds the arrive until they have landed.
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_dep[tid])), "r"(dep) : "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[slot]);
                 if (++slot == S2_NSLOT) { slot = 0; phase ^= 1u; }
@@ -524,7 +553,7 @@ static int launch2_t(const StageArgs2& A, const TMaps2& M, dim3 grid, cudaStream
         VK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    kern<<<grid, 32 * (S2_LT + 1 + S2_GWARP), smem, st>>>(A, M);
+    kern<<<grid, S2_THREADS, smem, st>>>(A, M);
     VK_LAUNCH("k_stage_2d2v");
     return VLASOV_OK;
 }
