@@ -820,6 +820,7 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
             const int64_t per = (int64_t)nmt * nlg * L->dom[1];
             // about one wave of 2 CTAs per SM, strips of at least 8 rows
             L->strips2 = (int)std::max<int64_t>(1, std::min<int64_t>(L->dom[0] / 8, (148 * 2 + per - 1) / per));
+            if (const char* e = std::getenv("VLASOV_STRIPS2")) L->strips2 = std::max(1, std::min(L->dom[0] / 4, atoi(e)));
             L->self_ghost_ok = true;
             L->n_vtiles = L->dom[2] * nmt;                 // moment partial planes
         }

@@ -28,6 +28,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "internal.h"
 #include "ptx.cuh"
 #include "scheme.cuh"
@@ -302,176 +304,198 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(
     auto Ebx = [&](int tq, int dy) { return gE[2 * (5 * tq + dy)]; };
 
     double W[4][3][2];        // f rows (mod 4) at vx lines l-1, l, l+1, vy m0, m0+1
-    double VX[4][2][2];       // vx-face averages (rows mod 4) at l-1/2, l+1/2
-    double VY[4][3];          // vy-face averages (rows mod 4) at m0-1/2, m0+1/2, m0+3/2
-    double Fxp[2] = {0.0, 0.0};
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-#pragma unroll
-        for (int b = 0; b < 3; ++b) { W[a][b][0] = W[a][b][1] = 0.0; VY[a][b] = 0.0; }
-        VX[a][0][0] = VX[a][0][1] = VX[a][1][0] = VX[a][1][1] = 0.0;
-    }
+    double VX[4][2][2];       // 12 x vx-face averages (rows mod 4) at l-1/2, l+1/2
+    double VY[4][3];          // 12 x vy-face averages (rows mod 4) at m0-1/2, m0+1/2, m0+3/2
+    double Fxp[2];            // 12 x x-fluxes at i - 1/2
     int slot = 0;
     uint32_t phase = 0;
-    for (int q0 = 0; q0 < Q; q0 += 4) {
+    // One row step q (row r = x0 - 2 + q, window slot K = q mod 4); OUT rows (q >= 4) produce output
+    // row i = r - 2.  `live` == false only in the last group: rows past the strip run without wait,
+    // stores or slot release (their arithmetic is discarded).  Straight-line code per K.
+    auto row = [&](auto Kc, auto OUTc, int q, bool live, double& rsK) {
+        constexpr int K = decltype(Kc)::value;
+        constexpr bool OUT = decltype(OUTc)::value;
+        constexpr int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;   // rows r-3, r-2, r-1
+        if (live) mbar_wait(S2_GWARP ? &ready_bar[slot] : &full_bar[slot], phase);
+        const double* SA = smem + slot * SIZE;
+        const double* SB = SA + 8 * S2_LW;
+        const double* SC = SB + 16 * S2_LW;
+        const double* SD = SC + 8 * S2_LW;
+        const double* SF = SA + S2_NLINE * S2_LW;
+        const double* SU = SF + S2_LT * S2_TM;
+        // ---- row r: x window, vx faces, vy faces
+        const double axr = -Ebx(q, 2);
+        const double2 c01 = lds2(SA + (w + 2) * S2_LW + cl - 2), c23 = lds2(SA + (w + 2) * S2_LW + cl),
+                      c45 = lds2(SA + (w + 2) * S2_LW + cl + 2);
+        const double2 am1 = line_pair(SA, w + 1, axr), ap1 = line_pair(SA, w + 3, axr);
+        const double2 am2 = line_pair(SA, w, axr), ap2 = line_pair(SA, w + 4, axr);
+        // one word of every shared-memory load of the row (slot-release dependency, below)
+        uint32_t dep = __double2hiint(c01.x) ^ __double2hiint(c23.x) ^ __double2hiint(c45.x) ^
+                       __double2hiint(am1.x) ^ __double2hiint(ap1.x) ^ __double2hiint(am2.x) ^ __double2hiint(ap2.x);
+        W[K][0][0] = am1.x; W[K][0][1] = am1.y;
+        W[K][1][0] = c23.x; W[K][1][1] = c23.y;
+        W[K][2][0] = ap1.x; W[K][2][1] = ap1.y;
+        {
+            const double ax = -Efx(q, 2), ay = -Efy(q, 2);
+            VX[K][0][0] = face12<RECON>(am2.x, am1.x, c23.x, ap1.x, ax);
+            VX[K][0][1] = face12<RECON>(am2.y, am1.y, c23.y, ap1.y, ax);
+            VX[K][1][0] = face12<RECON>(am1.x, c23.x, ap1.x, ap2.x, ax);
+            VX[K][1][1] = face12<RECON>(am1.y, c23.y, ap1.y, ap2.y, ax);
+            VY[K][0] = face12<RECON>(c01.x, c01.y, c23.x, c23.y, ay);
+            VY[K][1] = face12<RECON>(c01.y, c23.x, c23.y, c45.x, ay);
+            VY[K][2] = face12<RECON>(c23.x, c23.y, c45.x, c45.y, ay);
+        }
+        if (OUT || K == 3) {
+            double XF[3][2];
 #pragma unroll
-        for (int K = 0; K < 4; ++K) {
-            const int q = q0 + K;
-            if (q < Q) {
-                const int r = wrapi(x0 - 2 + q, A.nx);
-                mbar_wait(S2_GWARP ? &ready_bar[slot] : &full_bar[slot], phase);
-                const double* SA = smem + slot * SIZE;
-                const double* SB = SA + 8 * S2_LW;
-                const double* SC = SB + 16 * S2_LW;
-                const double* SD = SC + 8 * S2_LW;
-                const double* SF = SA + S2_NLINE * S2_LW;
-                const double* SU = SF + S2_LT * S2_TM;
-                // ---- row r: x window, vx faces, vy faces
-                const double axr = -Ebx(q, 2);
-                double2 c01 = lds2(SA + (w + 2) * S2_LW + cl - 2), c23 = lds2(SA + (w + 2) * S2_LW + cl),
-                        c45 = lds2(SA + (w + 2) * S2_LW + cl + 2);
-                const double2 am1 = line_pair(SA, w + 1, axr), ap1 = line_pair(SA, w + 3, axr);
-                const double2 am2 = line_pair(SA, w, axr), ap2 = line_pair(SA, w + 4, axr);
-                W[K][0][0] = am1.x; W[K][0][1] = am1.y;
-                W[K][1][0] = c23.x; W[K][1][1] = c23.y;
-                W[K][2][0] = ap1.x; W[K][2][1] = ap1.y;
-                {
-                    const double ax = -Efx(q, 2), ay = -Efy(q, 2);
-                    VX[K][0][0] = face12<RECON>(am2.x, am1.x, c23.x, ap1.x, ax);
-                    VX[K][0][1] = face12<RECON>(am2.y, am1.y, c23.y, ap1.y, ax);
-                    VX[K][1][0] = face12<RECON>(am1.x, c23.x, ap1.x, ap2.x, ax);
-                    VX[K][1][1] = face12<RECON>(am1.y, c23.y, ap1.y, ap2.y, ax);
-                    VY[K][0] = face12<RECON>(c01.x, c01.y, c23.x, c23.y, ay);
-                    VY[K][1] = face12<RECON>(c01.y, c23.x, c23.y, c45.x, ay);
-                    VY[K][2] = face12<RECON>(c23.x, c23.y, c45.x, c45.y, ay);
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+                for (int mm = 0; mm < 2; ++mm)
+                    XF[b][mm] = face12<RECON>(W[R0][b][mm], W[R1][b][mm], W[R2][b][mm], W[K][b][mm],
+                                              b == 0 ? vbxm : (b == 1 ? vbx : vbxp));
+            double Fxn[2];
+#pragma unroll
+            for (int mm = 0; mm < 2; ++mm) Fxn[mm] = vbx * XF[1][mm] + dvx24 * (XF[2][mm] - XF[0][mm]);
+            if (OUT) {
+                const int i = wrapi(x0 - 4 + q, A.nx);
+                // ---- y faces at (i, k -+ 1/2) for vy m0-1 .. m0+2 (lines k-2 .. k+2)
+                double2 t[5][3];
+                const double* yl[5] = {SC + w * S2_LW, SB + (w + 2) * S2_LW, SD + w * S2_LW,
+                                       SB + (8 + w + 2) * S2_LW, SC + (4 + w) * S2_LW};
+#pragma unroll
+                for (int d = 0; d < 5; ++d) {
+                    t[d][0] = lds2(yl[d] + cl - 2);
+                    t[d][1] = lds2(yl[d] + cl);
+                    t[d][2] = lds2(yl[d] + cl + 2);
                 }
-                const int R0 = (K + 1) & 3, R1 = (K + 2) & 3, R2 = (K + 3) & 3;   // rows r-3, r-2, r-1
-                // one word of every shared-memory load of the row (slot-release dependency, below)
-                uint32_t dep = __double2hiint(c01.x) ^ __double2hiint(c23.x) ^ __double2hiint(c45.x) ^
-                               __double2hiint(am1.x) ^ __double2hiint(ap1.x) ^ __double2hiint(am2.x) ^
-                               __double2hiint(ap2.x);
-                if (q >= 3) {
-                    double XF[3][2];
 #pragma unroll
-                    for (int b = 0; b < 3; ++b)
+                for (int d = 0; d < 5; ++d)
+                    dep ^= __double2hiint(t[d][0].x) ^ __double2hiint(t[d][1].x) ^ __double2hiint(t[d][2].x);
+                double YL[4], YH[4];
 #pragma unroll
-                        for (int mm = 0; mm < 2; ++mm)
-                            XF[b][mm] = face12<RECON>(W[R0][b][mm], W[R1][b][mm], W[R2][b][mm], W[K][b][mm],
-                                                        b == 0 ? vbxm : (b == 1 ? vbx : vbxp));
-                    double Fxn[2];
+                for (int a = 0; a < 4; ++a) {
+                    double y5[5];
 #pragma unroll
-                    for (int mm = 0; mm < 2; ++mm) Fxn[mm] = vbx * XF[1][mm] + dvx24 * (XF[2][mm] - XF[0][mm]);
-                    if (q >= 4) {
-                        const int i = wrapi(x0 - 4 + q, A.nx);
-                        // ---- y faces at (i, k -+ 1/2) for vy m0-1 .. m0+2 (lines k-2 .. k+2)
-                        double2 t[5][3];
-                        const double* yl[5] = {SC + w * S2_LW, SB + (w + 2) * S2_LW, SD + w * S2_LW,
-                                               SB + (8 + w + 2) * S2_LW, SC + (4 + w) * S2_LW};
+                    for (int d = 0; d < 5; ++d)
+                        y5[d] = (a == 0) ? t[d][0].y : (a == 1) ? t[d][1].x : (a == 2) ? t[d][1].y : t[d][2].x;
+                    YL[a] = face12<RECON>(y5[0], y5[1], y5[2], y5[3], vby[a]);
+                    YH[a] = face12<RECON>(y5[1], y5[2], y5[3], y5[4], vby[a]);
+                }
+                // ---- y-transverse velocity-face averages at (i, k -+ 1)
+                double VXk[2][2][2], VYk[2][3];
 #pragma unroll
-                        for (int d = 0; d < 5; ++d) {
-                            t[d][0] = lds2(yl[d] + cl - 2);
-                            t[d][1] = lds2(yl[d] + cl);
-                            t[d][2] = lds2(yl[d] + cl + 2);
-                        }
+                for (int sg = 0; sg < 2; ++sg) {
+                    const double* P = SB + sg * 8 * S2_LW;
+                    const double axk = -Ebx(q - 2, sg ? 3 : 1);
+                    const double2 bm1 = line_pair(P, w + 1, axk), bp1 = line_pair(P, w + 3, axk);
+                    const double2 bm2 = line_pair(P, w, axk), bp2 = line_pair(P, w + 4, axk);
+                    dep ^= __double2hiint(bm1.x) ^ __double2hiint(bp1.x) ^ __double2hiint(bm2.x) ^ __double2hiint(bp2.x);
+                    const double2 b01 = t[sg ? 3 : 1][0], b23 = t[sg ? 3 : 1][1], b45 = t[sg ? 3 : 1][2];
+                    const double ax = -Efx(q - 2, sg ? 3 : 1), ay = -Efy(q - 2, sg ? 3 : 1);
+                    VXk[sg][0][0] = face12<RECON>(bm2.x, bm1.x, b23.x, bp1.x, ax);
+                    VXk[sg][0][1] = face12<RECON>(bm2.y, bm1.y, b23.y, bp1.y, ax);
+                    VXk[sg][1][0] = face12<RECON>(bm1.x, b23.x, bp1.x, bp2.x, ax);
+                    VXk[sg][1][1] = face12<RECON>(bm1.y, b23.y, bp1.y, bp2.y, ax);
+                    VYk[sg][0] = face12<RECON>(b01.x, b01.y, b23.x, b23.y, ay);
+                    VYk[sg][1] = face12<RECON>(b01.y, b23.x, b23.y, b45.x, ay);
+                    VYk[sg][2] = face12<RECON>(b23.x, b23.y, b45.x, b45.y, ay);
+                }
+                const double exi = Efx(q - 2, 2), eyi = Efy(q - 2, 2);
+                const double cxi = (Efx(q - 1, 2) - Efx(q - 3, 2)) * (1.0 / 48.0);
+                const double cxk = (Efx(q - 2, 3) - Efx(q - 2, 1)) * (1.0 / 48.0);
+                const double cyi = (Efy(q - 1, 2) - Efy(q - 3, 2)) * (1.0 / 48.0);
+                const double cyk = (Efy(q - 2, 3) - Efy(q - 2, 1)) * (1.0 / 48.0);
+                double Fvy[3];
 #pragma unroll
-                        for (int d = 0; d < 5; ++d)
-                            dep ^= __double2hiint(t[d][0].x) ^ __double2hiint(t[d][1].x) ^ __double2hiint(t[d][2].x);
-                        double YL[4], YH[4];
+                for (int fc = 0; fc < 3; ++fc)
+                    Fvy[fc] = eyi * VY[R1][fc] + cyi * (VY[R2][fc] - VY[R0][fc]) + cyk * (VYk[1][fc] - VYk[0][fc]);
+                double2 fn = make_double2(0.0, 0.0), uu = make_double2(0.0, 0.0);
+                if (STAGE >= 2) fn = lds2(SF + w * S2_TM + 2 * lane);
+                if (STAGE == 4) uu = lds2(SU + w * S2_TM + 2 * lane);
+                dep ^= __double2hiint(fn.x) ^ __double2hiint(uu.x);
+                double o[2], un[2];
 #pragma unroll
-                        for (int a = 0; a < 4; ++a) {
-                            double y5[5];
-#pragma unroll
-                            for (int d = 0; d < 5; ++d)
-                                y5[d] = (a == 0) ? t[d][0].y : (a == 1) ? t[d][1].x : (a == 2) ? t[d][1].y : t[d][2].x;
-                            YL[a] = face12<RECON>(y5[0], y5[1], y5[2], y5[3], vby[a]);
-                            YH[a] = face12<RECON>(y5[1], y5[2], y5[3], y5[4], vby[a]);
-                        }
-                        // ---- y-transverse velocity-face averages at (i, k -+ 1)
-                        double VXk[2][2][2], VYk[2][3];
-#pragma unroll
-                        for (int sg = 0; sg < 2; ++sg) {
-                            const int kk = wrapi(k + (sg ? 1 : -1), A.ny);
-                            const double* P = SB + sg * 8 * S2_LW;
-                            const double axk = -Ebx(q - 2, sg ? 3 : 1);
-                            const double2 bm1 = line_pair(P, w + 1, axk), bp1 = line_pair(P, w + 3, axk);
-                            const double2 bm2 = line_pair(P, w, axk), bp2 = line_pair(P, w + 4, axk);
-                            dep ^= __double2hiint(bm1.x) ^ __double2hiint(bp1.x) ^ __double2hiint(bm2.x) ^
-                                   __double2hiint(bp2.x);
-                            const double2 b01 = t[sg ? 3 : 1][0], b23 = t[sg ? 3 : 1][1], b45 = t[sg ? 3 : 1][2];
-                            const double ax = -Efx(q - 2, sg ? 3 : 1), ay = -Efy(q - 2, sg ? 3 : 1);
-                            VXk[sg][0][0] = face12<RECON>(bm2.x, bm1.x, b23.x, bp1.x, ax);
-                            VXk[sg][0][1] = face12<RECON>(bm2.y, bm1.y, b23.y, bp1.y, ax);
-                            VXk[sg][1][0] = face12<RECON>(bm1.x, b23.x, bp1.x, bp2.x, ax);
-                            VXk[sg][1][1] = face12<RECON>(bm1.y, b23.y, bp1.y, bp2.y, ax);
-                            VYk[sg][0] = face12<RECON>(b01.x, b01.y, b23.x, b23.y, ay);
-                            VYk[sg][1] = face12<RECON>(b01.y, b23.x, b23.y, b45.x, ay);
-                            VYk[sg][2] = face12<RECON>(b23.x, b23.y, b45.x, b45.y, ay);
-                        }
-                        const double exi = Efx(q - 2, 2), eyi = Efy(q - 2, 2);
-                        const double cxi = (Efx(q - 1, 2) - Efx(q - 3, 2)) * (1.0 / 48.0);
-                        const double cxk = (Efx(q - 2, 3) - Efx(q - 2, 1)) * (1.0 / 48.0);
-                        const double cyi = (Efy(q - 1, 2) - Efy(q - 3, 2)) * (1.0 / 48.0);
-                        const double cyk = (Efy(q - 2, 3) - Efy(q - 2, 1)) * (1.0 / 48.0);
-                        double Fvy[3];
-#pragma unroll
-                        for (int fc = 0; fc < 3; ++fc)
-                            Fvy[fc] = eyi * VY[R1][fc] + cyi * (VY[R2][fc] - VY[R0][fc]) +
-                                      cyk * (VYk[1][fc] - VYk[0][fc]);
-                        double2 fn = make_double2(0.0, 0.0), uu = make_double2(0.0, 0.0);
-                        if (STAGE >= 2) fn = lds2(SF + w * S2_TM + 2 * lane);
-                        if (STAGE == 4) uu = lds2(SU + w * S2_TM + 2 * lane);
-                        dep ^= __double2hiint(fn.x) ^ __double2hiint(uu.x);
-                        double o[2], un[2];
-#pragma unroll
-                        for (int mm = 0; mm < 2; ++mm) {
-                            const double Fvxl = exi * VX[R1][0][mm] + cxi * (VX[R2][0][mm] - VX[R0][0][mm]) +
-                                                cxk * (VXk[1][0][mm] - VXk[0][0][mm]);
-                            const double Fvxh = exi * VX[R1][1][mm] + cxi * (VX[R2][1][mm] - VX[R0][1][mm]) +
-                                                cxk * (VXk[1][1][mm] - VXk[0][1][mm]);
-                            const double Fyl = vby[mm + 1] * YL[mm + 1] + dvy24 * (YL[mm + 2] - YL[mm]);
-                            const double Fyh = vby[mm + 1] * YH[mm + 1] + dvy24 * (YH[mm + 2] - YH[mm]);
-                            double kk = -(Fxn[mm] - Fxp[mm]) * rdx;
-                            kk = kk - (Fyh - Fyl) * rdy;
-                            kk = kk + (Fvxh - Fvxl) * rdvx;
-                            kk = kk + (Fvy[mm + 1] - Fvy[mm]) * rdvy;
-                            const double fs = W[R1][1][mm];
-                            const double fnm = mm ? fn.y : fn.x, um = mm ? uu.y : uu.x;
-                            if (STAGE == 0) {
-                                o[mm] = kk;
-                            } else if (STAGE == 1) {
-                                o[mm] = fs + (0.5 * A.dt) * kk;
-                            } else if (STAGE == 2) {
-                                un[mm] = fnm + (fs - fnm) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * kk;
-                                o[mm] = fnm + (0.5 * A.dt) * kk;
-                            } else if (STAGE == 3) {
-                                o[mm] = fnm + A.dt * kk;
-                            } else {
-                                o[mm] = um + (fs - fnm) * (1.0 / 3.0) + (A.dt * (1.0 / 6.0)) * kk;
-                            }
-                        }
-                        if (act) {
-                            const int64_t off = A.org + (int64_t)i * A.s0 + (int64_t)k * A.s1 + (int64_t)l * A.s2 + m0;
-                            *reinterpret_cast<double2*>(A.f_next + off) = make_double2(o[0], o[1]);
-                            if (STAGE == 2) *reinterpret_cast<double2*>(A.u_out + off) = make_double2(un[0], un[1]);
-                        }
-                        if (A.partials != nullptr) {
-                            double s = act ? (o[0] + o[1]) : 0.0;
-#pragma unroll
-                            for (int of = 16; of > 0; of >>= 1) s += __shfl_xor_sync(0xffffffffu, s, of);
-                            if (lane == 0 && lact)
-                                A.partials[((int64_t)l * gridDim.x + mt) * A.nx * A.ny + (int64_t)i * A.ny + k] = s;
-                        }
+                for (int mm = 0; mm < 2; ++mm) {
+                    const double Fvxl = exi * VX[R1][0][mm] + cxi * (VX[R2][0][mm] - VX[R0][0][mm]) +
+                                        cxk * (VXk[1][0][mm] - VXk[0][0][mm]);
+                    const double Fvxh = exi * VX[R1][1][mm] + cxi * (VX[R2][1][mm] - VX[R0][1][mm]) +
+                                        cxk * (VXk[1][1][mm] - VXk[0][1][mm]);
+                    const double Fyl = vby[mm + 1] * YL[mm + 1] + dvy24 * (YL[mm + 2] - YL[mm]);
+                    const double Fyh = vby[mm + 1] * YH[mm + 1] + dvy24 * (YH[mm + 2] - YH[mm]);
+                    double kk = -(Fxn[mm] - Fxp[mm]) * rdx;
+                    kk = kk - (Fyh - Fyl) * rdy;
+                    kk = kk + (Fvxh - Fvxl) * rdvx;
+                    kk = kk + (Fvy[mm + 1] - Fvy[mm]) * rdvy;
+                    const double fs = W[R1][1][mm];
+                    const double fnm = mm ? fn.y : fn.x, um = mm ? uu.y : uu.x;
+                    if (STAGE == 0) {
+                        o[mm] = kk;
+                    } else if (STAGE == 1) {
+                        o[mm] = fs + (0.5 * A.dt) * kk;
+                    } else if (STAGE == 2) {
+                        un[mm] = fnm + (fs - fnm) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * kk;
+                        o[mm] = fnm + (0.5 * A.dt) * kk;
+                    } else if (STAGE == 3) {
+                        o[mm] = fnm + A.dt * kk;
+                    } else {
+                        o[mm] = um + (fs - fnm) * (1.0 / 3.0) + (A.dt * (1.0 / 6.0)) * kk;
                     }
-                    Fxp[0] = Fxn[0];
-                    Fxp[1] = Fxn[1];
                 }
-                // Release the slot.  Shared loads are asynchronous and the compiler may schedule their
-                // consumers after the arrive: a volatile store of a value depending on every load of
-                // the row precedes it, so in-order issue holds the arrive until they have landed.
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_dep[tid])), "r"(dep) : "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty_bar[slot]);
-                if (++slot == S2_NSLOT) { slot = 0; phase ^= 1u; }
+                if (live && act) {
+                    const int64_t off = A.org + (int64_t)i * A.s0 + (int64_t)k * A.s1 + (int64_t)l * A.s2 + m0;
+                    *reinterpret_cast<double2*>(A.f_next + off) = make_double2(o[0], o[1]);
+                    if (STAGE == 2) *reinterpret_cast<double2*>(A.u_out + off) = make_double2(un[0], un[1]);
+                }
+                rsK = (live && act) ? (o[0] + o[1]) : 0.0;
+            }
+            Fxp[0] = Fxn[0];
+            Fxp[1] = Fxn[1];
+        }
+        if (live) {
+            // Release the slot.  Shared loads are asynchronous and the compiler may schedule their
+            // consumers after the arrive: a volatile store of a value depending on every load of
+            // the row precedes it, so in-order issue holds the arrive until they have landed.
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_dep[tid])), "r"(dep) : "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[slot]);
+            if (++slot == S2_NSLOT) { slot = 0; phase ^= 1u; }
+        }
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>;
+    {   // rows q = 0..3 (Q >= 5): windows and velocity faces, x-fluxes at x0 - 1/2 at q = 3
+        double dummy;
+        row(I0{}, std::false_type{}, 0, true, dummy);
+        row(I1{}, std::false_type{}, 1, true, dummy);
+        row(I2{}, std::false_type{}, 2, true, dummy);
+        row(I3{}, std::false_type{}, 3, true, dummy);
+    }
+    for (int q0 = 4; q0 < Q; q0 += 4) {
+        double rs[4];
+        row(I0{}, std::true_type{}, q0, true, rs[0]);
+        row(I1{}, std::true_type{}, q0 + 1, q0 + 1 < Q, rs[1]);
+        row(I2{}, std::true_type{}, q0 + 2, q0 + 2 < Q, rs[2]);
+        row(I3{}, std::true_type{}, q0 + 3, q0 + 3 < Q, rs[3]);
+        if (A.partials != nullptr) {
+            // warp sums of the group's 4 rows with one transposed butterfly (6 shuffles): lane L
+            // ends with row 2 bit4(L) + bit3(L); lanes L % 8 == 0 write it
+            const bool b16 = lane & 16, b8 = lane & 8;
+            double v0 = b16 ? rs[2] : rs[0], v1 = b16 ? rs[3] : rs[1];
+            const double w0 = b16 ? rs[0] : rs[2], w1 = b16 ? rs[1] : rs[3];
+            v0 += __shfl_xor_sync(0xffffffffu, w0, 16);
+            v1 += __shfl_xor_sync(0xffffffffu, w1, 16);
+            double u = b8 ? v1 : v0;
+            const double xv = b8 ? v0 : v1;
+            u += __shfl_xor_sync(0xffffffffu, xv, 8);
+            u += __shfl_xor_sync(0xffffffffu, u, 4);
+            u += __shfl_xor_sync(0xffffffffu, u, 2);
+            u += __shfl_xor_sync(0xffffffffu, u, 1);
+            const int qq = q0 + (b16 ? 2 : 0) + (b8 ? 1 : 0);
+            if ((lane & 7) == 0 && lact && qq < Q) {
+                const int i = wrapi(x0 - 4 + qq, A.nx);
+                A.partials[((int64_t)l * gridDim.x + mt) * A.nx * A.ny + (int64_t)i * A.ny + k] = u;
             }
         }
     }
