@@ -253,6 +253,77 @@ def run_amr(args, w, rank, world, local):
         dist.destroy_process_group()
 
 
+def run_vslab(args, w, rank, world, local):
+    """N2: the 1D+1V workload split into `world` velocity slabs, one per rank (strong scaling):
+    per stage the fused stage kernel, an NCCL all-reduce of the slab moments and the halo
+    exchange of two boundary velocity columns with each neighbour (paper_1204_3853_b200.vslab)."""
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    from paper_1204_3853_b200.vslab import DistComm, LocalComm, VSlabVlasov1D
+
+    h = inputs.spacing(w)
+    dt = inputs.fixed_dt(w)
+    comm = DistComm(rank, world) if world > 1 else LocalComm()
+    G = VSlabVlasov1D(w.ncells, w.lower, h, inputs.background_profile(w), world, [rank], comm)
+    G.set_state(inputs.initial_cell_averages(w))
+    for _ in range(args.warmup):
+        G.step(dt)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(G.stream)
+    for _ in range(args.steps):
+        G.step(dt)
+    ev1.record(G.stream)
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world, "cuda")
+    clk = clocks.stop()
+    value = w.cells * args.steps / (ms / 1e3)          # the whole problem, split over the ranks
+    # stage kernels of this rank (events around each launch; the collectives excluded)
+    S = G.slabs[0].S
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(4)]
+          for _ in range(args.steps)]
+    barrier()
+    with torch.cuda.stream(G.stream):
+        for k in range(args.steps):
+            for st in (1, 2, 3, 4):
+                ev[k][st - 1][0].record(G.stream)
+                S.stage_launch(st, dt)
+                ev[k][st - 1][1].record(G.stream)
+                G.comm.allreduce(G.slabs, [S.rhos[1] if st % 2 == 1 else S.rhos[0]])
+                G._halo(lambda X: X.buffers(st)[1])
+    barrier()
+    stage_ms = [float(np.mean([ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)])) for i in range(4)]
+    slab_cells = w.ncells[0] * (w.ncells[1] // world)
+    achieved = 104.0 * slab_cells / (sum(stage_ms) / 1e3) / 1e9
+    peak, peak_kind = read_peaks()
+    if rank == 0:
+        print(json.dumps({
+            "metric": "fp64 phase-space cell-updates/s per RK4 step", "value": value, "unit": "cell-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(w, {"parallelism": f"vslab x{world}", "slab": [w.ncells[0], w.ncells[1] // world],
+                                          "exchange": "per stage: NCCL all-reduce of the slab moments (nx doubles) + "
+                                                      "send/recv of 2 boundary velocity columns per neighbour",
+                                          "graph": "eager"}),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_kind": peak_kind, "kernel": "k_stage_1d1v of rank 0 (4 launches per step)",
+                         "algorithmic_bytes_per_cell_step": 104, "stage_ms": stage_ms},
+            "gpu_launches": 12 * args.steps, "clocks": clk}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -261,6 +332,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "vslab"],
+                    help="N > 1: independent replicas (default) or the velocity-slab decomposition (N2)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -282,6 +355,8 @@ def main():
     w = inputs.get(args.workload)
     if w.amr:
         return run_amr(args, w, rank, world, local)
+    if args.shard == "vslab":
+        return run_vslab(args, w, rank, world, local)
     h = inputs.spacing(w)
     dt = inputs.fixed_dt(w)
     f0 = inputs.initial_cell_averages(w)

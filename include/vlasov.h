@@ -282,6 +282,22 @@ int vlasov_level_fill_from(vlasov_level* level, double* f, const vlasov_level* o
  * dt = min(cfl / max_l(max|vbar|/dx_l + max|E_l|/dv_l), growth * dt_prev) from it.              */
 int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream);
 
+/* ---- velocity-slab decomposition of a uniform 1D+1V level -------- *
+ * Each GPU (rank) owns all x and a contiguous velocity slab, created as its own level (one block,
+ * lower[1] = the slab's lower velocity).  Per stage: the fused moment of every slab is reduced
+ * over the ranks (sum), and the two velocity ghost columns on each interior slab face are the
+ * neighbour's boundary columns (halo exchange).
+ * vlasov_level_set_moment_base: the fused stage moment writes rho = base - dv sum_v f_next
+ *   (default base 1; a slab decomposition uses 1 on one rank and 0 on the others, so that the
+ *   sum over ranks is rho = 1 - dv sum_v f).  One periodic block only.
+ * vlasov_vslab_pack: lo[2x + c] = f(x, c), hi[2x + c] = f(x, nv - 2 + c) for c = 0, 1 and every
+ *   interior row x (device arrays of 2 nx doubles; either may be NULL).
+ * vlasov_vslab_unpack: the inverse into the velocity ghost columns: f(x, -2 + c) = lo[2x + c],
+ *   f(x, nv + c) = hi[2x + c] (NULL leaves that side -- a physical boundary -- untouched).      */
+int vlasov_level_set_moment_base(vlasov_level* level, double base);
+int vlasov_vslab_pack(const vlasov_level* level, const double* f, double* lo, double* hi);
+int vlasov_vslab_unpack(const vlasov_level* level, double* f, const double* lo, const double* hi);
+
 /* ---- misc ------------------------------------------------------------------------------------ */
 const char* vlasov_last_error(void);
 int vlasov_device_ok(void);         /* 1 if a compute-capability 10.x device is current, else 0 */

@@ -68,6 +68,9 @@ _SIGS = {
     "vlasov_reduce_charge": (I32, [C.POINTER(P), I32, C.POINTER(P), D, D, I32, P]),
     "vlasov_inject_field_scaled": (I32, [P, P, PI32, D, P]),
     "vlasov_absmax": (I32, [P, I64, P, P]),
+    "vlasov_level_set_moment_base": (I32, [P, D]),
+    "vlasov_vslab_pack": (I32, [P, P, P, P]),
+    "vlasov_vslab_unpack": (I32, [P, P, P, P]),
     "vlasov_poisson_create": (I32, [I32, D, P, C.POINTER(P)]),
     "vlasov_poisson_solve": (I32, [P, P, P, P, I32]),
     "vlasov_poisson_destroy": (I32, [P]),

@@ -20,6 +20,7 @@ __all__ = [
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
     "vlasov_level_fill_from", "vlasov_absmax", "vlasov_device_ok", "vlasov_last_error",
+    "vlasov_level_set_moment_base", "vlasov_vslab_pack", "vlasov_vslab_unpack",
 ]
 
 
@@ -128,6 +129,18 @@ def vlasov_reduce_moment(levels, f_list, rho_finest):
     arr = (C.c_void_p * len(levels))(*[l.value if isinstance(l, C.c_void_p) else l for l in levels])
     fp = (C.c_void_p * len(levels))(*[(t.data_ptr() if t is not None else None) for t in f_list])
     return check(lib.vlasov_reduce_moment(arr, len(levels), fp, _ptr(rho_finest)))
+
+
+def vlasov_level_set_moment_base(h, base):
+    return check(lib.vlasov_level_set_moment_base(h, float(base)))
+
+
+def vlasov_vslab_pack(h, f, lo=None, hi=None):
+    return check(lib.vlasov_vslab_pack(h, _ptr(f), _ptr(lo), _ptr(hi)))
+
+
+def vlasov_vslab_unpack(h, f, lo=None, hi=None):
+    return check(lib.vlasov_vslab_unpack(h, _ptr(f), _ptr(lo), _ptr(hi)))
 
 
 def vlasov_absmax(x, out, stream=None):

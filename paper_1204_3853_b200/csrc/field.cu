@@ -191,6 +191,37 @@ __global__ void k_absmax(const double* __restrict__ x, int64_t n, double* __rest
     }
 }
 
+// velocity-slab halo: pack the two lowest / highest interior velocity columns of every interior
+// row into [nx][2] arrays, or unpack arrays into the two low / high ghost columns.  One thread per
+// (side, row, column pair); rows of a single block.
+__global__ void k_vslab(double* __restrict__ f, int64_t org, int64_t pitch, int nx, int nv, double* __restrict__ lo,
+                        double* __restrict__ hi, int pack) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * nx) return;
+    const int side = t / nx, x = t - side * nx;
+    double* buf = side ? hi : lo;
+    if (!buf) return;
+    double* row = f + org + (int64_t)x * pitch;                   // interior column 0 of row x
+    double* col = pack ? (side ? row + nv - 2 : row) : (side ? row + nv : row - 2);
+    double2* b2 = reinterpret_cast<double2*>(buf + 2 * x);
+    if (pack) {
+        *b2 = make_double2(col[0], col[1]);
+    } else {
+        const double2 v = *b2;
+        col[0] = v.x;
+        col[1] = v.y;
+    }
+}
+
+int launch_vslab(const vlasov_level* L, double* f, double* lo, double* hi, bool pack) {
+    const int nx = L->dom[0], nv = L->dom[1];
+    const int64_t pitch = L->block_str[0][0];
+    const int64_t org = L->block_off[0] + (int64_t)G * pitch + G;
+    k_vslab<<<(2 * nx + 127) / 128, 128, 0, L->stream>>>(f, org, pitch, nx, nv, lo, hi, pack ? 1 : 0);
+    VK_LAUNCH("k_vslab");
+    return VLASOV_OK;
+}
+
 int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st) {
     k_absmax<<<1, 1024, 0, st>>>(x, n, out);
     VK_LAUNCH("k_absmax");

@@ -132,6 +132,7 @@ int launch_reduce_mask(const MaskPlan* P, const double* const* f, int nlev, doub
 // ------------------------------------------------------------------ opaque structs
 struct vlasov_level {
     int ndim = 2, ncfg = 1;
+    double moment_base = 1.0;             // fused stage moment: rho = moment_base - dv sum_v f
     double lower[4] = {0, 0, 0, 0}, h[4] = {0, 0, 0, 0};
     int ratio[4] = {1, 1, 1, 1};
     int dom[4] = {0, 0, 0, 0};            // level domain cells per dim
@@ -215,6 +216,7 @@ int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_
                      double* E_lvl);
 int linear5_weights(int R, double* out /* R*5 */);
 int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st);
+int launch_vslab(const vlasov_level* L, double* f, double* lo, double* hi, bool pack);
 int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st,
                            double q = -1.0, double base = 1.0, int accumulate = 0);
 int launch_flux_registers(const vlasov_level* L, const double* f_fine, const double* E_fine, const double* f_coarse,

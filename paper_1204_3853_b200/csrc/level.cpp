@@ -1287,6 +1287,29 @@ int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const 
     return vlasov_reduce_charge(levels, nlev, f, -1.0, 1.0, 0, rho_finest);
 }
 
+int vlasov_level_set_moment_base(vlasov_level* L, double base) {
+    if (!L) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "moment base: one periodic block only");
+    L->moment_base = base;
+    return VLASOV_OK;
+}
+
+int vlasov_vslab_pack(const vlasov_level* L, const double* f, double* lo, double* hi) {
+    if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 2 || !L->single_block || L->dom[1] < 2)
+        return vk::fail(VLASOV_EUNSUPPORTED, "vslab: one 1D+1V block with >= 2 velocity cells");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_vslab(L, const_cast<double*>(f), lo, hi, true);
+}
+
+int vlasov_vslab_unpack(const vlasov_level* L, double* f, const double* lo, const double* hi) {
+    if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 2 || !L->single_block || L->dom[1] < 2)
+        return vk::fail(VLASOV_EUNSUPPORTED, "vslab: one 1D+1V block with >= 2 velocity cells");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_vslab(L, f, const_cast<double*>(lo), const_cast<double*>(hi), false);
+}
+
 int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream) {
     if (!x || !out || n < 0) return vk::fail(VLASOV_EINVAL, "null argument or n < 0");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");

@@ -57,6 +57,7 @@ struct StageArgs1 {
     const Tile1* tiles;
     const Block1* blocks;
     double dt, dx, dv, v_lo;   // v_lo: physical lower velocity of the level domain
+    double rho_base;           // fused moment: rho = rho_base - dv sum_v f (1 unless a velocity slab)
     int dom_x, dom_v, n_vtiles, tile_rows;
     // fused constraint evaluation (vlasov_rk4_stage_vp): E of the stage state from its moment
     const double* rho_in;      // nullable: rho of f_s (dom_x values); then E is computed and written
@@ -675,7 +676,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                 const int x = B.lo_x + T.x0 + rr;
                 double s = 0.0;
                 for (int t = 0; t < A.n_vtiles; ++t) s += __ldcg(A.partials + (int64_t)t * A.dom_x + x);
-                A.rho[x] = 1.0 - A.dv * s;
+                A.rho[x] = A.rho_base - A.dv * s;
             }
             if (tid == 0) A.tickets[T.strip] = 0u;     // reset for the next launch
         }
@@ -813,6 +814,7 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.dx = L->h[0];
     A.dv = L->h[1];
     A.v_lo = L->lower[1];
+    A.rho_base = L->moment_base;
     A.dom_x = L->dom[0];
     A.dom_v = L->dom[1];
     A.n_vtiles = L->n_vtiles;

@@ -1,0 +1,89 @@
+"""N2 on one GPU: the velocity-slab decomposition (paper_1204_3853_b200.vslab) emulated with all
+slabs in one process (LocalComm: the all-reduce of the slab moments and the halo exchange of the
+two boundary velocity columns as device copies), against the oracle and against the undivided GPU
+run.  The NCCL transport (DistComm) is the same sequence with torch.distributed collectives; its
+neighbour / reduction logic is covered on CPU by tests/test_multirank_cpu.py."""
+import numpy as np
+import pytest
+
+import inputs
+from oracle import uniform
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1204_3853_b200 import api  # noqa: E402
+from paper_1204_3853_b200.solver import UniformVlasov1D  # noqa: E402
+from paper_1204_3853_b200.vslab import LocalComm, VSlabVlasov1D, slab_ranges  # noqa: E402
+
+
+def _slab_run(w, nslabs, nsteps):
+    h = inputs.spacing(w)
+    G = VSlabVlasov1D(w.ncells, w.lower, h, inputs.background_profile(w), nslabs, range(nslabs), LocalComm())
+    f0 = inputs.initial_cell_averages(w)
+    G.set_state(f0)
+    dt = inputs.fixed_dt(w)
+    for _ in range(nsteps):
+        G.step(dt)
+    return np.concatenate(G.get_state(), axis=1), f0, dt
+
+
+def relerr(a, b):
+    return np.max(np.abs(a - b)) / np.max(np.abs(b))
+
+
+@pytest.mark.parametrize("nslabs", [2, 4])
+def test_c1_slabs_match_oracle(nslabs):
+    w = inputs.get("C1")
+    got, f0, dt = _slab_run(w, nslabs, 1)
+    ref, _ = uniform.problem_for(w).run(f0, dt, 1)
+    assert relerr(got, ref) < 1e-12
+    got, f0, dt = _slab_run(w, nslabs, 50)
+    ref, _ = uniform.problem_for(w).run(f0, dt, 50)
+    assert relerr(got, ref) < 1e-10
+
+
+def test_c2_four_slabs_hundred_steps():
+    w = inputs.get("C2")
+    got, f0, dt = _slab_run(w, 4, 100)
+    ref, _ = uniform.problem_for(w).run(f0, dt, 100)
+    assert relerr(got, ref) < 1e-10
+
+
+def test_slabs_equal_undivided_gpu_run():
+    """Same discretisation, only the moment's summation order and the ghost source differ."""
+    w = inputs.scaled(inputs.get("C4"), (128, 1024), (128, 1024))
+    got, f0, dt = _slab_run(w, 4, 5)
+    S = UniformVlasov1D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), inputs.background_profile(w))
+    S.set_state(f0)
+    for _ in range(5):
+        S.step(dt)
+    assert relerr(got, S.get_state()) < 1e-13
+
+
+def test_pack_unpack_columns():
+    w = inputs.scaled(inputs.get("C1"), (16, 32), (16, 32))
+    L = api.Level(2, w.ncells, w.lower, inputs.spacing(w), (1, 1), inputs.level0_boxes(w))
+    f = L.field(0.0)
+    data = np.arange(16 * 32, dtype=np.float64).reshape(16, 32)
+    L.set_domain(f, data)
+    lo = torch.zeros(32, dtype=torch.float64, device="cuda")
+    hi = torch.zeros(32, dtype=torch.float64, device="cuda")
+    api.vlasov_vslab_pack(L.h, f, lo, hi)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(lo.cpu().numpy().reshape(16, 2), data[:, 0:2])
+    np.testing.assert_array_equal(hi.cpu().numpy().reshape(16, 2), data[:, 30:32])
+    api.vlasov_vslab_unpack(L.h, f, hi, lo)             # ghosts: low <- hi columns, high <- lo columns
+    torch.cuda.synchronize()
+    g = L.patch_view(f, 0, 2).cpu().numpy()[2:-2]
+    np.testing.assert_array_equal(g[:, 0:2], data[:, 30:32])
+    np.testing.assert_array_equal(g[:, 34:36], data[:, 0:2])
+    np.testing.assert_array_equal(g[:, 2:34], data)
+
+
+def test_slab_ranges():
+    assert [len(r) for r in slab_ranges(64, 4)] == [16] * 4
+    with pytest.raises(ValueError):
+        slab_ranges(64, 3)
