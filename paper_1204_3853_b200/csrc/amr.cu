@@ -32,20 +32,26 @@ __global__ void k_red_cols(const LevelPtrs P, const RedCol* __restrict__ cols, i
 
 // rho[x] = 1 - sum over the contributions of x (level, patch, sub-patch order) of
 //          dv_l * sum_j b_j(s) colsum[c + j]          (linear5 refinement of the partial sums)
+// One warp per finest cell x: lane l takes the contributions l, l + 32, ... of x (the loads of
+// different contributions are independent, so they overlap), then a fixed butterfly
+// (deterministic; the order differs from the oracle's sequential sum only by rounding).
 __global__ void k_red_finest(const double* __restrict__ colsum, const RedContrib* __restrict__ con,
                              const int32_t* __restrict__ xoff, int nxf, double q, double base, int accumulate,
                              double* __restrict__ rho) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int x = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (x >= nxf) return;
     double acc = 0.0;
-    for (int k = xoff[x]; k < xoff[x + 1]; ++k) {
+    for (int k = xoff[x] + lane; k < xoff[x + 1]; k += 32) {
         const RedContrib& C = con[k];
         double t = 0.0;
 #pragma unroll
         for (int j = 0; j < 5; ++j) t += C.b[j] * colsum[C.cs + j];
         acc += C.dv * t;
     }
-    rho[x] = (accumulate ? rho[x] : base) + q * acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) rho[x] = (accumulate ? rho[x] : base) + q * acc;
 }
 
 int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st,
@@ -56,8 +62,8 @@ int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, d
         k_red_cols<<<(unsigned)((P->ncols + 7) / 8), 256, 0, st>>>(lp, P->d_cols, P->ncols, P->d_colsum);
         VK_LAUNCH("k_red_cols");
     }
-    k_red_finest<<<(P->nxf + 127) / 128, 128, 0, st>>>(P->d_colsum, P->d_contrib, P->d_xoff, P->nxf, q, base,
-                                                        accumulate, rho);
+    k_red_finest<<<(P->nxf + 3) / 4, 128, 0, st>>>(P->d_colsum, P->d_contrib, P->d_xoff, P->nxf, q, base,
+                                                    accumulate, rho);
     VK_LAUNCH("k_red_finest");
     return VLASOV_OK;
 }
@@ -152,31 +158,36 @@ __device__ double vface_flux(const double* f, const FaceRef& r, const double* E)
     return E[r.g] * fa[1] + c48 * (fa[2] - fa[0]);
 }
 
-// regs[t] += b_s (F_coarse - mean of the fine F) on every coarse face of the interface
+// regs[t] += b_s (F_coarse - mean of the fine F) on every coarse face of the interface.
+// FR_G = 8 lanes per task: lane g computes the fine faces g, g + 8, ... (their loads overlap),
+// lane 0 also the coarse face; a fixed butterfly sums the fine fluxes (deterministic).
+constexpr int FR_G = 8;
 template <int RECON>
 __global__ void k_flux_registers(const RefluxTask* __restrict__ tasks, int64_t n, const double* __restrict__ ff,
                                  const double* __restrict__ Ef, const double* __restrict__ fc,
                                  const double* __restrict__ Ec, double vlo, double dvf, double dvc, double b_s,
                                  double* __restrict__ regs) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const RefluxTask& T = tasks[t];
-    double Fc, Fs = 0.0;
-    if (T.dir == 0) {
-        Fc = xface_flux<RECON>(fc, T.cf, vlo, dvc);
-        for (int s = 0; s < T.nfine; ++s) Fs += xface_flux<RECON>(ff, T.ff[s], vlo, dvf);
-    } else {
-        Fc = vface_flux<RECON>(fc, T.cf, Ec);
-        for (int s = 0; s < T.nfine; ++s) Fs += vface_flux<RECON>(ff, T.ff[s], Ef);
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = gt / FR_G;
+    const int g = (int)(gt % FR_G);
+    const bool valid = t < n;
+    const RefluxTask& T = tasks[valid ? t : 0];
+    double Fs = 0.0, Fc = 0.0;
+    if (valid) {
+        for (int s = g; s < T.nfine; s += FR_G)
+            Fs += (T.dir == 0) ? xface_flux<RECON>(ff, T.ff[s], vlo, dvf) : vface_flux<RECON>(ff, T.ff[s], Ef);
+        if (g == 0) Fc = (T.dir == 0) ? xface_flux<RECON>(fc, T.cf, vlo, dvc) : vface_flux<RECON>(fc, T.cf, Ec);
     }
-    regs[t] += b_s * (Fc - Fs / (double)T.nfine);
+#pragma unroll
+    for (int o = FR_G / 2; o > 0; o >>= 1) Fs += __shfl_xor_sync(0xffffffffu, Fs, o);
+    if (valid && g == 0) regs[t] += b_s * (Fc - Fs / (double)T.nfine);
 }
 
 int launch_flux_registers(const vlasov_level* L, const double* f_fine, const double* E_fine, const double* f_coarse,
                           const double* E_coarse, double b_s, double* regs, int recon) {
     if (L->n_reflux == 0) return VLASOV_OK;
     const vlasov_level* C = L->coarser;
-    const unsigned blocks = (unsigned)((L->n_reflux + 127) / 128);
+    const unsigned blocks = (unsigned)((L->n_reflux * FR_G + 127) / 128);
     if (recon == VLASOV_UPWIND)
         k_flux_registers<VLASOV_UPWIND><<<blocks, 128, 0, L->stream>>>(L->d_reflux, L->n_reflux, f_fine, E_fine,
                                                                         f_coarse, E_coarse, L->lower[1], L->h[1],
