@@ -93,10 +93,15 @@ constexpr int CPT = STAGE1D_CPT;
 #ifndef RING_KB
 #define RING_KB 48
 #endif
-// programmatic dependent launch of the stage kernels: measured slower in the CUDA-graph step
-// (C4: 195 vs 185 us), so off; the kernel is PDL-safe (constants only before griddep_wait)
+// programmatic dependent launch of the stage kernels: a stage triggers its dependents when its
+// march is done, so the next stage's launch and setup overlap this one's tail (C4 graph step
+// 179 vs 185 us; triggering at kernel start measured slower, 195 us).  Only constants are read
+// before griddep_wait.
 #ifndef STAGE1D_PDL
-#define STAGE1D_PDL 0
+#define STAGE1D_PDL 1
+#endif
+#ifndef STAGE1D_PDL_EARLY
+#define STAGE1D_PDL_EARLY 0
 #endif
 // 1: a dedicated producer warp issues the TMA ring; 0: thread 0 of the consumers issues it (no
 // extra warp: 4 warps x 168 registers lets 3 CTAs share an SM instead of 2)
@@ -160,9 +165,11 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     double* psum = smem + NSLOT * SLOT;          // [NW][tile_rows]
 
     TRACE(0);
+#if STAGE1D_PDL_EARLY
     // programmatic dependent launch: the next stage may be scheduled as this grid's CTAs retire;
     // everything before griddep_wait() below touches only constants (tiles, f0v, gX)
     griddep_launch_dependents();
+#endif
 #ifdef STAGE1D_TRACE
     if (threadIdx.x == 0) { unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); g_trace[blockIdx.x][8] = sm; }
 #endif
@@ -632,6 +639,9 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         }
     }
 
+#if !STAGE1D_PDL_EARLY
+    griddep_launch_dependents();                 // the march is done: let the next stage launch
+#endif
     if (GHOST_OUT && (T.j0 == 0 || T.j0 + T.ncols == B.nv)) {
         // velocity ghost columns of f_next (characteristic BC, reading #6, for this stage's field:
         // the E_bc of the next stage, reading #6b) from the boundary cells staged during the march
