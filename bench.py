@@ -413,7 +413,7 @@ def main():
     achieved = STEP_BYTES * w.cells / (kern_ms_step / 1e3) / 1e9                   # GB/s over the 4 launches
     peak, peak_kind = read_peaks()
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "stage_traffic.json")
+    tp = os.path.join(ROOT, "profiles", f"stage_traffic_{w.name}.json")      # from an ncu capture of this workload
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("bytes_per_step_per_cell")

@@ -1,5 +1,6 @@
-"""Write profiles/stage_traffic.json (DRAM bytes per RK4 step of the 1D+1V stage kernels, read by
-bench.py's roofline.traffic) from an `ncu --set full` capture of the 4 stage launches of one step."""
+"""Write profiles/stage_traffic_<workload>.json (DRAM bytes per RK4 step of the stage kernels, read
+by bench.py's roofline.traffic) from an `ncu --set full` capture of the 4 stage launches of one step.
+usage: traffic_from_ncu.py REP CELLS WORKLOAD KERNEL_SUBSTRING"""
 import csv
 import io
 import json
@@ -9,6 +10,8 @@ import sys
 
 rep = sys.argv[1]
 cells = int(sys.argv[2]) if len(sys.argv) > 2 else 2048 * 4096
+wname = sys.argv[3] if len(sys.argv) > 3 else "C4"
+kname = sys.argv[4] if len(sys.argv) > 4 else "k_stage_1d1v"
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
@@ -24,18 +27,20 @@ def val(r, key, table):
 
 per = []
 for r in rows[2:]:
-    if "k_stage_1d1v" not in r[kn]:
+    if kname not in r[kn]:
         continue
     per.append({"kernel": r[kn][:60], "dram_read_bytes": val(r, "dram__bytes_read.sum", scale),
                 "dram_write_bytes": val(r, "dram__bytes_write.sum", scale),
                 "duration_us": val(r, "gpu__time_duration.sum", tscale)})
 per = per[:4]
 tot = sum(p["dram_read_bytes"] + p["dram_write_bytes"] for p in per)
-res = {"source": f"ncu --set full --clock-control none, {len(per)} stage launches of one C4 RK4 step ({rep})",
+if len(per) != 4:
+    sys.exit(f"need the 4 stage launches of one step, found {len(per)}")
+res = {"source": f"ncu --set full --clock-control none, {len(per)} stage launches of one {wname} RK4 step ({rep})",
        "bytes_per_step": tot, "bytes_per_step_per_cell": tot / cells, "algorithmic_bytes_per_step_per_cell": 104,
        "note": "ncu counts DRAM writes that leave L2 during the kernel; part of the last rows' writes are flushed "
                "after it, and rows still resident in L2 from the previous launch are not re-read",
        "per_launch": per}
-dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "stage_traffic.json")
+dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", f"stage_traffic_{wname}.json")
 json.dump(res, open(dst, "w"), indent=1)
 print(json.dumps(res, indent=1))
