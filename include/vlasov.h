@@ -191,6 +191,13 @@ int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const 
 int vlasov_reduce_charge(const vlasov_level* const* levels, int32_t nlev, const double* const* f, double q,
                          double base, int32_t accumulate, double* rho_finest);
 
+/* Current moment toward Vlasov-Maxwell (N4, reading #31), one uniform 1D+1V level (one
+ * block covering the domain): j[x] = (accumulate ? j[x] : 0) + q dv sum_v <v f>, with the
+ * fourth-order cell average of the product <v f>_j = vbar_j f_j + (dv/24)(f_{j+1} - f_{j-1}) (the
+ * product rule of the fluxes, reading #3); the velocity ghost columns of f must be current.
+ * Call once per species (accumulate = 0 for the first).  Deterministic (fixed order).        */
+int vlasov_reduce_current(const vlasov_level* level, const double* f, double q, int32_t accumulate, double* j);
+
 /* Alg.6 Mask Reduction: the same rho by refining every patch in x (linear5 with 2
  * ghost columns), masking the cells covered by the next finer level and summing over v -- the
  * paper's comparator of Alg.8 (sub-patch reduction = 64% of mask-reduction time).

@@ -77,3 +77,16 @@ def efield_from_rho(rho, dx):
 def ghost_periodic(a, g=G):
     """Periodic ghost extension of a configuration-space array along every axis."""
     return np.pad(a, [(g, g)] * a.ndim, mode="wrap")
+
+
+def current_density(f_ghosted, v_lo, dv, q=-1.0, g=G):
+    """Current moment j_i = q dv sum_j <v f>_ij of one species on a uniform 1D+1V level (N4, toward
+    Vlasov-Maxwell, P:68-78; reading #31): the fourth-order cell average of the product v f by the
+    same product rule as the fluxes (reading #3),
+        <v f>_j = vbar_j fbar_j + (dv / 24) (fbar_{j+1} - fbar_{j-1}),   vbar_j = v_lo + (j + 1/2) dv,
+    with fbar_{-1}, fbar_{nv} the velocity ghost values.  f_ghosted: (nx + 2g, nv + 2g)."""
+    f = np.asarray(f_ghosted, dtype=np.float64)[g:-g, :]
+    nv = f.shape[1] - 2 * g
+    vbar = v_lo + (np.arange(nv) + 0.5) * dv
+    vf = vbar[None, :] * f[:, g:g + nv] + (dv / 24.0) * (f[:, g + 1:g + 1 + nv] - f[:, g - 1:g - 1 + nv])
+    return q * dv * vf.sum(axis=1)

@@ -20,7 +20,7 @@ __all__ = [
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
     "vlasov_level_fill_from", "vlasov_absmax", "vlasov_device_ok", "vlasov_last_error",
-    "vlasov_level_set_moment_base", "vlasov_vslab_pack", "vlasov_vslab_unpack",
+    "vlasov_level_set_moment_base", "vlasov_vslab_pack", "vlasov_vslab_unpack", "vlasov_reduce_current",
 ]
 
 
@@ -129,6 +129,10 @@ def vlasov_reduce_moment(levels, f_list, rho_finest):
     arr = (C.c_void_p * len(levels))(*[l.value if isinstance(l, C.c_void_p) else l for l in levels])
     fp = (C.c_void_p * len(levels))(*[(t.data_ptr() if t is not None else None) for t in f_list])
     return check(lib.vlasov_reduce_moment(arr, len(levels), fp, _ptr(rho_finest)))
+
+
+def vlasov_reduce_current(h, f, q, accumulate, j):
+    return check(lib.vlasov_reduce_current(h, _ptr(f), float(q), int(bool(accumulate)), _ptr(j)))
 
 
 def vlasov_level_set_moment_base(h, base):

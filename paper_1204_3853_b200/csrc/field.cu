@@ -222,6 +222,34 @@ int launch_vslab(const vlasov_level* L, double* f, double* lo, double* hi, bool 
     return VLASOV_OK;
 }
 
+// j[x] = (acc ? j[x] : 0) + q dv sum_v (vbar_v f_v + dv/24 (f_{v+1} - f_{v-1})): one warp per row x,
+// lanes strided over v, fixed butterfly (deterministic)
+__global__ void k_current_1d(const double* __restrict__ f, int64_t org, int64_t pitch, int nx, int nv, double vlo,
+                             double dv, double q, int accumulate, double* __restrict__ j) {
+    const int lane = threadIdx.x & 31;
+    const int x = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (x >= nx) return;
+    const double* row = f + org + (int64_t)x * pitch;            // interior column 0 of row x
+    double s = 0.0, d = 0.0;
+    for (int v = lane; v < nv; v += 32) {
+        s += (vlo + ((double)v + 0.5) * dv) * row[v];
+        d += row[v + 1] - row[v - 1];
+    }
+    double t = s + (dv * (1.0 / 24.0)) * d;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) j[x] = (accumulate ? j[x] : 0.0) + q * dv * t;
+}
+
+int launch_current(const vlasov_level* L, const double* f, double q, int accumulate, double* j) {
+    const int nx = L->dom[0], nv = L->dom[1];
+    const int64_t pitch = L->block_str[0][0];
+    const int64_t org = L->block_off[0] + (int64_t)G * pitch + G;
+    k_current_1d<<<(nx + 3) / 4, 128, 0, L->stream>>>(f, org, pitch, nx, nv, L->lower[1], L->h[1], q, accumulate, j);
+    VK_LAUNCH("k_current_1d");
+    return VLASOV_OK;
+}
+
 int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st) {
     k_absmax<<<1, 1024, 0, st>>>(x, n, out);
     VK_LAUNCH("k_absmax");

@@ -217,6 +217,7 @@ int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_
 int linear5_weights(int R, double* out /* R*5 */);
 int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st);
 int launch_vslab(const vlasov_level* L, double* f, double* lo, double* hi, bool pack);
+int launch_current(const vlasov_level* L, const double* f, double q, int accumulate, double* j);
 int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st,
                            double q = -1.0, double base = 1.0, int accumulate = 0);
 int launch_flux_registers(const vlasov_level* L, const double* f_fine, const double* E_fine, const double* f_coarse,

@@ -1287,6 +1287,14 @@ int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const 
     return vlasov_reduce_charge(levels, nlev, f, -1.0, 1.0, 0, rho_finest);
 }
 
+int vlasov_reduce_current(const vlasov_level* L, const double* f, double q, int32_t accumulate, double* j) {
+    if (!L || !f || !j) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 2 || !L->single_block)
+        return vk::fail(VLASOV_EUNSUPPORTED, "current moment: one uniform 1D+1V block");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_current(L, f, q, accumulate, j);
+}
+
 int vlasov_level_set_moment_base(vlasov_level* L, double base) {
     if (!L) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "moment base: one periodic block only");

@@ -98,3 +98,36 @@ def test_split_electrons_superpose_on_gpu():
     for l in range(len(ref)):
         for x, y, z in zip(a[l], b[l], ref[l]):
             np.testing.assert_allclose(x + y, z, rtol=0, atol=1e-13 * np.abs(z).max())
+
+
+# ---------------------------------------------------------------- N4: current moment
+def test_current_moment_parity():
+    """vlasov_reduce_current (two species accumulated) against the oracle's current_density on
+    the C2 state after 5 GPU steps (ghosts refilled), and its closed form for the initial state
+    (j = 0: the profile is symmetric in v)."""
+    from oracle import field
+    from paper_1204_3853_b200 import api
+    from paper_1204_3853_b200.solver import UniformVlasov1D
+    w = inputs.get("C2")
+    h = inputs.spacing(w)
+    S = UniformVlasov1D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w))
+    S.set_state(inputs.initial_cell_averages(w))
+    j = torch.zeros(w.ncells[0], dtype=torch.float64, device="cuda")
+    api.vlasov_reduce_current(S.level.h, S.A, -1.0, 0, j)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(j.cpu().numpy())) < 1e-15
+    for _ in range(5):
+        S.step(inputs.fixed_dt(w))
+    with torch.cuda.stream(S.stream):
+        api.vlasov_fill_ghosts(S.level.h, S.A, None, None, S.E[0], S.f0v)
+        api.vlasov_reduce_current(S.level.h, S.A, -1.0, 0, j)
+        api.vlasov_reduce_current(S.level.h, S.A, 0.25, 1, j)          # a second species, same f
+    S.stream.synchronize()
+    fg = S.level.patch_view(S.A, 0, 2).cpu().numpy()
+    ref = field.current_density(fg, w.lower[1], h[1], q=-0.75)
+    got = j.cpu().numpy()
+    assert np.max(np.abs(ref)) > 1e-6
+    # j is a cancelling sum (v of both signs): the rounding bound scales with dv sum |v f|
+    vbar = w.lower[1] + (np.arange(w.ncells[1]) + 0.5) * h[1]
+    scale = 0.75 * h[1] * np.sum(np.abs(vbar[None, :] * fg[2:-2, 2:-2]), axis=1)
+    assert np.all(np.abs(got - ref) <= 1e-14 * scale)
