@@ -541,14 +541,23 @@ __global__ void k_vghost_2d2v(double* __restrict__ f, int64_t org, int64_t s0, i
     }
 }
 
-// rho[i][k] = 1 - dvx dvy sum_p partials[p][i][k]  (fixed order: deterministic)
+// rho[i][k] = 1 - dvx dvy sum_p partials[p][i][k]: block (32 cells, 8 plane groups); group g sums
+// the planes g, g + 8, ... of its cell, the 8 group sums are added in group order (deterministic)
 __global__ void k_moment_2d2v_finish(const double* __restrict__ partials, int np, int ncfg, double dvv,
                                      double* __restrict__ rho) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ncfg) return;
+    __shared__ double sg[8][33];
+    const int c = blockIdx.x * 32 + threadIdx.x, g = threadIdx.y;
     double s = 0.0;
-    for (int p = 0; p < np; ++p) s += partials[(int64_t)p * ncfg + t];
-    rho[t] = 1.0 - dvv * s;
+    if (c < ncfg)
+        for (int p = g; p < np; p += 8) s += partials[(int64_t)p * ncfg + c];
+    sg[g][threadIdx.x] = s;
+    __syncthreads();
+    if (g == 0 && c < ncfg) {
+        double t = sg[0][threadIdx.x];
+#pragma unroll
+        for (int k = 1; k < 8; ++k) t += sg[k][threadIdx.x];
+        rho[c] = 1.0 - dvv * t;
+    }
 }
 
 // rho from a stored state (one warp per configuration cell)
@@ -664,8 +673,8 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
                                 : dispatch2<VLASOV_CENTERED4>(stage, A, M, grid, L->stream);
     if (rc || !rho) return rc;
     const int ncfg = A.nx * A.ny;
-    k_moment_2d2v_finish<<<(ncfg + 127) / 128, 128, 0, L->stream>>>(L->d_partials, A.nvx * nmt, ncfg,
-                                                                     A.hvx * A.hvy, rho);
+    k_moment_2d2v_finish<<<(ncfg + 31) / 32, dim3(32, 8), 0, L->stream>>>(L->d_partials, A.nvx * nmt, ncfg,
+                                                                          A.hvx * A.hvy, rho);
     VK_LAUNCH("k_moment_2d2v_finish");
     return VLASOV_OK;
 }
