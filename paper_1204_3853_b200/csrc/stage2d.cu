@@ -507,37 +507,32 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(
 // Only the ghosts the stage stencils read are derived (vx ghosts at interior vy and vice versa).
 __global__ void k_vghost_2d2v(double* __restrict__ f, int64_t org, int64_t s0, int64_t s1, int64_t s2, int nx, int ny,
                               int nvx, int nvy, const double* __restrict__ E_bc, const double* __restrict__ f0v) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n1 = (int64_t)nx * ny * nvx, n2 = (int64_t)nx * ny * nvy;
-    if (t >= n1 + n2) return;
+    // block = one (x, y) column: threads [0, nvx) the vy ghosts of vx line li, threads
+    // [nvx, nvx + nvy) the vx ghosts at vy index li; all loads issued before the stores
+    const int c = blockIdx.x;                                     // i * ny + k
+    const int i = c / ny, k = c - (c / ny) * ny;
     const int nyg = ny + 4;
-    const bool vy = t < n1;
-    const int64_t u = vy ? t : t - n1;
-    const int inner = vy ? nvx : nvy;
-    const int li = (int)(u % inner);
-    const int64_t xy = u / inner;
-    const int i = (int)(xy / ny), k = (int)(xy % ny);
     const int64_t col = (int64_t)(i + 2) * nyg + (k + 2);
-    const double a = -__ldg(E_bc + (vy ? (int64_t)(nx + 4) * nyg : 0) + col);
     double* base = f + org + (int64_t)i * s0 + (int64_t)k * s1;
-    const int64_t st = vy ? 1 : s2;                               // stride along the ghosted dim
-    double* line = vy ? base + (int64_t)li * s2 : base + li;     // element 0 of the ghosted dim
-    const int n = vy ? nvy : nvx;
-    auto prof = [&](int g) {                                      // profile at ghosted index g of the dim
-        return vy ? __ldg(f0v + (int64_t)(li + 2) * (nvy + 4) + (g + 2)) : __ldg(f0v + (int64_t)(g + 2) * (nvy + 4) + (li + 2));
-    };
-    {   // low side
-        const double f0 = line[0], f1 = line[st], f2 = line[2 * st], f3 = line[3 * st];
-        const bool out = a < 0.0;
-        line[-st] = out ? 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3 : prof(-1);
-        line[-2 * st] = out ? 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3 : prof(-2);
-    }
-    {   // high side
+    for (int t = threadIdx.x; t < nvx + nvy; t += blockDim.x) {
+        const bool vy = t < nvx;
+        const int li = vy ? t : t - nvx;
+        const double a = -__ldg(E_bc + (vy ? (int64_t)(nx + 4) * nyg : 0) + col);
+        const int64_t st = vy ? 1 : s2;                           // stride along the ghosted dim
+        double* line = vy ? base + (int64_t)li * s2 : base + li;  // element 0 of the ghosted dim
+        const int n = vy ? nvy : nvx;
+        const double* pr = vy ? f0v + (int64_t)(li + 2) * (nvy + 4) + 2 : f0v + 2 * (int64_t)(nvy + 4) + (li + 2);
+        const int64_t pst = vy ? 1 : nvy + 4;                     // profile at ghosted index g: pr[g * pst]
         double* e = line + (int64_t)(n - 1) * st;
-        const double f0 = e[0], f1 = e[-st], f2 = e[-2 * st], f3 = e[-3 * st];
-        const bool out = a > 0.0;
-        e[st] = out ? 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3 : prof(n);
-        e[2 * st] = out ? 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3 : prof(n + 1);
+        const double l0 = line[0], l1 = line[st], l2 = line[2 * st], l3 = line[3 * st];
+        const double h0 = e[0], h1 = e[-st], h2 = e[-2 * st], h3 = e[-3 * st];
+        const double pm1 = __ldg(pr - pst), pm2 = __ldg(pr - 2 * pst);
+        const double pn = __ldg(pr + (int64_t)n * pst), pn1 = __ldg(pr + (int64_t)(n + 1) * pst);
+        const bool out_lo = a < 0.0, out_hi = a > 0.0;
+        line[-st] = out_lo ? 4.0 * l0 - 6.0 * l1 + 4.0 * l2 - l3 : pm1;
+        line[-2 * st] = out_lo ? 10.0 * l0 - 20.0 * l1 + 15.0 * l2 - 4.0 * l3 : pm2;
+        e[st] = out_hi ? 4.0 * h0 - 6.0 * h1 + 4.0 * h2 - h3 : pn;
+        e[2 * st] = out_hi ? 10.0 * h0 - 20.0 * h1 + 15.0 * h2 - 4.0 * h3 : pn1;
     }
 }
 
@@ -664,8 +659,7 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
         (rc = encode_map(L, f_n ? f_n : f_s, S2_TM, 4, &M.fn4)) || (rc = encode_map(L, u ? u : f_s, S2_TM, 4, &M.u4)))
         return rc;
     if (S2_GLOBAL_GHOSTS) {
-        const int64_t nt = (int64_t)A.nx * A.ny * (A.nvx + A.nvy);
-        k_vghost_2d2v<<<(unsigned)((nt + 255) / 256), 256, 0, L->stream>>>(const_cast<double*>(f_s), A.org, A.s0, A.s1,
+        k_vghost_2d2v<<<(unsigned)(A.nx * A.ny), 128, 0, L->stream>>>(const_cast<double*>(f_s), A.org, A.s0, A.s1,
                                                                            A.s2, A.nx, A.ny, A.nvx, A.nvy, E_bc, f0v);
         VK_LAUNCH("k_vghost_2d2v");
     }
