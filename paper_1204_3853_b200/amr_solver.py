@@ -302,7 +302,12 @@ class AmrVlasov1D:
         return new_boxes
 
     def cells(self):
-        return sum(int(np.prod([hi[d] - lo[d] + 1 for d in range(2)])) for L in self.levels for lo, hi in L.boxes)
+        """Cells on all levels (cached per hierarchy: the per-step host cost stays O(1))."""
+        key = tuple(L.h.value for L in self.levels)
+        if getattr(self, "_cells_key", None) != key:
+            self._cells = sum((hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) for L in self.levels for lo, hi in L.boxes)
+            self._cells_key = key
+        return self._cells
 
 
 class MultiSpeciesVlasov1D:

@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "ptx.cuh"
 #include "scheme.cuh"
 
 namespace vk {
@@ -18,6 +19,8 @@ struct LevelPtrs {
 // colsum[c] = sum over the sub-patch's velocity range of column c (one warp per grown column)
 __global__ void k_red_cols(const LevelPtrs P, const RedCol* __restrict__ cols, int64_t ncols,
                            double* __restrict__ colsum) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int lane = threadIdx.x & 31;
     const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (c >= ncols) return;
@@ -38,6 +41,8 @@ __global__ void k_red_cols(const LevelPtrs P, const RedCol* __restrict__ cols, i
 __global__ void k_red_finest(const double* __restrict__ colsum, const RedContrib* __restrict__ con,
                              const int32_t* __restrict__ xoff, int nxf, double q, double base, int accumulate,
                              double* __restrict__ rho) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int lane = threadIdx.x & 31;
     const int x = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (x >= nxf) return;
@@ -59,12 +64,11 @@ int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, d
     LevelPtrs lp;
     for (int l = 0; l < MAXLEV; ++l) lp.f[l] = l < nlev ? f[l] : nullptr;
     if (P->ncols > 0) {
-        k_red_cols<<<(unsigned)((P->ncols + 7) / 8), 256, 0, st>>>(lp, P->d_cols, P->ncols, P->d_colsum);
-        VK_LAUNCH("k_red_cols");
+        VK_CUDA(launch_pdl(k_red_cols, dim3((unsigned)((P->ncols + 7) / 8)), dim3(256), 0, st, lp,
+                           (const RedCol*)P->d_cols, (int64_t)P->ncols, P->d_colsum));
     }
-    k_red_finest<<<(P->nxf + 3) / 4, 128, 0, st>>>(P->d_colsum, P->d_contrib, P->d_xoff, P->nxf, q, base,
-                                                    accumulate, rho);
-    VK_LAUNCH("k_red_finest");
+    VK_CUDA(launch_pdl(k_red_finest, dim3((P->nxf + 3) / 4), dim3(128), 0, st, (const double*)P->d_colsum,
+                       (const RedContrib*)P->d_contrib, (const int32_t*)P->d_xoff, P->nxf, q, base, accumulate, rho));
     return VLASOV_OK;
 }
 
@@ -167,6 +171,8 @@ __global__ void k_flux_registers(const RefluxTask* __restrict__ tasks, int64_t n
                                  const double* __restrict__ Ef, const double* __restrict__ fc,
                                  const double* __restrict__ Ec, double vlo, double dvf, double dvc, double b_s,
                                  double* __restrict__ regs) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t t = gt / FR_G;
     const int g = (int)(gt % FR_G);
@@ -188,15 +194,9 @@ int launch_flux_registers(const vlasov_level* L, const double* f_fine, const dou
     if (L->n_reflux == 0) return VLASOV_OK;
     const vlasov_level* C = L->coarser;
     const unsigned blocks = (unsigned)((L->n_reflux * FR_G + 127) / 128);
-    if (recon == VLASOV_UPWIND)
-        k_flux_registers<VLASOV_UPWIND><<<blocks, 128, 0, L->stream>>>(L->d_reflux, L->n_reflux, f_fine, E_fine,
-                                                                        f_coarse, E_coarse, L->lower[1], L->h[1],
-                                                                        C->h[1], b_s, regs);
-    else
-        k_flux_registers<VLASOV_CENTERED4><<<blocks, 128, 0, L->stream>>>(L->d_reflux, L->n_reflux, f_fine, E_fine,
-                                                                           f_coarse, E_coarse, L->lower[1], L->h[1],
-                                                                           C->h[1], b_s, regs);
-    VK_LAUNCH("k_flux_registers");
+    auto kern = recon == VLASOV_UPWIND ? k_flux_registers<VLASOV_UPWIND> : k_flux_registers<VLASOV_CENTERED4>;
+    VK_CUDA(launch_pdl(kern, dim3(blocks), dim3(128), 0, L->stream, (const RefluxTask*)L->d_reflux, (int64_t)L->n_reflux,
+                       f_fine, E_fine, f_coarse, E_coarse, L->lower[1], L->h[1], C->h[1], b_s, regs));
     return VLASOV_OK;
 }
 
@@ -207,6 +207,8 @@ int launch_flux_registers(const vlasov_level* L, const double* f_fine, const dou
 __global__ void k_reflux(const RefluxTask* __restrict__ tasks, const int64_t* __restrict__ cells,
                          const int32_t* __restrict__ off, int64_t ncells, const double* __restrict__ regs,
                          double dt, double dxc, double dvc, double* __restrict__ fc) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncells) return;
     double d = 0.0;
@@ -221,6 +223,8 @@ __global__ void k_reflux(const RefluxTask* __restrict__ tasks, const int64_t* __
 
 __global__ void k_average_down(const AvgTask* __restrict__ tasks, int64_t n, int Rx, int Rv,
                                const double* __restrict__ ff, double* __restrict__ fc) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const AvgTask T = tasks[t];
@@ -233,14 +237,15 @@ __global__ void k_average_down(const AvgTask* __restrict__ tasks, int64_t n, int
 int launch_average_down(const vlasov_level* L, const double* f_fine, double* f_coarse, const double* regs, double dt) {
     const vlasov_level* C = L->coarser;
     if (regs && L->n_reflux_cells > 0) {
-        k_reflux<<<(unsigned)((L->n_reflux_cells + 127) / 128), 128, 0, L->stream>>>(
-            L->d_reflux, L->d_reflux_cells, L->d_reflux_off, L->n_reflux_cells, regs, dt, C->h[0], C->h[1], f_coarse);
-        VK_LAUNCH("k_reflux");
+        VK_CUDA(launch_pdl(k_reflux, dim3((unsigned)((L->n_reflux_cells + 127) / 128)), dim3(128), 0, L->stream,
+                           (const RefluxTask*)L->d_reflux, (const int64_t*)L->d_reflux_cells,
+                           (const int32_t*)L->d_reflux_off, (int64_t)L->n_reflux_cells, regs, dt, C->h[0], C->h[1],
+                           f_coarse));
     }
     if (L->n_avg > 0) {
-        k_average_down<<<(unsigned)((L->n_avg + 127) / 128), 128, 0, L->stream>>>(
-            L->d_avg, L->n_avg, L->coarse_ratio[0], L->coarse_ratio[1], f_fine, f_coarse);
-        VK_LAUNCH("k_average_down");
+        VK_CUDA(launch_pdl(k_average_down, dim3((unsigned)((L->n_avg + 127) / 128)), dim3(128), 0, L->stream,
+                           (const AvgTask*)L->d_avg, (int64_t)L->n_avg, L->coarse_ratio[0], L->coarse_ratio[1], f_fine,
+                           f_coarse));
     }
     return VLASOV_OK;
 }

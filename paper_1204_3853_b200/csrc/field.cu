@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace vk {
 
@@ -42,6 +43,8 @@ template <bool G_SMEM>
 __global__ void __launch_bounds__(CIRC_TX * CIRC_TY) k_circulant(const double* __restrict__ rho,
                                                                   const double* __restrict__ g, int n, int ghost,
                                                                   double* __restrict__ out) {
+    griddep_wait();
+    griddep_launch_dependents();
     extern __shared__ double sm[];
     double* s_rho = sm;                                  // [n]
     double* s_part = sm + n;                             // [CIRC_TY][CIRC_OUT]
@@ -117,18 +120,20 @@ int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E,
     }
     auto kern = gs ? k_circulant<true> : k_circulant<false>;
     if (E) {
-        kern<<<blocks, CIRC_TX * CIRC_TY, smem, P->stream>>>(rho, P->d_gE, n, ghost, E);
-        VK_LAUNCH("k_circulant(E)");
+        VK_CUDA(launch_pdl(kern, dim3(blocks), dim3(CIRC_TX * CIRC_TY), smem, P->stream, rho, (const double*)P->d_gE, n,
+                           ghost, E));
     }
     if (phi) {
-        kern<<<blocks, CIRC_TX * CIRC_TY, smem, P->stream>>>(rho, P->d_gphi, n, ghost, phi);
-        VK_LAUNCH("k_circulant(phi)");
+        VK_CUDA(launch_pdl(kern, dim3(blocks), dim3(CIRC_TX * CIRC_TY), smem, P->stream, rho, (const double*)P->d_gphi,
+                           n, ghost, phi));
     }
     return VLASOV_OK;
 }
 
 // E_lvl[i + 2] = scale * mean_{s<R} E_f[R i + s]; periodic ghosts i = -2, -1, n, n+1.
 __global__ void k_inject_1d(const double* __restrict__ Ef, int nf, int R, int n, double scale, double* __restrict__ El) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n + 4) return;
     int i = t - 2;
@@ -142,7 +147,8 @@ int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest
     const int n = L->dom[0];
     if (n_finest % n) return fail(VLASOV_EINVAL, "inject: finest size not a multiple of the level size");
     const int R = n_finest / n;
-    k_inject_1d<<<(n + 4 + 127) / 128, 128, 0, L->stream>>>(E_finest, n_finest, R, n, scale, E_lvl);
+    VK_CUDA(launch_pdl(k_inject_1d, dim3((n + 4 + 127) / 128), dim3(128), 0, L->stream, E_finest, n_finest, R, n, scale,
+                       E_lvl));
     VK_LAUNCH("k_inject_1d");
     return VLASOV_OK;
 }

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <array>
+#include <utility>
 #include <memory>
 #include <string>
 #include <vector>
@@ -24,6 +25,29 @@ int fail(int code, const std::string& msg);
 int cuda_check(cudaError_t e, const char* what);
 #define VK_CUDA(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return ::vk::cuda_check(_e, #call); } while (0)
 #define VK_LAUNCH(what) do { cudaError_t _e = cudaGetLastError(); if (_e != cudaSuccess) return ::vk::cuda_check(_e, what); } while (0)
+
+// Launch with programmatic dependent launch allowed: the kernel may start while the previous
+// kernel on the stream retires, so it must execute griddep_wait() (ptx.cuh) before it reads
+// anything earlier kernels wrote.  The small AMR / field kernels call griddep_wait() and
+// griddep_launch_dependents() first thing, so their launch latencies overlap along the stream.
+#ifndef VK_PDL
+#define VK_PDL 1
+#endif
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = VK_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------ boxes
 struct Box {

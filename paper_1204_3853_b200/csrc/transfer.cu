@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace vk {
 
@@ -59,6 +60,8 @@ template <int INTERP>
 __global__ void k_fill_copy_cf(double* __restrict__ f, const double* __restrict__ fsrc,
                                const int64_t* __restrict__ copies, int64_t ncopy, const double* __restrict__ fc, const CFTask* __restrict__ cf, int64_t ncf,
                                const double* __restrict__ b5, int Rx, int Rv) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < ncopy) {
         f[copies[2 * t]] = fsrc[copies[2 * t + 1]];
@@ -80,6 +83,8 @@ __global__ void k_fill_copy_cf(double* __restrict__ f, const double* __restrict_
 
 __global__ void k_fill_phys(double* __restrict__ f, const PhysTask* __restrict__ tasks, int64_t n,
                             const double* __restrict__ E_bc, const double* __restrict__ f0v, int nv) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const PhysTask T = tasks[t];
@@ -106,19 +111,15 @@ int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double
     if (L->n_cf > 0 && f_coarse == nullptr) return fail(VLASOV_EINVAL, "fill_ghosts: coarse data required");
     if (n1 > 0) {
         const int64_t blocks = (n1 + 255) / 256;
-        if (interp == VLASOV_WENO5)
-            k_fill_copy_cf<VLASOV_WENO5><<<(unsigned)blocks, 256, 0, L->stream>>>(
-                f, f, L->d_copy, L->n_copy, f_coarse, L->d_cf, L->n_cf, L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
-        else
-            k_fill_copy_cf<VLASOV_LINEAR5><<<(unsigned)blocks, 256, 0, L->stream>>>(
-                f, f, L->d_copy, L->n_copy, f_coarse, L->d_cf, L->n_cf, L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
-        VK_LAUNCH("k_fill_copy_cf");
+        auto kern = interp == VLASOV_WENO5 ? k_fill_copy_cf<VLASOV_WENO5> : k_fill_copy_cf<VLASOV_LINEAR5>;
+        VK_CUDA(launch_pdl(kern, dim3((unsigned)blocks), dim3(256), 0, L->stream, f, (const double*)f,
+                           (const int64_t*)L->d_copy, (int64_t)L->n_copy, f_coarse, (const CFTask*)L->d_cf,
+                           (int64_t)L->n_cf, (const double*)L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]));
     }
     if (L->n_phys > 0) {
         if (E_bc == nullptr || f0v == nullptr) return fail(VLASOV_EINVAL, "fill_ghosts: E_bc and f0v required");
-        k_fill_phys<<<(unsigned)((L->n_phys + 255) / 256), 256, 0, L->stream>>>(f, L->d_phys, L->n_phys, E_bc, f0v,
-                                                                             L->dom[1]);
-        VK_LAUNCH("k_fill_phys");
+        VK_CUDA(launch_pdl(k_fill_phys, dim3((unsigned)((L->n_phys + 255) / 256)), dim3(256), 0, L->stream, f,
+                           (const PhysTask*)L->d_phys, (int64_t)L->n_phys, E_bc, f0v, L->dom[1]));
     }
     return VLASOV_OK;
 }
