@@ -71,8 +71,11 @@ class AmrVlasov1D:
         self.regs.append(None if coarser is None else torch.zeros(max(1, n), dtype=torch.float64, device="cuda"))
 
     def _make_field_plan(self):
-        self.nxf = self.levels[-1].info.domain_cells[0]
-        self.dxf = self.dx0[0] / self.levels[-1].ratio[0]
+        nxf = self.levels[-1].info.domain_cells[0]
+        dxf = self.dx0[0] / self.levels[-1].ratio[0]
+        if getattr(self, "poisson", None) is not None and (nxf, dxf) == (self.nxf, self.dxf):
+            return                          # same finest mesh after a regrid: keep the plan
+        self.nxf, self.dxf = nxf, dxf
         self.poisson = api.Poisson(self.nxf, self.dxf, self.stream)
         self.rho = torch.zeros(self.nxf, dtype=torch.float64, device="cuda")
         self.E_f = torch.zeros(self.nxf, dtype=torch.float64, device="cuda")

@@ -24,6 +24,11 @@ void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_check(cudaError_t e, const char* what);
 #define VK_CUDA(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return ::vk::cuda_check(_e, #call); } while (0)
+// Level / plan metadata is allocated stream-ordered (cudaMallocAsync on the owner's stream, pooled):
+// a regrid's level create / destroy then neither blocks on cudaMalloc nor synchronises the device.
+inline void dfree(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
 #define VK_LAUNCH(what) do { cudaError_t _e = cudaGetLastError(); if (_e != cudaSuccess) return ::vk::cuda_check(_e, what); } while (0)
 
 // Launch with programmatic dependent launch allowed: the kernel may start while the previous
@@ -121,6 +126,7 @@ struct AvgTask {              // one covered coarse cell (reading #14
 constexpr int MAXLEV = 8;     // levels of one hierarchy handled by the reduction
 struct RedPlan {              // Alg.8 sub-patch reduction plan (built on the host, level.cpp)
     std::vector<uint64_t> uids;   // the hierarchy it was built for
+    cudaStream_t st = nullptr;    // stream its device arrays were allocated on (stream-ordered)
     int nxf = 0;                  // finest configuration cells
     int64_t ncols = 0, ncontrib = 0;
     RedCol* d_cols = nullptr;
@@ -139,6 +145,7 @@ struct MaskCol {              // Alg.6: one coarse x column of one patch, refine
 };
 struct MaskPlan {             // Alg.6 Mask Reduction plan (comparator of Alg.8)
     std::vector<uint64_t> uids;
+    cudaStream_t st = nullptr;
     int nxf = 0;
     int64_t ncols = 0, npart = 0;
     MaskCol* d_cols = nullptr;
@@ -248,6 +255,11 @@ int launch_flux_registers(const vlasov_level* L, const double* f_fine, const dou
                           const double* E_coarse, double b_s, double* regs, int recon);
 int launch_average_down(const vlasov_level* L, const double* f_fine, double* f_coarse, const double* regs, double dt);
 int launch_tags(const vlasov_level* L, const double* f, double tol, int buffer, uint8_t* tags);
-int launch_fill_from(const vlasov_level* L, double* f, const double* f_old, const std::vector<int64_t>& copies,
+struct RectCopy {              // fill_from: one old-patch / new-patch overlap rectangle (1D+1V)
+    int64_t dst, src;         // level-array index of the rectangle's first cell (new / old)
+    int32_t dpitch, spitch;   // x strides (doubles) of the new / old block
+    int32_t nx, nv;
+};
+int launch_fill_from(const vlasov_level* L, double* f, const double* f_old, const std::vector<RectCopy>& rects,
                      const double* f_coarse, const std::vector<CFTask>& cfs, int interp);
 }  // namespace vk

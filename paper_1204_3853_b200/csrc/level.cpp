@@ -137,22 +137,22 @@ int linear5_weights(int R, double* out) {
 }
 void free_mask_plan(MaskPlan* p) {
     if (!p) return;
-    cudaFree(p->d_cols);
-    cudaFree(p->d_mask);
-    cudaFree(p->d_w);
-    cudaFree(p->d_part);
-    cudaFree(p->d_xoff);
-    cudaFree(p->d_idx);
-    cudaFree(p->d_dv);
+    dfree(p->d_cols, p->st);
+    dfree(p->d_mask, p->st);
+    dfree(p->d_w, p->st);
+    dfree(p->d_part, p->st);
+    dfree(p->d_xoff, p->st);
+    dfree(p->d_idx, p->st);
+    dfree(p->d_dv, p->st);
     delete p;
 }
 
 void free_red_plan(RedPlan* p) {
     if (!p) return;
-    cudaFree(p->d_cols);
-    cudaFree(p->d_colsum);
-    cudaFree(p->d_contrib);
-    cudaFree(p->d_xoff);
+    dfree(p->d_cols, p->st);
+    dfree(p->d_colsum, p->st);
+    dfree(p->d_contrib, p->st);
+    dfree(p->d_xoff, p->st);
     delete p;
 }
 }  // namespace vk
@@ -165,29 +165,29 @@ template <class T>
 int upload(T** dptr, const std::vector<T>& h, cudaStream_t st) {
     *dptr = nullptr;
     if (h.empty()) return VLASOV_OK;
-    VK_CUDA(cudaMalloc((void**)dptr, h.size() * sizeof(T)));
+    VK_CUDA(cudaMallocAsync((void**)dptr, h.size() * sizeof(T), st));
     VK_CUDA(cudaMemcpyAsync(*dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     return VLASOV_OK;
 }
 
 void free_level(vlasov_level* L) {
     if (!L) return;
-    cudaFree(L->d_blocks1);
-    cudaFree(L->d_tiles_wide);
-    cudaFree(L->d_tiles_narrow);
-    cudaFree(L->d_copy);
-    cudaFree(L->d_cf);
-    cudaFree(L->d_phys);
-    cudaFree(L->d_reflux);
-    cudaFree(L->d_reflux_cells);
-    cudaFree(L->d_reflux_off);
-    cudaFree(L->d_avg);
+    vk::dfree(L->d_blocks1, L->stream);
+    vk::dfree(L->d_tiles_wide, L->stream);
+    vk::dfree(L->d_tiles_narrow, L->stream);
+    vk::dfree(L->d_copy, L->stream);
+    vk::dfree(L->d_cf, L->stream);
+    vk::dfree(L->d_phys, L->stream);
+    vk::dfree(L->d_reflux, L->stream);
+    vk::dfree(L->d_reflux_cells, L->stream);
+    vk::dfree(L->d_reflux_off, L->stream);
+    vk::dfree(L->d_avg, L->stream);
     vk::free_red_plan(L->red_plan);
     vk::free_mask_plan(L->mask_plan);
-    cudaFree(L->d_b5);
-    cudaFree(L->d_partials);
-    cudaFree(L->d_tickets);
-    cudaFree(L->d_rawtags);
+    vk::dfree(L->d_b5, L->stream);
+    vk::dfree(L->d_partials, L->stream);
+    vk::dfree(L->d_tickets, L->stream);
+    vk::dfree(L->d_rawtags, L->stream);
     delete L;
 }
 
@@ -665,6 +665,7 @@ int build_red_plan(const vlasov_level* const* levels, int nlev, vk::RedPlan** ou
     }
     xoff[nxf] = (int32_t)con.size();
     vk::RedPlan* P = new vk::RedPlan();
+    P->st = Lf->stream;
     for (int l = 0; l < nlev; ++l) P->uids.push_back(levels[l]->uid);
     P->nxf = nxf;
     P->ncols = (int64_t)cols.size();
@@ -676,7 +677,7 @@ int build_red_plan(const vlasov_level* const* levels, int nlev, vk::RedPlan** ou
         vk::free_red_plan(P);
         return rc;
     }
-    if (!cols.empty()) VK_CUDA(cudaMalloc((void**)&P->d_colsum, sizeof(double) * cols.size()));
+    if (!cols.empty()) VK_CUDA(cudaMallocAsync((void**)&P->d_colsum, sizeof(double) * cols.size(), st));
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) { vk::free_red_plan(P); return vk::cuda_check(e, "reduction plan upload"); }
     *out = P;
@@ -842,13 +843,13 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
     }
     if (!L->single_block && L->ndim == 2) {      // tag scratch of multi-patch levels (regrid)
         int64_t tb = (int64_t)L->dom[0] * L->dom[1];
-        VK_CUDA(cudaMalloc((void**)&L->d_rawtags, (size_t)tb));
+        VK_CUDA(cudaMallocAsync((void**)&L->d_rawtags, (size_t)tb, L->stream));
     }
     if (L->single_block && L->ndim == 4)
-        VK_CUDA(cudaMalloc((void**)&L->d_partials, sizeof(double) * (size_t)L->n_vtiles * L->dom[0] * L->dom[1]));
+        VK_CUDA(cudaMallocAsync((void**)&L->d_partials, sizeof(double) * (size_t)L->n_vtiles * L->dom[0] * L->dom[1], L->stream));
     if (L->single_block && L->ndim == 2) {
-        VK_CUDA(cudaMalloc((void**)&L->d_partials, sizeof(double) * (size_t)L->n_vtiles * L->dom[0]));
-        VK_CUDA(cudaMalloc((void**)&L->d_tickets, sizeof(unsigned) * (size_t)std::max(1, L->n_strips)));
+        VK_CUDA(cudaMallocAsync((void**)&L->d_partials, sizeof(double) * (size_t)L->n_vtiles * L->dom[0], L->stream));
+        VK_CUDA(cudaMallocAsync((void**)&L->d_tickets, sizeof(unsigned) * (size_t)std::max(1, L->n_strips), L->stream));
         VK_CUDA(cudaMemsetAsync(L->d_tickets, 0, sizeof(unsigned) * (size_t)std::max(1, L->n_strips), L->stream));
     }
     if ((rc = upload(&L->d_blocks1, L->h_blocks1, L->stream)) ||
@@ -1391,6 +1392,7 @@ static int build_mask_plan(const vlasov_level* const* levels, int nlev, vk::Mask
     }
     xoff[nxf] = (int32_t)idx.size();
     vk::MaskPlan* P = new vk::MaskPlan();
+    P->st = Lf->stream;
     for (int l = 0; l < nlev; ++l) P->uids.push_back(levels[l]->uid);
     P->nxf = nxf;
     P->ncols = (int64_t)cols.size();
@@ -1402,7 +1404,7 @@ static int build_mask_plan(const vlasov_level* const* levels, int nlev, vk::Mask
         vk::free_mask_plan(P);
         return rc;
     }
-    if (npart) VK_CUDA(cudaMalloc((void**)&P->d_part, sizeof(double) * (size_t)npart));
+    if (npart) VK_CUDA(cudaMallocAsync((void**)&P->d_part, sizeof(double) * (size_t)npart, st));
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) { vk::free_mask_plan(P); return vk::cuda_check(e, "mask plan upload"); }
     *out = P;
@@ -1476,15 +1478,15 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
     int rc;
     if ((rc = upload(&P->d_gE, gE, P->stream)) || (rc = upload(&P->d_gphi, gphi, P->stream)) ||
         (rc = upload(&P->d_gX, gX, P->stream))) {
-        cudaFree(P->d_gE);
-        cudaFree(P->d_gphi);
-        cudaFree(P->d_gX);
+        vk::dfree(P->d_gE, P->stream);
+        vk::dfree(P->d_gphi, P->stream);
+        vk::dfree(P->d_gX, P->stream);
         delete P;
         return rc;
     }
     cudaError_t e = cudaStreamSynchronize(P->stream);
     if (e != cudaSuccess) {
-        cudaFree(P->d_gE); cudaFree(P->d_gphi); cudaFree(P->d_gX);
+        vk::dfree(P->d_gE, P->stream); vk::dfree(P->d_gphi, P->stream); vk::dfree(P->d_gX, P->stream);
         delete P;
         return vk::cuda_check(e, "poisson upload");
     }
@@ -1501,10 +1503,10 @@ int vlasov_poisson_solve(vlasov_poisson* P, const double* rho, double* phi, doub
 
 int vlasov_poisson_destroy(vlasov_poisson* P) {
     if (P) {
+        vk::dfree(P->d_gE, P->stream);
+        vk::dfree(P->d_gphi, P->stream);
+        vk::dfree(P->d_gX, P->stream);
         cudaStreamSynchronize(P->stream);
-        cudaFree(P->d_gE);
-        cudaFree(P->d_gphi);
-        cudaFree(P->d_gX);
         delete P;
     }
     return VLASOV_OK;
@@ -1565,47 +1567,63 @@ int vlasov_level_fill_from(vlasov_level* L, double* f, const vlasov_level* old, 
         for (int d = 0; d < L->ndim; ++d)
             if (old->ratio[d] != L->ratio[d]) return vk::fail(VLASOV_EINVAL, "fill_from: old level resolution differs");
     }
-    // copy where an old patch holds the cell (same-level data wins), else interpolate
-    Owner oown;
-    if (old) oown = make_owner(old, old->blocks);
+    // copy where an old patch holds the cell (same-level data wins): one rectangle per
+    // (new patch, old patch) overlap; the cells of a new patch no old patch covers interpolate
     Owner cown;
     const vlasov_level* C = L->coarser;
     if (C) cown = make_owner(C, C->blocks);
-    std::vector<int64_t> copies;
+    std::vector<vk::RectCopy> rects;
     std::vector<vk::CFTask> cfs;
+    std::vector<char> cover;
     int err = VLASOV_OK;
     for (size_t p = 0; p < L->boxes.size(); ++p) {
+        const vk::Box& P = L->boxes[p];
         const int blk = L->patch_block[p];
-        for_each_cell(L->boxes[p], L->ndim, [&](const int* c) {
-            if (err) return;
-            const int64_t dst = cell_addr(L, blk, c);
-            const int ob = old ? oown.find(c) : -1;
-            if (ob >= 0) {
-                copies.push_back(dst);
-                copies.push_back(cell_addr(old, ob, c));
-                return;
+        const int nx = vk::box_ncells_dim(P, 0), nv = vk::box_ncells_dim(P, 1);
+        cover.assign((size_t)nx * nv, 0);
+        if (old) {
+            for (size_t q = 0; q < old->boxes.size(); ++q) {
+                const vk::Box I = vk::box_intersect(P, old->boxes[q], L->ndim);
+                if (vk::box_empty(I, L->ndim)) continue;
+                const int ob = old->patch_block[q];
+                vk::RectCopy r;
+                r.dst = cell_addr(L, blk, I.lo);
+                r.src = cell_addr(old, ob, I.lo);
+                r.dpitch = (int32_t)L->block_str[blk][0];
+                r.spitch = (int32_t)old->block_str[ob][0];
+                r.nx = vk::box_ncells_dim(I, 0);
+                r.nv = vk::box_ncells_dim(I, 1);
+                rects.push_back(r);
+                for (int x = I.lo[0]; x <= I.hi[0]; ++x)
+                    std::fill(cover.begin() + (size_t)(x - P.lo[0]) * nv + (I.lo[1] - P.lo[1]),
+                              cover.begin() + (size_t)(x - P.lo[0]) * nv + (I.hi[1] - P.lo[1]) + 1, (char)1);
             }
-            if (!C || !coarser || !f_coarse) {
-                err = vk::fail(VLASOV_EINVAL, "fill_from: cell without old data needs the coarser level");
-                return;
+        }
+        for (int x = 0; x < nx && !err; ++x)
+            for (int v = 0; v < nv; ++v) {
+                if (cover[(size_t)x * nv + v]) continue;
+                const int c[4] = {P.lo[0] + x, P.lo[1] + v, 0, 0};
+                if (!C || !coarser || !f_coarse) {
+                    err = vk::fail(VLASOV_EINVAL, "fill_from: cell without old data needs the coarser level");
+                    break;
+                }
+                int cc[4] = {0, 0, 0, 0};
+                for (int d = 0; d < L->ndim; ++d) cc[d] = vk::floordiv(c[d], L->coarse_ratio[d]);
+                const int cq = cown.find(cc);
+                if (cq < 0) { err = vk::fail(VLASOV_ESTENCIL, "fill_from: coarse parent missing"); break; }
+                vk::CFTask t;
+                t.dst = cell_addr(L, blk, c);
+                t.csrc = cell_addr(C, cq, cc);
+                for (int d = 0; d < 4; ++d) {
+                    t.cstride[d] = d < L->ndim ? (int32_t)C->block_str[cq][d] : 0;
+                    t.sub[d] = d < L->ndim ? (int8_t)(c[d] - cc[d] * L->coarse_ratio[d]) : 0;
+                }
+                cfs.push_back(t);
             }
-            int cc[4] = {0, 0, 0, 0};
-            for (int d = 0; d < L->ndim; ++d) cc[d] = vk::floordiv(c[d], L->coarse_ratio[d]);
-            const int cq = cown.find(cc);
-            if (cq < 0) { err = vk::fail(VLASOV_ESTENCIL, "fill_from: coarse parent missing"); return; }
-            vk::CFTask t;
-            t.dst = dst;
-            t.csrc = cell_addr(C, cq, cc);
-            for (int d = 0; d < 4; ++d) {
-                t.cstride[d] = d < L->ndim ? (int32_t)C->block_str[cq][d] : 0;
-                t.sub[d] = d < L->ndim ? (int8_t)(c[d] - cc[d] * L->coarse_ratio[d]) : 0;
-            }
-            cfs.push_back(t);
-        });
         if (err) return err;
     }
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
-    return vk::launch_fill_from(L, f, f_old, copies, f_coarse, cfs, interp);
+    return vk::launch_fill_from(L, f, f_old, rects, f_coarse, cfs, interp);
 }
 
 }  // extern "C"

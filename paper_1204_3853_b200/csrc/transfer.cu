@@ -127,29 +127,41 @@ int launch_fill(vlasov_level* L, double* f, const double* f_coarse, const double
 // Regrid data motion (vlasov_level_fill_from): the task lists depend on the old level, so they
 // are built per call and staged through stream-ordered scratch; the call synchronises its stream
 // (a regrid is a host decision point anyway).
-int launch_fill_from(const vlasov_level* L, double* f, const double* f_old, const std::vector<int64_t>& copies,
+// fill_from: one block per overlap rectangle, threads strided over its cells (v fastest)
+__global__ void k_copy_rects(double* __restrict__ f, const double* __restrict__ fo, const RectCopy* __restrict__ R) {
+    const RectCopy r = R[blockIdx.x];
+    const int64_t n = (int64_t)r.nx * r.nv;
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+        const int x = (int)(t / r.nv), v = (int)(t - (int64_t)x * r.nv);
+        f[r.dst + (int64_t)x * r.dpitch + v] = fo[r.src + (int64_t)x * r.spitch + v];
+    }
+}
+
+int launch_fill_from(const vlasov_level* L, double* f, const double* f_old, const std::vector<RectCopy>& rects,
                      const double* f_coarse, const std::vector<CFTask>& cfs, int interp) {
-    const int64_t ncopy = (int64_t)copies.size() / 2, ncf = (int64_t)cfs.size();
-    if (ncopy + ncf == 0) return VLASOV_OK;
-    int64_t* d_copy = nullptr;
+    const int64_t nrect = (int64_t)rects.size(), ncf = (int64_t)cfs.size();
+    if (nrect + ncf == 0) return VLASOV_OK;
+    RectCopy* d_rect = nullptr;
     CFTask* d_cf = nullptr;
-    if (ncopy) {
-        VK_CUDA(cudaMallocAsync((void**)&d_copy, copies.size() * sizeof(int64_t), L->stream));
-        VK_CUDA(cudaMemcpyAsync(d_copy, copies.data(), copies.size() * sizeof(int64_t), cudaMemcpyHostToDevice, L->stream));
+    if (nrect) {
+        VK_CUDA(cudaMallocAsync((void**)&d_rect, rects.size() * sizeof(RectCopy), L->stream));
+        VK_CUDA(cudaMemcpyAsync(d_rect, rects.data(), rects.size() * sizeof(RectCopy), cudaMemcpyHostToDevice, L->stream));
+        k_copy_rects<<<(unsigned)nrect, 256, 0, L->stream>>>(f, f_old, d_rect);
+        VK_LAUNCH("k_copy_rects");
     }
     if (ncf) {
         VK_CUDA(cudaMallocAsync((void**)&d_cf, cfs.size() * sizeof(CFTask), L->stream));
         VK_CUDA(cudaMemcpyAsync(d_cf, cfs.data(), cfs.size() * sizeof(CFTask), cudaMemcpyHostToDevice, L->stream));
+        const unsigned blocks = (unsigned)((ncf + 255) / 256);
+        if (interp == VLASOV_WENO5)
+            k_fill_copy_cf<VLASOV_WENO5><<<blocks, 256, 0, L->stream>>>(f, f, nullptr, 0, f_coarse, d_cf, ncf, L->d_b5,
+                                                                          L->coarse_ratio[0], L->coarse_ratio[1]);
+        else
+            k_fill_copy_cf<VLASOV_LINEAR5><<<blocks, 256, 0, L->stream>>>(f, f, nullptr, 0, f_coarse, d_cf, ncf,
+                                                                            L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
+        VK_LAUNCH("k_fill_copy_cf(fill_from)");
     }
-    const unsigned blocks = (unsigned)((ncopy + ncf + 255) / 256);
-    if (interp == VLASOV_WENO5)
-        k_fill_copy_cf<VLASOV_WENO5><<<blocks, 256, 0, L->stream>>>(f, f_old, d_copy, ncopy, f_coarse, d_cf, ncf, L->d_b5,
-                                                                      L->coarse_ratio[0], L->coarse_ratio[1]);
-    else
-        k_fill_copy_cf<VLASOV_LINEAR5><<<blocks, 256, 0, L->stream>>>(f, f_old, d_copy, ncopy, f_coarse, d_cf, ncf,
-                                                                        L->d_b5, L->coarse_ratio[0], L->coarse_ratio[1]);
-    VK_LAUNCH("k_fill_copy_cf(fill_from)");
-    if (d_copy) cudaFreeAsync(d_copy, L->stream);
+    if (d_rect) cudaFreeAsync(d_rect, L->stream);
     if (d_cf) cudaFreeAsync(d_cf, L->stream);
     VK_CUDA(cudaStreamSynchronize(L->stream));
     return VLASOV_OK;
