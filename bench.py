@@ -412,14 +412,18 @@ def main():
     kern_ms_step = float(per_stage_avg.sum())
     achieved = STEP_BYTES * w.cells / (kern_ms_step / 1e3) / 1e9                   # GB/s over the 4 launches
     peak, peak_kind = read_peaks()
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"stage_traffic_{w.name}.json")      # from an ncu capture of this workload
+    # DRAM bytes of the stage kernels from an ncu --set full capture of this workload, per launch
+    # (the average of the 4 stage launches of a step, like `achieved`), and per step
+    traffic, traffic_step = None, None
+    tp = os.path.join(ROOT, "profiles", f"stage_traffic_{w.name}.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("bytes_per_step_per_cell")
-            traffic = None if traffic is None else float(traffic) * w.cells
+            tpc = json.load(open(tp)).get("bytes_per_step_per_cell")
+            if tpc is not None:
+                traffic_step = float(tpc) * w.cells
+                traffic = traffic_step / 4.0
         except Exception:
-            traffic = None
+            traffic, traffic_step = None, None
 
     # ---------------------------------------------------------------- end to end (host buffers)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -456,6 +460,8 @@ def main():
                 "graph": f"CUDA graph, 1 RK4 step ({S.launches_per_step()} launches)"}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "traffic_per_step": traffic_step,
+                         "algorithmic_bytes_per_launch": STEP_BYTES * w.cells / 4.0,
                          "kernel": ("k_stage_1d1v" if w.ncfg == 1 else "k_stage_2d2v") + " (4 launches per step)",
                          "algorithmic_bytes_per_cell_step": STEP_BYTES,
                          "stage_ms": [float(x) for x in per_stage_avg],
