@@ -196,7 +196,6 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     double* sE = psum + NW * A.tile_rows;        // E of rows x0-2 .. x0+nrows+1
     double* sEbc = sE + (A.tile_rows + 4);       // E_bc of the same rows (SELF)
     const bool field = SELF && (A.rho_in != nullptr);
-    if (SELF && tid < 4) s_f0[tid] = __ldg(A.f0v + (tid < 2 ? tid : A.dom_v + tid));
     if (tid == 0) {
         for (int s = 0; s < NSLOT; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -287,6 +286,9 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         if (!field) sE[t] = __ldg(A.E + gi);
         if (SELF && A.E_bc) sEbc[t] = __ldg(A.E_bc + gi);
     }
+    // the unperturbed profile at the velocity ghost columns (read after the setup barrier: a
+    // global load there would sit on every CTA's start-up path)
+    if (SELF && tid < 4) s_f0[tid] = __ldg(A.f0v + (tid < 2 ? tid : A.dom_v + tid));
     named_bar_sync(1, NT);
     if (!PWARPS && tid == 0) {                   // consumer thread 0 primes the ring
         issue_field();
