@@ -139,6 +139,8 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(
         }
         fence_mbar_init();
     }
+    // programmatic dependent launch: nothing above read memory earlier kernels write
+    griddep_wait();
     // Stage what the ghost values need besides the slots: E_bc (x, y components) of the strip's
     // rows at y = k-2 .. k+2, the unperturbed profile at the vy ghost cells of the CTA's vx lines
     // and at the vx ghost lines (characteristic condition, reading #6).
@@ -499,6 +501,7 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(
             }
         }
     }
+    griddep_launch_dependents();                 // the march is done: let the next kernel launch
 }
 
 // Velocity ghost frame of f (characteristic condition, reading #6, a = -E_bc of the (x, y) column):
@@ -507,6 +510,8 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(
 // Only the ghosts the stage stencils read are derived (vx ghosts at interior vy and vice versa).
 __global__ void k_vghost_2d2v(double* __restrict__ f, int64_t org, int64_t s0, int64_t s1, int64_t s2, int nx, int ny,
                               int nvx, int nvy, const double* __restrict__ E_bc, const double* __restrict__ f0v) {
+    griddep_wait();
+    griddep_launch_dependents();
     // block = one (x, y) column: threads [0, nvx) the vy ghosts of vx line li, threads
     // [nvx, nvx + nvy) the vx ghosts at vy index li; all loads issued before the stores
     const int c = blockIdx.x;                                     // i * ny + k
@@ -540,6 +545,8 @@ __global__ void k_vghost_2d2v(double* __restrict__ f, int64_t org, int64_t s0, i
 // the planes g, g + 8, ... of its cell, the 8 group sums are added in group order (deterministic)
 __global__ void k_moment_2d2v_finish(const double* __restrict__ partials, int np, int ncfg, double dvv,
                                      double* __restrict__ rho) {
+    griddep_wait();
+    griddep_launch_dependents();
     __shared__ double sg[8][33];
     const int c = blockIdx.x * 32 + threadIdx.x, g = threadIdx.y;
     double s = 0.0;
@@ -581,8 +588,7 @@ static int launch2_t(const StageArgs2& A, const TMaps2& M, dim3 grid, cudaStream
         VK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    kern<<<grid, S2_THREADS, smem, st>>>(A, M);
-    VK_LAUNCH("k_stage_2d2v");
+    VK_CUDA(launch_pdl(kern, grid, dim3(S2_THREADS), smem, st, A, M));
     return VLASOV_OK;
 }
 
@@ -659,17 +665,15 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
         (rc = encode_map(L, f_n ? f_n : f_s, S2_TM, 4, &M.fn4)) || (rc = encode_map(L, u ? u : f_s, S2_TM, 4, &M.u4)))
         return rc;
     if (S2_GLOBAL_GHOSTS) {
-        k_vghost_2d2v<<<(unsigned)(A.nx * A.ny), 128, 0, L->stream>>>(const_cast<double*>(f_s), A.org, A.s0, A.s1,
-                                                                           A.s2, A.nx, A.ny, A.nvx, A.nvy, E_bc, f0v);
-        VK_LAUNCH("k_vghost_2d2v");
+        VK_CUDA(launch_pdl(k_vghost_2d2v, dim3((unsigned)(A.nx * A.ny)), dim3(128), 0, L->stream,
+                           const_cast<double*>(f_s), A.org, A.s0, A.s1, A.s2, A.nx, A.ny, A.nvx, A.nvy, E_bc, f0v));
     }
     rc = recon == VLASOV_UPWIND ? dispatch2<VLASOV_UPWIND>(stage, A, M, grid, L->stream)
                                 : dispatch2<VLASOV_CENTERED4>(stage, A, M, grid, L->stream);
     if (rc || !rho) return rc;
     const int ncfg = A.nx * A.ny;
-    k_moment_2d2v_finish<<<(ncfg + 31) / 32, dim3(32, 8), 0, L->stream>>>(L->d_partials, A.nvx * nmt, ncfg,
-                                                                          A.hvx * A.hvy, rho);
-    VK_LAUNCH("k_moment_2d2v_finish");
+    VK_CUDA(launch_pdl(k_moment_2d2v_finish, dim3((ncfg + 31) / 32), dim3(32, 8), 0, L->stream,
+                       (const double*)L->d_partials, A.nvx * nmt, ncfg, A.hvx * A.hvy, rho));
     return VLASOV_OK;
 }
 
