@@ -196,20 +196,21 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     double* sE = psum + NW * A.tile_rows;        // E of rows x0-2 .. x0+nrows+1
     double* sEbc = sE + (A.tile_rows + 4);       // E_bc of the same rows (SELF)
     const bool field = SELF && (A.rho_in != nullptr);
-    if (tid == 0) {
-        for (int s = 0; s < NSLOT; ++s) {
-            mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], NW);
-        }
-        mbar_init(&field_bar, 1);
-        mbar_init(&e_bar, 1);
+    // one mbarrier per thread (sequential inits by one thread cost ~35 ns each, ~1 us for a
+    // 12-slot ring); every initialising thread fences its own inits
+    if (tid < 2 * NSLOT + 2) {
+        uint64_t* bar = tid < NSLOT ? &full_bar[tid] : tid < 2 * NSLOT ? &empty_bar[tid - NSLOT]
+                      : tid == 2 * NSLOT ? &field_bar : &e_bar;
+        mbar_init(bar, (tid >= NSLOT && tid < 2 * NSLOT) ? (uint32_t)NW : 1u);
         fence_mbar_init();
     }
     // fused field in a cluster (the v-tiles of one row strip): every CTA's barrier is initialised
     // and armed before any CTA pushes E rows into its shared memory
     const uint32_t crank = field ? cluster_ctarank() : 0u, csize = field ? cluster_nctarank() : 1u;
-    if (tid == 0 && csize > 1) mbar_arrive_expect_tx(&e_bar, (uint32_t)Q * 8u);
     __syncthreads();
+    // (after the barrier that orders the inits; before this thread's cluster arrive, so no remote
+    // push can reach e_bar first)
+    if (tid == 0 && csize > 1) mbar_arrive_expect_tx(&e_bar, (uint32_t)Q * 8u);
     // consumers arrive now and wait only before their first remote store; the producer waits at once
     if (field && csize > 1) {
         if (PWARPS && warp >= NW) cluster_sync_all();
