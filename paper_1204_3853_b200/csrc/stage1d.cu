@@ -130,7 +130,13 @@ struct StageGeom {
     static constexpr int NFN = (STAGE >= 2 ? 1 : 0) + (STAGE == 4 ? 1 : 0);
     static constexpr int SLOT = SEG + NFN * TV;              // doubles per ring slot
     // ring depth: ~RING_KB of row data per CTA, 3..16 slots (a slot is consumed in one row step)
-    static constexpr int NSLOT_RAW = (RING_KB * 1024) / (SLOT * 8);
+    // ring size per stage (measured on C4: stage 2 best at 48 KB, stages 3 and 4 at 64 KB)
+#ifdef RING_KB_ALL
+    static constexpr int RKB = RING_KB_ALL;
+#else
+    static constexpr int RKB = STAGE >= 3 ? 64 : RING_KB;
+#endif
+    static constexpr int NSLOT_RAW = (RKB * 1024) / (SLOT * 8);
     static constexpr int NSLOT = NSLOT_RAW < 4 ? 4 : (NSLOT_RAW > 16 ? 16 : NSLOT_RAW);
     static constexpr int NW = NT / 32;
     static size_t smem_bytes(int tile_rows) {
