@@ -46,7 +46,7 @@ constexpr int S2_LW = S2_TM + 4;          // doubles per line segment in a slot
 #define S2_MAXNREG_ON 0
 #endif
 #ifndef S2_NSLOT_CFG
-#define S2_NSLOT_CFG 3
+#define S2_NSLOT_CFG 4
 #endif
 constexpr int S2_NSLOT = S2_NSLOT_CFG;
 // 1: the velocity ghost frame of f_s is derived in global memory by k_vghost_2d2v before the stage
