@@ -7,27 +7,31 @@ import numpy as np
 import pytest
 
 import inputs
-from oracle import uniform
+from oracle import scheme, uniform
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
-from paper_1204_3853_b200 import api  # noqa: E402
+from paper_1204_3853_b200 import _lib, api  # noqa: E402
 from paper_1204_3853_b200.solver import UniformVlasov1D  # noqa: E402
 from paper_1204_3853_b200.vslab import LocalComm, VSlabVlasov1D, slab_ranges  # noqa: E402
 
 
-def _slab_run(w, nslabs, nsteps):
+def _slab_run(w, nslabs, nsteps, recon=scheme.CENTERED4):
     h = inputs.spacing(w)
-    G = VSlabVlasov1D(w.ncells, w.lower, h, inputs.background_profile(w), nslabs, range(nslabs), LocalComm())
+    G = VSlabVlasov1D(w.ncells, w.lower, h, inputs.background_profile(w), nslabs, range(nslabs), LocalComm(),
+                      recon=RECON[recon])
     f0 = inputs.initial_cell_averages(w)
     G.set_state(f0)
     dt = inputs.fixed_dt(w)
     for _ in range(nsteps):
         G.step(dt)
     return np.concatenate(G.get_state(), axis=1), f0, dt
+
+
+RECON = {scheme.CENTERED4: _lib.CENTERED4, scheme.UPWIND: _lib.UPWIND}
 
 
 def relerr(a, b):
@@ -43,6 +47,15 @@ def test_c1_slabs_match_oracle(nslabs):
     got, f0, dt = _slab_run(w, nslabs, 50)
     ref, _ = uniform.problem_for(w).run(f0, dt, 50)
     assert relerr(got, ref) < 1e-10
+
+
+def test_upwind_slabs_match_oracle():
+    """UPWIND reconstruction (data-dependent face weights) across the slab faces: the halo carries
+    the two neighbour columns its stencils read."""
+    w = inputs.get("C1")
+    got, f0, dt = _slab_run(w, 2, 10, scheme.UPWIND)
+    ref, _ = uniform.problem_for(w, scheme.UPWIND).run(f0, dt, 10)
+    assert relerr(got, ref) < 1e-11
 
 
 def test_c2_four_slabs_hundred_steps():
