@@ -226,9 +226,13 @@ int device_ok_impl() {
 
 // owner lookup over the level domain: which block (or patch) holds a cell (-1: none)
 struct Owner {
+    // cell -> index of the box holding it (-1: none).  1D+1V: per x row, the boxes' v intervals
+    // sorted by their start (binary search; no dense map of the level domain to build and clear);
+    // 2D+2V: a dense map (those levels are single blocks).
     int nd = 2;
     int dom[4] = {0, 0, 0, 0};
     std::vector<int32_t> id;
+    std::vector<std::vector<std::array<int32_t, 3>>> rows;   // [x] -> {v_lo, v_hi, box}
     int64_t lin(const int* c) const {
         int64_t i = 0;
         for (int d = 0; d < nd; ++d) i = i * dom[d] + c[d];
@@ -237,6 +241,15 @@ struct Owner {
     int find(const int* c) const {
         for (int d = 0; d < nd; ++d)
             if (c[d] < 0 || c[d] >= dom[d]) return -1;
+        if (nd == 2) {
+            const auto& r = rows[c[0]];
+            int lo = 0, hi = (int)r.size() - 1;
+            while (lo <= hi) {                   // last interval starting at or below c[1]
+                const int mid = (lo + hi) >> 1;
+                if (r[mid][0] <= c[1]) lo = mid + 1; else hi = mid - 1;
+            }
+            return (hi >= 0 && c[1] <= r[hi][1]) ? r[hi][2] : -1;
+        }
         return id[lin(c)];
     }
 };
@@ -249,19 +262,22 @@ Owner make_owner(const vlasov_level* L, const std::vector<Box>& bs) {
         o.dom[d] = L->dom[d];
         tot *= L->dom[d];
     }
+    if (L->ndim == 2) {
+        o.rows.assign(L->dom[0], {});
+        for (size_t p = 0; p < bs.size(); ++p)
+            for (int x = bs[p].lo[0]; x <= bs[p].hi[0]; ++x)
+                o.rows[x].push_back({bs[p].lo[1], bs[p].hi[1], (int32_t)p});
+        for (auto& r : o.rows) std::sort(r.begin(), r.end());
+        return o;
+    }
     o.id.assign(tot, -1);
     for (size_t p = 0; p < bs.size(); ++p) {
         const Box& b = bs[p];
         int c[4];
-        if (L->ndim == 2) {
-            for (c[0] = b.lo[0]; c[0] <= b.hi[0]; ++c[0])
-                for (c[1] = b.lo[1]; c[1] <= b.hi[1]; ++c[1]) o.id[o.lin(c)] = (int32_t)p;
-        } else {
-            for (c[0] = b.lo[0]; c[0] <= b.hi[0]; ++c[0])
-                for (c[1] = b.lo[1]; c[1] <= b.hi[1]; ++c[1])
-                    for (c[2] = b.lo[2]; c[2] <= b.hi[2]; ++c[2])
-                        for (c[3] = b.lo[3]; c[3] <= b.hi[3]; ++c[3]) o.id[o.lin(c)] = (int32_t)p;
-        }
+        for (c[0] = b.lo[0]; c[0] <= b.hi[0]; ++c[0])
+            for (c[1] = b.lo[1]; c[1] <= b.hi[1]; ++c[1])
+                for (c[2] = b.lo[2]; c[2] <= b.hi[2]; ++c[2])
+                    for (c[3] = b.lo[3]; c[3] <= b.hi[3]; ++c[3]) o.id[o.lin(c)] = (int32_t)p;
     }
     return o;
 }
@@ -744,15 +760,23 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         total += vk::box_ncells(b, nd);
         L->boxes.push_back(b);
     }
-    {   // disjointness via an owner map
-        Owner o;
-        o.nd = nd;
+    {   // disjointness
         int64_t tot = 1;
-        for (int d = 0; d < nd; ++d) { o.dom[d] = L->dom[d]; tot *= L->dom[d]; }
-        std::vector<uint8_t> cnt(tot, 0);
+        for (int d = 0; d < nd; ++d) tot *= L->dom[d];
         bool overlap = false;
-        for (const Box& b : L->boxes)
-            for_each_cell(b, nd, [&](const int* c) { if (cnt[o.lin(c)]++) overlap = true; });
+        if (nd == 2) {                           // per row: sorted v intervals must not overlap
+            const Owner o = make_owner(L, L->boxes);
+            for (const auto& r : o.rows)
+                for (size_t k = 1; k < r.size(); ++k)
+                    if (r[k][0] <= r[k - 1][1]) overlap = true;
+        } else {
+            Owner o;
+            o.nd = nd;
+            for (int d = 0; d < nd; ++d) o.dom[d] = L->dom[d];
+            std::vector<uint8_t> cnt(tot, 0);
+            for (const Box& b : L->boxes)
+                for_each_cell(b, nd, [&](const int* c) { if (cnt[o.lin(c)]++) overlap = true; });
+        }
         if (overlap) { free_level(L); return vk::fail(VLASOV_ENEST, "boxes overlap"); }
         if (!coarser && total != tot) { free_level(L); return vk::fail(VLASOV_ENEST, "level 0 must tile the domain"); }
         if (coarser) {   // proper nesting: coarse parents of every fine cell on the coarser level
