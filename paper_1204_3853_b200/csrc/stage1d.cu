@@ -436,11 +436,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     // SELF: the edge threads stage f_next's boundary cells; its velocity ghost columns for this
     // stage's field E are written after the march, off the critical path
     const bool lo_edge = (GM == 1) && edge_lo, hi_edge = (GM == 1) && edge_hi;
-#ifdef STAGE1D_NOGHOSTOUT   // experiments only (carried ghosts then go stale)
-    constexpr bool GHOST_OUT = false;
-#else
     constexpr bool GHOST_OUT = SELF && STAGE >= 1;
-#endif
 
     double W[4][CPT + 2];                        // f_s rows (mod 4) at columns c0-1 .. c0+4
     double VF[4][CPT + 1];                       // 12 x v-faces (mod 4) at c0-1/2 .. c0+CPT-1/2

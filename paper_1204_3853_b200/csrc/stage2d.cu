@@ -39,12 +39,6 @@ namespace vk {
 constexpr int S2_LT = 4;                  // vx lines (consumer warps) per CTA
 constexpr int S2_TM = 64;                 // vy cells per tile (2 per lane)
 constexpr int S2_LW = S2_TM + 4;          // doubles per line segment in a slot
-#ifndef S2_MAXNREG
-#define S2_MAXNREG 200
-#endif
-#ifndef S2_MAXNREG_ON
-#define S2_MAXNREG_ON 0
-#endif
 #ifndef S2_NSLOT_CFG
 #define S2_NSLOT_CFG 4
 #endif
@@ -106,12 +100,7 @@ constexpr bool S2_PWG_ON = S2_PWG && S2_GWARP == 0;
 constexpr int S2_THREADS = S2_PWG_ON ? 32 * (S2_LT + 4) : 32 * (S2_LT + 1 + S2_GWARP);
 
 template <int STAGE, int RECON>
-#if S2_MAXNREG_ON
-__global__ void __maxnreg__(S2_MAXNREG) k_stage_2d2v(
-#else
-__global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(
-#endif
-    const StageArgs2 A, const __grid_constant__ TMaps2 M) {
+__global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(const StageArgs2 A, const __grid_constant__ TMaps2 M) {
     using SL = Slot2<STAGE>;
     constexpr int SIZE = SL::SIZE;
     extern __shared__ __align__(128) double smem[];
