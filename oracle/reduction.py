@@ -82,8 +82,12 @@ def subpatch_reduce(levels, data, dv0, nx0):
     return 1.0 - subpatch_moment(levels, data, dv0, nx0)
 
 
-def subpatch_moment(levels, data, dv0, nx0):
-    """Alg.8 velocity moment n = sum_l dv_l sum_v f (reading #13) on the finest configuration mesh."""
+def subpatch_moment(levels, data, dv0, nx0, first=False, vlo=0.0):
+    """Alg.8 velocity moment n = sum_l dv_l sum_v f (reading #13) on the finest configuration mesh.
+    first=True: the first moment sum_l dv_l sum_v <v f> instead (N4 current, reading #31): per
+    sub-patch column the fourth-order product rule sum_j vbar_j f_j + (dv/24)(f_{j1+1} + f_{j1} -
+    f_{j0} - f_{j0-1}) over its velocity range j0..j1 (the telescoped (dv/24)(f_{j+1} - f_{j-1})),
+    vbar_j the exact cell-average velocity of level cell j, vlo the domain's lower velocity."""
     rxf = _finest_rx(levels)
     total = np.zeros(nx0 * rxf)
     partials = []
@@ -98,7 +102,13 @@ def subpatch_moment(levels, data, dv0, nx0):
                 x0, x1 = s[0][0] - b[0][0], s[1][0] - b[0][0]     # patch-local interior x range
                 j0, j1 = s[0][1] - b[0][1], s[1][1] - b[0][1]
                 # grow by G in x, sum over the sub-patch v range including the ghost columns
-                tmp = np.sum(fg[G + x0 - G: G + x1 + G + 1, G + j0: G + j1 + 1], axis=1)
+                rows = fg[G + x0 - G: G + x1 + G + 1, :]
+                if first:
+                    vbar = vlo + (b[0][1] + np.arange(j0, j1 + 1) + 0.5) * dv
+                    tmp = rows[:, G + j0: G + j1 + 1] @ vbar + (dv / 24.0) * (
+                        rows[:, G + j1 + 1] + rows[:, G + j1] - rows[:, G + j0] - rows[:, G + j0 - 1])
+                else:
+                    tmp = np.sum(rows[:, G + j0: G + j1 + 1], axis=1)
                 fine = _refine_x_rows(tmp[:, None], R)[:, 0]      # refine the 1D partial sums
                 pp[x0 * R: (x1 + 1) * R] += dv * fine             # into the partial patch
             partials.append((b[0][0] * R, pp))

@@ -131,8 +131,13 @@ def vlasov_reduce_moment(levels, f_list, rho_finest):
     return check(lib.vlasov_reduce_moment(arr, len(levels), fp, _ptr(rho_finest)))
 
 
-def vlasov_reduce_current(h, f, q, accumulate, j):
-    return check(lib.vlasov_reduce_current(h, _ptr(f), float(q), int(bool(accumulate)), _ptr(j)))
+def vlasov_reduce_current(levels, f_list, q, accumulate, j):
+    """levels / f_list: one level handle and its field, or the hierarchy's lists (coarse first)."""
+    if not isinstance(levels, (list, tuple)):
+        levels, f_list = [levels], [f_list]
+    arr = (C.c_void_p * len(levels))(*[l.value if isinstance(l, C.c_void_p) else l for l in levels])
+    fp = (C.c_void_p * len(levels))(*[t.data_ptr() for t in f_list])
+    return check(lib.vlasov_reduce_current(arr, len(levels), fp, float(q), int(bool(accumulate)), _ptr(j)))
 
 
 def vlasov_level_set_moment_base(h, base):

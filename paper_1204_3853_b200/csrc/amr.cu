@@ -59,6 +59,45 @@ __global__ void k_red_finest(const double* __restrict__ colsum, const RedContrib
     if (lane == 0) rho[x] = (accumulate ? rho[x] : base) + q * acc;
 }
 
+// first moment of each grown sub-patch column (N4 current, reading #31): sum_j vbar_j f_j +
+// (dv/24)(f_{nv} + f_{nv-1} - f_0 - f_{-1}); one warp per column, fixed butterfly
+struct LevelV {
+    double vlo[MAXLEV], dv[MAXLEV];
+};
+__global__ void k_red_cols_first(const LevelPtrs P, const LevelV V, const RedCol* __restrict__ cols, int64_t ncols,
+                                 double* __restrict__ colsum) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (c >= ncols) return;
+    const RedCol C = cols[c];
+    const double* p = P.f[C.level] + C.addr;
+    const double vlo = V.vlo[C.level], dv = V.dv[C.level];
+    double s = 0.0;
+    for (int j = lane; j < C.nv; j += 32) s += (vlo + ((double)(C.j0 + j) + 0.5) * dv) * p[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) colsum[c] = s + (dv * (1.0 / 24.0)) * ((p[C.nv] + p[C.nv - 1]) - (p[0] + p[-1]));
+}
+
+int launch_reduce_first_subpatch(const RedPlan* P, const double* const* f, int nlev, const double* vlo,
+                                 const double* dv, double* j, cudaStream_t st, double q, int accumulate) {
+    LevelPtrs lp;
+    LevelV lv;
+    for (int l = 0; l < MAXLEV; ++l) {
+        lp.f[l] = l < nlev ? f[l] : nullptr;
+        lv.vlo[l] = l < nlev ? vlo[l] : 0.0;
+        lv.dv[l] = l < nlev ? dv[l] : 0.0;
+    }
+    if (P->ncols > 0)
+        VK_CUDA(launch_pdl(k_red_cols_first, dim3((unsigned)((P->ncols + 7) / 8)), dim3(256), 0, st, lp, lv,
+                           (const RedCol*)P->d_cols, (int64_t)P->ncols, P->d_colsum));
+    VK_CUDA(launch_pdl(k_red_finest, dim3((P->nxf + 3) / 4), dim3(128), 0, st, (const double*)P->d_colsum,
+                       (const RedContrib*)P->d_contrib, (const int32_t*)P->d_xoff, P->nxf, q, 0.0, accumulate, j));
+    return VLASOV_OK;
+}
+
 int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st,
                            double q, double base, int accumulate) {
     LevelPtrs lp;

@@ -96,6 +96,7 @@ struct RedCol {               // one grown x-column of one Alg.8 sub-patch
     int64_t addr;             // index of the column's first velocity cell in its level array
     int32_t nv;               // velocity cells summed (the sub-patch's v extent)
     int32_t level;            // index of the level in the hierarchy
+    int32_t j0;               // level velocity index of the column's first cell (first moment)
 };
 struct RedContrib {           // one refined partial sum landing on one finest x cell
     int64_t cs;               // index of the first of the 5 stencil column sums (columns c-2..c+2)
@@ -249,6 +250,8 @@ int linear5_weights(int R, double* out /* R*5 */);
 int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st);
 int launch_vslab(const vlasov_level* L, double* f, double* lo, double* hi, bool pack);
 int launch_current(const vlasov_level* L, const double* f, double q, int accumulate, double* j);
+int launch_reduce_first_subpatch(const RedPlan* P, const double* const* f, int nlev, const double* vlo,
+                                 const double* dv, double* j, cudaStream_t st, double q, int accumulate);
 int launch_reduce_subpatch(const RedPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st,
                            double q = -1.0, double base = 1.0, int accumulate = 0);
 int launch_flux_registers(const vlasov_level* L, const double* f_fine, const double* E_fine, const double* f_coarse,

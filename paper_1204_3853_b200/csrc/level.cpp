@@ -660,6 +660,7 @@ int build_red_plan(const vlasov_level* const* levels, int nlev, vk::RedPlan** ou
                     rc.addr = cell_addr(L, blk, cc);
                     rc.nv = vk::box_ncells_dim(sp, 1);
                     rc.level = l;
+                    rc.j0 = sp.lo[1];
                     cols.push_back(rc);
                 }
                 for (int xc = sp.lo[0]; xc <= sp.hi[0]; ++xc)
@@ -1312,12 +1313,29 @@ int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const 
     return vlasov_reduce_charge(levels, nlev, f, -1.0, 1.0, 0, rho_finest);
 }
 
-int vlasov_reduce_current(const vlasov_level* L, const double* f, double q, int32_t accumulate, double* j) {
-    if (!L || !f || !j) return vk::fail(VLASOV_EINVAL, "null argument");
-    if (L->ndim != 2 || !L->single_block)
-        return vk::fail(VLASOV_EUNSUPPORTED, "current moment: one uniform 1D+1V block");
+int vlasov_reduce_current(const vlasov_level* const* levels, int32_t nlev, const double* const* f, double q,
+                          int32_t accumulate, double* j) {
+    if (!levels || nlev < 1 || !f || !j) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (nlev > vk::MAXLEV) return vk::fail(VLASOV_EUNSUPPORTED, "more than 8 levels");
+    for (int l = 0; l < nlev; ++l) {
+        if (!levels[l] || !f[l]) return vk::fail(VLASOV_EINVAL, "reduce_current: level / field pointer required");
+        if (levels[l]->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "current moment: 1D+1V levels");
+    }
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
-    return vk::launch_current(L, f, q, accumulate, j);
+    if (nlev == 1 && levels[0]->single_block) return vk::launch_current(levels[0], f[0], q, accumulate, j);
+    const vlasov_level* Lf = levels[nlev - 1];
+    bool fresh = Lf->red_plan != nullptr && (int)Lf->red_plan->uids.size() == nlev;
+    for (int l = 0; fresh && l < nlev; ++l) fresh = Lf->red_plan->uids[l] == levels[l]->uid;
+    if (!fresh) {
+        vk::free_red_plan(Lf->red_plan);
+        Lf->red_plan = nullptr;
+        vk::RedPlan* P = nullptr;
+        if (int rc = build_red_plan(levels, nlev, &P)) return rc;
+        Lf->red_plan = P;
+    }
+    double vlo[vk::MAXLEV], dv[vk::MAXLEV];
+    for (int l = 0; l < nlev; ++l) { vlo[l] = levels[l]->lower[1]; dv[l] = levels[l]->h[1]; }
+    return vk::launch_reduce_first_subpatch(Lf->red_plan, f, nlev, vlo, dv, j, Lf->stream, q, accumulate);
 }
 
 int vlasov_level_set_moment_base(vlasov_level* L, double base) {

@@ -103,6 +103,37 @@ def test_subpatch_reduction_parity(seed):
     np.testing.assert_allclose(rho, ref_mask, rtol=0, atol=1e-12 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_subpatch_current_parity(seed):
+    """N4 current moment on random hierarchies (vlasov_reduce_current, Alg.8 with the first moment
+    per sub-patch column, reading #31) against the oracle's subpatch_moment(first=True); two
+    species accumulated (q = -1, then 0.25 on the same data)."""
+    rat, lb = random_hierarchy(seed)
+    H = drv.hierarchy(W, lb, rat)
+    data = _ic_data(H, noise_seed=seed)
+    rng = np.random.default_rng(200 + seed)
+    E_bc = [0.3 * rng.uniform(-1, 1, W.ncells[0] * r[0]) for r in rat]
+    G = _gpu(rat, lb)
+    j = torch.zeros(G.rho.numel(), dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(G.stream):
+        for L, b, lvl in zip(G.levels, G.bufs, data):
+            L.set_patches(b["A"], [a[2:-2, 2:-2] for a in lvl])
+        Eg = [torch.as_tensor(np.pad(e, 2, mode="wrap")).cuda() for e in E_bc]
+        G._fill([b["A"] for b in G.bufs], Eg)
+        api.vlasov_reduce_current(G.handles, [b["A"] for b in G.bufs], -1.0, 0, j)
+        api.vlasov_reduce_current(G.handles, [b["A"] for b in G.bufs], 0.25, 1, j)
+    ghosted = G.get_state(ghost=2)
+    got = j.cpu().numpy()
+    m1 = reduction.subpatch_moment(H.levels, ghosted, H.h0[1], H.ncells0[0], first=True, vlo=W.lower[1])
+    ref = -0.75 * m1
+    assert np.max(np.abs(ref)) > 1e-8
+    # cancelling sum (v of both signs): bound by the magnitude moment
+    mag = [[np.abs(a) for a in lvl] for lvl in ghosted]
+    scale = 0.75 * np.abs(reduction.subpatch_moment(H.levels, mag, H.h0[1], H.ncells0[0], first=False)) * \
+        max(abs(W.lower[1]), abs(W.lower[1] + W.ncells[1] * H.h0[1]))
+    np.testing.assert_array_less(np.abs(got - ref), 1e-13 * scale.max() + 1e-300)
+
+
 @pytest.mark.parametrize("seed", range(10))
 def test_mask_reduction_parity(seed):
     """Alg.6 Mask Reduction on the GPU (the paper's comparator) against the oracle's

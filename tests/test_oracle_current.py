@@ -55,3 +55,27 @@ def test_shifted_maxwellian_closed_form():
         m = (special.erf((edges[1:] - u) / math.sqrt(2)) - special.erf((edges[:-1] - u) / math.sqrt(2))) / 2 / dv
         j = field.current_density(_ghosted(1, n * m), -10.0, dv, q=-1.0)
         assert abs(j[0] - (-n * u)) < 1e-13
+
+
+def test_hierarchy_first_moment_single_level_equals_uniform():
+    """Alg.8 first moment (reading #31) on a level split into patches along v and x: the product
+    rule's boundary terms telescope across patch faces, so it equals current_density of the whole
+    ghosted level (up to rounding)."""
+    import inputs
+    from oracle import amr, boxes, interp, reduction, scheme
+    w = inputs.scaled(inputs.get("C3"), (16, 32), (8, 8))
+    lb = [[boxes.box(*b) for b in inputs.level0_boxes(w)]]
+    H = amr.Hierarchy(w.lower, inputs.spacing(w), w.ncells, lb, [(1, 1)],
+                      lambda r: inputs.background_profile(w, r), scheme.CENTERED4, interp.LINEAR5)
+    f = inputs.initial_cell_averages(w) * (1.0 + 0.1 * inputs.random_field(w.ncells, 3))
+    data = H.new_data()
+    for p, b in enumerate(H.levels[0].boxes):
+        data[0][p][2:-2, 2:-2] = f[b[0][0]:b[1][0] + 1, b[0][1]:b[1][1] + 1]
+    amr.fill_ghosts(H, data, [np.full(w.ncells[0], 0.05)])
+    got = reduction.subpatch_moment(H.levels, data, H.h0[1], w.ncells[0], first=True, vlo=w.lower[1])
+    # the whole level, ghosted, assembled from the patches' filled frames
+    fg = np.zeros((w.ncells[0] + 4, w.ncells[1] + 4))
+    for p, b in enumerate(H.levels[0].boxes):
+        fg[b[0][0]:b[1][0] + 5, b[0][1]:b[1][1] + 5] = data[0][p]
+    want = -field.current_density(fg, w.lower[1], H.h0[1], q=-1.0)
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-13 * np.abs(want).max())
