@@ -75,7 +75,13 @@ def test_compute_entry_points_validate_then_need_a_device():
     P = C.c_void_p()
     assert lib.vlasov_poisson_create(4, 0.1, None, C.byref(P)) == _lib.EINVAL        # n >= 5
     assert lib.vlasov_poisson_create(16, -1.0, None, C.byref(P)) == _lib.EINVAL
+    Ls = (C.c_void_p * 1)(L)
+    fs = (C.c_void_p * 1)(C.cast(buf, C.c_void_p))
+    assert lib.vlasov_reduce_current(Ls, 0, fs, -1.0, 0, buf) == _lib.EINVAL       # nlev >= 1
+    assert lib.vlasov_reduce_current(Ls, 1, fs, -1.0, 0, None) == _lib.EINVAL     # j required
+    assert lib.vlasov_reduce_current(Ls, 1, (C.c_void_p * 1)(None), -1.0, 0, buf) == _lib.EINVAL
     if not api.vlasov_device_ok():
+        assert lib.vlasov_reduce_current(Ls, 1, fs, -1.0, 0, buf) == _lib.ECUDA
         assert lib.vlasov_rk4_stage(L, 1, 0.1, buf, buf, buf, buf, buf, None, None, 0, None) == _lib.ECUDA
         assert lib.vlasov_fill_ghosts(L, buf, None, None, buf, buf, 0) == _lib.ECUDA
         assert lib.vlasov_inject_field(L, buf, (C.c_int32 * 2)(16, 1), buf) == _lib.ECUDA
