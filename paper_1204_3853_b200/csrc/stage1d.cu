@@ -20,6 +20,7 @@
 // (atomic ticket) adds the v-tiles in tile order -> rho = 1 - dv sum (deterministic).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.h"
@@ -68,6 +69,7 @@ struct StageArgs1 {
     const double* gX;          // gX[m] = g[(m - GX_PAD) mod n], m in [0, 2n + GX_PAD + GX_TAIL)
     int nstrip1;               // > 0: single block, tiles computed from blockIdx (no table load)
     Block1 blk0;               // that block
+    int xshift;                // single block: strips start xshift rows later (periodic wrap; L2 reuse)
 };
 
 // the fused prologue stages the whole (periodically extended) Green's function in shared memory
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         T.block = 0;
         T.x0 = (int)((int64_t)B.nx * st / A.nstrip1);
         T.nrows = (int)((int64_t)B.nx * (st + 1) / A.nstrip1) - T.x0;
+        T.x0 += A.xshift;                        // rows x0 .. x0+nrows-1 taken mod nx (wr below)
         T.j0 = vt * TV;
         T.ncols = min(TV, B.nv - T.j0);
         T.pvt = vt;
@@ -226,6 +229,9 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
 
     // row r (block-local interior index, may be -2..nx+1): interior column 0 of that row
     auto rowbase = [&](int r) -> int64_t { return B.off + (int64_t)(r + G) * B.pitch + G; };
+    // single block: a shifted strip may run past the last row; its rows wrap periodically
+    const int wrapn = A.nstrip1 > 0 ? B.nx : 0x40000000;
+    auto wr = [&](int r) -> int { return r >= wrapn ? r - wrapn : r; };
 
     // fused field: rho and the Green's function (twice: periodic extension) staged by the TMA engine
     double* s_edge = sEbc + (A.tile_rows + 4);   // [tile_rows][2 sides][CPT] boundary cells of f_next
@@ -237,6 +243,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         const int r = T.x0 - 2 + q;
         int rs = r;
         if (SELF) rs = (r < 0) ? r + B.nx : (r >= B.nx ? r - B.nx : r);
+        else rs = wr(r);
         const bool out_row = (q >= 4);
         uint32_t bytes = seg_bytes;
         if (NEED_FN && out_row) bytes += row_bytes;
@@ -244,8 +251,8 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         double* dst = smem + sl * SLOT;
         mbar_arrive_expect_tx(&full_bar[sl], bytes);
         bulk_g2s(dst, A.f_s + rowbase(rs) + T.j0 - 2, seg_bytes, &full_bar[sl]);
-        if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(r - 2) + T.j0, row_bytes, &full_bar[sl]);
-        if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(r - 2) + T.j0, row_bytes, &full_bar[sl]);
+        if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl]);
+        if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl]);
     };
     // fused field: this CTA computes rows [tb, te) of the tile's Q rows of E (the strip's v-tiles
     // of a cluster split them); row tb + t is x = gxu0 + t (unwrapped, gxu0 in [0, n)); they read
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     if (!PWARPS && tid == 0) issue_field_const();
     griddep_wait();                              // E, E_bc, f_s, f_n, u, rho of the previous stages
     for (int t = tid; t < Q; t += NT) {
-        const int gi = B.lo_x + T.x0 - 2 + t + G;  // index in the ghosted level E array
+        const int gi = B.lo_x + wr(T.x0 - 2 + t) + G;  // index in the ghosted level E array
         if (!field) sE[t] = __ldg(A.E + gi);
         if (SELF && A.E_bc) sEbc[t] = __ldg(A.E_bc + gi);
     }
@@ -396,7 +403,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                     s_part[t] = e;
                 }
                 if (t >= 2 && t < Q - 2) {       // owned rows + periodic ghosts
-                    const int x = B.lo_x + T.x0 - 2 + t;
+                    const int x = B.lo_x + wr(T.x0 - 2 + t);
                     A.E_out[x + G] = e;
                     if (x < G) A.E_out[x + G + n] = e;
                     if (x >= n - G) A.E_out[x + G - n] = e;
@@ -537,8 +544,9 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
             }
             if (NEED_FN) fnuu ^= __double2hiint(fn[0]) ^ __double2hiint(fn[2]);
             if (NEED_U) fnuu ^= __double2hiint(uu[0]) ^ __double2hiint(uu[2]);
-            double* op = A.f_next + rowbase(i) + c0;
-            double* up = A.u_out + rowbase(i) + c0;
+            const int64_t ib = rowbase(wr(i));
+            double* op = A.f_next + ib + c0;
+            double* up = A.u_out + ib + c0;
             if (SELF || nact == CPT) {
                 if (live && act) {
 #pragma unroll
@@ -663,12 +671,12 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                 g = a < 0.0 ? make_double2(10.0 * se[0] - 20.0 * se[1] + 15.0 * se[2] - 4.0 * se[3],
                                            4.0 * se[0] - 6.0 * se[1] + 4.0 * se[2] - se[3])
                             : make_double2(s_f0[0], s_f0[1]);
-                *reinterpret_cast<double2*>(A.f_next + rowbase(i) - 2) = g;
+                *reinterpret_cast<double2*>(A.f_next + rowbase(wr(i)) - 2) = g;
             } else {
                 g = a > 0.0 ? make_double2(4.0 * se[3] - 6.0 * se[2] + 4.0 * se[1] - se[0],
                                            10.0 * se[3] - 20.0 * se[2] + 15.0 * se[1] - 4.0 * se[0])
                             : make_double2(s_f0[2], s_f0[3]);
-                *reinterpret_cast<double2*>(A.f_next + rowbase(i) + B.nv) = g;
+                *reinterpret_cast<double2*>(A.f_next + rowbase(wr(i)) + B.nv) = g;
             }
         }
     }
@@ -678,7 +686,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
             double s = psum[rr];
 #pragma unroll
             for (int w = 1; w < NW; ++w) s += psum[w * A.tile_rows + rr];
-            A.partials[(int64_t)T.pvt * A.dom_x + B.lo_x + T.x0 + rr] = s;
+            A.partials[(int64_t)T.pvt * A.dom_x + B.lo_x + wr(T.x0 + rr)] = s;
         }
         // last CTA of this row strip finalises rho in v-tile order (deterministic)
         __threadfence();
@@ -688,7 +696,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         if (s_ticket == (unsigned)(A.n_vtiles - 1)) {
             __threadfence();
             for (int rr = tid; rr < T.nrows; rr += NT) {
-                const int x = B.lo_x + T.x0 + rr;
+                const int x = B.lo_x + wr(T.x0 + rr);
                 double s = 0.0;
                 for (int t = 0; t < A.n_vtiles; ++t) s += __ldcg(A.partials + (int64_t)t * A.dom_x + x);
                 A.rho[x] = A.rho_base - A.dv * s;
@@ -801,6 +809,12 @@ int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n) {
              StageGeom<4, NT_NARROW>::smem_bytes(tile_rows) + field_smem_bytes(n));
 }
 
+// strip shift of the even stages in quarters of a strip (VLASOV_XSHIFT, experiments; default 2)
+static int shift_quarters() {
+    static const int q = [] { const char* e = getenv("VLASOV_XSHIFT"); return e ? atoi(e) : 2; }();
+    return q;
+}
+
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
                       double* rho, const double* rho_in, const double* gE, double* E_out, const double* gX) {
@@ -812,6 +826,9 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.g_smem = (rho_in && g_in_smem(L->dom[0])) ? 1 : 0;
     A.gX = gX;
     A.nstrip1 = L->single_block ? L->n_strips : 0;
+    // L2 reuse between stages: even stages start their strips half a strip later, so each CTA
+    // first reads the rows the previous stage wrote last (still in L2)
+    A.xshift = (A.nstrip1 > 0 && (stage % 2) == 0) ? L->dom[0] / A.nstrip1 * shift_quarters() / 4 : 0;
     if (!L->h_blocks1.empty()) A.blk0 = L->h_blocks1[0];
     A.f_s = f_s;
     A.f_n = f_n;
