@@ -278,3 +278,38 @@ def test_stage_kernels_deterministic_and_self_equals_stored(shape):
         for k in range(3):
             np.testing.assert_array_equal(outs[0][k], outs[1][k])
             np.testing.assert_allclose(outs[0][k], outs[2][k], rtol=0, atol=1e-14 * np.abs(outs[2][k]).max())
+
+
+_SHIFT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import inputs
+from paper_1204_3853_b200 import api
+from paper_1204_3853_b200.solver import UniformVlasov1D
+w = inputs.scaled(inputs.get("C4"), (512, 4096), (64, 64))
+h = inputs.spacing(w)
+S = UniformVlasov1D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w))
+S.set_state(inputs.initial_cell_averages(w))
+for _ in range(3):
+    S.step(inputs.fixed_dt(w))
+torch.cuda.synchronize()
+np.save({out!r}, np.concatenate([S.get_state().ravel(), S.rhos[0].cpu().numpy()]))
+"""
+
+
+def test_strip_shift_changes_no_result(tmp_path):
+    """The even stages' strip shift (L2 reuse, DESIGN 6.1) is a reordering of independent row
+    work: three fused RK4 steps with and without it (VLASOV_XSHIFT) are bitwise equal."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for q in ("0", "2", "1"):
+        out = str(tmp_path / f"s{q}.npy")
+        code = _SHIFT_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), out=out)
+        env = dict(os.environ, VLASOV_XSHIFT=q)
+        subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+        res[q] = np.load(out)
+    assert np.array_equal(res["0"], res["2"])
+    assert np.array_equal(res["0"], res["1"])
