@@ -194,9 +194,7 @@ def run_amr(args, w, rank, world, local):
 
     import inputs
     from paper_1204_3853_b200.amr_solver import AmrVlasov1D
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)          # (the process group, if any, is initialised by main)
     a = w.amr
     dt = inputs.fixed_dt(w, a["ratio"])
     G = AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), [inputs.level0_boxes(w)], [(1, 1)],

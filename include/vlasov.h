@@ -150,9 +150,13 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
  * rows are never read), and the velocity ghosts of f_s follow the characteristic v-boundary
  * condition (reading #6) either derived in-kernel from E_bc (E_bc non-NULL, exactly as
  * vlasov_fill_ghosts(E_bc, f0v) would) or, with E_bc == NULL ("carried ghosts"), read from f_s's
- * velocity ghost columns.  With f0v non-NULL the stage also writes f_next's velocity ghost columns
+ * velocity ghost columns.  Stage 1 always derives them in-kernel from its own field E, which is
+ * E(f_n), the end-of-step constraint evaluation of Alg.5 (reading #6b); E_bc is
+ * ignored at stage 1.  With f0v non-NULL the stage also writes f_next's velocity ghost columns
  * (interior rows) for the field E of this stage -- the E_bc of the next stage (reading #6b) -- so a
- * chain of stages with E_bc == NULL needs one vlasov_fill_ghosts of the initial state only.
+ * chain of stages with E_bc == NULL needs no ghost fill at all.  Only the velocity faces the
+ * level marks physical (vlasov_level_set_velocity_faces; default both) get the boundary
+ * condition in-kernel; a non-physical face keeps the ghost columns stored in f_s.
  * With f0v == NULL (E_bc must be NULL too) the ghost frame of f_s must have been filled by
  * vlasov_fill_ghosts.
  * rho_next (nullable; single block covering the domain only): receives the velocity moment of
@@ -306,6 +310,11 @@ int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream);
  * vlasov_vslab_unpack: the inverse into the velocity ghost columns: f(x, -2 + c) = lo[2x + c],
  *   f(x, nv + c) = hi[2x + c] (NULL leaves that side -- a physical boundary -- untouched).      */
 int vlasov_level_set_moment_base(vlasov_level* level, double base);
+/* vlasov_level_set_velocity_faces: which velocity faces of a one-block periodic level are physical
+ * boundaries (1) -- the stage kernels apply the characteristic condition there -- and which are
+ * interior slab faces (0) whose ghost columns the caller provides (vlasov_vslab_unpack).  Default
+ * (1, 1).                                                                                         */
+int vlasov_level_set_velocity_faces(vlasov_level* level, int32_t phys_lo, int32_t phys_hi);
 int vlasov_vslab_pack(const vlasov_level* level, const double* f, double* lo, double* hi);
 int vlasov_vslab_unpack(const vlasov_level* level, double* f, const double* lo, const double* hi);
 

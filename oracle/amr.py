@@ -193,10 +193,19 @@ def average_down(H, data):
                     mean[ov[0][0] - cbox[0][0]: ov[1][0] - cbox[0][0] + 1, ov[0][1] - cbox[0][1]: ov[1][1] - cbox[0][1] + 1]
 
 
+def end_of_step_constraints(H, data, E_bc):
+    """Alg.5's ComputeInstantaneousConstraints(f_new) after ComputeUpdate: ghosts of
+    f_new (with the latest field E_bc for the boundary condition, reading #6b), then the
+    constraints.  Its E is the boundary-condition field of the next step's stage 1."""
+    fill_ghosts(H, data, E_bc)
+    E_new, _ = constraints(H, data)
+    return E_new
+
+
 def step(H, data, E_bc, dt):
     """One synchronous RK4 step (Alg.5, one hierarchy).  ``data`` holds f_old (interiors);
-    E_bc: per-level E of the previous constraint evaluation (reading #6b).
-    Returns (new data, E_bc for the next step, flux ledger of the last F*)."""
+    E_bc: per-level E of the previous constraint evaluation, E(f_old) (reading #6b).
+    Returns (new data, E(f_new) = the end-of-step constraint evaluation, flux ledger of F*)."""
     L = len(H.levels)
     f_old = [[_interior(a).copy() for a in lvl] for lvl in data]
     k = [[np.zeros_like(a) for a in lvl] for lvl in f_old]
@@ -221,7 +230,7 @@ def step(H, data, E_bc, dt):
         for p in range(len(H.levels[l].boxes)):
             _interior(new[l][p])[...] = f_old[l][p] + dt * scheme.divergence(F_acc[l][p], H.h(l))
     average_down(H, new)
-    return new, E_bc, F_acc
+    return new, end_of_step_constraints(H, new, E_bc), F_acc
 
 
 # --------------------------------------------------------------------------- tags / regrid

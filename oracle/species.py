@@ -62,7 +62,9 @@ def start(species, datas, rho_bg):
 def step(species, datas, A_bc, dt, rho_bg):
     """One synchronous RK4 step of all species (Alg.5 with several hierarchies, Alg.1-4 per
     hierarchy).  A_bc[s]: per-level effective field of species s from the previous constraint
-    evaluation (reading #6b).  Returns (new datas, A_bc for the next step)."""
+    evaluation (reading #6b).  Returns (new datas, A_bc for the next step = the end-of-step
+    constraint evaluation of Alg.5: ghosts of f_new with the stage-4 field, then
+    the joint constraints)."""
     RK_ALPHA, RK_B = amr.RK_ALPHA, amr.RK_B
     f_old = [[[amr._interior(a).copy() for a in lvl] for lvl in data] for data in datas]
     k = [[[np.zeros_like(a) for a in lvl] for lvl in fo] for fo in f_old]
@@ -95,4 +97,7 @@ def step(species, datas, A_bc, dt, rho_bg):
                 amr._interior(new[l][p])[...] = f_old[i][l][p] + dt * scheme.divergence(F_acc[i][l][p], H.h(l))
         amr.average_down(H, new)
         news.append(new)
-    return news, A_bc
+    for i, sp in enumerate(species):                                       # Alg.5: constraints(f_new)
+        amr.fill_ghosts(sp.H, news[i], A_bc[i])
+    A_new, _ = constraints(species, news, rho_bg)
+    return news, A_new

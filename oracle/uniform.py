@@ -12,11 +12,12 @@
                      E = constraints(f_pred); E_bc = E     (Alg.5)
                      k, F = RHS(f_pred, E); F* += b_s F    (Alg.3)
       f_new = f_old + dt * div(F*)                         (Alg.4)
-  Reading #6b: Alg.5 evaluates the predictor state (with its boundary condition) BEFORE the
-  constraints, so the boundary condition of a predictor state uses the E of the previous
-  constraint evaluation (stage s-1; stage 4 of the previous step for s = 1; E = 0 before the
-  very first evaluation).  The end-of-step ComputeInstantaneousConstraints(f_new) of Alg.5 is
-  the stage-1 evaluation of the next step (same state, evaluated once).
+  Reading #6b: Alg.5 evaluates the predictor state (with its boundary condition)
+  BEFORE the constraints, so the boundary condition of a predictor state uses the E of the
+  previous constraint evaluation: stage s >= 2 the E of stage s-1; stage 1 the E of the
+  end-of-step ComputeInstantaneousConstraints(f_new) of the previous step, i.e. E(f_n) (at
+  n = 0 the initial evaluation E(f_0)).  On one periodic level the moment does not read ghost
+  cells, so E(f_n) is also the stage-1 field: stage 1 uses E_bc = E.
 """
 from __future__ import annotations
 
@@ -136,7 +137,8 @@ class UniformProblem:
 
     def step(self, f_old, E_bc, dt):
         """One RK4 step (Alg.5 with one hierarchy / one level).  ``E_bc`` is the E of the
-        previous constraint evaluation (reading #6b).  Returns (f_new, E_bc_next, F_acc)."""
+        previous constraint evaluation, E(f_old) (reading #6b).  Returns (f_new, E(f_new), F_acc):
+        the step ends with Alg.5's ComputeInstantaneousConstraints(f_new)."""
         k = np.zeros_like(f_old)
         F_acc = None
         for s in range(4):
@@ -147,7 +149,7 @@ class UniformProblem:
                 [Fa + RK_B[s] * Fd for Fa, Fd in zip(F_acc, F)]
             E_bc = E
         f_new = f_old + dt * scheme.divergence(F_acc, self.h)         # Alg.4
-        return f_new, E_bc, F_acc
+        return f_new, self.constraints(f_new), F_acc                   # Alg.5: constraints(f_new)
 
     def run(self, f0, dt, nsteps, callback=None):
         """Advance nsteps; callback(n, f_n, E(f_n)) after each step (E = stage-1 field)."""

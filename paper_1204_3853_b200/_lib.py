@@ -69,6 +69,7 @@ _SIGS = {
     "vlasov_inject_field_scaled": (I32, [P, P, PI32, D, P]),
     "vlasov_absmax": (I32, [P, I64, P, P]),
     "vlasov_level_set_moment_base": (I32, [P, D]),
+    "vlasov_level_set_velocity_faces": (I32, [P, I32, I32]),
     "vlasov_reduce_current": (I32, [P, I32, P, D, I32, P]),
     "vlasov_vslab_pack": (I32, [P, P, P, P]),
     "vlasov_vslab_unpack": (I32, [P, P, P, P]),

@@ -16,6 +16,8 @@ One RK4 step = Alg.5 with one hierarchy, Alg.1-4 over the levels (P:
                                                     coarse-fine interface (Alg.3 F_accum)
     vlasov_average_down level L-1 .. 1              Alg.4: refluxing (flux substitution) and
                                                     coarse := mean of fine
+    vlasov_fill_ghosts + constraints of f_new       Alg.5's ComputeInstantaneousConstraints(f_new)
+                                                    (P:676-684): the E_bc of the next stage 1
 
 Regrid (C3 rule, reading #18): tags on level 0, dilation, fixed fine tiles,
 vlasov_level_fill_from (copy old fine where it overlaps, else interpolate from level 0), then a
@@ -157,6 +159,7 @@ class AmrVlasov1D:
             self._stage(s, dt)
         for l in range(len(self.levels) - 1, 0, -1):
             api.vlasov_average_down(self.levels[l].h, self.bufs[l]["A"], self.bufs[l - 1]["A"], self.regs[l], dt)
+        self._initial_constraints()          # Alg.5: constraints(f_new), reading #6b
 
     def step_graph(self, dt: float):
         """One step through a CUDA graph of the step's launches (captured on first use for the
@@ -196,8 +199,9 @@ class AmrVlasov1D:
     def launches_per_step(self) -> int:
         nl = len(self.levels)
         # per stage: fill (copy/CF + phys) per level, reduction (2), Poisson (1), inject per level,
-        # stage kernel per level, flux registers per fine level; then refluxing + average-down
-        return 4 * (2 * nl + 2 + 1 + nl + nl + (nl - 1)) + 2 * (nl - 1)
+        # stage kernel per level, flux registers per fine level; then refluxing + average-down and
+        # the end-of-step constraint evaluation (fill, reduction, Poisson, inject)
+        return 4 * (2 * nl + 2 + 1 + nl + nl + (nl - 1)) + 2 * (nl - 1) + (2 * nl + 2 + 1 + nl)
 
     # ------------------------------------------------------------------ regrid (C3 rule)
     def tags_level0(self, tol, buffer):
@@ -386,6 +390,11 @@ class MultiSpeciesVlasov1D:
             for h in self.sp:
                 for l in range(len(h.levels) - 1, 0, -1):
                     api.vlasov_average_down(h.levels[l].h, h.bufs[l]["A"], h.bufs[l - 1]["A"], h.regs[l], dt)
+            # Alg.5: the joint constraints of f_new (the next stage 1's boundary field, reading #6b)
+            A = [[b["A"] for b in h.bufs] for h in self.sp]
+            for h, fs in zip(self.sp, A):
+                h._fill(fs, [E[h.cur] for E in h.E])
+            self._constraints(A, [[E[h.cur] for E in h.E] for h in self.sp])
 
     def get_state(self):
         return [h.get_state() for h in self.sp]

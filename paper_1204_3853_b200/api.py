@@ -20,7 +20,7 @@ __all__ = [
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
     "vlasov_level_fill_from", "vlasov_absmax", "vlasov_device_ok", "vlasov_last_error",
-    "vlasov_level_set_moment_base", "vlasov_vslab_pack", "vlasov_vslab_unpack", "vlasov_reduce_current",
+    "vlasov_level_set_moment_base", "vlasov_level_set_velocity_faces", "vlasov_vslab_pack", "vlasov_vslab_unpack", "vlasov_reduce_current",
 ]
 
 
@@ -142,6 +142,10 @@ def vlasov_reduce_current(levels, f_list, q, accumulate, j):
 
 def vlasov_level_set_moment_base(h, base):
     return check(lib.vlasov_level_set_moment_base(h, float(base)))
+
+
+def vlasov_level_set_velocity_faces(h, phys_lo, phys_hi):
+    return check(lib.vlasov_level_set_velocity_faces(h, int(bool(phys_lo)), int(bool(phys_hi))))
 
 
 def vlasov_vslab_pack(h, f, lo=None, hi=None):

@@ -22,8 +22,21 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
+STAMP = OUT + ".flags"      # the flag set the .so was built with (an experiment build is never reused)
+
+
+def _flag_stamp():
+    return " ".join(FLAGS + EXTRA)
+
+
 def needs_build():
     if not os.path.exists(OUT):
+        return True
+    try:
+        with open(STAMP) as fh:
+            if fh.read() != _flag_stamp():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(OUT)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
@@ -59,6 +72,8 @@ def build(force=False, verbose=False):
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
                            "-lcudart"])
     os.replace(tmp, OUT)
+    with open(STAMP, "w") as fh:
+        fh.write(_flag_stamp())
     return OUT
 
 

@@ -165,6 +165,7 @@ int launch_reduce_mask(const MaskPlan* P, const double* const* f, int nlev, doub
 struct vlasov_level {
     int ndim = 2, ncfg = 1;
     double moment_base = 1.0;             // fused stage moment: rho = moment_base - dv sum_v f
+    int vphys[2] = {1, 1};                // velocity faces that are physical boundaries (lo, hi)
     double lower[4] = {0, 0, 0, 0}, h[4] = {0, 0, 0, 0};
     int ratio[4] = {1, 1, 1, 1};
     int dom[4] = {0, 0, 0, 0};            // level domain cells per dim

@@ -1248,6 +1248,8 @@ int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, con
     if (recon != VLASOV_CENTERED4 && recon != VLASOV_UPWIND) return vk::fail(VLASOV_EINVAL, "bad recon");
     if (rho_next && !L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "fused moment needs a single-block level");
     if (E_bc && !f0v) return vk::fail(VLASOV_EINVAL, "E_bc needs f0v");
+    // neighbouring CTAs read halo rows of f_s while others write f_next rows
+    if (f_next == f_s) return vk::fail(VLASOV_EINVAL, "f_next must not alias f_s");
     if (f0v && !L->self_ghost_ok)
         return vk::fail(VLASOV_EUNSUPPORTED, "in-kernel ghosts need one periodic block with nv a multiple of 4");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
@@ -1276,6 +1278,9 @@ int vlasov_rk4_stage_vp(vlasov_level* L, const vlasov_poisson* plan, int32_t sta
     if (plan->n > 4096 || plan->n % 2)
         return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage_vp: needs an even n <= 4096 (else use poisson_solve)");
     if (rho_next == rho_s) return vk::fail(VLASOV_EINVAL, "rk4_stage_vp: rho_next must not alias rho_s");
+    // CTAs write rows of E_s while others read E_bc
+    if (E_bc && E_bc == E_s) return vk::fail(VLASOV_EINVAL, "rk4_stage_vp: E_bc must not alias E_s");
+    if (f_next == f_s) return vk::fail(VLASOV_EINVAL, "f_next must not alias f_s");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E_s,
                                  E_bc, f0v, recon, rho_next, rho_s, plan->d_gE, E_s, plan->d_gX);
@@ -1342,6 +1347,14 @@ int vlasov_level_set_moment_base(vlasov_level* L, double base) {
     if (!L) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "moment base: one periodic block only");
     L->moment_base = base;
+    return VLASOV_OK;
+}
+
+int vlasov_level_set_velocity_faces(vlasov_level* L, int32_t phys_lo, int32_t phys_hi) {
+    if (!L) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!L->single_block || L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "velocity faces: one periodic 1D+1V block only");
+    L->vphys[0] = phys_lo ? 1 : 0;
+    L->vphys[1] = phys_hi ? 1 : 0;
     return VLASOV_OK;
 }
 

@@ -38,7 +38,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define TRACE(i) do { if (threadIdx.x == 0) g_trace[blockIdx.x][i] = gtimer(); } while (0)
+#define TRACE(i) do { if (threadIdx.x == 0 && blockIdx.x < 2048) g_trace[blockIdx.x][i] = gtimer(); } while (0)
 #else
 #define TRACE(i) do { } while (0)
 #endif
@@ -59,6 +59,7 @@ struct StageArgs1 {
     const Block1* blocks;
     double dt, dx, dv, v_lo;   // v_lo: physical lower velocity of the level domain
     double rho_base;           // fused moment: rho = rho_base - dv sum_v f (1 unless a velocity slab)
+    int phys_lo, phys_hi;      // SELF: velocity faces with the characteristic BC (else slab faces)
     int dom_x, dom_v, n_vtiles, tile_rows;
     // fused constraint evaluation (vlasov_rk4_stage_vp): E of the stage state from its moment
     const double* rho_in;      // nullable: rho of f_s (dom_x values); then E is computed and written
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     griddep_launch_dependents();
 #endif
 #ifdef STAGE1D_TRACE
-    if (threadIdx.x == 0) { unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); g_trace[blockIdx.x][8] = sm; }
+    if (threadIdx.x == 0 && blockIdx.x < 2048) { unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); g_trace[blockIdx.x][8] = sm; }
 #endif
     Tile1 T;
     Block1 B;
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     for (int t = tid; t < Q; t += NT) {
         const int gi = B.lo_x + wr(T.x0 - 2 + t) + G;  // index in the ghosted level E array
         if (!field) sE[t] = __ldg(A.E + gi);
-        if (SELF && A.E_bc) sEbc[t] = __ldg(A.E_bc + gi);
+        if (SELF && A.E_bc && STAGE != 1) sEbc[t] = __ldg(A.E_bc + gi);
     }
     // the unperturbed profile at the velocity ghost columns (read after the setup barrier: a
     // global load there would sit on every CTA's start-up path)
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         // shared-memory banks) with a sliding window of g, so each g value loaded serves EROWS
         // rows; fixed chunk order and transposed butterflies -> deterministic.
 #ifdef STAGE1D_TRACE
-        if (tid == 0) { g_trace[blockIdx.x][9] = te - tb; }
+        if (tid == 0 && blockIdx.x < 2048) { g_trace[blockIdx.x][9] = te - tb; }
 #endif
         const int C = ((n + 31) / 32) | 1;
         const int kc0 = min(n, C * lane), kc1 = min(n, kc0 + C);
@@ -439,10 +440,14 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     // the thread holding domain cells 0..3 / nv-4 .. nv-1 (SELF: level nv % 4 == 0)
     const bool edge_lo = SELF && (B.lo_v + c0 == 0);
     const bool edge_hi = SELF && (B.lo_v + c0 + CPT == A.dom_v);
-    // GM 1: input v-ghosts derived in-kernel from E_bc; GM 2: read from f_s's ghost columns.
+    // GM 1: input v-ghosts derived in-kernel from E_bc; GM 2: read from f_s's ghost columns, except
+    // at stage 1, whose boundary field is its own E = E(f_n) (the end-of-step constraint evaluation
+    // of Alg.5, reading #6b): derived in-kernel from E.  Only at physical velocity faces.
     // SELF: the edge threads stage f_next's boundary cells; its velocity ghost columns for this
     // stage's field E are written after the march, off the critical path
-    const bool lo_edge = (GM == 1) && edge_lo, hi_edge = (GM == 1) && edge_hi;
+    constexpr bool BC_IN = (GM == 1) || (GM == 2 && STAGE == 1);
+    const bool lo_edge = BC_IN && edge_lo && A.phys_lo, hi_edge = BC_IN && edge_hi && A.phys_hi;
+    const double* Ebcf = (STAGE == 1) ? E : Ebc;   // the field deciding the direction
     constexpr bool GHOST_OUT = SELF && STAGE >= 1;
 
     double W[4][CPT + 2];                        // f_s rows (mod 4) at columns c0-1 .. c0+4
@@ -483,8 +488,8 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
 #pragma unroll
             for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + TV + cl + m); uu[m] = p.x; uu[m + 1] = p.y; }
         }
-        if (GM == 1 && (lo_edge || hi_edge)) {   // characteristic BC (reading #6), a = -E_bc
-            const double a = -Ebc[r];
+        if (BC_IN && (lo_edge || hi_edge)) {     // characteristic BC (reading #6), a = -E_bc
+            const double a = -Ebcf[r];
             if (lo_edge) {
                 if (a < 0.0) {
                     v[1] = 4.0 * v[2] - 6.0 * v[3] + 4.0 * v[4] - v[5];
@@ -847,6 +852,8 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.dv = L->h[1];
     A.v_lo = L->lower[1];
     A.rho_base = L->moment_base;
+    A.phys_lo = L->vphys[0];
+    A.phys_hi = L->vphys[1];
     A.dom_x = L->dom[0];
     A.dom_v = L->dom[1];
     A.n_vtiles = L->n_vtiles;

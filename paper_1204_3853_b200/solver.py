@@ -6,7 +6,9 @@ One RK4 step = Alg.5 with one hierarchy and one level.  Per stage s 
                                                                     finest x resolution is the
                                                                     identity, P:1291-1337)
     vlasov_rk4_stage(s, f_s, E_s, E_bc = E_{s-1})  -> f_{s+1}, rho_{s+1}
-        (ghosts of f_s derived in-kernel = Alg.2 exchange + BC with the latest field, reading #6b;
+        (ghosts of f_s derived in-kernel = Alg.2 exchange + BC with the latest field, reading #6b:
+         E_{s-1} for s >= 2, and for s = 1 E(f_n) = E_1 -- the end-of-step constraint evaluation
+         of Alg.5, which on one periodic level is the stage-1 field itself;
          face averages, fluxes, divergence, RK4 combine P:233-410; moment P:295-297)
 With ``self_ghost=False`` the ghost frame is filled by vlasov_fill_ghosts instead (generic path).
 Buffers: A = f_n, B = f2/f4, C = f3, U = u.  E alternates between two buffers so that stage s
@@ -62,8 +64,6 @@ class UniformVlasov1D:
             # first constraint evaluation (t = 0): moment of f_n, field -> E_bc of stage 1
             api.vlasov_reduce_moment([self.level.h], [self.A], self.rho)
             self.poisson.solve(self.rho, None, self.E[0], 2)
-            if self.carry:    # velocity ghosts of f_n for E_bc = E[0] (stage 1 reads them)
-                api.vlasov_fill_ghosts(self.level.h, self.A, None, None, self.E[0], self.f0v)
         self.stream.synchronize()
 
     def get_state(self) -> np.ndarray:
@@ -100,7 +100,8 @@ class UniformVlasov1D:
             api.vlasov_rk4_stage(L, s, dt, self.A, f_s, self.U, f_next, E_cur, None if self.carry else E_bc,
                                  self.f0v, self.recon, self.rho)
         else:
-            api.vlasov_fill_ghosts(L, f_s, None, None, E_bc, self.f0v)
+            # stage 1: the boundary field is E(f_n) = this stage's field (reading #6b)
+            api.vlasov_fill_ghosts(L, f_s, None, None, E_cur if s == 1 else E_bc, self.f0v)
             api.vlasov_rk4_stage(L, s, dt, self.A, f_s, self.U, f_next, E_cur, None, None, self.recon, self.rho)
 
     def _stage(self, s, dt):

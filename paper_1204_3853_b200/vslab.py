@@ -93,6 +93,7 @@ class _Slab:
                                  np.asarray(f0v_full)[vr.start:vr.start + nvs + 4], recon, stream=stream,
                                  fused=True, carry_ghosts=True)
         api.vlasov_level_set_moment_base(self.S.level.h, 1.0 if j == 0 else 0.0)
+        api.vlasov_level_set_velocity_faces(self.S.level.h, j == 0, j == nslabs - 1)
         nx = w_ncells[0]
         with torch.cuda.stream(self.S.stream):
             z = lambda: torch.zeros(2 * nx, dtype=torch.float64, device="cuda")   # noqa: E731

@@ -65,11 +65,14 @@ def test_compute_entry_points_validate_then_need_a_device():
     rc, L = _create(g, (1, 1), [((0, 0), (15, 31))])
     assert rc == _lib.OK
     buf = (C.c_double * 64)()
+    nxt = (C.c_double * 64)()
     # validation errors first
     assert lib.vlasov_rk4_stage(L, 0, 0.1, buf, buf, buf, buf, buf, None, None, 0, None) == _lib.EINVAL
     assert lib.vlasov_rk4_stage(L, 2, 0.1, None, buf, buf, buf, buf, None, None, 0, None) == _lib.EINVAL
     assert lib.vlasov_rk4_stage(L, 1, 0.1, buf, buf, buf, buf, buf, None, None, 7, None) == _lib.EINVAL
     assert lib.vlasov_rk4_stage(L, 1, 0.1, buf, buf, buf, buf, buf, buf, None, 0, None) == _lib.EINVAL
+    # f_next aliasing f_s: neighbouring CTAs read halo rows of f_s (a cross-CTA race)
+    assert lib.vlasov_rk4_stage(L, 2, 0.1, buf, buf, buf, buf, buf, None, None, 0, None) == _lib.EINVAL
     assert lib.vlasov_tag_cells(L, buf, 0.1, -1, buf) == _lib.EINVAL
     assert lib.vlasov_average_down(L, buf, buf, None, 0.1) == _lib.EINVAL           # no coarser level
     P = C.c_void_p()
@@ -82,7 +85,7 @@ def test_compute_entry_points_validate_then_need_a_device():
     assert lib.vlasov_reduce_current(Ls, 1, (C.c_void_p * 1)(None), -1.0, 0, buf) == _lib.EINVAL
     if not api.vlasov_device_ok():
         assert lib.vlasov_reduce_current(Ls, 1, fs, -1.0, 0, buf) == _lib.ECUDA
-        assert lib.vlasov_rk4_stage(L, 1, 0.1, buf, buf, buf, buf, buf, None, None, 0, None) == _lib.ECUDA
+        assert lib.vlasov_rk4_stage(L, 1, 0.1, buf, buf, buf, nxt, buf, None, None, 0, None) == _lib.ECUDA
         assert lib.vlasov_fill_ghosts(L, buf, None, None, buf, buf, 0) == _lib.ECUDA
         assert lib.vlasov_inject_field(L, buf, (C.c_int32 * 2)(16, 1), buf) == _lib.ECUDA
         assert lib.vlasov_poisson_create(16, 0.1, None, C.byref(P)) in (_lib.ECUDA, _lib.OK)

@@ -313,3 +313,49 @@ def test_strip_shift_changes_no_result(tmp_path):
         res[q] = np.load(out)
     assert np.array_equal(res["0"], res["2"])
     assert np.array_equal(res["0"], res["1"])
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_stage1_boundary_uses_own_field(mode):
+    """Reading #6b (Alg.5): stage 1's characteristic boundary condition uses E(f_n), the
+    stage's own field -- not whatever the velocity ghost columns of f_n hold (carried modes) nor
+    the E_bc buffer (in-kernel E_bc modes).  Both are made adversarial (junk ghost columns, E_bc of
+    the opposite sign) on a state with O(1) boundary values; the step must still equal the
+    oracle's (tests/test_oracle_alg5.py pins that the boundary field matters here)."""
+    import test_oracle_alg5 as alg5
+    w, prob, f0, dt = alg5.heavy_tail_problem()
+    kw = MODES[mode]
+    S = UniformVlasov1D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w),
+                        inputs.background_profile(w), self_ghost=kw.get("self_ghost", True),
+                        fused=kw.get("fused") if kw.get("self_ghost", True) else False,
+                        carry_ghosts=kw.get("carry_ghosts", True))
+    S.set_state(f0)
+    with torch.cuda.stream(S.stream):
+        g = S.level.patch_view(S.A, 0, 2)
+        g[:, 0:2] = 1.0e3                    # junk velocity ghosts of f_n
+        g[:, -2:] = -1.0e3
+        S.E[0].neg_()                        # E_bc buffer of stage 1: the opposite sign
+    f, E_bc = f0, prob.constraints(f0)
+    for n in range(3):
+        S.step(dt)
+        f, E_bc, _ = prob.step(f, E_bc, dt)
+        got = S.get_state()
+        assert relerr(got, f) < 1e-12, (n, relerr(got, f))
+
+
+def test_stage_vp_rejects_aliasing():
+    """E_bc aliasing E_s (other CTAs write E_s rows) and f_next aliasing f_s (halo rows) are races:
+    the fused stage entry point refuses them (VLASOV_EINVAL)."""
+    w = inputs.get("C1")
+    S = UniformVlasov1D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w),
+                        inputs.background_profile(w), fused=True)
+    S.set_state(inputs.initial_cell_averages(w))
+    L, P = S.level.h, S.poisson.h
+    with pytest.raises(_lib.VlasovError):
+        api.vlasov_rk4_stage_vp(L, P, 2, 0.01, S.A, S.B, S.U, S.C, S.rhos[0], S.E[1], S.E[1], S.f0v,
+                                _lib.CENTERED4, S.rhos[1])
+    with pytest.raises(_lib.VlasovError):
+        api.vlasov_rk4_stage_vp(L, P, 2, 0.01, S.A, S.B, S.U, S.B, S.rhos[0], S.E[1], None, S.f0v,
+                                _lib.CENTERED4, S.rhos[1])
+    with pytest.raises(_lib.VlasovError):
+        api.vlasov_rk4_stage(L, 3, 0.01, S.A, S.C, S.U, S.C, S.E[1], None, S.f0v, _lib.CENTERED4, None)
