@@ -64,6 +64,9 @@ class UniformVlasov1D:
             # first constraint evaluation (t = 0): moment of f_n, field -> E_bc of stage 1
             api.vlasov_reduce_moment([self.level.h], [self.A], self.rho)
             self.poisson.solve(self.rho, None, self.E[0], 2)
+            # ghost frame of f_n for E(f_n) (stage 1 derives its own velocity ghosts; this is for the
+            # other consumers of the state's ghosts, e.g. vlasov_reduce_current)
+            api.vlasov_fill_ghosts(self.level.h, self.A, None, None, self.E[0], self.f0v)
         self.stream.synchronize()
 
     def get_state(self) -> np.ndarray:

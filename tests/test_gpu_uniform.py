@@ -271,7 +271,8 @@ def test_stage_kernels_deterministic_and_self_equals_stored(shape):
             if mode == "self":
                 api.vlasov_rk4_stage(L.h, stage, 1e-3, fnx, fsx, u, out, E, Ebc, fbg, 0, rho)
             else:
-                api.vlasov_fill_ghosts(L.h, fsx, None, None, Ebc, fbg)
+                # stage 1 derives its boundary from its own field E (reading #6b), later stages from E_bc
+                api.vlasov_fill_ghosts(L.h, fsx, None, None, E if stage == 1 else Ebc, fbg)
                 api.vlasov_rk4_stage(L.h, stage, 1e-3, fnx, fsx, u, out, E, None, None, 0, rho)
             torch.cuda.synchronize()
             outs.append((L.get_domain(out), L.get_domain(u), rho.cpu().numpy().copy()))
