@@ -296,6 +296,16 @@ int vlasov_level_fill_from(vlasov_level* level, double* f, const vlasov_level* o
  * out[0] (device) = max_i |x_i| over n doubles, on `cuda_stream`; deterministic.  The drivers form
  * dt = min(cfl / max_l(max|vbar|/dx_l + max|E_l|/dv_l), growth * dt_prev) from it.              */
 int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream);
+/* vlasov_next_dt: the adaptive step of Alg.1/5 "Compute next dt" ("50% of
+ * the local stability condition", growth <= 10%, any decrease; reading #29) for a 1D+1V hierarchy
+ * levels[0..nlev-1] (coarse first) with E[l] the ghosted E array of level l (device, dom_x + 4
+ * doubles) from the last constraint evaluation:
+ *   dt = min(cfl / max_l(vmax / dx_l + max|E_l| / dv_l), growth * dt_prev),
+ * vmax = max |cell-centre velocity| over the finest level's velocity domain.  Host call: launches
+ * one reduction per level on its stream and synchronises them; *dt_out is written on the host.
+ * Errors: EINVAL (null pointers, nlev < 1, non-positive cfl / growth / dt_prev, 2D+2V level).     */
+int vlasov_next_dt(const vlasov_level* const* levels, int32_t nlev, const double* const* E, double dt_prev,
+                   double cfl, double growth, double* dt_out);
 
 /* ---- velocity-slab decomposition of a uniform 1D+1V level -------- *
  * Each GPU (rank) owns all x and a contiguous velocity slab, created as its own level (one block,

@@ -68,6 +68,7 @@ _SIGS = {
     "vlasov_reduce_charge": (I32, [C.POINTER(P), I32, C.POINTER(P), D, D, I32, P]),
     "vlasov_inject_field_scaled": (I32, [P, P, PI32, D, P]),
     "vlasov_absmax": (I32, [P, I64, P, P]),
+    "vlasov_next_dt": (I32, [C.POINTER(P), I32, C.POINTER(P), D, D, D, C.POINTER(D)]),
     "vlasov_level_set_moment_base": (I32, [P, D]),
     "vlasov_level_set_velocity_faces": (I32, [P, I32, I32]),
     "vlasov_reduce_current": (I32, [P, I32, P, D, I32, P]),

@@ -177,24 +177,10 @@ class AmrVlasov1D:
         with torch.cuda.stream(self.stream):
             self._graph.replay()
 
-    def next_dt(self, dt_prev, cfl=0.5, growth=1.1, vmax=None):
-        """Adaptive step (reading #17): dt = min(cfl / rate, growth * dt_prev) with
-        rate = max over levels of (max|vbar|/dx_l + max|E_l|/dv_l), E_l the last constraint
-        evaluation; max|E_l| by vlasov_absmax on the device (one 8-byte read per level)."""
-        if vmax is None:
-            L = self.levels[-1]
-            dv = self.dx0[1] / L.ratio[1]
-            nv = L.info.domain_cells[1]
-            vmax = max(abs(self.lower[1] + 0.5 * dv), abs(self.lower[1] + (nv - 0.5) * dv))
-        out = torch.zeros(len(self.levels), dtype=torch.float64, device="cuda")
-        with torch.cuda.stream(self.stream):
-            for l, E in enumerate(self.E):
-                api.vlasov_absmax(E[self.cur], out[l:l + 1], self.stream)
-        self.stream.synchronize()
-        em = out.cpu().numpy()
-        rate = max(vmax / (self.dx0[0] / L.ratio[0]) + em[l] / (self.dx0[1] / L.ratio[1])
-                   for l, L in enumerate(self.levels))
-        return min(cfl / rate, growth * dt_prev)
+    def next_dt(self, dt_prev, cfl=0.5, growth=1.1):
+        """Adaptive step (reading #29) from the last constraint evaluation: one C-ABI
+        call (vlasov_next_dt; max|E_l| reduced on the device, the rate formed in the library)."""
+        return api.vlasov_next_dt(self.handles, [E[self.cur] for E in self.E], dt_prev, cfl, growth)
 
     def launches_per_step(self) -> int:
         nl = len(self.levels)
@@ -223,11 +209,9 @@ class AmrVlasov1D:
         vlasov_cluster_tags (P:468-475, reading #28); smallest / largest are level-1 patch sizes
          in level-1 cells, converted to level-0 cells (ceil / floor by the ratio)."""
         tags = self.tags_level0(tol, buffer)
-        sm = [-(-smallest[d] // ratio[d]) for d in range(2)]
-        lg = [max(sm[d], largest[d] // ratio[d]) for d in range(2)]
-        coarse = api.vlasov_cluster_tags(tags, sm, lg, efficiency)
-        fine = sorted(((lo[0] * ratio[0], lo[1] * ratio[1]), ((hi[0] + 1) * ratio[0] - 1, (hi[1] + 1) * ratio[1] - 1))
-                      for lo, hi in coarse)
+        # clustering with the level-1 patch sizes converted to level-0 cells, refinement by the ratio
+        # and sorting: all in the library (level 0 covers the domain, so nesting restricts nothing)
+        fine = api.vlasov_regrid_boxes(self.levels[0].h, tags, ratio, smallest, largest, efficiency)
         return self.regrid_to(fine, ratio)
 
     def tags_level(self, k, tol, buffer):

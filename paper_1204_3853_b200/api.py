@@ -19,7 +19,7 @@ __all__ = [
     "vlasov_fill_ghosts", "vlasov_rhs", "vlasov_rk4_stage", "vlasov_rk4_stage_vp", "vlasov_reduce_moment", "vlasov_reduce_moment_mask", "vlasov_reduce_charge", "vlasov_inject_field_scaled",
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
-    "vlasov_level_fill_from", "vlasov_absmax", "vlasov_device_ok", "vlasov_last_error",
+    "vlasov_level_fill_from", "vlasov_absmax", "vlasov_next_dt", "vlasov_device_ok", "vlasov_last_error",
     "vlasov_level_set_moment_base", "vlasov_level_set_velocity_faces", "vlasov_vslab_pack", "vlasov_vslab_unpack", "vlasov_reduce_current",
 ]
 
@@ -158,6 +158,15 @@ def vlasov_vslab_unpack(h, f, lo=None, hi=None):
 
 def vlasov_absmax(x, out, stream=None):
     return check(lib.vlasov_absmax(_ptr(x), x.numel(), _ptr(out), _stream_ptr(stream)))
+
+
+def vlasov_next_dt(levels, E_list, dt_prev, cfl=0.5, growth=1.1):
+    """Adaptive time step of a 1D+1V hierarchy (levels coarse first, E_list their ghosted E arrays)."""
+    arr = (C.c_void_p * len(levels))(*[l.value if isinstance(l, C.c_void_p) else l for l in levels])
+    ep = (C.c_void_p * len(levels))(*[t.data_ptr() for t in E_list])
+    out = C.c_double(0.0)
+    check(lib.vlasov_next_dt(arr, len(levels), ep, float(dt_prev), float(cfl), float(growth), C.byref(out)))
+    return out.value
 
 
 def vlasov_reduce_charge(levels, f_list, q, base, accumulate, rho_finest):

@@ -192,6 +192,7 @@ struct vlasov_level {
     double* d_partials = nullptr;         // moment scratch [n_vtiles][dom_x]
     uint8_t* d_rawtags = nullptr;         // raw tags of a multi-patch level (level domain)
     unsigned* d_tickets = nullptr;        // per-strip arrival tickets
+    double* d_scalar = nullptr;           // one device double (max|E| of vlasov_next_dt)
     bool self_ghost_ok = false;           // single periodic block, nv % 4 == 0: in-kernel ghosts
     // ghost fill
     int64_t n_copy = 0, n_cf = 0, n_phys = 0;

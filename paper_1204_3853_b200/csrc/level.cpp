@@ -188,6 +188,7 @@ void free_level(vlasov_level* L) {
     vk::dfree(L->d_partials, L->stream);
     vk::dfree(L->d_tickets, L->stream);
     vk::dfree(L->d_rawtags, L->stream);
+    vk::dfree(L->d_scalar, L->stream);
     delete L;
 }
 
@@ -866,6 +867,7 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         *out = L;
         return VLASOV_OK;
     }
+    VK_CUDA(cudaMallocAsync((void**)&L->d_scalar, sizeof(double), L->stream));
     if (!L->single_block && L->ndim == 2) {      // tag scratch of multi-patch levels (regrid)
         int64_t tb = (int64_t)L->dom[0] * L->dom[1];
         VK_CUDA(cudaMallocAsync((void**)&L->d_rawtags, (size_t)tb, L->stream));
@@ -1378,6 +1380,33 @@ int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream) {
     if (!x || !out || n < 0) return vk::fail(VLASOV_EINVAL, "null argument or n < 0");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     return vk::launch_absmax(x, n, out, (cudaStream_t)cuda_stream);
+}
+
+// Adaptive time step (reading #29): dt = min(cfl / rate, growth * dt_prev),
+// rate = max_l (vmax / dx_l + max|E_l| / dv_l), vmax = the largest |cell-centre velocity| of the
+// finest level's velocity domain; max|E_l| on the device (k_absmax), one 8-byte read per level.
+int vlasov_next_dt(const vlasov_level* const* levels, int32_t nlev, const double* const* E, double dt_prev,
+                   double cfl, double growth, double* dt_out) {
+    if (!levels || !E || !dt_out || nlev < 1) return vk::fail(VLASOV_EINVAL, "null argument or nlev < 1");
+    if (!(cfl > 0.0) || !(growth > 0.0) || !(dt_prev > 0.0)) return vk::fail(VLASOV_EINVAL, "next_dt: cfl, growth, dt_prev > 0");
+    for (int l = 0; l < nlev; ++l)
+        if (!levels[l] || !E[l] || levels[l]->ndim != 2) return vk::fail(VLASOV_EINVAL, "next_dt: 1D+1V level and E per level");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    const vlasov_level* Lf = levels[nlev - 1];
+    const double dvf = Lf->h[1];
+    const double vlo = Lf->lower[1] + 0.5 * dvf, vhi = Lf->lower[1] + ((double)Lf->dom[1] - 0.5) * dvf;
+    const double vmax = std::max(std::fabs(vlo), std::fabs(vhi));
+    std::vector<double> em(nlev, 0.0);
+    for (int l = 0; l < nlev; ++l) {
+        const vlasov_level* L = levels[l];
+        if (int rc = vk::launch_absmax(E[l], (int64_t)L->dom[0] + 2 * vk::G, L->d_scalar, L->stream)) return rc;
+        VK_CUDA(cudaMemcpyAsync(&em[l], L->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, L->stream));
+    }
+    for (int l = 0; l < nlev; ++l) VK_CUDA(cudaStreamSynchronize(levels[l]->stream));
+    double rate = 0.0;
+    for (int l = 0; l < nlev; ++l) rate = std::max(rate, vmax / levels[l]->h[0] + em[l] / levels[l]->h[1]);
+    *dt_out = std::min(cfl / rate, growth * dt_prev);
+    return VLASOV_OK;
 }
 
 // Alg.6 Mask Reduction: every patch refined in x (linear5, ghost columns current),

@@ -83,6 +83,11 @@ def test_compute_entry_points_validate_then_need_a_device():
     assert lib.vlasov_reduce_current(Ls, 0, fs, -1.0, 0, buf) == _lib.EINVAL       # nlev >= 1
     assert lib.vlasov_reduce_current(Ls, 1, fs, -1.0, 0, None) == _lib.EINVAL     # j required
     assert lib.vlasov_reduce_current(Ls, 1, (C.c_void_p * 1)(None), -1.0, 0, buf) == _lib.EINVAL
+    dto = C.c_double()
+    assert lib.vlasov_next_dt(Ls, 0, fs, 0.01, 0.5, 1.1, C.byref(dto)) == _lib.EINVAL      # nlev >= 1
+    assert lib.vlasov_next_dt(Ls, 1, fs, 0.01, 0.0, 1.1, C.byref(dto)) == _lib.EINVAL      # cfl > 0
+    assert lib.vlasov_next_dt(Ls, 1, fs, -1.0, 0.5, 1.1, C.byref(dto)) == _lib.EINVAL      # dt_prev > 0
+    assert lib.vlasov_next_dt(Ls, 1, fs, 0.01, 0.5, 1.1, None) == _lib.EINVAL              # output required
     if not api.vlasov_device_ok():
         assert lib.vlasov_reduce_current(Ls, 1, fs, -1.0, 0, buf) == _lib.ECUDA
         assert lib.vlasov_rk4_stage(L, 1, 0.1, buf, buf, buf, nxt, buf, None, None, 0, None) == _lib.ECUDA

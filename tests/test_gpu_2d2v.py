@@ -99,3 +99,19 @@ def test_c5_full_size_one_step():
     w = inputs.get("C5")
     _, got, ref = _run(w, 1)
     assert relerr(got, ref) < 1e-12
+
+
+def test_c5_full_size_ten_steps_bench_launch():
+    # BASELINE.json C5 at full size in the bench's launch configuration (one-step CUDA graph,
+    # replayed): 10 steps within 1e-11
+    w = inputs.get("C5")
+    f0 = inputs.initial_cell_averages(w)
+    dt = inputs.fixed_dt(w)
+    S = _solver(w)
+    S.set_state(f0)
+    S.capture(dt, steps=1)                   # runs one eager step first
+    for _ in range(9):
+        S.replay()
+    got = S.get_state()
+    ref, _ = uniform.problem_for(w).run(f0, dt, 10)
+    assert relerr(got, ref) < 1e-11

@@ -244,6 +244,14 @@ def test_c4_full_size_one_step():
     assert relerr(got, ref) < 1e-12
 
 
+def test_c4_full_size_ten_steps_bench_launch():
+    # the bench's launch configuration (fused field, carried ghosts, one-step CUDA graph replayed)
+    # at BASELINE.json's full C4 size: 10 steps within 1e-11 (between the 1-step 1e-12 and the
+    # 100-step 1e-10 bounds of the north star)
+    got, ref = _run_both(inputs.get("C4"), 10, graph=True)
+    assert relerr(got, ref) < 1e-11
+
+
 @pytest.mark.parametrize("shape", [(1024, 4096), (300, 1100)])
 def test_stage_kernels_deterministic_and_self_equals_stored(shape):
     """Every stage instance twice on identical inputs (bitwise equal: no race between the TMA
