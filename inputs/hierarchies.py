@@ -64,3 +64,48 @@ def random_hierarchy(seed, nx0=16, nv0=32, nlevels=None, ratios=(2, 4), max_boxe
         levels.append(sorted(boxes))
         rat.append((cur[0] * r[0], cur[1] * r[1]))
     return rat, levels
+
+
+def random_hierarchy_4d(seed, n0=(8, 8, 8, 8), patch0=(8, 8, 4, 8), nlevels=2, ratios=(2,), max_boxes=2):
+    """Random properly nested 2D+2V hierarchy (N3): level 0 tiles the (x, y, v_x, v_y) domain with
+    patch0 boxes; every finer box is the refinement (ratio per dim from `ratios`) of a box of
+    cells of the coarser level lying one coarse cell inside its union (x, y periodic; cells
+    beyond the velocity domain count as covered, so fine boxes may touch it).  Returns
+    (ratios_to_level0, level_boxes)."""
+    import itertools
+    rng = np.random.default_rng(seed)
+    lv0 = []
+    for lo in itertools.product(*[range(0, n0[d], patch0[d]) for d in range(4)]):
+        lv0.append((tuple(lo), tuple(min(lo[d] + patch0[d], n0[d]) - 1 for d in range(4))))
+    levels, rat = [sorted(lv0)], [(1, 1, 1, 1)]
+    for _ in range(1, nlevels):
+        r = tuple(int(rng.choice(ratios)) for _ in range(4))
+        cur = rat[-1]
+        nl = tuple(n0[d] * cur[d] for d in range(4))
+        cov = np.zeros(nl, bool)
+        for lo, hi in levels[-1]:
+            cov[tuple(slice(lo[d], hi[d] + 1) for d in range(4))] = True
+        pad = np.pad(cov, ((0, 0), (0, 0), (1, 1), (1, 1)), constant_values=True)
+        inner = np.ones_like(cov)
+        for off in itertools.product((-1, 0, 1), repeat=4):
+            sh = np.roll(np.roll(pad, off[0], axis=0), off[1], axis=1)
+            inner &= sh[:, :, 1 + off[2]: 1 + off[2] + nl[2], 1 + off[3]: 1 + off[3] + nl[3]]
+        boxes, taken = [], np.zeros_like(cov)
+        for _b in range(int(rng.integers(1, max_boxes + 1))):
+            for _try in range(40):
+                w = [int(rng.integers(2, max(3, nl[d] // 2 + 1))) for d in range(4)]
+                lo = [int(rng.integers(0, nl[d] - w[d] + 1)) for d in range(4)]
+                # velocity extent: touch the boundary or stay >= 2 coarse cells away from it
+                ok = all(lo[d] == 0 or lo[d] >= 2 for d in (2, 3)) and \
+                    all(lo[d] + w[d] == nl[d] or lo[d] + w[d] <= nl[d] - 2 for d in (2, 3))
+                sl = tuple(slice(lo[d], lo[d] + w[d]) for d in range(4))
+                if ok and inner[sl].all() and not taken[sl].any():
+                    taken[sl] = True
+                    boxes.append((tuple(lo[d] * r[d] for d in range(4)),
+                                  tuple((lo[d] + w[d]) * r[d] - 1 for d in range(4))))
+                    break
+        if not boxes:
+            break
+        levels.append(sorted(boxes))
+        rat.append(tuple(cur[d] * r[d] for d in range(4)))
+    return rat, levels

@@ -89,6 +89,14 @@ WORKLOADS = {
         (2 * math.pi, 2 * math.pi, 6.0, 6.0), (16, 16, 16, 16), "landau2d", 0.01,
         (1.0, 1.0), "prescribed", 50,
         description="2D+2V stress case, 64^4 in 16^4 patches, prescribed E=0.1(cos x, sin y)"),
+    # NEXT row N3 (not a BASELINE.json config): the C5 geometry and initial data with the
+    # self-consistent field of the 2D periodic Poisson problem (reading #32) instead of the
+    # prescribed one; the 2D+2V AMR tests use scaled-down versions of it
+    "C5P": Workload(
+        "C5P", 2, (64, 64, 64, 64), (0.0, 0.0, -6.0, -6.0),
+        (2 * math.pi, 2 * math.pi, 6.0, 6.0), (16, 16, 16, 16), "landau2d", 0.01,
+        (1.0, 1.0), "poisson", 50,
+        description="N3: 2D+2V Vlasov-Poisson, C5 geometry, self-consistent 2D periodic field"),
 }
 
 

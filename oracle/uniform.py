@@ -100,7 +100,8 @@ class UniformProblem:
     lower, h      physical lower corner and spacings per axis
     shape         interior cells per axis
     fbg           unperturbed velocity profile on the ghosted velocity range
-    field_mode    'poisson' (1D+1V, E from the periodic Poisson solve) or 'prescribed'
+    field_mode    'poisson' (E from the periodic Poisson solve: 1D, or 2D for 2D+2V, field2d) or
+                  'prescribed'
     E_prescribed  (ncfg, *cfg_shape) cell-averaged field for 'prescribed'
     """
 
@@ -124,8 +125,10 @@ class UniformProblem:
         """Cell-averaged field on the configuration mesh (no ghosts), shape (ncfg, *cfg)."""
         if self.field_mode == "prescribed":
             return self.E_prescribed.copy()
-        assert self.ncfg == 1
         rho = field.moment_rho(f, self.dv_volume)
+        if self.ncfg == 2:                                   # 2D+2V self-consistent field (N3)
+            from . import field2d
+            return field2d.efield_from_rho_2d(rho, self.h[0], self.h[1])
         return field.efield_from_rho(rho, self.h[0])[None, :]
 
     def ghosted_field(self, E):

@@ -29,17 +29,26 @@ per = []
 for r in rows[2:]:
     if kname not in r[kn]:
         continue
+    i = hdr.index("lts__t_sectors_srcunit_tex_op_write.sum")
+    l2w = float(r[i].replace(",", "")) * 32.0          # sectors the SMs wrote into L2 (32 B each)
     per.append({"kernel": r[kn][:60], "dram_read_bytes": val(r, "dram__bytes_read.sum", scale),
                 "dram_write_bytes": val(r, "dram__bytes_write.sum", scale),
+                "l2_write_bytes_from_sm": l2w,
                 "duration_us": val(r, "gpu__time_duration.sum", tscale)})
 per = per[:4]
-tot = sum(p["dram_read_bytes"] + p["dram_write_bytes"] for p in per)
+# Traffic charged to a launch: its DRAM reads plus every sector it dirtied in L2.  ncu's
+# dram__bytes_write.sum only sees write-backs that happen while the kernel runs; a streaming kernel
+# whose output (67-134 MB) largely fits the 126 MB L2 leaves most of it dirty at exit and it is
+# written back during later launches.  Each dirtied sector is written to DRAM exactly once (the
+# kernels write every output sector once), so reads + L2 writes is the launch's DRAM traffic.
+tot = sum(p["dram_read_bytes"] + max(p["dram_write_bytes"], p["l2_write_bytes_from_sm"]) for p in per)
 if len(per) != 4:
     sys.exit(f"need the 4 stage launches of one step, found {len(per)}")
 res = {"source": f"ncu --set full --clock-control none, {len(per)} stage launches of one {wname} RK4 step ({rep})",
        "bytes_per_step": tot, "bytes_per_step_per_cell": tot / cells, "algorithmic_bytes_per_step_per_cell": 104,
-       "note": "ncu counts DRAM writes that leave L2 during the kernel; part of the last rows' writes are flushed "
-               "after it, and rows still resident in L2 from the previous launch are not re-read",
+       "definition": "per launch: dram__bytes_read.sum + max(dram__bytes_write.sum, 32 x "
+                     "lts__t_sectors_srcunit_tex_op_write.sum) (every sector the kernel dirties in L2 is "
+                     "written back once, during or after the launch)",
        "per_launch": per}
 dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", f"stage_traffic_{wname}.json")
 json.dump(res, open(dst, "w"), indent=1)
