@@ -407,7 +407,7 @@ def main():
         S = UniformVlasov1D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w))
     else:
         S = UniformVlasov2D(w.ncells, w.lower, h, inputs.level0_boxes(w), inputs.background_profile(w),
-                            inputs.prescribed_field(w))
+                            inputs.prescribed_field(w) if w.field == "prescribed" else None, field=w.field)
     S.set_state(f0)
     S.capture(dt, steps=1)                       # one warm-up step inside
     for _ in range(args.warmup - 1):

@@ -307,6 +307,22 @@ int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream);
 int vlasov_next_dt(const vlasov_level* const* levels, int32_t nlev, const double* const* E, double dt_prev,
                    double cfl, double growth, double* dt_out);
 
+/* ---- 2D periodic field of a 2D+2V problem (NEXT row N3; reading #32) ----------------------- *
+ * The paper's 1D fourth-order Poisson discretisation generalised dimension by
+ * dimension (as its fluxes and interpolation are):
+ *   [30 phi - 16 (phi_{i+-1,k}) + (phi_{i+-2,k})] / dx^2 + [same along k] / dy^2 = 12 rho,
+ *   rho projected to mean zero, phi of mean zero, E = -(D4_x phi, D4_y phi).
+ * vlasov_poisson2d_create: exact discrete Green's functions of E_x and E_y (host, long double,
+ *   uploaded once; nx, ny >= 5, nx ny <= 26000).  Synchronises `cuda_stream`.
+ * vlasov_poisson2d_solve: rho (device, nx ny row-major [x][y]) -> E (device, the 2D level field
+ *   layout [2][(nx + 4)(ny + 4)]: component, then ghosted x, ghosted y; the 2 periodic ghost
+ *   layers are written too); one launch on the plan's stream; deterministic.               */
+typedef struct vlasov_poisson2d vlasov_poisson2d;
+int vlasov_poisson2d_create(int32_t nx, int32_t ny, double dx, double dy, void* cuda_stream,
+                            vlasov_poisson2d** out);
+int vlasov_poisson2d_solve(const vlasov_poisson2d* plan, const double* rho, double* E);
+int vlasov_poisson2d_destroy(vlasov_poisson2d* plan);
+
 /* ---- velocity-slab decomposition of a uniform 1D+1V level -------- *
  * Each GPU (rank) owns all x and a contiguous velocity slab, created as its own level (one block,
  * lower[1] = the slab's lower velocity).  Per stage: the fused moment of every slab is reduced

@@ -19,7 +19,8 @@ __all__ = [
     "vlasov_fill_ghosts", "vlasov_rhs", "vlasov_rk4_stage", "vlasov_rk4_stage_vp", "vlasov_reduce_moment", "vlasov_reduce_moment_mask", "vlasov_reduce_charge", "vlasov_inject_field_scaled",
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
-    "vlasov_level_fill_from", "vlasov_absmax", "vlasov_next_dt", "vlasov_device_ok", "vlasov_last_error",
+    "vlasov_level_fill_from", "vlasov_absmax", "vlasov_next_dt", "vlasov_poisson2d_create",
+    "vlasov_poisson2d_solve", "Poisson2D", "vlasov_device_ok", "vlasov_last_error",
     "vlasov_level_set_moment_base", "vlasov_level_set_velocity_faces", "vlasov_vslab_pack", "vlasov_vslab_unpack", "vlasov_reduce_current",
 ]
 
@@ -358,6 +359,35 @@ class Poisson:
         try:
             if getattr(self, "h", None):
                 lib.vlasov_poisson_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def vlasov_poisson2d_create(nx, ny, dx, dy, stream=None):
+    h = C.c_void_p()
+    check(lib.vlasov_poisson2d_create(int(nx), int(ny), float(dx), float(dy), _stream_ptr(stream), C.byref(h)))
+    return h
+
+
+def vlasov_poisson2d_solve(h, rho, E):
+    return check(lib.vlasov_poisson2d_solve(h, _ptr(rho), _ptr(E)))
+
+
+class Poisson2D:
+    """2D periodic field plan (N3, reading #32): rho (nx ny) -> ghosted E [2][(nx+4)(ny+4)]."""
+
+    def __init__(self, nx, ny, dx, dy, stream=None):
+        self.nx, self.ny = nx, ny
+        self.h = vlasov_poisson2d_create(nx, ny, dx, dy, stream)
+
+    def solve(self, rho, E):
+        vlasov_poisson2d_solve(self.h, rho, E)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib.vlasov_poisson2d_destroy(self.h)
                 self.h = None
         except Exception:
             pass

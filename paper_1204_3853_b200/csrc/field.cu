@@ -263,3 +263,118 @@ int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st) {
 }
 
 }  // namespace vk
+
+namespace vk {
+
+// 2D periodic field (N3, reading #32): E_c(i, k) = sum_{i', k'} g_c((i - i') mod nx, (k - k') mod ny)
+// (rho(i', k') - mean rho), c = x, y, with the exact discrete Green's functions of the 2D fourth-
+// order operator composed with -D4 (host, long double).  CTA = one output row i (all k): the
+// projected rho and both Green's functions staged in shared memory (nx ny <= P2_SMEM_MAX), thread
+// group t sums a fixed i' range for its outputs, the partials are added in group order
+// (deterministic); the CTA writes its row of the ghosted E arrays and the periodic ghost copies.
+constexpr int P2_THREADS = 256, P2_SMEM_MAX = 8192;
+
+template <bool G_SMEM>
+__global__ void __launch_bounds__(P2_THREADS) k_poisson2d(const double* __restrict__ rho, const double* __restrict__ gx,
+                                                           const double* __restrict__ gy, int nx, int ny,
+                                                           double* __restrict__ E) {
+    griddep_wait();
+    griddep_launch_dependents();
+    extern __shared__ double sm[];
+    const int n = nx * ny;
+    double* s_rho = sm;                                   // [n]
+    double* s_gx = sm + n;                                // [n] (G_SMEM)
+    double* s_gy = s_gx + n;                              // [n] (G_SMEM)
+    double* s_part = G_SMEM ? s_gy + n : s_gx;            // [2][P2_THREADS]
+    __shared__ double s_red[P2_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc = 0.0;
+    for (int t = tid; t < n; t += P2_THREADS) {
+        const double v = rho[t];
+        s_rho[t] = v;
+        acc += v;
+        if (G_SMEM) { s_gx[t] = gx[t]; s_gy[t] = gy[t]; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) s_red[warp] = acc;
+    __syncthreads();
+    double mean = 0.0;
+#pragma unroll
+    for (int w = 0; w < P2_THREADS / 32; ++w) mean += s_red[w];
+    mean /= (double)n;
+    const double* Gx = G_SMEM ? s_gx : gx;
+    const double* Gy = G_SMEM ? s_gy : gy;
+    const int i = blockIdx.x;
+    const int ngrp = P2_THREADS / ny > 0 ? P2_THREADS / ny : 1;      // thread groups per output
+    const int nyg = ny + 4;
+    for (int k0 = 0; k0 < ny; k0 += P2_THREADS / ngrp) {
+        const int kk = k0 + tid % (P2_THREADS / ngrp), grp = tid / (P2_THREADS / ngrp);
+        double ax = 0.0, ay = 0.0;
+        if (kk < ny && grp < ngrp) {
+            const int ib = (int)((int64_t)nx * grp / ngrp), ie = (int)((int64_t)nx * (grp + 1) / ngrp);
+            for (int ip = ib; ip < ie; ++ip) {
+                const int di = i - ip < 0 ? i - ip + nx : i - ip;
+                const double* rr = s_rho + ip * ny;
+                const double* gxr = Gx + di * ny;
+                const double* gyr = Gy + di * ny;
+                for (int kp = 0; kp < ny; ++kp) {
+                    const int dk = kk - kp < 0 ? kk - kp + ny : kk - kp;
+                    const double r = rr[kp] - mean;
+                    ax = fma(gxr[dk], r, ax);
+                    ay = fma(gyr[dk], r, ay);
+                }
+            }
+        }
+        __syncthreads();
+        s_part[tid] = ax;
+        s_part[P2_THREADS + tid] = ay;
+        __syncthreads();
+        if (grp == 0 && kk < ny) {
+            const int per = P2_THREADS / ngrp;
+            double ex = 0.0, ey = 0.0;
+            for (int g = 0; g < ngrp; ++g) { ex += s_part[g * per + tid % per]; ey += s_part[P2_THREADS + g * per + tid % per]; }
+            // own row and the periodic ghost rows / columns (x ghosts: rows i -+ nx)
+            for (int c = 0; c < 2; ++c) {
+                const double e = c ? ey : ex;
+                double* Ec = E + (int64_t)c * (nx + 4) * nyg;
+                const int rows[3] = {i + 2, i + 2 + nx, i + 2 - nx};
+                for (int r = 0; r < 3; ++r) {
+                    const int gr = rows[r];
+                    if (gr < 0 || gr >= nx + 4) continue;
+                    double* row = Ec + (int64_t)gr * nyg;
+                    row[kk + 2] = e;
+                    if (kk < 2) row[kk + 2 + ny] = e;
+                    if (kk >= ny - 2) row[kk + 2 - ny] = e;
+                }
+            }
+        }
+    }
+}
+
+int launch_poisson2d(const vlasov_poisson2d* P, const double* rho, double* E) {
+    const int n = P->nx * P->ny;
+    if (n <= P2_SMEM_MAX) {
+        const size_t smem = (size_t)(3 * n + 2 * P2_THREADS) * sizeof(double);
+        static bool cfg = false;
+        if (!cfg) {
+            VK_CUDA(cudaFuncSetAttribute(k_poisson2d<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            cfg = true;
+        }
+        VK_CUDA(launch_pdl(k_poisson2d<true>, dim3(P->nx), dim3(P2_THREADS), smem, P->stream, rho,
+                           (const double*)P->d_gx, (const double*)P->d_gy, P->nx, P->ny, E));
+    } else {
+        const size_t smem = (size_t)(n + 2 * P2_THREADS) * sizeof(double);
+        if (smem > 220 * 1024) return fail(VLASOV_EUNSUPPORTED, "poisson2d: nx * ny too large");
+        static bool cfg = false;
+        if (!cfg) {
+            VK_CUDA(cudaFuncSetAttribute(k_poisson2d<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            cfg = true;
+        }
+        VK_CUDA(launch_pdl(k_poisson2d<false>, dim3(P->nx), dim3(P2_THREADS), smem, P->stream, rho,
+                           (const double*)P->d_gx, (const double*)P->d_gy, P->nx, P->ny, E));
+    }
+    return VLASOV_OK;
+}
+
+}  // namespace vk

@@ -227,7 +227,16 @@ struct vlasov_poisson {
     double* d_gX = nullptr;               // gX[m] = gE[(m - GX_PAD) mod n], m < 2n + GX_PAD + GX_TAIL
 };
 
+struct vlasov_poisson2d {
+    int nx = 0, ny = 0;
+    double dx = 0, dy = 0;
+    cudaStream_t stream = nullptr;
+    double* d_gx = nullptr;               // [nx][ny] Green's function of E_x (row-major, (m, n))
+    double* d_gy = nullptr;               // [nx][ny] Green's function of E_y
+};
+
 namespace vk {
+int launch_poisson2d(const vlasov_poisson2d* P, const double* rho, double* E);
 // ------------------------------------------------------------------ kernels (launchers)
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s,
                       double* u, double* f_next, const double* E, const double* E_bc,

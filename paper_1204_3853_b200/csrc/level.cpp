@@ -1515,6 +1515,91 @@ int vlasov_reduce_moment_mask(const vlasov_level* const* levels, int32_t nlev, c
     return vk::launch_reduce_mask(Lf->mask_plan, f, nlev, rho_finest, Lf->stream);
 }
 
+// 2D periodic field (N3, reading #32): exact discrete Green's functions of
+//   Lambda(p, q) phi^ = 12 rho^,  Lambda = lambda(th_p) / dx^2 + lambda(th_q) / dy^2,
+//   lambda(th) = 30 - 32 cos th + 2 cos 2th,  E = -(D4_x, D4_y) phi,
+// in long double on the host (separable sums, O(nx ny (nx + ny))):
+//   g_x(m, n) = (1/N) sum_{(p,q) != 0} S_x(p) / Lambda sin(th_p m) cos(th_q n),  S_x = (16 sin th - 2 sin 2th)/dx
+//   g_y(m, n) = (1/N) sum_{(p,q) != 0} S_y(q) / Lambda cos(th_p m) sin(th_q n)
+int vlasov_poisson2d_create(int32_t nx, int32_t ny, double dx, double dy, void* cuda_stream, vlasov_poisson2d** out) {
+    if (!out) return vk::fail(VLASOV_EINVAL, "null argument");
+    *out = nullptr;
+    if (nx < 5 || ny < 5 || !(dx > 0) || !(dy > 0)) return vk::fail(VLASOV_EINVAL, "poisson2d: need nx, ny >= 5 and dx, dy > 0");
+    if ((int64_t)nx * ny > 26000) return vk::fail(VLASOV_EUNSUPPORTED, "poisson2d: nx * ny > 26000");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    const long double PI = 3.141592653589793238462643383279502884L;
+    auto lam = [](long double th) { return 30.0L - 32.0L * cosl(th) + 2.0L * cosl(2.0L * th); };
+    std::vector<long double> lx(nx), ly(ny), Sx(nx), Sy(ny);
+    for (int p = 0; p < nx; ++p) {
+        const long double th = 2.0L * PI * p / nx;
+        lx[p] = lam(th) / ((long double)dx * dx);
+        Sx[p] = (16.0L * sinl(th) - 2.0L * sinl(2.0L * th)) / dx;
+    }
+    for (int q = 0; q < ny; ++q) {
+        const long double th = 2.0L * PI * q / ny;
+        ly[q] = lam(th) / ((long double)dy * dy);
+        Sy[q] = (16.0L * sinl(th) - 2.0L * sinl(2.0L * th)) / dy;
+    }
+    auto cs = [&](int k, int n, bool s) { const long double th = 2.0L * PI * (long double)k / n; return s ? sinl(th) : cosl(th); };
+    // T(p, n) = sum_q cos(th_q n) / Lambda,  U(p, n) = sum_q S_y(q) sin(th_q n) / Lambda
+    std::vector<long double> T((size_t)nx * ny, 0.0L), U((size_t)nx * ny, 0.0L);
+    for (int p = 0; p < nx; ++p)
+        for (int q = 0; q < ny; ++q) {
+            if (p == 0 && q == 0) continue;
+            const long double il = 1.0L / (lx[p] + ly[q]);
+            for (int n = 0; n < ny; ++n) {
+                const int kq = (int)(((int64_t)q * n) % ny);
+                T[(size_t)p * ny + n] += il * cs(kq, ny, false);
+                U[(size_t)p * ny + n] += il * Sy[q] * cs(kq, ny, true);
+            }
+        }
+    std::vector<double> gx((size_t)nx * ny), gy((size_t)nx * ny);
+    const long double N = (long double)nx * ny;
+    for (int m = 0; m < nx; ++m)
+        for (int n = 0; n < ny; ++n) {
+            long double ax = 0.0L, ay = 0.0L;
+            for (int p = 0; p < nx; ++p) {
+                const int kp = (int)(((int64_t)p * m) % nx);
+                ax += Sx[p] * cs(kp, nx, true) * T[(size_t)p * ny + n];
+                ay += cs(kp, nx, false) * U[(size_t)p * ny + n];
+            }
+            gx[(size_t)m * ny + n] = (double)(ax / N);
+            gy[(size_t)m * ny + n] = (double)(ay / N);
+        }
+    vlasov_poisson2d* P = new vlasov_poisson2d();
+    P->nx = nx; P->ny = ny; P->dx = dx; P->dy = dy;
+    P->stream = (cudaStream_t)cuda_stream;
+    int rc;
+    if ((rc = upload(&P->d_gx, gx, P->stream)) || (rc = upload(&P->d_gy, gy, P->stream))) {
+        vk::dfree(P->d_gx, P->stream);
+        vk::dfree(P->d_gy, P->stream);
+        delete P;
+        return rc;
+    }
+    cudaError_t e = cudaStreamSynchronize(P->stream);
+    if (e != cudaSuccess) {
+        vk::dfree(P->d_gx, P->stream); vk::dfree(P->d_gy, P->stream);
+        delete P;
+        return vk::cuda_check(e, "poisson2d upload");
+    }
+    *out = P;
+    return VLASOV_OK;
+}
+
+int vlasov_poisson2d_solve(const vlasov_poisson2d* P, const double* rho, double* E) {
+    if (!P || !rho || !E) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_poisson2d(P, rho, E);
+}
+
+int vlasov_poisson2d_destroy(vlasov_poisson2d* P) {
+    if (!P) return VLASOV_OK;
+    vk::dfree(P->d_gx, P->stream);
+    vk::dfree(P->d_gy, P->stream);
+    delete P;
+    return VLASOV_OK;
+}
+
 int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisson** out) {
     if (!out) return vk::fail(VLASOV_EINVAL, "null argument");
     *out = nullptr;

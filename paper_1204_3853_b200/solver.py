@@ -141,18 +141,24 @@ class UniformVlasov1D:
 
 
 class UniformVlasov2D:
-    """Uniform 2D+2V level (BASELINE.json C5) with a prescribed configuration-space field
-    E(x, y) injected from a 2D mesh.  Per stage s = 1..4 one fused stage kernel
-    (in-kernel periodic x, y and characteristic vx, vy ghosts with E_bc = E, since a prescribed
-    field is its own previous constraint evaluation) whose epilogue writes per-(vx line, vy tile)
-    moment partials, and a tiny kernel summing them in a fixed order into rho(x, y)
-    (the 4D -> 2D reduction, P:295-297 / P:1061-1072)."""
+    """Uniform 2D+2V level.  field="prescribed" (BASELINE.json C5): a prescribed configuration-space
+    field E(x, y) injected from a 2D mesh, its own previous constraint evaluation, so
+    E_bc = E.  field="poisson" (N3, C5P): the self-consistent field of the 2D periodic Poisson
+    problem (reading #32), re-evaluated at every predictor state (Alg.5).
+    Per stage s = 1..4: the velocity ghost frame of f_s (characteristic condition with E_bc:
+    E_{s-1}, or E(f_n) = E_1 at s = 1, reading #6b), one fused stage kernel whose epilogue writes
+    per-(vx line, vy tile) moment partials, a tiny kernel summing them in a fixed order into
+    rho(x, y) (the 4D -> 2D reduction, P:295-297 / P:1061-1072), and with field="poisson" the 2D
+    field solve E(f_{s+1}) = -grad phi(rho) (vlasov_poisson2d_solve)."""
 
-    def __init__(self, ncells, lower, dx, boxes, f0v: np.ndarray, E_mesh: np.ndarray, recon: int = CENTERED4,
-                 stream: Optional[torch.cuda.Stream] = None):
+    def __init__(self, ncells, lower, dx, boxes, f0v: np.ndarray, E_mesh: Optional[np.ndarray] = None,
+                 recon: int = CENTERED4, stream: Optional[torch.cuda.Stream] = None, field: str = "prescribed"):
         self.stream = stream or torch.cuda.Stream()
         self.ncells = tuple(ncells)
         self.recon = recon
+        self.field = field
+        if field not in ("prescribed", "poisson"):
+            raise ValueError(field)
         with torch.cuda.stream(self.stream):
             self.level = api.Level(4, ncells, lower, dx, (1, 1, 1, 1), boxes, stream=self.stream)
             if self.level.info.nblocks != 1:
@@ -161,11 +167,16 @@ class UniformVlasov2D:
             self.B = self.level.field()
             self.C = self.level.field()
             self.U = self.level.field()
-            self.E = self.level.efield()
-            Em = torch.as_tensor(np.ascontiguousarray(E_mesh), dtype=torch.float64).cuda()
-            api.vlasov_inject_field(self.level.h, Em, E_mesh.shape[1:], self.E)
             self.rho = torch.zeros(ncells[0] * ncells[1], dtype=torch.float64, device="cuda")
             self.f0v = torch.as_tensor(np.ascontiguousarray(f0v), dtype=torch.float64).cuda()
+            if field == "prescribed":
+                self.E = self.level.efield()
+                Em = torch.as_tensor(np.ascontiguousarray(E_mesh), dtype=torch.float64).cuda()
+                api.vlasov_inject_field(self.level.h, Em, E_mesh.shape[1:], self.E)
+            else:
+                self.poisson = api.Poisson2D(ncells[0], ncells[1], dx[0], dx[1], self.stream)
+                self.Es = [self.level.efield(), self.level.efield()]
+                self.cur = 0                       # Es[cur] holds E(f_s) of the next stage
         self.stream.synchronize()
         self.graph = None
 
@@ -173,6 +184,9 @@ class UniformVlasov2D:
         with torch.cuda.stream(self.stream):
             self.level.set_domain(self.A, f_full)
             api.vlasov_reduce_moment([self.level.h], [self.A], self.rho)
+            if self.field == "poisson":
+                self.cur = 0
+                self.poisson.solve(self.rho, self.Es[0])       # E(f_0), the first evaluation (Alg.5)
         self.stream.synchronize()
 
     def get_state(self) -> np.ndarray:
@@ -183,17 +197,30 @@ class UniformVlasov2D:
         self.stream.synchronize()
         return self.rho.cpu().numpy().reshape(self.ncells[0], self.ncells[1])
 
+    def field_state(self) -> np.ndarray:
+        """E(f_n) (field="poisson"): (2, nx, ny) interior values of the last constraint evaluation."""
+        self.stream.synchronize()
+        nx, ny = self.ncells[:2]
+        return self.Es[self.cur].view(2, nx + 4, ny + 4)[:, 2:-2, 2:-2].cpu().numpy()
+
     def stage_launch(self, s, dt):
         A, B, C = self.A, self.B, self.C
         f_s, f_next = {1: (A, B), 2: (B, C), 3: (C, B), 4: (B, A)}[s]
-        api.vlasov_rk4_stage(self.level.h, s, dt, A, f_s, self.U, f_next, self.E, self.E, self.f0v, self.recon,
-                             self.rho)
+        if self.field == "prescribed":
+            E, E_bc = self.E, self.E
+        else:
+            E = self.Es[self.cur]
+            E_bc = E if s == 1 else self.Es[1 - self.cur]  # stage 1: E(f_n) (reading #6b)
+        api.vlasov_rk4_stage(self.level.h, s, dt, A, f_s, self.U, f_next, E, E_bc, self.f0v, self.recon, self.rho)
 
     def field_launch(self, s):
-        pass                      # prescribed field: nothing to solve
+        if self.field == "poisson":                        # E(f_{s+1}) from the fused moment
+            self.poisson.solve(self.rho, self.Es[1 - self.cur])
+            self.cur = 1 - self.cur
 
     def _stage(self, s, dt):
         self.stage_launch(s, dt)
+        self.field_launch(s)
 
     def step(self, dt: float):
         with torch.cuda.stream(self.stream):
@@ -216,4 +243,5 @@ class UniformVlasov2D:
             self.graph.replay()
 
     def launches_per_step(self) -> int:
-        return 4 * 2              # stage kernel + moment finish per stage
+        # velocity ghost frame + stage kernel + moment finish (+ 2D field solve) per stage
+        return 4 * (3 if self.field == "prescribed" else 4)
