@@ -317,6 +317,12 @@ int vlasov_next_dt(const vlasov_level* const* levels, int32_t nlev, const double
  * vlasov_poisson2d_solve: rho (device, nx ny row-major [x][y]) -> E (device, the 2D level field
  *   layout [2][(nx + 4)(ny + 4)]: component, then ghosted x, ghosted y; the 2 periodic ghost
  *   layers are written too); one launch on the plan's stream; deterministic.               */
+/* vlasov_inject_field_ghosted: as vlasov_inject_field for a 2D+2V level, from a finest field in the
+ * ghosted level layout [2][(n_finest[0] + 4)(n_finest[1] + 4)] (the output of
+ * vlasov_poisson2d_solve): E_lvl (ghosted, periodic ghosts written) = mean over the R_x x R_y
+ * finest cells of each level cell.                                 */
+int vlasov_inject_field_ghosted(vlasov_level* level, const double* E_finest, const int32_t n_finest[2],
+                                double* E_lvl);
 typedef struct vlasov_poisson2d vlasov_poisson2d;
 int vlasov_poisson2d_create(int32_t nx, int32_t ny, double dx, double dy, void* cuda_stream,
                             vlasov_poisson2d** out);

@@ -77,6 +77,7 @@ _SIGS = {
     "vlasov_poisson_create": (I32, [I32, D, P, C.POINTER(P)]),
     "vlasov_poisson_solve": (I32, [P, P, P, P, I32]),
     "vlasov_poisson_destroy": (I32, [P]),
+    "vlasov_inject_field_ghosted": (I32, [P, P, PI32, P]),
     "vlasov_poisson2d_create": (I32, [I32, I32, D, D, P, C.POINTER(P)]),
     "vlasov_poisson2d_solve": (I32, [P, P, P]),
     "vlasov_poisson2d_destroy": (I32, [P]),

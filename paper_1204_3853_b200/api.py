@@ -20,7 +20,7 @@ __all__ = [
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
     "vlasov_level_fill_from", "vlasov_absmax", "vlasov_next_dt", "vlasov_poisson2d_create",
-    "vlasov_poisson2d_solve", "Poisson2D", "vlasov_device_ok", "vlasov_last_error",
+    "vlasov_poisson2d_solve", "Poisson2D", "vlasov_inject_field_ghosted", "vlasov_device_ok", "vlasov_last_error",
     "vlasov_level_set_moment_base", "vlasov_level_set_velocity_faces", "vlasov_vslab_pack", "vlasov_vslab_unpack", "vlasov_reduce_current",
 ]
 
@@ -391,3 +391,8 @@ class Poisson2D:
                 self.h = None
         except Exception:
             pass
+
+
+def vlasov_inject_field_ghosted(h, E_finest, n_finest, E_lvl):
+    n = (C.c_int32 * 2)(*n_finest)
+    return check(lib.vlasov_inject_field_ghosted(h, _ptr(E_finest), n, _ptr(E_lvl)))

@@ -155,7 +155,7 @@ int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest
 
 // 2D configuration space, C = 2 components: El[c][(i+2)*(ny+4) + (k+2)] = mean over Rx x Ry.
 __global__ void k_inject_2d(const double* __restrict__ Ef, int nfx, int nfy, int Rx, int Ry, int nx,
-                            int ny, double* __restrict__ El) {
+                            int ny, double* __restrict__ El, int gin) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int nxg = nx + 4, nyg = ny + 4;
     if (t >= 2 * nxg * nyg) return;
@@ -166,16 +166,17 @@ __global__ void k_inject_2d(const double* __restrict__ Ef, int nfx, int nfy, int
     double s = 0.0;
     for (int a = 0; a < Rx; ++a)
         for (int b = 0; b < Ry; ++b)
-            s += Ef[(int64_t)c * nfx * nfy + (int64_t)(i * Rx + a) * nfy + (k * Ry + b)];
+            s += Ef[(int64_t)c * (nfx + 2 * gin) * (nfy + 2 * gin) + (int64_t)(i * Rx + a + gin) * (nfy + 2 * gin) +
+                    (k * Ry + b + gin)];
     El[t] = (Rx * Ry == 1) ? s : s / (double)(Rx * Ry);
 }
 
-int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest, double* E_lvl) {
+int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest, double* E_lvl, int gin) {
     const int nx = L->dom[0], ny = L->dom[1];
     if (n_finest[0] % nx || n_finest[1] % ny) return fail(VLASOV_EINVAL, "inject: size mismatch");
     const int tot = 2 * (nx + 4) * (ny + 4);
     k_inject_2d<<<(tot + 255) / 256, 256, 0, L->stream>>>(E_finest, n_finest[0], n_finest[1],
-                                                            n_finest[0] / nx, n_finest[1] / ny, nx, ny, E_lvl);
+                                                            n_finest[0] / nx, n_finest[1] / ny, nx, ny, E_lvl, gin);
     VK_LAUNCH("k_inject_2d");
     return VLASOV_OK;
 }

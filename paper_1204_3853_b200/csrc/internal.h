@@ -124,6 +124,37 @@ struct AvgTask {              // one covered coarse cell (reading #14
     int32_t pad;
 };
 
+// ---- 2D+2V hierarchies (NEXT row N3) ----
+struct PhysTask4 {            // characteristic velocity BC of one 2D+2V column side (reading #6)
+    int64_t cell0;            // boundary cell (velocity index 0 or n-1 along vd) in the level array
+    int32_t stride;           // level-array stride along vd (doubles)
+    int32_t e_idx;            // level E array index: component vd-2, wrapped (x, y) + 2 ghosts
+    int32_t p_idx;            // f0v index of the first ghost layer (vd index -1 or n)
+    int16_t side;             // 0 low, 1 high
+    int16_t pstep;            // f0v stride along vd
+};
+struct Red4Col {              // one grown (x, y) column of one 4D Alg.8 sub-patch
+    int64_t addr;             // index of the column's first velocity cell (lo_vx, lo_vy)
+    int32_t nvx, nvy;         // the sub-patch's velocity extent
+    int32_t s2;               // vx stride of the patch's block
+    int32_t level;
+};
+struct Red4Contrib {          // one refined 2D partial sum landing on one finest (x, y) cell
+    int64_t cs;               // column (x_c - 2, y_c - 2) of the sub-patch's grown grid
+    int32_t ystride;          // columns per grown x row (n_y of the sub-patch + 4)
+    int32_t pad;
+    double dvv;               // dvx dvy of the sub-patch's level (reading #13)
+    double bx[5], by[5];      // linear5 weights of the finest cell's sub-offsets (reading #12)
+};
+struct Mask4Item {            // Alg.6 4D: one finest (x, y) cell of one patch's refined footprint
+    int64_t addr;             // cell (x_c - 2, y_c - 2, lo_vx, lo_vy) of the patch
+    int64_t mask;             // patch-mask offset of (x_c, y_c, 0, 0)
+    int32_t s0, s1, s2;       // block strides of x, y, vx
+    int32_t nvx, nvy, level;
+    int32_t mstride0, mstride1;   // mask strides of x, y (nvx nvy ny, nvx nvy)
+    int32_t wx, wy;           // offsets of the 5 linear5 weights (x, y) in the weight table
+};
+
 constexpr int MAXLEV = 8;     // levels of one hierarchy handled by the reduction
 struct RedPlan {              // Alg.8 sub-patch reduction plan (built on the host, level.cpp)
     std::vector<uint64_t> uids;   // the hierarchy it was built for
@@ -158,6 +189,34 @@ struct MaskPlan {             // Alg.6 Mask Reduction plan (comparator of Alg.8,
     double* d_dv = nullptr;       // dv of the contribution's level
 };
 void free_mask_plan(MaskPlan* p);
+struct RedPlan4 {             // 4D -> 2D Alg.8 plan (N3)
+    std::vector<uint64_t> uids;
+    cudaStream_t st = nullptr;
+    int nxf = 0, nyf = 0;
+    int64_t ncols = 0, ncontrib = 0;
+    Red4Col* d_cols = nullptr;
+    double* d_colsum = nullptr;
+    Red4Contrib* d_contrib = nullptr;
+    int32_t* d_off = nullptr;     // CSR over finest (x, y) [nxf nyf + 1]
+};
+struct MaskPlan4 {            // 4D -> 2D Alg.6 plan (N3 comparator)
+    std::vector<uint64_t> uids;
+    cudaStream_t st = nullptr;
+    int nxf = 0, nyf = 0;
+    int64_t nitems = 0;
+    Mask4Item* d_items = nullptr;
+    uint8_t* d_mask = nullptr;    // mu per patch cell (1: not covered by the next finer level)
+    double* d_w = nullptr;        // linear5 weight table
+    double* d_part = nullptr;     // per-item partial sums
+    double* d_dvv = nullptr;      // dvx dvy per item
+    int32_t* d_off = nullptr;     // CSR over finest (x, y)
+    int32_t* d_idx = nullptr;     // item index per contribution
+};
+void free_red_plan4(RedPlan4* p);
+void free_mask_plan4(MaskPlan4* p);
+int launch_reduce_subpatch4(const RedPlan4* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
+int launch_reduce_mask4(const MaskPlan4* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
+int launch_fill4(vlasov_level* L, double* f, const double* f_coarse, const double* E_bc, const double* f0v, int interp);
 int launch_reduce_mask(const MaskPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
 }  // namespace vk
 
@@ -211,6 +270,12 @@ struct vlasov_level {
     // Alg.8 plan cached on the finest level of the hierarchy it was built for
     mutable vk::RedPlan* red_plan = nullptr;
     mutable vk::MaskPlan* mask_plan = nullptr;
+    mutable vk::RedPlan4* red_plan4 = nullptr;
+    mutable vk::MaskPlan4* mask_plan4 = nullptr;
+    // 2D+2V multi-patch levels (N3): velocity BC tasks, v_x pass first
+    vk::PhysTask4* d_phys4 = nullptr;
+    int64_t n_phys4[2] = {0, 0};
+    bool ghost4_built = false;            // task lists of a 2D+2V level (built lazily for a single block)
     // 2D+2V
     int64_t e_doubles = 0;
     int strips2 = 1;                      // x strips of the 2D+2V stage kernel
@@ -255,8 +320,7 @@ int launch_moment_direct(const vlasov_level* L, const double* f, double* rho, do
                          int accumulate = 0);
 int launch_poisson(vlasov_poisson* P, const double* rho, double* phi, double* E, int ghost);
 int launch_inject_1d(const vlasov_level* L, const double* E_finest, int n_finest, double* E_lvl, double scale = 1.0);
-int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest,
-                     double* E_lvl);
+int launch_inject_2d(const vlasov_level* L, const double* E_finest, const int32_t* n_finest, double* E_lvl, int gin = 0);
 int linear5_weights(int R, double* out /* R*5 */);
 int launch_absmax(const double* x, int64_t n, double* out, cudaStream_t st);
 int launch_vslab(const vlasov_level* L, double* f, double* lo, double* hi, bool pack);

@@ -189,6 +189,9 @@ void free_level(vlasov_level* L) {
     vk::dfree(L->d_tickets, L->stream);
     vk::dfree(L->d_rawtags, L->stream);
     vk::dfree(L->d_scalar, L->stream);
+    vk::dfree(L->d_phys4, L->stream);
+    vk::free_red_plan4(L->red_plan4);
+    vk::free_mask_plan4(L->mask_plan4);
     delete L;
 }
 
@@ -483,6 +486,232 @@ int build_ghost_tasks(vlasov_level* L, const vlasov_level* C, std::vector<int64_
             }
         }
     }
+    return VLASOV_OK;
+}
+
+std::vector<Box> subpatches_of(const vlasov_level* const* levels, int nlev, int li, int patch);
+
+// Characteristic velocity condition of a 2D+2V multi-patch level (reading #6): for each patch
+// touching a velocity boundary, one task per column side, v_x pass first (columns over the whole
+// ghosted extent of x, y, v_y), then v_y (over the ghosted x, y, v_x), as the oracle (amr4).
+int build_phys4_tasks(const vlasov_level* L, std::vector<vk::PhysTask4>& tasks, int64_t counts[2]) {
+    counts[0] = counts[1] = 0;
+    const int nyg = L->dom[1] + 4, nvyg = L->dom[3] + 4;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int vd = 2 + pass, od = 5 - vd;                    // the other velocity dim
+        for (size_t b = 0; b < L->blocks.size(); ++b) {
+            const Box& B = L->blocks[b];
+            const int n = vk::box_ncells_dim(B, vd);
+            const int dlo = B.lo[vd], dhi = L->dom[vd] - 1 - B.hi[vd];
+            if ((dlo > 0 && dlo < vk::G) || (dhi > 0 && dhi < vk::G))
+                return vk::fail(VLASOV_EINVAL, "2D+2V: a patch must touch the velocity boundary or stay >= 2 cells from it");
+            for (int side = 0; side < 2; ++side) {
+                if (side == 0 ? dlo != 0 : dhi != 0) continue;
+                if (n < 4) return vk::fail(VLASOV_EINVAL, "blocks touching a velocity boundary need >= 4 cells along it");
+                for (int x = B.lo[0] - vk::G; x <= B.hi[0] + vk::G; ++x)
+                    for (int y = B.lo[1] - vk::G; y <= B.hi[1] + vk::G; ++y)
+                        for (int o = B.lo[od] - vk::G; o <= B.hi[od] + vk::G; ++o) {
+                            int c[4] = {x, y, 0, 0};
+                            c[vd] = side == 0 ? 0 : L->dom[vd] - 1;
+                            c[od] = o;
+                            vk::PhysTask4 t;
+                            t.cell0 = cell_addr(L, (int)b, c);
+                            t.stride = (int32_t)L->block_str[b][vd];
+                            t.e_idx = (int32_t)((int64_t)pass * (L->dom[0] + 4) * nyg +
+                                                (int64_t)(wrap(x, L->dom[0]) + 2) * nyg + (wrap(y, L->dom[1]) + 2));
+                            int pv[2];                            // f0v coordinates (vx, vy) of the first ghost layer
+                            pv[vd - 2] = side == 0 ? -1 : L->dom[vd];
+                            pv[od - 2] = o;
+                            t.p_idx = (pv[0] + 2) * nvyg + (pv[1] + 2);
+                            t.pstep = (int16_t)(vd == 2 ? nvyg : 1);
+                            t.side = (int16_t)side;
+                            tasks.push_back(t);
+                        }
+            }
+        }
+        counts[pass] = (int64_t)tasks.size() - (pass ? counts[0] : 0);
+    }
+    return VLASOV_OK;
+}
+
+// Alg.8 Sub-Patch Reduction plan of a 2D+2V hierarchy (N3): grown (x, y) columns of every
+// sub-patch (Alg.7) and, per finest (x, y) cell, its refined contributions in (level, patch,
+// sub-patch) order with the linear5 weights of its sub-offsets
+int build_red_plan4(const vlasov_level* const* levels, int nlev, vk::RedPlan4** out) {
+    *out = nullptr;
+    const vlasov_level* Lf = levels[nlev - 1];
+    const int nxf = Lf->dom[0], nyf = Lf->dom[1];
+    std::vector<vk::Red4Col> cols;
+    std::vector<std::vector<vk::Red4Contrib>> per((size_t)nxf * nyf);
+    for (int l = 0; l < nlev; ++l) {
+        const vlasov_level* L = levels[l];
+        if (L->ndim != 4) return vk::fail(VLASOV_EINVAL, "reduce_moment: mixed 1D+1V / 2D+2V levels");
+        if (nxf % L->dom[0] || nyf % L->dom[1]) return vk::fail(VLASOV_EINVAL, "finest (x, y) resolution not a multiple of a level's");
+        if (l > 0 && (L->coarser != levels[l - 1] || L->coarser_uid != levels[l - 1]->uid))
+            return vk::fail(VLASOV_ESTALE, "reduce_moment: levels are not a hierarchy (coarser mismatch)");
+        const int Rx = nxf / L->dom[0], Ry = nyf / L->dom[1];
+        if (Rx > vk::MAXR * vk::MAXR || Ry > vk::MAXR * vk::MAXR) return vk::fail(VLASOV_EUNSUPPORTED, "ratio to the finest level too large");
+        std::vector<double> wx((size_t)Rx * 5), wy((size_t)Ry * 5);
+        vk::linear5_weights(Rx, wx.data());
+        vk::linear5_weights(Ry, wy.data());
+        for (size_t p = 0; p < L->boxes.size(); ++p) {
+            const int blk = L->patch_block[p];
+            for (const Box& sp : subpatches_of(levels, nlev, l, (int)p)) {
+                const int64_t base = (int64_t)cols.size();
+                const int nxs = vk::box_ncells_dim(sp, 0), nys = vk::box_ncells_dim(sp, 1);
+                for (int a = 0; a < nxs + 2 * vk::G; ++a)
+                    for (int c = 0; c < nys + 2 * vk::G; ++c) {
+                        int cc[4] = {sp.lo[0] - vk::G + a, sp.lo[1] - vk::G + c, sp.lo[2], sp.lo[3]};
+                        vk::Red4Col rc;
+                        rc.addr = cell_addr(L, blk, cc);
+                        rc.nvx = vk::box_ncells_dim(sp, 2);
+                        rc.nvy = vk::box_ncells_dim(sp, 3);
+                        rc.s2 = (int32_t)L->block_str[blk][2];
+                        rc.level = l;
+                        cols.push_back(rc);
+                    }
+                for (int xc = sp.lo[0]; xc <= sp.hi[0]; ++xc)
+                    for (int yc = sp.lo[1]; yc <= sp.hi[1]; ++yc)
+                        for (int sx = 0; sx < Rx; ++sx)
+                            for (int sy = 0; sy < Ry; ++sy) {
+                                vk::Red4Contrib k;
+                                k.cs = base + (int64_t)(xc - sp.lo[0]) * (nys + 2 * vk::G) + (yc - sp.lo[1]);
+                                k.ystride = nys + 2 * vk::G;
+                                k.pad = 0;
+                                k.dvv = L->h[2] * L->h[3];
+                                for (int j = 0; j < 5; ++j) {
+                                    k.bx[j] = wx[(size_t)sx * 5 + j];
+                                    k.by[j] = wy[(size_t)sy * 5 + j];
+                                }
+                                per[(size_t)(xc * Rx + sx) * nyf + (yc * Ry + sy)].push_back(k);
+                            }
+            }
+        }
+    }
+    std::vector<vk::Red4Contrib> con;
+    std::vector<int32_t> off((size_t)nxf * nyf + 1, 0);
+    for (size_t c = 0; c < per.size(); ++c) {
+        off[c] = (int32_t)con.size();
+        con.insert(con.end(), per[c].begin(), per[c].end());
+    }
+    off[per.size()] = (int32_t)con.size();
+    vk::RedPlan4* P = new vk::RedPlan4();
+    P->st = Lf->stream;
+    for (int l = 0; l < nlev; ++l) P->uids.push_back(levels[l]->uid);
+    P->nxf = nxf;
+    P->nyf = nyf;
+    P->ncols = (int64_t)cols.size();
+    P->ncontrib = (int64_t)con.size();
+    int rc;
+    if ((rc = upload(&P->d_cols, cols, P->st)) || (rc = upload(&P->d_contrib, con, P->st)) ||
+        (rc = upload(&P->d_off, off, P->st))) {
+        vk::free_red_plan4(P);
+        return rc;
+    }
+    if (!cols.empty()) VK_CUDA(cudaMallocAsync((void**)&P->d_colsum, sizeof(double) * cols.size(), P->st));
+    cudaError_t e = cudaStreamSynchronize(P->st);
+    if (e != cudaSuccess) { vk::free_red_plan4(P); return vk::cuda_check(e, "reduction plan upload"); }
+    *out = P;
+    return VLASOV_OK;
+}
+
+// Alg.6 Mask Reduction plan of a 2D+2V hierarchy (N3 comparator): one item per (patch, finest
+// (x, y) cell of its refined footprint); mask per patch cell (0 where the next finer level covers)
+int build_mask_plan4(const vlasov_level* const* levels, int nlev, vk::MaskPlan4** out) {
+    *out = nullptr;
+    const vlasov_level* Lf = levels[nlev - 1];
+    const int nxf = Lf->dom[0], nyf = Lf->dom[1];
+    std::vector<vk::Mask4Item> items;
+    std::vector<uint8_t> mask;
+    std::vector<double> w;
+    std::map<int, int> woff;
+    std::vector<std::vector<std::pair<int32_t, double>>> per((size_t)nxf * nyf);
+    auto weights = [&](int R) {
+        if (!woff.count(R)) {
+            woff[R] = (int)w.size();
+            std::vector<double> b((size_t)R * 5);
+            vk::linear5_weights(R, b.data());
+            w.insert(w.end(), b.begin(), b.end());
+        }
+        return woff[R];
+    };
+    for (int l = 0; l < nlev; ++l) {
+        const vlasov_level* L = levels[l];
+        if (L->ndim != 4) return vk::fail(VLASOV_EINVAL, "reduce_moment_mask: mixed 1D+1V / 2D+2V levels");
+        if (nxf % L->dom[0] || nyf % L->dom[1]) return vk::fail(VLASOV_EINVAL, "finest (x, y) resolution not a multiple of a level's");
+        if (l > 0 && (L->coarser != levels[l - 1] || L->coarser_uid != levels[l - 1]->uid))
+            return vk::fail(VLASOV_ESTALE, "reduce_moment_mask: levels are not a hierarchy (coarser mismatch)");
+        const int Rx = nxf / L->dom[0], Ry = nyf / L->dom[1];
+        if (Rx > vk::MAXR || Ry > vk::MAXR) return vk::fail(VLASOV_EUNSUPPORTED, "mask reduction: ratio to the finest level > 16");
+        const int wx0 = weights(Rx), wy0 = weights(Ry);
+        int rr[4] = {1, 1, 1, 1};
+        if (l + 1 < nlev)
+            for (int d = 0; d < 4; ++d) rr[d] = levels[l + 1]->ratio[d] / L->ratio[d];
+        for (size_t p = 0; p < L->boxes.size(); ++p) {
+            const Box& b = L->boxes[p];
+            const int blk = L->patch_block[p];
+            int n[4];
+            for (int d = 0; d < 4; ++d) n[d] = vk::box_ncells_dim(b, d);
+            const int64_t moff = (int64_t)mask.size();
+            std::vector<uint8_t> mu((size_t)n[0] * n[1] * n[2] * n[3], 1);
+            if (l + 1 < nlev)
+                for (const Box& fb : levels[l + 1]->boxes) {
+                    const Box cb = vk::box_intersect(vk::box_coarsen(fb, rr, 4), b, 4);
+                    if (vk::box_empty(cb, 4)) continue;
+                    for_each_cell(cb, 4, [&](const int* c) {
+                        mu[(((size_t)(c[0] - b.lo[0]) * n[1] + (c[1] - b.lo[1])) * n[2] + (c[2] - b.lo[2])) * n[3] +
+                           (c[3] - b.lo[3])] = 0;
+                    });
+                }
+            mask.insert(mask.end(), mu.begin(), mu.end());
+            for (int xc = b.lo[0]; xc <= b.hi[0]; ++xc)
+                for (int yc = b.lo[1]; yc <= b.hi[1]; ++yc)
+                    for (int sx = 0; sx < Rx; ++sx)
+                        for (int sy = 0; sy < Ry; ++sy) {
+                            vk::Mask4Item it;
+                            int cc[4] = {xc - 2, yc - 2, b.lo[2], b.lo[3]};
+                            it.addr = cell_addr(L, blk, cc);
+                            it.mask = moff + ((int64_t)(xc - b.lo[0]) * n[1] + (yc - b.lo[1])) * n[2] * n[3];
+                            it.s0 = (int32_t)L->block_str[blk][0];
+                            it.s1 = (int32_t)L->block_str[blk][1];
+                            it.s2 = (int32_t)L->block_str[blk][2];
+                            it.nvx = n[2];
+                            it.nvy = n[3];
+                            it.level = l;
+                            it.mstride0 = n[1] * n[2] * n[3];
+                            it.mstride1 = n[2] * n[3];
+                            it.wx = wx0 + 5 * sx;
+                            it.wy = wy0 + 5 * sy;
+                            per[(size_t)(xc * Rx + sx) * nyf + (yc * Ry + sy)].push_back(
+                                {(int32_t)items.size(), L->h[2] * L->h[3]});
+                            items.push_back(it);
+                        }
+        }
+    }
+    std::vector<int32_t> off(per.size() + 1, 0), idx;
+    std::vector<double> dvv;
+    for (size_t c = 0; c < per.size(); ++c) {
+        off[c] = (int32_t)idx.size();
+        for (auto& pr : per[c]) { idx.push_back(pr.first); dvv.push_back(pr.second); }
+    }
+    off[per.size()] = (int32_t)idx.size();
+    vk::MaskPlan4* P = new vk::MaskPlan4();
+    P->st = Lf->stream;
+    for (int l = 0; l < nlev; ++l) P->uids.push_back(levels[l]->uid);
+    P->nxf = nxf;
+    P->nyf = nyf;
+    P->nitems = (int64_t)items.size();
+    int rc;
+    if ((rc = upload(&P->d_items, items, P->st)) || (rc = upload(&P->d_mask, mask, P->st)) ||
+        (rc = upload(&P->d_w, w, P->st)) || (rc = upload(&P->d_dvv, dvv, P->st)) ||
+        (rc = upload(&P->d_off, off, P->st)) || (rc = upload(&P->d_idx, idx, P->st))) {
+        vk::free_mask_plan4(P);
+        return rc;
+    }
+    if (!items.empty()) VK_CUDA(cudaMallocAsync((void**)&P->d_part, sizeof(double) * items.size(), P->st));
+    cudaError_t e = cudaStreamSynchronize(P->st);
+    if (e != cudaSuccess) { vk::free_mask_plan4(P); return vk::cuda_check(e, "mask plan upload"); }
+    *out = P;
     return VLASOV_OK;
 }
 
@@ -829,16 +1058,21 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
     std::vector<int64_t> reflux_cells;
     std::vector<int32_t> reflux_off;
     std::vector<vk::AvgTask> avg;
+    std::vector<vk::PhysTask4> phys4;
     if (nd == 2) {
         rc = build_tiles_1d(L, device_ok_impl() != 0);
         if (!rc) rc = build_ghost_tasks(L, coarser, copies, cfs, phys);
         if (!rc && coarser) rc = build_amr_tasks(L, coarser, reflux, reflux_cells, reflux_off, avg);
+    } else if (!L->single_block) {
+        // 2D+2V hierarchy level (N3): one block per patch, ghost tasks (siblings / periodic
+        // images, coarse-fine) and the characteristic velocity tasks (v_x pass, then v_y pass)
+        rc = build_ghost_tasks(L, coarser, copies, cfs, phys);
+        if (!rc) rc = build_phys4_tasks(L, phys4, L->n_phys4);
+        L->ghost4_built = true;
     } else {
         // 2D+2V: uniform levels stored as one block covering the periodic domain (in-kernel
         // ghosts); the stage kernel marches along x in strips sized for about one wave
-        if (!L->single_block)
-            rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V: only levels whose boxes tile the whole domain");
-        else if (L->field_doubles >= ((int64_t)1 << 31))
+        if (L->field_doubles >= ((int64_t)1 << 31))
             rc = vk::fail(VLASOV_EUNSUPPORTED, "2D+2V: level block larger than 2^31 doubles");
         else if (L->dom[3] % 2 || L->dom[2] % 4 || L->dom[2] < 4 || L->dom[3] < 4)
             rc = vk::fail(VLASOV_EINVAL, "2D+2V: need nvx % 4 == 0, nvy even and >= 4 cells per velocity dim");
@@ -860,9 +1094,8 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
     L->n_reflux_cells = (int64_t)reflux_cells.size();
     L->n_avg = (int64_t)avg.size();
     L->avg_count = L->coarse_ratio[0] * L->coarse_ratio[1];
-    std::vector<double> b5(2 * vk::MAXR * 5, 0.0);
-    vk::linear5_weights(L->coarse_ratio[0], b5.data());
-    vk::linear5_weights(L->coarse_ratio[1], b5.data() + 5 * vk::MAXR);
+    std::vector<double> b5(4 * vk::MAXR * 5, 0.0);
+    for (int d = 0; d < nd; ++d) vk::linear5_weights(L->coarse_ratio[d], b5.data() + (size_t)d * 5 * vk::MAXR);
     if (!device_ok_impl()) {            // host metadata only (queries work, compute calls fail)
         *out = L;
         return VLASOV_OK;
@@ -884,6 +1117,7 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         (rc = upload(&L->d_tiles_narrow, L->h_tiles_narrow, L->stream)) ||
         (rc = upload(&L->d_copy, copies, L->stream)) || (rc = upload(&L->d_cf, cfs, L->stream)) ||
         (rc = upload(&L->d_phys, phys, L->stream)) || (rc = upload(&L->d_b5, b5, L->stream)) ||
+        (rc = upload(&L->d_phys4, phys4, L->stream)) ||
         (rc = upload(&L->d_reflux, reflux, L->stream)) || (rc = upload(&L->d_reflux_cells, reflux_cells, L->stream)) ||
         (rc = upload(&L->d_reflux_off, reflux_off, L->stream)) || (rc = upload(&L->d_avg, avg, L->stream))) {
         free_level(L);
@@ -1225,11 +1459,31 @@ int vlasov_regrid_boxes(const vlasov_level* L, const uint8_t* tags, const int32_
 int vlasov_fill_ghosts(vlasov_level* L, double* f, const vlasov_level* coarser, const double* f_coarse,
                        const double* E_bc, const double* f0v, int32_t interp) {
     if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
-    if (L->ndim == 4)
-        return vk::fail(VLASOV_EUNSUPPORTED, "fill_ghosts: 2D+2V levels derive their ghosts inside the stage kernel");
+    if (L->ndim == 4 && !L->ghost4_built) {
+        // a 2D+2V level stored as one block (the stage kernel derives its ghosts itself): the task
+        // lists of the ghost frame (periodic images, velocity condition) are built on first use
+        std::vector<int64_t> copies;
+        std::vector<vk::CFTask> cfs;
+        std::vector<vk::PhysTask> phys;
+        std::vector<vk::PhysTask4> phys4;
+        int rc = build_ghost_tasks(L, L->coarser, copies, cfs, phys);
+        if (!rc) rc = build_phys4_tasks(L, phys4, L->n_phys4);
+        if (!rc && device_ok_impl()) {
+            vk::dfree(L->d_copy, L->stream);
+            vk::dfree(L->d_cf, L->stream);
+            if ((rc = upload(&L->d_copy, copies, L->stream)) || (rc = upload(&L->d_cf, cfs, L->stream)) ||
+                (rc = upload(&L->d_phys4, phys4, L->stream)))
+                return rc;
+            L->n_copy = (int64_t)copies.size() / 2;
+            L->n_cf = (int64_t)cfs.size();
+        }
+        if (rc) return rc;
+        L->ghost4_built = true;
+    }
     if (L->n_cf > 0 && (coarser != L->coarser || !coarser || coarser->uid != L->coarser_uid))
         return vk::fail(VLASOV_ESTALE, "fill_ghosts: coarser level does not match the one of level_create");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    if (L->ndim == 4) return vk::launch_fill4(L, f, f_coarse, E_bc, f0v, interp);
     return vk::launch_fill(L, f, f_coarse, E_bc, f0v, interp);
 }
 
@@ -1303,6 +1557,20 @@ int vlasov_reduce_charge(const vlasov_level* const* levels, int32_t nlev, const 
         return vk::launch_moment_2d2v(levels[0], f[0], rho_finest);
     }
     const vlasov_level* Lf = levels[nlev - 1];
+    if (Lf->ndim == 4) {                            // 2D+2V hierarchy: Alg.8 4D -> 2D (N3)
+        if (q != -1.0 || base != 1.0 || accumulate)
+            return vk::fail(VLASOV_EUNSUPPORTED, "reduce_charge: 2D+2V levels compute the electron density 1 - n only");
+        bool fresh4 = Lf->red_plan4 != nullptr && (int)Lf->red_plan4->uids.size() == nlev;
+        for (int l = 0; fresh4 && l < nlev; ++l) fresh4 = Lf->red_plan4->uids[l] == levels[l]->uid;
+        if (!fresh4) {
+            vk::free_red_plan4(Lf->red_plan4);
+            Lf->red_plan4 = nullptr;
+            vk::RedPlan4* P = nullptr;
+            if (int rc = build_red_plan4(levels, nlev, &P)) return rc;
+            Lf->red_plan4 = P;
+        }
+        return vk::launch_reduce_subpatch4(Lf->red_plan4, f, nlev, rho_finest, Lf->stream);
+    }
     bool fresh = Lf->red_plan != nullptr && (int)Lf->red_plan->uids.size() == nlev;
     for (int l = 0; fresh && l < nlev; ++l) fresh = Lf->red_plan->uids[l] == levels[l]->uid;
     if (!fresh) {                                   // observer: rebuild after a regrid
@@ -1503,6 +1771,18 @@ int vlasov_reduce_moment_mask(const vlasov_level* const* levels, int32_t nlev, c
         if (!levels[l] || !f[l]) return vk::fail(VLASOV_EINVAL, "reduce_moment_mask: level / field pointer required");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     const vlasov_level* Lf = levels[nlev - 1];
+    if (Lf->ndim == 4) {                            // 2D+2V hierarchy: Alg.6 4D -> 2D (N3)
+        bool fresh4 = Lf->mask_plan4 != nullptr && (int)Lf->mask_plan4->uids.size() == nlev;
+        for (int l = 0; fresh4 && l < nlev; ++l) fresh4 = Lf->mask_plan4->uids[l] == levels[l]->uid;
+        if (!fresh4) {
+            vk::free_mask_plan4(Lf->mask_plan4);
+            Lf->mask_plan4 = nullptr;
+            vk::MaskPlan4* P = nullptr;
+            if (int rc = build_mask_plan4(levels, nlev, &P)) return rc;
+            Lf->mask_plan4 = P;
+        }
+        return vk::launch_reduce_mask4(Lf->mask_plan4, f, nlev, rho_finest, Lf->stream);
+    }
     bool fresh = Lf->mask_plan != nullptr && (int)Lf->mask_plan->uids.size() == nlev;
     for (int l = 0; fresh && l < nlev; ++l) fresh = Lf->mask_plan->uids[l] == levels[l]->uid;
     if (!fresh) {
@@ -1686,6 +1966,13 @@ int vlasov_inject_field(vlasov_level* L, const double* E_finest, const int32_t n
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (L->ndim == 2) return vk::launch_inject_1d(L, E_finest, n_finest[0], E_lvl);
     return vk::launch_inject_2d(L, E_finest, n_finest, E_lvl);
+}
+
+int vlasov_inject_field_ghosted(vlasov_level* L, const double* E_finest, const int32_t n_finest[2], double* E_lvl) {
+    if (!L || !E_finest || !n_finest || !E_lvl) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "inject_field_ghosted: 2D+2V levels");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_inject_2d(L, E_finest, n_finest, E_lvl, vk::G);
 }
 
 int vlasov_inject_field_scaled(vlasov_level* L, const double* E_finest, const int32_t n_finest[2], double scale,

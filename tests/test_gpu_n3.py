@@ -72,3 +72,97 @@ def test_c5p_graph_equals_oracle():
 def test_c5p_full_size_one_step():
     _, got, ref, _ = _c5p_run(inputs.get("C5P"), 1)
     assert relerr(got, ref) < 1e-12
+
+
+# ---------------------------------------------------------------- 2D+2V hierarchies
+from inputs.hierarchies import random_hierarchy_4d  # noqa: E402
+from oracle import amr4, boxes, interp  # noqa: E402
+from paper_1204_3853_b200 import _lib  # noqa: E402
+
+W4 = inputs.scaled(inputs.get("C5P"), (8, 8, 8, 8), (8, 8, 4, 8))
+MODE = {interp.LINEAR5: _lib.LINEAR5, interp.WENO5: _lib.WENO5}
+
+
+def _oracle_hier(rat, lb, mode=interp.LINEAR5):
+    return amr4.Hierarchy4(W4.lower, inputs.spacing(W4), W4.ncells, lb, rat,
+                           lambda r: inputs.background_profile(W4, r), interp_mode=mode)
+
+
+def _gpu_hier(rat, lb, stream):
+    levels = []
+    for r, b in zip(rat, lb):
+        levels.append(api.Level(4, W4.ncells, W4.lower, inputs.spacing(W4), r, b,
+                                coarser=levels[-1] if levels else None, stream=stream))
+    return levels
+
+
+def _setup(seed, mode=interp.LINEAR5):
+    rat, lb = random_hierarchy_4d(seed)
+    H = _oracle_hier(rat, lb, mode)
+    rng = np.random.default_rng(seed)
+    data = H.new_data()
+    for l, lvl in enumerate(H.levels):
+        for p, b in enumerate(lvl.boxes):
+            amr4._interior(data[l][p])[...] = inputs.initial_cell_averages(W4, lvl.ratio, b) * (
+                1.0 + 0.1 * rng.standard_normal(boxes.size(b)))
+    E_bc = [0.2 * rng.standard_normal((2,) + tuple(H.ncells0[d] * lvl.ratio[d] for d in range(2))) for lvl in H.levels]
+    stream = torch.cuda.Stream()
+    levels = _gpu_hier(rat, lb, stream)
+    with torch.cuda.stream(stream):
+        fs = []
+        for L, lvl_data in zip(levels, data):
+            f = L.field(0.0)
+            L.set_patches(f, [amr4._interior(a) for a in lvl_data])
+            fs.append(f)
+        Eg = [torch.as_tensor(np.stack([np.pad(E[c], 2, mode="wrap") for c in range(2)]).ravel()).cuda()
+              for E in E_bc]
+        f0v = [torch.as_tensor(inputs.background_profile(W4, lvl.ratio).ravel()).cuda() for lvl in H.levels]
+        for l, L in enumerate(levels):
+            api.vlasov_fill_ghosts(L.h, fs[l], levels[l - 1].h if l else None, fs[l - 1] if l else None, Eg[l],
+                                   f0v[l], MODE[mode])
+    stream.synchronize()
+    amr4.fill_ghosts(H, data, E_bc)
+    return H, data, levels, fs, stream
+
+
+@pytest.mark.parametrize("mode", [interp.LINEAR5, interp.WENO5])
+@pytest.mark.parametrize("seed", range(3))
+def test_fill_ghosts_4d_parity(seed, mode):
+    """Alg.2 in 4D (siblings / periodic images, coarse-fine linear5 / WENO5 from the 5^4 coarse
+    block, the characteristic v_x then v_y condition) on seeded random 2D+2V hierarchies: every
+    value of every ghosted patch against the oracle."""
+    H, data, levels, fs, _ = _setup(seed, mode)
+    for l, L in enumerate(levels):
+        for p, got in enumerate(L.get_patches(fs[l], ghost=2)):
+            ref = data[l][p]
+            np.testing.assert_allclose(got, ref, rtol=0, atol=1e-13 * np.abs(ref).max(), err_msg=f"level {l} patch {p}")
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_reductions_and_field_4d_parity(seed):
+    """4D -> 2D Alg.8 Sub-Patch and Alg.6 Mask reductions (vlasov_reduce_moment[_mask] on 2D+2V
+    hierarchies) against the oracle's, and the constraint evaluation's per-level field (2D Poisson
+    on the finest (x, y) mesh, injection to every level)."""
+    H, data, levels, fs, stream = _setup(seed)
+    NX, NY = H.ncfg_finest()
+    rho8 = torch.zeros(NX * NY, dtype=torch.float64, device="cuda")
+    rho6 = torch.zeros_like(rho8)
+    Ef = torch.zeros(2 * (NX + 4) * (NY + 4), dtype=torch.float64, device="cuda")
+    hf = H.h(len(H.levels) - 1)
+    with torch.cuda.stream(stream):
+        api.vlasov_reduce_moment([L.h for L in levels], fs, rho8)
+        api.vlasov_reduce_moment_mask([L.h for L in levels], fs, rho6)
+        P = api.Poisson2D(NX, NY, hf[0], hf[1], stream)
+        P.solve(rho8, Ef)
+        El = [L.efield() for L in levels]
+        for L, e in zip(levels, El):
+            api.vlasov_inject_field_ghosted(L.h, Ef, (NX, NY), e)
+    stream.synchronize()
+    n_ref = amr4.subpatch_moment(H, data)
+    np.testing.assert_allclose(rho8.cpu().numpy().reshape(NX, NY), 1.0 - n_ref, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(rho6.cpu().numpy().reshape(NX, NY), 1.0 - amr4.mask_moment(H, data), rtol=0, atol=1e-13)
+    E_ref, _ = amr4.constraints(H, data)
+    for l, (L, e) in enumerate(zip(levels, El)):
+        nx, ny = H.ncells0[0] * H.levels[l].ratio[0], H.ncells0[1] * H.levels[l].ratio[1]
+        got = e.view(2, nx + 4, ny + 4)[:, 2:-2, 2:-2].cpu().numpy()
+        np.testing.assert_allclose(got, E_ref[l], rtol=0, atol=1e-12 * np.abs(E_ref[-1]).max() + 1e-15)
