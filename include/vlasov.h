@@ -317,6 +317,30 @@ int vlasov_next_dt(const vlasov_level* const* levels, int32_t nlev, const double
  * vlasov_poisson2d_solve: rho (device, nx ny row-major [x][y]) -> E (device, the 2D level field
  *   layout [2][(nx + 4)(ny + 4)]: component, then ghosted x, ghosted y; the 2 periodic ghost
  *   layers are written too); one launch on the plan's stream; deterministic.               */
+/* ---- 2D+2V hierarchies in the paper's F* form (NEXT row N3; Alg.3-4) ---- *
+ * vlasov_level_face_doubles: doubles of a 2D+2V level's F* buffer (caller-owned device array):
+ *   per patch, per dim d, the face array of the patch's cells with n_d + 1 along d (row-major
+ *   x, y, v_x, v_y).
+ * vlasov_rk4_stage_fstar: stage s of Alg.3 on every patch from the ghosted predictor f_s (ghosts
+ *   filled by vlasov_fill_ghosts): the face fluxes (P:263-282 dimension by dimension, +1/48 of
+ *   reading #3), F* = b_1 F (s = 1) or F* += b_s F, and f_next = f_n + alpha_{s+1} dt k(f_s)
+ *   (interior; stages 1-3; NULL at stage 4).  E: the level's ghosted E array.  f_next must not
+ *   alias f_s.
+ * vlasov_fstar_coarsen: Alg.4 "coarsen fluxes down to level l-1": every coarse F* face lying
+ *   under a face of a patch of `fine` := the mean of the fine F* over it (reading #14; x, y
+ *   periodic images).  Call finest -> coarsest before the coarser level's update.
+ * vlasov_fstar_update: f_new = f_n + dt div(F*) on the interiors (ComputeUpdate);
+ *   f_new may alias f_n.  vlasov_average_down(fine, f_fine, f_coarse, NULL, dt) then sets the
+ *   covered coarse cells to the mean of their fine cells.                        */
+int vlasov_level_face_doubles(const vlasov_level* level, int64_t* n);
+int vlasov_rk4_stage_fstar(vlasov_level* level, int32_t stage, double dt, const double* f_n,
+                           const double* f_s, double* f_next, const double* E, int32_t recon,
+                           double* Fstar);
+int vlasov_fstar_coarsen(const vlasov_level* fine, const double* F_fine, const vlasov_level* coarse,
+                         double* F_coarse);
+int vlasov_fstar_update(vlasov_level* level, double dt, const double* f_n, const double* Fstar,
+                        double* f_new);
+
 /* vlasov_inject_field_ghosted: as vlasov_inject_field for a 2D+2V level, from a finest field in the
  * ghosted level layout [2][(n_finest[0] + 4)(n_finest[1] + 4)] (the output of
  * vlasov_poisson2d_solve): E_lvl (ghosted, periodic ghosts written) = mean over the R_x x R_y

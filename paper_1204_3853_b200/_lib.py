@@ -78,6 +78,10 @@ _SIGS = {
     "vlasov_poisson_solve": (I32, [P, P, P, P, I32]),
     "vlasov_poisson_destroy": (I32, [P]),
     "vlasov_inject_field_ghosted": (I32, [P, P, PI32, P]),
+    "vlasov_level_face_doubles": (I32, [P, PI64]),
+    "vlasov_rk4_stage_fstar": (I32, [P, I32, D, P, P, P, P, I32, P]),
+    "vlasov_fstar_coarsen": (I32, [P, P, P, P]),
+    "vlasov_fstar_update": (I32, [P, D, P, P, P]),
     "vlasov_poisson2d_create": (I32, [I32, I32, D, D, P, C.POINTER(P)]),
     "vlasov_poisson2d_solve": (I32, [P, P, P]),
     "vlasov_poisson2d_destroy": (I32, [P]),

@@ -20,7 +20,8 @@ __all__ = [
     "vlasov_poisson_create", "vlasov_poisson_solve", "vlasov_poisson_destroy", "vlasov_inject_field",
     "vlasov_flux_register_accumulate", "vlasov_average_down", "vlasov_tag_cells", "vlasov_tags_to_boxes", "vlasov_cluster_tags", "vlasov_regrid_boxes",
     "vlasov_level_fill_from", "vlasov_absmax", "vlasov_next_dt", "vlasov_poisson2d_create",
-    "vlasov_poisson2d_solve", "Poisson2D", "vlasov_inject_field_ghosted", "vlasov_device_ok", "vlasov_last_error",
+    "vlasov_poisson2d_solve", "Poisson2D", "vlasov_inject_field_ghosted", "vlasov_level_face_doubles",
+    "vlasov_rk4_stage_fstar", "vlasov_fstar_coarsen", "vlasov_fstar_update", "vlasov_device_ok", "vlasov_last_error",
     "vlasov_level_set_moment_base", "vlasov_level_set_velocity_faces", "vlasov_vslab_pack", "vlasov_vslab_unpack", "vlasov_reduce_current",
 ]
 
@@ -396,3 +397,22 @@ class Poisson2D:
 def vlasov_inject_field_ghosted(h, E_finest, n_finest, E_lvl):
     n = (C.c_int32 * 2)(*n_finest)
     return check(lib.vlasov_inject_field_ghosted(h, _ptr(E_finest), n, _ptr(E_lvl)))
+
+
+def vlasov_level_face_doubles(h):
+    n = C.c_int64()
+    check(lib.vlasov_level_face_doubles(h, C.byref(n)))
+    return n.value
+
+
+def vlasov_rk4_stage_fstar(h, stage, dt, f_n, f_s, f_next, E, recon, Fstar):
+    return check(lib.vlasov_rk4_stage_fstar(h, int(stage), float(dt), _ptr(f_n), _ptr(f_s), _ptr(f_next), _ptr(E),
+                                            int(recon), _ptr(Fstar)))
+
+
+def vlasov_fstar_coarsen(fine, F_fine, coarse, F_coarse):
+    return check(lib.vlasov_fstar_coarsen(fine, _ptr(F_fine), coarse, _ptr(F_coarse)))
+
+
+def vlasov_fstar_update(h, dt, f_n, Fstar, f_new):
+    return check(lib.vlasov_fstar_update(h, float(dt), _ptr(f_n), _ptr(Fstar), _ptr(f_new)))

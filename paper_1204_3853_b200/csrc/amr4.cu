@@ -14,6 +14,7 @@
 
 #include "internal.h"
 #include "ptx.cuh"
+#include "scheme.cuh"
 
 namespace vk {
 
@@ -290,6 +291,237 @@ void free_mask_plan4(MaskPlan4* p) {
     dfree(p->d_off, p->st);
     dfree(p->d_idx, p->st);
     delete p;
+}
+
+}  // namespace vk
+
+namespace vk {
+
+// ------------------------------------------------------------------ RK4 in the F* form (4D AMR)
+// One stage of Alg.3 on every patch of a 2D+2V level from the ghosted predictor state
+// f_s: the face fluxes of P:263-282 generalised dimension by dimension (one transverse term on
+// configuration faces, one (1/48) product term per configuration dim on velocity faces, +1/48 by
+// reading #3), F* += b_s F on every face (the paper's flux accumulation), and the next
+// predictor f_{s+1} = f_n + alpha_{s+1} dt k(f_s) (Alg.2).  One thread per cell; every
+// cell computes its low and high faces (a face is computed by both neighbours; these levels are
+// small and latency-bound).  The level update (vlasov_fstar_update), Alg.4's flux coarsening
+// (vlasov_fstar_coarsen) and average-down complete the step.
+
+template <int RECON>
+__device__ __forceinline__ double fval(const double* __restrict__ f, int64_t c, int64_t st, double upw) {
+    // face between c and c + st from the cells c - st .. c + 2 st
+    return face_avg<RECON>(f[c - st], f[c], f[c + st], f[c + 2 * st], upw);
+}
+
+struct Stage4Args {
+    const Patch4* patches;
+    int npatch;
+    const double* f_s;
+    const double* f_n;
+    double* f_next;            // nullable (stage 4)
+    const double* E;           // [2][(nx+4)(ny+4)] ghosted level field
+    double* Fstar;
+    double dt, b_s, alpha_next;
+    double h[4];
+    double vlo[2];             // lower velocity corner of the level domain
+    int nx, ny;                // level (x, y) domain, for the E array
+};
+
+template <int STAGE, int RECON>
+__global__ void k_stage4_fstar(const Stage4Args A) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const Patch4 P = A.patches[blockIdx.y];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t ncell = (int64_t)P.n[0] * P.n[1] * P.n[2] * P.n[3];
+    if (t >= ncell) return;
+    int q[4];
+    int64_t r = t;
+    q[3] = (int)(r % P.n[3]); r /= P.n[3];
+    q[2] = (int)(r % P.n[2]); r /= P.n[2];
+    q[1] = (int)(r % P.n[1]); r /= P.n[1];
+    q[0] = (int)r;
+    const int64_t s[4] = {P.s[0], P.s[1], P.s[2], 1};
+    const int64_t c = P.org + q[0] * s[0] + q[1] * s[1] + q[2] * s[2] + q[3];
+    const double* f = A.f_s;
+    const int gx = P.lo[0] + q[0], gy = P.lo[1] + q[1], gl = P.lo[2] + q[2], gm = P.lo[3] + q[3];
+    const int nyg = A.ny + 4;
+    const int64_t ec = (int64_t)(A.nx + 4) * nyg;
+    auto Eat = [&](int comp, int di, int dk) { return A.E[comp * ec + (int64_t)(gx + di + 2) * nyg + (gy + dk + 2)]; };
+    auto vb = [&](int d, int j) { return A.vlo[d] + ((double)j + 0.5) * A.h[2 + d]; };
+    double F[4][2];
+    // configuration faces: x (d = 0, transverse along v_x), y (d = 1, transverse along v_y)
+    for (int d = 0; d < 2; ++d) {
+        const int vd = 2 + d;
+        const double v = vb(d, d == 0 ? gl : gm);
+        for (int side = 0; side < 2; ++side) {
+            const int64_t cf = c + (side == 0 ? -s[d] : 0);                 // face between cf and cf + s[d]
+            const double fm = fval<RECON>(f, cf, s[d], v);
+            const double fl = fval<RECON>(f, cf - s[vd], s[d], v - A.h[vd]);
+            const double fh = fval<RECON>(f, cf + s[vd], s[d], v + A.h[vd]);
+            F[d][side] = v * fm + (A.h[vd] / 24.0) * (fh - fl);
+        }
+    }
+    // velocity faces: v_x (d = 2, field E_x), v_y (d = 3, field E_y); product terms along x and y
+    for (int d = 2; d < 4; ++d) {
+        const int comp = d - 2;
+        const double e = Eat(comp, 0, 0);
+        const double cx = (1.0 / 48.0) * (Eat(comp, 1, 0) - Eat(comp, -1, 0));
+        const double cy = (1.0 / 48.0) * (Eat(comp, 0, 1) - Eat(comp, 0, -1));
+        for (int side = 0; side < 2; ++side) {
+            const int64_t cf = c + (side == 0 ? -s[d] : 0);
+            const double fm = fval<RECON>(f, cf, s[d], -e);
+            const double fxm = fval<RECON>(f, cf - s[0], s[d], -Eat(comp, -1, 0));
+            const double fxp = fval<RECON>(f, cf + s[0], s[d], -Eat(comp, 1, 0));
+            const double fym = fval<RECON>(f, cf - s[1], s[d], -Eat(comp, 0, -1));
+            const double fyp = fval<RECON>(f, cf + s[1], s[d], -Eat(comp, 0, 1));
+            F[d][side] = e * fm + cx * (fxp - fxm) + cy * (fyp - fym);
+        }
+    }
+    double k = -(F[0][1] - F[0][0]) / A.h[0];
+    k = k + (-(F[1][1] - F[1][0]) / A.h[1]);
+    k = k + (F[2][1] - F[2][0]) / A.h[2];
+    k = k + (F[3][1] - F[3][0]) / A.h[3];
+    // F* on the faces this cell owns: its low faces, and its high faces at the patch top
+    for (int d = 0; d < 4; ++d) {
+        int nf[4] = {P.n[0], P.n[1], P.n[2], P.n[3]};
+        nf[d] += 1;
+        int64_t idx = 0;
+        for (int e = 0; e < 4; ++e) idx = idx * nf[e] + q[e];              // low face of the cell
+        double* Fd = A.Fstar + P.foff[d];
+        int64_t sd = 1;
+        for (int e = 3; e > d; --e) sd *= nf[e];                           // stride of dim d in the face array
+        if (STAGE == 1) Fd[idx] = A.b_s * F[d][0];
+        else Fd[idx] += A.b_s * F[d][0];
+        if (q[d] == P.n[d] - 1) {
+            if (STAGE == 1) Fd[idx + sd] = A.b_s * F[d][1];
+            else Fd[idx + sd] += A.b_s * F[d][1];
+        }
+    }
+    if (STAGE < 4) A.f_next[c] = A.f_n[c] + A.alpha_next * A.dt * k;
+}
+
+// f_new = f_n + dt div(F*) on every cell of the level (Alg.4 ComputeUpdate)
+__global__ void k_fstar_update(const Patch4* __restrict__ patches, const double* __restrict__ f_n,
+                               const double* __restrict__ Fstar, double4 h, double dt, double* __restrict__ f_new) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const Patch4 P = patches[blockIdx.y];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t ncell = (int64_t)P.n[0] * P.n[1] * P.n[2] * P.n[3];
+    if (t >= ncell) return;
+    int q[4];
+    int64_t r = t;
+    q[3] = (int)(r % P.n[3]); r /= P.n[3];
+    q[2] = (int)(r % P.n[2]); r /= P.n[2];
+    q[1] = (int)(r % P.n[1]); r /= P.n[1];
+    q[0] = (int)r;
+    const double hh[4] = {h.x, h.y, h.z, h.w};
+    double k = 0.0;
+    for (int d = 0; d < 4; ++d) {
+        int nf[4] = {P.n[0], P.n[1], P.n[2], P.n[3]};
+        nf[d] += 1;
+        int64_t idx = 0;
+        for (int e = 0; e < 4; ++e) idx = idx * nf[e] + q[e];
+        int64_t sd = 1;
+        for (int e = 3; e > d; --e) sd *= nf[e];
+        const double* Fd = Fstar + P.foff[d];
+        const double term = (Fd[idx + sd] - Fd[idx]) / hh[d];
+        k = d == 0 ? -term : (d < 2 ? k - term : k + term);
+    }
+    const int64_t c = P.org + q[0] * P.s[0] + q[1] * P.s[1] + q[2] * P.s[2] + q[3];
+    f_new[c] = f_n[c] + dt * k;
+}
+
+// Alg.4 "coarsen fluxes down to level l-1": every coarse F* face under a fine patch face := the
+// mean of the R^3 fine F* faces over it (reading #14)
+__global__ void k_fstar_coarsen(const FaceAvgTask* __restrict__ tasks, int64_t n, const double* __restrict__ Ff,
+                                double* __restrict__ Fc) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const FaceAvgTask T = tasks[t];
+    double s = 0.0;
+    for (int a = 0; a < T.r[0]; ++a)
+        for (int b = 0; b < T.r[1]; ++b)
+            for (int c = 0; c < T.r[2]; ++c) s += Ff[T.fine + a * T.st[0] + b * T.st[1] + c * T.st[2]];
+    Fc[T.coarse] = s / (double)(T.r[0] * T.r[1] * T.r[2]);
+}
+
+// average-down in 4D: covered coarse cell := mean of its R^4 fine cells
+__global__ void k_average_down4(const AvgTask4* __restrict__ tasks, int64_t n, const double* __restrict__ ff,
+                                double* __restrict__ fc) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const AvgTask4 T = tasks[t];
+    double s = 0.0;
+    for (int a = 0; a < T.r[0]; ++a)
+        for (int b = 0; b < T.r[1]; ++b)
+            for (int c = 0; c < T.r[2]; ++c)
+                for (int d = 0; d < T.r[3]; ++d)
+                    s += ff[T.fine + a * T.st[0] + b * T.st[1] + c * T.st[2] + d];
+    fc[T.coarse] = s / (double)(T.r[0] * T.r[1] * T.r[2] * T.r[3]);
+}
+
+template <int STAGE, int RECON>
+static int launch_s4(const Stage4Args& A, int maxcells, cudaStream_t st) {
+    VK_CUDA(launch_pdl(k_stage4_fstar<STAGE, RECON>, dim3((unsigned)((maxcells + 127) / 128), (unsigned)A.npatch),
+                       dim3(128), 0, st, A));
+    return VLASOV_OK;
+}
+
+int launch_stage4_fstar(const vlasov_level* L, int stage, double dt, const double* f_n, const double* f_s,
+                        double* f_next, const double* E, int recon, double* Fstar) {
+    static const double B[4] = {1.0 / 6.0, 1.0 / 3.0, 1.0 / 3.0, 1.0 / 6.0};
+    static const double ALPHA[4] = {0.0, 0.5, 0.5, 1.0};
+    Stage4Args A;
+    A.patches = L->d_patch4;
+    A.npatch = (int)L->boxes.size();
+    A.f_s = f_s;
+    A.f_n = f_n;
+    A.f_next = f_next;
+    A.E = E;
+    A.Fstar = Fstar;
+    A.dt = dt;
+    A.b_s = B[stage - 1];
+    A.alpha_next = stage < 4 ? ALPHA[stage] : 0.0;
+    for (int d = 0; d < 4; ++d) A.h[d] = L->h[d];
+    A.vlo[0] = L->lower[2];
+    A.vlo[1] = L->lower[3];
+    A.nx = L->dom[0];
+    A.ny = L->dom[1];
+    const int mc = L->max_patch_cells;
+    const bool up = recon == VLASOV_UPWIND;
+    switch (stage) {
+        case 1: return up ? launch_s4<1, VLASOV_UPWIND>(A, mc, L->stream) : launch_s4<1, VLASOV_CENTERED4>(A, mc, L->stream);
+        case 2: return up ? launch_s4<2, VLASOV_UPWIND>(A, mc, L->stream) : launch_s4<2, VLASOV_CENTERED4>(A, mc, L->stream);
+        case 3: return up ? launch_s4<3, VLASOV_UPWIND>(A, mc, L->stream) : launch_s4<3, VLASOV_CENTERED4>(A, mc, L->stream);
+        default: return up ? launch_s4<4, VLASOV_UPWIND>(A, mc, L->stream) : launch_s4<4, VLASOV_CENTERED4>(A, mc, L->stream);
+    }
+}
+
+int launch_fstar_update(const vlasov_level* L, double dt, const double* f_n, const double* Fstar, double* f_new) {
+    VK_CUDA(launch_pdl(k_fstar_update, dim3((unsigned)((L->max_patch_cells + 127) / 128), (unsigned)L->boxes.size()),
+                       dim3(128), 0, L->stream, (const Patch4*)L->d_patch4, f_n, Fstar,
+                       make_double4(L->h[0], L->h[1], L->h[2], L->h[3]), dt, f_new));
+    return VLASOV_OK;
+}
+
+int launch_fstar_coarsen(const vlasov_level* L, const double* F_fine, double* F_coarse) {
+    if (L->n_fcoarsen4 == 0) return VLASOV_OK;
+    VK_CUDA(launch_pdl(k_fstar_coarsen, dim3((unsigned)((L->n_fcoarsen4 + 127) / 128)), dim3(128), 0, L->stream,
+                       (const FaceAvgTask*)L->d_fcoarsen4, (int64_t)L->n_fcoarsen4, F_fine, F_coarse));
+    return VLASOV_OK;
+}
+
+int launch_average_down4(const vlasov_level* L, const double* f_fine, double* f_coarse) {
+    if (L->n_avg4 == 0) return VLASOV_OK;
+    VK_CUDA(launch_pdl(k_average_down4, dim3((unsigned)((L->n_avg4 + 127) / 128)), dim3(128), 0, L->stream,
+                       (const AvgTask4*)L->d_avg4, (int64_t)L->n_avg4, f_fine, f_coarse));
+    return VLASOV_OK;
 }
 
 }  // namespace vk

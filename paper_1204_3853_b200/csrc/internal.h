@@ -155,6 +155,23 @@ struct Mask4Item {            // Alg.6 4D: one finest (x, y) cell of one patch's
     int32_t wx, wy;           // offsets of the 5 linear5 weights (x, y) in the weight table
 };
 
+struct Patch4 {               // one patch of a 2D+2V level (N3 stepping in the F* form)
+    int64_t org;              // index of its interior cell lo in the level array
+    int64_t s[3];             // strides of x, y, v_x (v_y: 1)
+    int32_t lo[4], n[4];      // box lo and cells per dim (level index space)
+    int64_t foff[4];          // offsets of its 4 face arrays in the level's F* buffer
+};
+struct FaceAvgTask {          // Alg.4: one coarse F* face := mean of the R^3 fine faces over it
+    int64_t coarse, fine;     // coarse face index; first fine face
+    int64_t st[3];            // fine face strides of the 3 transverse dims
+    int32_t r[3], pad;
+};
+struct AvgTask4 {             // average-down: one covered coarse cell := mean of R^4 fine cells
+    int64_t coarse, fine;
+    int64_t st[3];            // fine strides of x, y, v_x (v_y: 1)
+    int32_t r[4];
+};
+
 constexpr int MAXLEV = 8;     // levels of one hierarchy handled by the reduction
 struct RedPlan {              // Alg.8 sub-patch reduction plan (built on the host, level.cpp)
     std::vector<uint64_t> uids;   // the hierarchy it was built for
@@ -217,6 +234,11 @@ void free_mask_plan4(MaskPlan4* p);
 int launch_reduce_subpatch4(const RedPlan4* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
 int launch_reduce_mask4(const MaskPlan4* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
 int launch_fill4(vlasov_level* L, double* f, const double* f_coarse, const double* E_bc, const double* f0v, int interp);
+int launch_stage4_fstar(const vlasov_level* L, int stage, double dt, const double* f_n, const double* f_s,
+                        double* f_next, const double* E, int recon, double* Fstar);
+int launch_fstar_update(const vlasov_level* L, double dt, const double* f_n, const double* Fstar, double* f_new);
+int launch_fstar_coarsen(const vlasov_level* L, const double* F_fine, double* F_coarse);
+int launch_average_down4(const vlasov_level* L, const double* f_fine, double* f_coarse);
 int launch_reduce_mask(const MaskPlan* P, const double* const* f, int nlev, double* rho, cudaStream_t st);
 }  // namespace vk
 
@@ -276,6 +298,13 @@ struct vlasov_level {
     vk::PhysTask4* d_phys4 = nullptr;
     int64_t n_phys4[2] = {0, 0};
     bool ghost4_built = false;            // task lists of a 2D+2V level (built lazily for a single block)
+    vk::Patch4* d_patch4 = nullptr;       // F*-form stepping of 2D+2V levels
+    int64_t face_doubles = 0;             // size of the level's F* buffer
+    int64_t max_patch_cells = 0;
+    vk::FaceAvgTask* d_fcoarsen4 = nullptr;   // Alg.4 flux coarsening into the coarser level
+    int64_t n_fcoarsen4 = 0;
+    vk::AvgTask4* d_avg4 = nullptr;       // average-down into the coarser level
+    int64_t n_avg4 = 0;
     // 2D+2V
     int64_t e_doubles = 0;
     int strips2 = 1;                      // x strips of the 2D+2V stage kernel

@@ -190,6 +190,9 @@ void free_level(vlasov_level* L) {
     vk::dfree(L->d_rawtags, L->stream);
     vk::dfree(L->d_scalar, L->stream);
     vk::dfree(L->d_phys4, L->stream);
+    vk::dfree(L->d_patch4, L->stream);
+    vk::dfree(L->d_fcoarsen4, L->stream);
+    vk::dfree(L->d_avg4, L->stream);
     vk::free_red_plan4(L->red_plan4);
     vk::free_mask_plan4(L->mask_plan4);
     delete L;
@@ -490,6 +493,133 @@ int build_ghost_tasks(vlasov_level* L, const vlasov_level* C, std::vector<int64_
 }
 
 std::vector<Box> subpatches_of(const vlasov_level* const* levels, int nlev, int li, int patch);
+
+// F*-form stepping of a 2D+2V level (N3): per-patch face layout (dim d: the patch's cells with
+// n_d + 1 along d, row-major), and w.r.t. the coarser level the Alg.4 flux-coarsening tasks
+// (every coarse face of every coarse patch that coincides with a fine patch face, periodic images
+// in x and y) and the average-down tasks
+int build_fstar4(vlasov_level* L, const vlasov_level* C, std::vector<vk::Patch4>& pt,
+                 std::vector<vk::FaceAvgTask>& fc, std::vector<vk::AvgTask4>& av) {
+    int64_t foff = 0;
+    std::vector<std::array<int64_t, 4>> offs;
+    for (size_t p = 0; p < L->boxes.size(); ++p) {
+        const Box& b = L->boxes[p];
+        const int blk = L->patch_block[p];
+        vk::Patch4 P;
+        int lo[4];
+        for (int d = 0; d < 4; ++d) { lo[d] = b.lo[d]; P.lo[d] = b.lo[d]; P.n[d] = vk::box_ncells_dim(b, d); }
+        P.org = cell_addr(L, blk, lo);
+        for (int d = 0; d < 3; ++d) P.s[d] = L->block_str[blk][d];
+        int64_t ncell = 1;
+        for (int d = 0; d < 4; ++d) ncell *= P.n[d];
+        L->max_patch_cells = std::max(L->max_patch_cells, ncell);
+        std::array<int64_t, 4> o;
+        for (int d = 0; d < 4; ++d) {
+            P.foff[d] = o[d] = foff;
+            foff += ncell / P.n[d] * (P.n[d] + 1);
+        }
+        offs.push_back(o);
+        pt.push_back(P);
+    }
+    L->face_doubles = foff;
+    if (!C) return VLASOV_OK;
+    const int* rr = L->coarse_ratio;
+    for (const Box& fb : L->boxes)
+        for (int d = 0; d < 4; ++d)
+            if (fb.lo[d] % rr[d] || (fb.hi[d] + 1) % rr[d])
+                return vk::fail(VLASOV_EINVAL, "fine boxes must be unions of refined coarse cells");
+    // coarse patch face layout (the same rule as for L)
+    std::vector<std::array<int64_t, 4>> coffs;
+    {
+        int64_t o = 0;
+        for (const Box& cb : C->boxes) {
+            int64_t ncell = 1;
+            for (int d = 0; d < 4; ++d) ncell *= vk::box_ncells_dim(cb, d);
+            std::array<int64_t, 4> a;
+            for (int d = 0; d < 4; ++d) { a[d] = o; o += ncell / vk::box_ncells_dim(cb, d) * (vk::box_ncells_dim(cb, d) + 1); }
+            coffs.push_back(a);
+        }
+    }
+    auto face_index = [](const int* n, int d, const int* q) {   // q: face coords (q[d] in 0..n_d)
+        int64_t idx = 0;
+        for (int e = 0; e < 4; ++e) idx = idx * (n[e] + (e == d ? 1 : 0)) + q[e];
+        return idx;
+    };
+    for (size_t p = 0; p < L->boxes.size(); ++p) {
+        const Box& fb = L->boxes[p];
+        int nf[4];
+        for (int d = 0; d < 4; ++d) nf[d] = vk::box_ncells_dim(fb, d);
+        const Box cbx = vk::box_coarsen(fb, rr, 4);
+        for (int d = 0; d < 4; ++d) {
+            int fst[4];                                          // fine face-array strides
+            {
+                int64_t s = 1;
+                for (int e = 3; e >= 0; --e) { fst[e] = (int)s; s *= nf[e] + (e == d ? 1 : 0); }
+            }
+            for (int side = 0; side < 2; ++side) {
+                const int cface = side == 0 ? cbx.lo[d] : cbx.hi[d] + 1;      // coarse face = low face of cell cface
+                const int ff = side == 0 ? 0 : nf[d];                        // fine face index along d
+                const int nimg = d < 2 ? 3 : 1;
+                for (int im = 0; im < nimg; ++im) {
+                    const int shift = im == 0 ? 0 : (im == 1 ? -C->dom[d] : C->dom[d]);
+                    const int cf = cface + shift;
+                    for (size_t cp = 0; cp < C->boxes.size(); ++cp) {
+                        const Box& cb = C->boxes[cp];
+                        if (cf < cb.lo[d] || cf > cb.hi[d] + 1) continue;
+                        int lo[4], hi[4];
+                        bool ok = true;
+                        for (int e = 0; e < 4 && ok; ++e) {
+                            if (e == d) continue;
+                            lo[e] = std::max(cbx.lo[e], cb.lo[e]);
+                            hi[e] = std::min(cbx.hi[e], cb.hi[e]);
+                            ok = lo[e] <= hi[e];
+                        }
+                        if (!ok) continue;
+                        int cn[4];
+                        for (int e = 0; e < 4; ++e) cn[e] = vk::box_ncells_dim(cb, e);
+                        int c[4];
+                        c[d] = cf;
+                        const int e0 = d == 0 ? 1 : 0, e1 = (d <= 1) ? 2 : 1, e2 = d == 3 ? 2 : 3;
+                        for (c[e0] = lo[e0]; c[e0] <= hi[e0]; ++c[e0])
+                            for (c[e1] = lo[e1]; c[e1] <= hi[e1]; ++c[e1])
+                                for (c[e2] = lo[e2]; c[e2] <= hi[e2]; ++c[e2]) {
+                                    int qc[4], qf[4];
+                                    for (int e = 0; e < 4; ++e) {
+                                        qc[e] = c[e] - cb.lo[e];
+                                        qf[e] = e == d ? ff : c[e] * rr[e] - fb.lo[e];
+                                    }
+                                    vk::FaceAvgTask t;
+                                    t.coarse = coffs[cp][d] + face_index(cn, d, qc);
+                                    t.fine = offs[p][d] + face_index(nf, d, qf);
+                                    const int es[3] = {e0, e1, e2};
+                                    for (int k = 0; k < 3; ++k) { t.st[k] = fst[es[k]]; t.r[k] = rr[es[k]]; }
+                                    t.pad = 0;
+                                    fc.push_back(t);
+                                }
+                    }
+                }
+            }
+        }
+        // average-down tasks
+        const int fblk = L->patch_block[p];
+        for (size_t cp = 0; cp < C->boxes.size(); ++cp) {
+            const Box ov = vk::box_intersect(C->boxes[cp], cbx, 4);
+            if (vk::box_empty(ov, 4)) continue;
+            const int cblk = C->patch_block[cp];
+            for_each_cell(ov, 4, [&](const int* c) {
+                vk::AvgTask4 t;
+                int fc0[4];
+                for (int e = 0; e < 4; ++e) fc0[e] = c[e] * rr[e];
+                t.coarse = cell_addr(C, cblk, c);
+                t.fine = cell_addr(L, fblk, fc0);
+                for (int e = 0; e < 3; ++e) t.st[e] = L->block_str[fblk][e];
+                for (int e = 0; e < 4; ++e) t.r[e] = rr[e];
+                av.push_back(t);
+            });
+        }
+    }
+    return VLASOV_OK;
+}
 
 // Characteristic velocity condition of a 2D+2V multi-patch level (reading #6): for each patch
 // touching a velocity boundary, one task per column side, v_x pass first (columns over the whole
@@ -1086,7 +1216,13 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
             L->n_vtiles = L->dom[2] * nmt;                 // moment partial planes
         }
     }
+    std::vector<vk::Patch4> patch4;
+    std::vector<vk::FaceAvgTask> fcoarsen4;
+    std::vector<vk::AvgTask4> avg4;
+    if (!rc && nd == 4) rc = build_fstar4(L, coarser, patch4, fcoarsen4, avg4);
     if (rc) { free_level(L); return rc; }
+    L->n_fcoarsen4 = (int64_t)fcoarsen4.size();
+    L->n_avg4 = (int64_t)avg4.size();
     L->n_copy = (int64_t)copies.size() / 2;
     L->n_cf = (int64_t)cfs.size();
     L->n_phys = (int64_t)phys.size();
@@ -1117,7 +1253,8 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         (rc = upload(&L->d_tiles_narrow, L->h_tiles_narrow, L->stream)) ||
         (rc = upload(&L->d_copy, copies, L->stream)) || (rc = upload(&L->d_cf, cfs, L->stream)) ||
         (rc = upload(&L->d_phys, phys, L->stream)) || (rc = upload(&L->d_b5, b5, L->stream)) ||
-        (rc = upload(&L->d_phys4, phys4, L->stream)) ||
+        (rc = upload(&L->d_phys4, phys4, L->stream)) || (rc = upload(&L->d_patch4, patch4, L->stream)) ||
+        (rc = upload(&L->d_fcoarsen4, fcoarsen4, L->stream)) || (rc = upload(&L->d_avg4, avg4, L->stream)) ||
         (rc = upload(&L->d_reflux, reflux, L->stream)) || (rc = upload(&L->d_reflux_cells, reflux_cells, L->stream)) ||
         (rc = upload(&L->d_reflux_off, reflux_off, L->stream)) || (rc = upload(&L->d_avg, avg, L->stream))) {
         free_level(L);
@@ -1968,6 +2105,41 @@ int vlasov_inject_field(vlasov_level* L, const double* E_finest, const int32_t n
     return vk::launch_inject_2d(L, E_finest, n_finest, E_lvl);
 }
 
+int vlasov_level_face_doubles(const vlasov_level* L, int64_t* n) {
+    if (!L || !n) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "face_doubles: 2D+2V levels (F* form)");
+    *n = L->face_doubles;
+    return VLASOV_OK;
+}
+
+int vlasov_rk4_stage_fstar(vlasov_level* L, int32_t stage, double dt, const double* f_n, const double* f_s,
+                           double* f_next, const double* E, int32_t recon, double* Fstar) {
+    if (!L || !f_n || !f_s || !E || !Fstar) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage_fstar: 2D+2V levels");
+    if (stage < 1 || stage > 4) return vk::fail(VLASOV_EINVAL, "stage must be 1..4");
+    if (stage < 4 && !f_next) return vk::fail(VLASOV_EINVAL, "f_next required for stages 1..3");
+    if (f_next && f_next == f_s) return vk::fail(VLASOV_EINVAL, "f_next must not alias f_s");
+    if (recon != VLASOV_CENTERED4 && recon != VLASOV_UPWIND) return vk::fail(VLASOV_EINVAL, "bad recon");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_stage4_fstar(L, stage, dt, f_n, f_s, f_next, E, recon, Fstar);
+}
+
+int vlasov_fstar_coarsen(const vlasov_level* fine, const double* F_fine, const vlasov_level* coarse, double* F_coarse) {
+    if (!fine || !F_fine || !coarse || !F_coarse) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (fine->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "fstar_coarsen: 2D+2V levels");
+    if (fine->coarser != coarse || coarse->uid != fine->coarser_uid)
+        return vk::fail(VLASOV_ESTALE, "fstar_coarsen: coarse level does not match the one of level_create");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_fstar_coarsen(fine, F_fine, F_coarse);
+}
+
+int vlasov_fstar_update(vlasov_level* L, double dt, const double* f_n, const double* Fstar, double* f_new) {
+    if (!L || !f_n || !Fstar || !f_new) return vk::fail(VLASOV_EINVAL, "null argument");
+    if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "fstar_update: 2D+2V levels");
+    if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    return vk::launch_fstar_update(L, dt, f_n, Fstar, f_new);
+}
+
 int vlasov_inject_field_ghosted(vlasov_level* L, const double* E_finest, const int32_t n_finest[2], double* E_lvl) {
     if (!L || !E_finest || !n_finest || !E_lvl) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "inject_field_ghosted: 2D+2V levels");
@@ -1998,8 +2170,11 @@ int vlasov_flux_register_accumulate(vlasov_level* fine, const double* f_fine, co
 int vlasov_average_down(vlasov_level* fine, const double* f_fine, double* f_coarse, const double* regs, double dt) {
     if (!fine || !f_fine || !f_coarse) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!fine->coarser) return vk::fail(VLASOV_EINVAL, "average_down: level has no coarser level");
-    if (fine->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "average_down: 1D+1V only");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
+    if (fine->ndim == 4) {                        // F* form: refluxing is the flux coarsening (Alg.4)
+        if (regs) return vk::fail(VLASOV_EINVAL, "average_down: 2D+2V levels take no flux registers");
+        return vk::launch_average_down4(fine, f_fine, f_coarse);
+    }
     return vk::launch_average_down(fine, f_fine, f_coarse, regs, dt);
 }
 

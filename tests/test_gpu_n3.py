@@ -166,3 +166,67 @@ def test_reductions_and_field_4d_parity(seed):
         nx, ny = H.ncells0[0] * H.levels[l].ratio[0], H.ncells0[1] * H.levels[l].ratio[1]
         got = e.view(2, nx + 4, ny + 4)[:, 2:-2, 2:-2].cpu().numpy()
         np.testing.assert_allclose(got, E_ref[l], rtol=0, atol=1e-12 * np.abs(E_ref[-1]).max() + 1e-15)
+
+
+# ---------------------------------------------------------------- 2D+2V AMR steps (F* form)
+from paper_1204_3853_b200.amr4_solver import AmrVlasov2D2V  # noqa: E402
+
+
+def _amr_pair(rat, lb, w, init, fbg_fn=None):
+    fbg_fn = fbg_fn or (lambda r: inputs.background_profile(w, r))
+    H = amr4.Hierarchy4(w.lower, inputs.spacing(w), w.ncells, lb, rat, fbg_fn)
+    G = AmrVlasov2D2V(w.ncells, w.lower, inputs.spacing(w), lb, rat, fbg_fn)
+    data = H.new_data()
+    for l, lvl in enumerate(H.levels):
+        for p, b in enumerate(lvl.boxes):
+            amr4._interior(data[l][p])[...] = init(lvl.ratio, b)
+    G.set_state([[amr4._interior(a) for a in lvl] for lvl in data])
+    return H, data, G
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_amr4_steps_parity_random_hierarchies(seed):
+    """Two RK4 steps of the 2D+2V hierarchy (Alg.5 with Alg.1-4 in the F* form: 4D ghost fill,
+    Alg.8 4D -> 2D reduction, 2D field, fluxes, F* accumulation, flux coarsening, update,
+    average-down, end-of-step constraints) against the oracle's amr4.step on random hierarchies."""
+    rat, lb = random_hierarchy_4d(seed)
+    rng = np.random.default_rng(seed + 10)
+    noise = {}
+
+    def init(r, b):
+        v = inputs.initial_cell_averages(W4, r, b)
+        return v * (1.0 + 0.05 * rng.standard_normal(v.shape))
+    H, data, G = _amr_pair(rat, lb, W4, init)
+    E = amr4.start(H, data)
+    dt = inputs.fixed_dt(W4, rat[-1])
+    for n in range(2):
+        data, E, _ = amr4.step(H, data, E, dt)
+        G.step(dt)
+        got = G.get_state()
+        for l in range(len(data)):
+            for p in range(len(data[l])):
+                ref = amr4._interior(data[l][p])
+                np.testing.assert_allclose(got[l][p], ref, rtol=0, atol=1e-12 * np.abs(ref).max(),
+                                           err_msg=f"step {n} level {l} patch {p}")
+    for e_got, e_ref in zip(G.field_state(), E):
+        np.testing.assert_allclose(e_got, e_ref, rtol=0, atol=1e-12 * max(1e-30, np.abs(E[-1]).max()))
+
+
+def test_amr4_composite_mass_conserved_on_gpu():
+    """The oracle's 4D mass-ledger pin (tests/test_oracle_n3.py) on the GPU: nothing crosses the
+    velocity boundary, so the composite mass is conserved to round-off through the step (Alg.4 flux
+    coarsening at the coarse-fine interface)."""
+    import test_oracle_n3 as on3
+    w = inputs.scaled(inputs.get("C5P"), (8, 8, 24, 24), (8, 8, 24, 24))
+    rat = [(1, 1, 1, 1), (2, 2, 2, 2)]
+    lb = [[((0, 0, 0, 0), (7, 7, 23, 23))], [((4, 2, 18, 20), (11, 9, 29, 27))]]
+    H, data, G = _amr_pair(rat, lb, w, lambda r, b: on3._compact_v(w, r, b),
+                           fbg_fn=lambda r: np.zeros((24 * r[2] + 4, 24 * r[3] + 4)))
+    with torch.cuda.stream(G.stream):                 # start from an averaged-down state
+        api.vlasov_average_down(G.levels[1].h, G.bufs[1]["A"], G.bufs[0]["A"], None, 0.0)
+    vol = float(np.prod(inputs.spacing(w)))
+    M0 = G.get_state()[0][0].sum() * vol
+    G.step(inputs.fixed_dt(w, (2, 2, 2, 2)))
+    f0 = G.get_state()[0][0]
+    assert np.all(f0[:, :, :2, :] == 0.0) and np.all(f0[:, :, -2:, :] == 0.0)
+    assert abs(f0.sum() * vol - M0) < 1e-13 * M0
