@@ -6,8 +6,10 @@ B200 copy bandwidth.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--workload C4]
 
-N > 1 runs under torchrun: every rank advances its own C4 problem (replicas; see DESIGN.md
-"Multi-GPU"), the time is the max over ranks, value = all cells updated / time.
+N > 1 runs under torchrun: the velocity-slab decomposition (N2; every rank owns a C4-sized slab of
+an nx x (nv N) problem; NCCL all-reduce of the moments and halo exchange every stage), the time is
+the max over ranks, value = all cells updated / time (weak scaling).  N = 1 is the single-GPU C4
+run.  --shard replicas: N independent C4 problems instead.
 """
 from __future__ import annotations
 
@@ -297,22 +299,36 @@ def run_amr(args, w, rank, world, local):
 
 
 def run_vslab(args, w, rank, world, local):
-    """N2: the 1D+1V workload split into `world` velocity slabs, one per rank (strong scaling):
-    per stage the fused stage kernel, an NCCL all-reduce of the slab moments and the halo
-    exchange of two boundary velocity columns with each neighbour (paper_1204_3853_b200.vslab)."""
+    """N2: the 1D+1V workload decomposed into velocity slabs,
+    one per rank, weak scaling: every rank owns a slab of w's size, so the global problem is
+    nx x (nv N) on the same velocity interval (dv / N).  Per stage: the fused stage kernel, the
+    NCCL all-reduce of the slab moments (nx doubles) and the exchange of 2 boundary velocity
+    columns with each neighbour on a second communicator (concurrently), all captured in one CUDA
+    graph per step; value = global cells x steps / max-over-ranks device time."""
     import torch
     import torch.distributed as dist
+    from dataclasses import replace
 
     import inputs
     from paper_1204_3853_b200.vslab import DistComm, LocalComm, VSlabVlasov1D
 
-    h = inputs.spacing(w)
-    dt = inputs.fixed_dt(w)
-    comm = DistComm(rank, world) if world > 1 else LocalComm()
-    G = VSlabVlasov1D(w.ncells, w.lower, h, inputs.background_profile(w), world, [rank], comm)
-    G.set_state(inputs.initial_cell_averages(w))
+    wg = replace(w, ncells=(w.ncells[0], w.ncells[1] * world), name=f"{w.name}-vslab{world}")
+    h = inputs.spacing(wg)
+    dt = inputs.fixed_dt(wg)
+    comm = DistComm.with_p2p_group(rank, world) if world > 1 else LocalComm()
+    G = VSlabVlasov1D(wg.ncells, wg.lower, h, inputs.background_profile(wg), world, [rank], comm)
+    G.set_state(lambda vr: inputs.initial_cell_averages(
+        wg, None, ((0, vr.start), (wg.ncells[0] - 1, vr.stop - 1))))
+    graph = "CUDA graph, 1 RK4 step (stage kernels, pack / unpack, NCCL)"
+    try:
+        G.capture(dt)
+        step = G.replay
+    except Exception as exc:                          # NCCL capture unsupported here: eager steps
+        graph = f"eager ({type(exc).__name__} in capture)"
+        torch.cuda.synchronize()
+        step = lambda: G.step(dt)                      # noqa: E731
     for _ in range(args.warmup):
-        G.step(dt)
+        step()
     torch.cuda.synchronize()
 
     def barrier():
@@ -326,13 +342,13 @@ def run_vslab(args, w, rank, world, local):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(G.stream)
     for _ in range(args.steps):
-        G.step(dt)
+        step()
     ev1.record(G.stream)
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1), world, "cuda")
     clk = clocks.stop()
-    value = w.cells * args.steps / (ms / 1e3)          # the whole problem, split over the ranks
-    # stage kernels of this rank (events around each launch; the collectives excluded)
+    value = wg.cells * args.steps / (ms / 1e3)
+    # stage kernels of this rank: events around each launch in an eager pass
     S = G.slabs[0].S
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(4)]
           for _ in range(args.steps)]
@@ -343,26 +359,48 @@ def run_vslab(args, w, rank, world, local):
                 ev[k][st - 1][0].record(G.stream)
                 S.stage_launch(st, dt)
                 ev[k][st - 1][1].record(G.stream)
-                G.comm.allreduce(G.slabs, [S.rhos[1] if st % 2 == 1 else S.rhos[0]])
-                G._halo(lambda X: X.buffers(st)[1])
+                works = G.comm.allreduce(G.slabs, [S.rhos[1] if st % 2 == 1 else S.rhos[0]])
+                G._halo(lambda X: X.buffers(st)[1], works)
     barrier()
     stage_ms = [float(np.mean([ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)])) for i in range(4)]
-    slab_cells = w.ncells[0] * (w.ncells[1] // world)
-    achieved = 104.0 * slab_cells / (sum(stage_ms) / 1e3) / 1e9
+    slab_cells = w.cells
+    achieved = STEP_BYTES * slab_cells / (sum(stage_ms) / 1e3) / 1e9
     peak, peak_kind = read_peaks()
+    # end to end: the rank's slab state host -> device before and device -> host after every step
+    host = torch.empty(S.A.numel(), dtype=torch.float64).pin_memory()
+    host.copy_(S.A)
+    nE = max(3, args.steps // 4)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(G.stream):
+        e0.record(G.stream)
+        for _ in range(nE):
+            S.A.copy_(host, non_blocking=True)
+            step()
+            host.copy_(S.A, non_blocking=True)
+        e1.record(G.stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / nE, world, "cuda")
     if rank == 0:
         print(json.dumps({
             "metric": "fp64 phase-space cell-updates/s per RK4 step", "value": value, "unit": "cell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(w, {"parallelism": f"vslab x{world}", "slab": [w.ncells[0], w.ncells[1] // world],
-                                          "exchange": "per stage: NCCL all-reduce of the slab moments (nx doubles) + "
-                                                      "send/recv of 2 boundary velocity columns per neighbour",
-                                          "graph": "eager"}),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(w, {"workload": w.name, "global_grid": list(wg.ncells), "slab": list(w.ncells),
+                                          "parallelism": f"vslab x{world}",
+                                          "exchange": "per stage: NCCL all-reduce of the slab moments (nx doubles) "
+                                                      "and send/recv of 2 boundary velocity columns per neighbour "
+                                                      "(second communicator, concurrent)",
+                                          "graph": graph,
+                                          "l2": "inputs larger than L2 (4 fields of 64 MiB per rank)"}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_kind": peak_kind, "kernel": "k_stage_1d1v of rank 0 (4 launches per step)",
-                         "algorithmic_bytes_per_cell_step": 104, "stage_ms": stage_ms},
-            "gpu_launches": 12 * args.steps, "clocks": clk}))
+                         "timing": "CUDA events around each stage launch (eager pass after the timed region)",
+                         "algorithmic_bytes_per_cell_step": STEP_BYTES, "stage_ms_eager": stage_ms},
+            "e2e": {"value": wg.cells / (e2e_ms / 1e3), "unit": "cell-updates/s",
+                    "h2d_bytes_per_step": S.A.numel() * 8, "d2h_bytes_per_step": S.A.numel() * 8,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": (4 + 8) * args.steps, "clocks": clk, "cpu_baseline": None}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -375,8 +413,9 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shard", default="replicas", choices=["replicas", "vslab"],
-                    help="N > 1: independent replicas (default) or the velocity-slab decomposition (N2)")
+    ap.add_argument("--shard", default="vslab", choices=["replicas", "vslab"],
+                    help="N > 1: the velocity-slab decomposition (N2, default; weak scaling, NCCL all-reduce + "
+                         "halo per stage) or independent replicas")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -398,7 +437,7 @@ def main():
     w = inputs.get(args.workload)
     if w.amr:
         return run_amr(args, w, rank, world, local)
-    if args.shard == "vslab":
+    if args.shard == "vslab" and (world > 1 or "--shard" in sys.argv):
         return run_vslab(args, w, rank, world, local)
     h = inputs.spacing(w)
     dt = inputs.fixed_dt(w)

@@ -47,6 +47,7 @@ class LocalComm:
             total += b
         for b in bufs:
             b.copy_(total)
+        return []
 
     def exchange(self, slabs):
         n = len(slabs)
@@ -55,33 +56,47 @@ class LocalComm:
                 s.lo_recv.copy_(slabs[j - 1].hi_send)
             if j < n - 1:
                 s.hi_recv.copy_(slabs[j + 1].lo_send)
+        return []
 
 
 class DistComm:
-    """One slab per rank (rank r owns slab r of `world`): torch.distributed collectives."""
+    """One slab per rank (rank r owns slab r of `world`): torch.distributed collectives.
 
-    def __init__(self, rank: int, world: int, group=None):
+    Both transports are stream-ordered: with NCCL, torch runs each operation on the
+    communicator's internal stream after an event on the caller's current stream, and
+    `work.wait()` makes the caller's stream wait for it (the host does not block), so a whole
+    step can be captured in one CUDA graph (VSlabVlasov1D.capture).  The moment all-reduce and
+    the halo send/recv use two process groups (two NCCL communicators, two internal streams):
+    the 16 KiB all-reduce and the 32 KiB neighbour exchange of a stage run concurrently."""
+
+    def __init__(self, rank: int, world: int, group=None, p2p_group=None):
         import torch.distributed as dist
         self.dist = dist
         self.rank, self.world, self.group = rank, world, group
+        self.p2p_group = p2p_group if p2p_group is not None else group
+
+    @classmethod
+    def with_p2p_group(cls, rank: int, world: int):
+        """All ranks must call this together: a second communicator for the halo exchange."""
+        import torch.distributed as dist
+        return cls(rank, world, None, dist.new_group(list(range(world))))
 
     def allreduce(self, slabs, bufs):
-        for b in bufs:
-            self.dist.all_reduce(b, op=self.dist.ReduceOp.SUM, group=self.group)
+        works = [self.dist.all_reduce(b, op=self.dist.ReduceOp.SUM, group=self.group, async_op=True) for b in bufs]
+        return works
 
     def exchange(self, slabs):
         (s,) = slabs
         dist, r, n = self.dist, self.rank, self.world
+        g = self.p2p_group
         ops = []
         if r > 0:
-            ops.append(dist.P2POp(dist.isend, s.lo_send, r - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, s.lo_recv, r - 1, self.group))
+            ops.append(dist.P2POp(dist.isend, s.lo_send, r - 1, g))
+            ops.append(dist.P2POp(dist.irecv, s.lo_recv, r - 1, g))
         if r < n - 1:
-            ops.append(dist.P2POp(dist.isend, s.hi_send, r + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, s.hi_recv, r + 1, self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+            ops.append(dist.P2POp(dist.isend, s.hi_send, r + 1, g))
+            ops.append(dist.P2POp(dist.irecv, s.hi_recv, r + 1, g))
+        return dist.batch_isend_irecv(ops) if ops else []
 
 
 class _Slab:
@@ -132,14 +147,17 @@ class VSlabVlasov1D:
         self.slabs = [_Slab(j, nslabs, self.ranges[j], ncells, lower, dx, f0v_full, recon, self.stream) for j in owned]
 
     # ------------------------------------------------------------------ state
-    def set_state(self, f_full: np.ndarray):
-        """f_full: the whole nx x nv state (each slab takes its velocity range)."""
+    def set_state(self, f_full):
+        """f_full: the whole nx x nv state (each slab takes its velocity range), or a callable
+        vrange -> the nx x len(vrange) state of that velocity range (only the owned slabs)."""
         with torch.cuda.stream(self.stream):
             for s in self.slabs:
                 S = s.S
-                S.level.set_domain(S.A, np.ascontiguousarray(f_full[:, s.vr.start:s.vr.stop]))
+                a = f_full(s.vr) if callable(f_full) else f_full[:, s.vr.start:s.vr.stop]
+                S.level.set_domain(S.A, np.ascontiguousarray(a))
                 api.vlasov_reduce_charge([S.level.h], [S.A], -1.0, 1.0 if s.j == 0 else 0.0, 0, S.rhos[0])
-            self.comm.allreduce(self.slabs, [s.S.rhos[0] for s in self.slabs])
+            for wk in self.comm.allreduce(self.slabs, [s.S.rhos[0] for s in self.slabs]):
+                wk.wait()
             for s in self.slabs:
                 S = s.S
                 S.poisson.solve(S.rhos[0], None, S.E[0], 2)
@@ -150,10 +168,12 @@ class VSlabVlasov1D:
     def get_state(self) -> List[np.ndarray]:
         return [s.S.get_state() for s in self.slabs]
 
-    def _halo(self, field_of):
+    def _halo(self, field_of, extra_works=()):
         for s in self.slabs:
             s.pack(field_of(s.S))
-        self.comm.exchange(self.slabs)
+        works = list(extra_works) + list(self.comm.exchange(self.slabs))
+        for w in works:                      # stream-ordered: the current stream waits, not the host
+            w.wait()
         for s in self.slabs:
             s.unpack(field_of(s.S))
 
@@ -162,10 +182,28 @@ class VSlabVlasov1D:
         for s in self.slabs:
             s.S.stage_launch(st, dt)
         rho_next = [(s.S.rhos[1] if st % 2 == 1 else s.S.rhos[0]) for s in self.slabs]
-        self.comm.allreduce(self.slabs, rho_next)
-        self._halo(lambda S: S.buffers(st)[1])
+        # the moment all-reduce and the halo exchange are issued back to back (two communicators)
+        # and waited for together before the next stage
+        works = self.comm.allreduce(self.slabs, rho_next)
+        self._halo(lambda S: S.buffers(st)[1], works)
 
     def step(self, dt: float):
         with torch.cuda.stream(self.stream):
             for st in (1, 2, 3, 4):
                 self.stage(st, dt)
+
+    def capture(self, dt: float):
+        """One step as a CUDA graph (the stage kernels, pack / unpack and the NCCL operations);
+        one eager step first (NCCL communicators and lazily built plans exist before capture)."""
+        self.step(dt)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            for st in (1, 2, 3, 4):
+                self.stage(st, dt)
+        self.graph = g
+        return g
+
+    def replay(self):
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()

@@ -100,3 +100,49 @@ def test_slab_ranges():
     assert [len(r) for r in slab_ranges(64, 4)] == [16] * 4
     with pytest.raises(ValueError):
         slab_ranges(64, 3)
+
+
+_NCCL_SCRIPT = r"""
+import os, sys, socket, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, {root!r})
+import inputs
+from paper_1204_3853_b200.vslab import DistComm, LocalComm, VSlabVlasov1D
+s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+w = inputs.scaled(inputs.get("C4"), (256, 512), (64, 64))
+h = inputs.spacing(w); dt = inputs.fixed_dt(w)
+out = []
+for comm in (DistComm.with_p2p_group(0, 1), LocalComm()):
+    G = VSlabVlasov1D(w.ncells, w.lower, h, inputs.background_profile(w), 1, [0], comm)
+    G.set_state(inputs.initial_cell_averages(w))
+    if isinstance(comm, DistComm):
+        G.capture(dt)                       # NCCL all-reduce captured in the step graph
+        for _ in range(2):
+            G.replay()
+    else:
+        for _ in range(3):
+            G.step(dt)
+    torch.cuda.synchronize()
+    out.append(G.get_state()[0])
+np.save({out!r}, np.stack(out))
+dist.destroy_process_group()
+"""
+
+
+def test_distcomm_nccl_graph_single_rank(tmp_path):
+    """The NCCL transport itself (DistComm: all-reduce on one communicator, halo on a second) in a
+    one-rank NCCL process group, with the step captured in a CUDA graph: bitwise the LocalComm run
+    (one slab: the all-reduce is the identity and there are no neighbours).  Multi-rank logic:
+    tests/test_multirank_cpu.py (gloo, 2 and 3 ranks)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "o.npy")
+    r = subprocess.run([sys.executable, "-c", _NCCL_SCRIPT.format(root=root, out=out)], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    a, b = np.load(out)
+    np.testing.assert_array_equal(a, b)

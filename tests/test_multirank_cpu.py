@@ -69,11 +69,12 @@ def _slab_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1204_3853_b200.vslab import DistComm
-    comm = DistComm(rank, world)
+    comm = DistComm.with_p2p_group(rank, world)         # halo on its own communicator
     s = _FakeSlab(rank, world)
-    comm.exchange([s])
     rho = torch.arange(4, dtype=torch.float64) + (1.0 if rank == 0 else 0.0) - rank   # base 1 on rank 0
-    comm.allreduce([s], [rho])
+    works = list(comm.allreduce([s], [rho])) + list(comm.exchange([s]))   # both in flight at once
+    for w in works:
+        w.wait()
     q.put((rank, s.lo_recv[0].item(), s.hi_recv[0].item(), rho.tolist()))
     dist.barrier()
     dist.destroy_process_group()
