@@ -319,6 +319,8 @@ struct vlasov_poisson {
     double* d_gE = nullptr;
     double* d_gphi = nullptr;
     double* d_gX = nullptr;               // gX[m] = gE[(m - GX_PAD) mod n], m < 2n + GX_PAD + GX_TAIL
+    double* d_hs = nullptr;               // split field: h(m), m = -16 .. 16 (null: Toeplitz field)
+    double K2 = 0.0, Kn = 0.0;            // split field: dx / 2, dx / n
 };
 
 struct vlasov_poisson2d {
@@ -335,7 +337,8 @@ int launch_poisson2d(const vlasov_poisson2d* P, const double* rho, double* E);
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s,
                       double* u, double* f_next, const double* E, const double* E_bc,
                       const double* f0v, int recon, double* rho, const double* rho_in = nullptr,
-                      const double* gE = nullptr, double* E_out = nullptr, const double* gX = nullptr);
+                      const double* gE = nullptr, double* E_out = nullptr, const double* gX = nullptr,
+                      const double* hs = nullptr, double K2 = 0.0, double Kn = 0.0);
 int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
                       double* rho);

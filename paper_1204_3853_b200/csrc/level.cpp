@@ -200,6 +200,13 @@ void free_level(vlasov_level* L) {
 
 inline int wrap(int x, int n) { return ((x % n) + n) % n; }
 
+// fused field of the 1D+1V stage: O(n) split of the Green's function (default) or the Toeplitz
+// rows of round 1 (VLASOV_FIELD=toeplitz, experiments)
+bool split_field() {
+    static const bool s = [] { const char* e = std::getenv("VLASOV_FIELD"); return !(e && std::string(e) == "toeplitz"); }();
+    return s;
+}
+
 int device_ok_uncached() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) {
@@ -358,7 +365,7 @@ int build_tiles_1d(vlasov_level* L, bool have_device) {
         // the fused-field launch groups the v-tiles of a strip into one cluster: one wave of
         // clusters (the unfused launch uses the same tiles)
         L->cluster_size = 1;
-        if (have_device && L->single_block && nvt >= 2 && L->dom[0] <= 4096) {
+        if (have_device && L->single_block && nvt >= 2 && L->dom[0] <= 4096 && !split_field()) {
             // cluster size: the divisor of nvt (<= 8) that keeps the most strips in one wave
             int64_t best = 0;
             for (int cs = std::min(8, nvt); cs >= 2; --cs) {
@@ -1676,7 +1683,8 @@ int vlasov_rk4_stage_vp(vlasov_level* L, const vlasov_poisson* plan, int32_t sta
     if (f_next == f_s) return vk::fail(VLASOV_EINVAL, "f_next must not alias f_s");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     return vk::launch_stage_1d1v(L, stage, dt, stage == 1 ? const_cast<double*>(f_s) : f_n, f_s, u, f_next, E_s,
-                                 E_bc, f0v, recon, rho_next, rho_s, plan->d_gE, E_s, plan->d_gX);
+                                 E_bc, f0v, recon, rho_next, rho_s, plan->d_gE, E_s, plan->d_gX,
+                                 split_field() ? plan->d_hs : nullptr, plan->K2, plan->Kn);
 }
 
 int vlasov_reduce_charge(const vlasov_level* const* levels, int32_t nlev, const double* const* f, double q,
@@ -2053,6 +2061,20 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
     // gE is stored periodically extended (2n + 4 values, gE[j] = g[j mod n]); gX (fused stage
     // kernel) is the same with GX_PAD / GX_TAIL values of padding, gX[m] = g[(m - GX_PAD) mod n],
     // so that the prologue reads g[(i - k) mod n] = gX[GX_PAD + n + i - k] without a modulo
+    // split of gE: S_m = dx [cot(th/2)/2 + sin th / (2 (7 - cos th))], and
+    // (1/n) sum_m cot(th_m/2) sin(th_m d) = 1 - 2d/n (0 < d < n), so gE(d) = (dx/2)(1 - 2d/n)[d != 0]
+    // + h(d) with h(d) = (dx/n) sum_m sin th_m sin(th_m d) / (2 (7 - cos th_m)), which decays like
+    // (7 - sqrt 48)^|d| = 0.0718^|d| (|h(16)| < 1e-18 max|gE|): only h(-16 .. 16) is kept
+    std::vector<double> hs(33, 0.0);
+    for (int m = -16; m <= 16; ++m) {
+        const int d = ((m % n) + n) % n;
+        long double a = 0.0L;
+        for (int q = 1; q < n; ++q) {
+            const int k = (int)(((int64_t)q * d) % n);
+            a += s[q] * s[k] / (2.0L * (7.0L - c[q]));
+        }
+        hs[m + 16] = (double)((long double)dx * a / n);
+    }
     std::vector<double> gX(2 * (size_t)n + vk::GX_PAD + vk::GX_TAIL);
     for (size_t m = 0; m < gX.size(); ++m) gX[m] = gE[((int64_t)m - vk::GX_PAD + 4 * (int64_t)n) % n];
     gE.resize(2 * (size_t)n + 4);
@@ -2062,8 +2084,10 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
     P->dx = dx;
     P->stream = (cudaStream_t)cuda_stream;
     int rc;
+    P->K2 = 0.5 * dx;
+    P->Kn = dx / n;
     if ((rc = upload(&P->d_gE, gE, P->stream)) || (rc = upload(&P->d_gphi, gphi, P->stream)) ||
-        (rc = upload(&P->d_gX, gX, P->stream))) {
+        (rc = upload(&P->d_gX, gX, P->stream)) || (n >= 64 && (rc = upload(&P->d_hs, hs, P->stream)))) {
         vk::dfree(P->d_gE, P->stream);
         vk::dfree(P->d_gphi, P->stream);
         vk::dfree(P->d_gX, P->stream);
@@ -2073,6 +2097,7 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
     cudaError_t e = cudaStreamSynchronize(P->stream);
     if (e != cudaSuccess) {
         vk::dfree(P->d_gE, P->stream); vk::dfree(P->d_gphi, P->stream); vk::dfree(P->d_gX, P->stream);
+        vk::dfree(P->d_hs, P->stream);
         delete P;
         return vk::cuda_check(e, "poisson upload");
     }
@@ -2092,6 +2117,7 @@ int vlasov_poisson_destroy(vlasov_poisson* P) {
         vk::dfree(P->d_gE, P->stream);
         vk::dfree(P->d_gphi, P->stream);
         vk::dfree(P->d_gX, P->stream);
+        vk::dfree(P->d_hs, P->stream);
         cudaStreamSynchronize(P->stream);
         delete P;
     }

@@ -68,6 +68,10 @@ struct StageArgs1 {
     int cluster;               // CTAs per cluster of the fused launch (the v-tiles of a strip)
     int g_smem;                // fused field: gX staged in shared memory too
     const double* gX;          // gX[m] = g[(m - GX_PAD) mod n], m in [0, 2n + GX_PAD + GX_TAIL)
+    // O(n) field (split of the exact Green's function): E_i = K2 (sum r - r_i)
+    //   - Kn (i sum r - sum_k k r_k + n sum_{k>i} r_k) + sum_{|m|<=HM} hs[m + HM] r_{i-m}
+    const double* hs;          // nullable: the fast-decaying part h(m), m = -HM .. HM
+    double K2, Kn;             // dx / 2, dx / n
     int nstrip1;               // > 0: single block, tiles computed from blockIdx (no table load)
     Block1 blk0;               // that block
     int xshift;                // single block: strips start xshift rows later (periodic wrap; L2 reuse)
@@ -80,10 +84,12 @@ static bool g_in_smem(int n) { return n <= G_SMEM_MAX_N; }
 // shared memory of the fused field prologue: rho [n], row results [PART_MAX >= tile_rows + 4],
 // the window of gX the CTA's rows need [<= n + PART_MAX + 32]
 constexpr int PART_MAX = 136;
-static size_t field_smem_bytes(int n) {
+static size_t field_smem_bytes(int n, bool split = false) {
+    if (split) return (size_t)(2 * n + PART_MAX + 2 * (n / 32 + 2)) * sizeof(double);
     return (size_t)(n + PART_MAX + (g_in_smem(n) ? n + PART_MAX + 32 : 0)) * sizeof(double);
 }
 constexpr int EROWS = 8;   // rows of E per warp group in the fused prologue (Toeplitz blocking)
+constexpr int HM = 16;     // half-width of the local part of the split Green's function
 
 // CPT = 4 cells per consumer thread, TV = 4*NT cells per v-tile.
 #ifndef STAGE1D_CPT
@@ -311,7 +317,89 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     }
 
     // ---------------------------------------------------------------- consumers
-    if (field) {
+    if (field && A.hs != nullptr) {
+        // Constraint evaluation of the stage state (Alg.5) in O(n): the exact discrete
+        // Green's function of E = -D4 phi is a sawtooth plus a part decaying like 0.0718^|m|
+        // (DESIGN.md 6.1), so with r = rho - mean
+        //   E_i = K2 (sum r - r_i) - Kn (i sum r - sum_k k r_k + n S_i) + sum_{|m|<=HM} h(m) r_{i-m},
+        //   S_i = sum_{k>i} r_k.
+        // Every CTA computes the sums in the same fixed order (32-cell chunks: warp shuffle scans,
+        // then one sequential pass over the chunk sums), so E does not depend on the tiling.
+        const int n = A.dom_x;
+        const double* s_rho = f_rho;
+        const int nch = (n + 31) >> 5;
+        double* s_sufl = f_rho + n + PART_MAX;   // [n] suffix sums of r within each chunk
+        double* s_cs = s_sufl + n;               // [nch + 1] chunk sums -> sums of the later chunks; [nch]: sum r
+        double* s_ct = s_cs + nch + 1;           // [nch + 1] chunk sums of k r_k; [nch]: sum k r_k
+        mbar_wait(&field_bar, 0);
+        TRACE(2);
+        {   // mean: as below (warp quarters, warp partials in warp order)
+            const int kb = (int)((int64_t)n * warp / NW), ke = (int)((int64_t)n * (warp + 1) / NW);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int k = kb + lane;
+            for (; k + 96 < ke; k += 128) {
+                a0 += s_rho[k]; a1 += s_rho[k + 32]; a2 += s_rho[k + 64]; a3 += s_rho[k + 96];
+            }
+            for (; k < ke; k += 32) a0 += s_rho[k];
+            double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) psum[warp] = acc;
+        }
+        named_bar_sync(1, NT);
+        double mean = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) mean += psum[w];
+        mean /= (double)n;
+        TRACE(3);
+        for (int c = warp; c < nch; c += NW) {
+            const int k = 32 * c + lane;
+            const double r = k < n ? s_rho[k] - mean : 0.0;
+            double sfx = r;                      // inclusive suffix over the lanes (Kogge-Stone)
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double t = __shfl_down_sync(0xffffffffu, sfx, o);
+                if (lane + o < 32) sfx += t;
+            }
+            if (k < n) s_sufl[k] = sfx;
+            double kr = (double)k * r;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) kr += __shfl_xor_sync(0xffffffffu, kr, o);
+            if (lane == 0) { s_cs[c] = sfx; s_ct[c] = kr; }
+        }
+        named_bar_sync(1, NT);
+        if (tid == 0) {
+            double acc = 0.0, t1 = 0.0;
+            for (int c = nch - 1; c >= 0; --c) { const double cc = s_cs[c]; s_cs[c] = acc; acc += cc; }
+            for (int c = 0; c < nch; ++c) t1 += s_ct[c];
+            s_cs[nch] = acc;
+            s_ct[nch] = t1;
+        }
+        named_bar_sync(1, NT);
+        const double sumr = s_cs[nch], T1 = s_ct[nch];
+        for (int t = tid; t < Q; t += NT) {
+            const int i = ((B.lo_x + T.x0 - 2 + t) % n + n) % n;       // row of the periodic domain
+            const double ri = s_rho[i] - mean;
+            const double sgt = (i + 1 < n) ? s_sufl[i + 1] + s_cs[(i + 1) >> 5] : 0.0;
+            double e = A.K2 * (sumr - ri) - A.Kn * ((double)i * sumr - T1 + (double)n * sgt);
+#pragma unroll 11
+            for (int m = -HM; m <= HM; ++m) {
+                int k = i - m;
+                k += (k < 0) ? n : 0;
+                k -= (k >= n) ? n : 0;
+                e = fma(__ldg(A.hs + m + HM), s_rho[k] - mean, e);
+            }
+            sE[t] = e;
+            if (T.pvt == 0 && t >= 2 && t < Q - 2) {     // owned rows + periodic ghosts, once per strip
+                const int x = B.lo_x + wr(T.x0 - 2 + t);
+                A.E_out[x + G] = e;
+                if (x < G) A.E_out[x + G + n] = e;
+                if (x >= n - G) A.E_out[x + G - n] = e;
+            }
+        }
+        TRACE(4);
+        named_bar_sync(1, NT);
+    } else if (field) {
         // Constraint evaluation of the stage state (Alg.5) while the producer fills the
         // ring: E_i = sum_k g[(i - k) mod n] (rho_k - mean) for the rows of this tile (projection to
         // mean zero, applied on the fly), from rho and the periodically extended g staged
@@ -715,7 +803,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
 template <int STAGE, int RECON, int NT, int GM>
 static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t st) {
     using SG = StageGeom<STAGE, NT>;
-    const size_t smem = SG::smem_bytes(tile_rows) + (A.rho_in ? field_smem_bytes(A.dom_x) : 0);
+    const size_t smem = SG::smem_bytes(tile_rows) + (A.rho_in ? field_smem_bytes(A.dom_x, A.hs != nullptr) : 0);
     auto kern = k_stage_1d1v<STAGE, RECON, NT, GM>;
     static bool configured = false;   // per template instantiation
     if (!configured) {
@@ -734,7 +822,7 @@ static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = STAGE1D_PDL;
     ++na;
-    if (A.rho_in && A.cluster > 1) {   // fused field: the v-tiles of a row strip form one cluster
+    if (A.rho_in && A.cluster > 1 && !A.hs) {   // Toeplitz field: the v-tiles of a strip form one cluster
         at[na].id = cudaLaunchAttributeClusterDimension;
         at[na].val.clusterDim.x = (unsigned)A.cluster;
         at[na].val.clusterDim.y = 1;
@@ -822,13 +910,17 @@ static int shift_quarters() {
 
 int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
-                      double* rho, const double* rho_in, const double* gE, double* E_out, const double* gX) {
+                      double* rho, const double* rho_in, const double* gE, double* E_out, const double* gX,
+                      const double* hs, double K2, double Kn) {
     StageArgs1 A;
+    A.hs = rho_in ? hs : nullptr;
+    A.K2 = K2;
+    A.Kn = Kn;
     A.rho_in = rho_in;
     A.gE = gE;
     A.E_out = E_out;
-    A.cluster = rho_in ? L->cluster_size : 1;
-    A.g_smem = (rho_in && g_in_smem(L->dom[0])) ? 1 : 0;
+    A.cluster = (rho_in && !A.hs) ? L->cluster_size : 1;
+    A.g_smem = (rho_in && !A.hs && g_in_smem(L->dom[0])) ? 1 : 0;
     A.gX = gX;
     A.nstrip1 = L->single_block ? L->n_strips : 0;
     // L2 reuse between stages: even stages start their strips half a strip later, so each CTA
