@@ -85,7 +85,7 @@ static bool g_in_smem(int n) { return n <= G_SMEM_MAX_N; }
 // the window of gX the CTA's rows need [<= n + PART_MAX + 32]
 constexpr int PART_MAX = 136;
 static size_t field_smem_bytes(int n, bool split = false) {
-    if (split) return (size_t)(2 * n + PART_MAX + 2 * (n / 32 + 2)) * sizeof(double);
+    if (split) return (size_t)(n + PART_MAX + 2 * (n / 32 + 2)) * sizeof(double);
     return (size_t)(n + PART_MAX + (g_in_smem(n) ? n + PART_MAX + 32 : 0)) * sizeof(double);
 }
 constexpr int EROWS = 8;   // rows of E per warp group in the fused prologue (Toeplitz blocking)
@@ -323,13 +323,13 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         // (DESIGN.md 6.1), so with r = rho - mean
         //   E_i = K2 (sum r - r_i) - Kn (i sum r - sum_k k r_k + n S_i) + sum_{|m|<=HM} h(m) r_{i-m},
         //   S_i = sum_{k>i} r_k.
-        // Every CTA computes the sums in the same fixed order (32-cell chunks: warp shuffle scans,
-        // then one sequential pass over the chunk sums), so E does not depend on the tiling.
+        // Every CTA computes the sums in the same fixed order (32-cell chunks, one thread each; a
+        // warp scan over the chunk sums; per row the rest of its chunk), so E does not depend on
+        // the tiling.
         const int n = A.dom_x;
         const double* s_rho = f_rho;
         const int nch = (n + 31) >> 5;
-        double* s_sufl = f_rho + n + PART_MAX;   // [n] suffix sums of r within each chunk
-        double* s_cs = s_sufl + n;               // [nch + 1] chunk sums -> sums of the later chunks; [nch]: sum r
+        double* s_cs = f_rho + n + PART_MAX;     // [nch + 1] chunk sums -> sums of the later chunks; [nch]: sum r
         double* s_ct = s_cs + nch + 1;           // [nch + 1] chunk sums of k r_k; [nch]: sum k r_k
         mbar_wait(&field_bar, 0);
         TRACE(2);
@@ -352,35 +352,46 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         for (int w = 0; w < NW; ++w) mean += psum[w];
         mean /= (double)n;
         TRACE(3);
-        for (int c = warp; c < nch; c += NW) {
-            const int k = 32 * c + lane;
-            const double r = k < n ? s_rho[k] - mean : 0.0;
-            double sfx = r;                      // inclusive suffix over the lanes (Kogge-Stone)
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double t = __shfl_down_sync(0xffffffffu, sfx, o);
-                if (lane + o < 32) sfx += t;
+        for (int c = tid; c < nch; c += NT) {    // chunk sums of r and k r (one thread per chunk)
+            const int k0 = 32 * c, k1 = min(n, k0 + 32);
+            double cs = 0.0, ct = 0.0;
+            for (int k = k0; k < k1; ++k) {
+                const double r = s_rho[k] - mean;
+                cs += r;
+                ct = fma((double)k, r, ct);
             }
-            if (k < n) s_sufl[k] = sfx;
-            double kr = (double)k * r;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) kr += __shfl_xor_sync(0xffffffffu, kr, o);
-            if (lane == 0) { s_cs[c] = sfx; s_ct[c] = kr; }
+            s_cs[c] = cs;
+            s_ct[c] = ct;
         }
         named_bar_sync(1, NT);
-        if (tid == 0) {
-            double acc = 0.0, t1 = 0.0;
-            for (int c = nch - 1; c >= 0; --c) { const double cc = s_cs[c]; s_cs[c] = acc; acc += cc; }
-            for (int c = 0; c < nch; ++c) t1 += s_ct[c];
-            s_cs[nch] = acc;
-            s_ct[nch] = t1;
+        if (warp == 0) {                         // suffix sums of the chunk sums, sum r, sum k r
+            const int per = (nch + 31) >> 5, c0 = lane * per, c1 = min(nch, c0 + per);
+            double tot = 0.0, t1 = 0.0;
+            for (int c = c1 - 1; c >= c0; --c) { tot += s_cs[c]; t1 += s_ct[c]; }
+            double suf = tot;                    // inclusive suffix over the lanes (Kogge-Stone)
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double t = __shfl_down_sync(0xffffffffu, suf, o);
+                if (lane + o < 32) suf += t;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+            const double all = __shfl_sync(0xffffffffu, suf, 0);
+            double acc = suf - tot;              // chunks of the higher lanes
+            for (int c = c1 - 1; c >= c0; --c) { const double cc = s_cs[c]; s_cs[c] = acc; acc += cc; }
+            if (lane == 0) { s_cs[nch] = all; s_ct[nch] = t1; }
         }
         named_bar_sync(1, NT);
         const double sumr = s_cs[nch], T1 = s_ct[nch];
         for (int t = tid; t < Q; t += NT) {
             const int i = ((B.lo_x + T.x0 - 2 + t) % n + n) % n;       // row of the periodic domain
             const double ri = s_rho[i] - mean;
-            const double sgt = (i + 1 < n) ? s_sufl[i + 1] + s_cs[(i + 1) >> 5] : 0.0;
+            double sgt = 0.0;                    // S_i = sum_{k > i} r_k: rest of i+1's chunk, later chunks
+            if (i + 1 < n) {
+                const int ce = min(n, (((i + 1) >> 5) + 1) << 5);
+                for (int k = i + 1; k < ce; ++k) sgt += s_rho[k] - mean;
+                sgt += s_cs[(i + 1) >> 5];
+            }
             double e = A.K2 * (sumr - ri) - A.Kn * ((double)i * sumr - T1 + (double)n * sgt);
 #pragma unroll 11
             for (int m = -HM; m <= HM; ++m) {
