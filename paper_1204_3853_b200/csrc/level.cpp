@@ -200,10 +200,11 @@ void free_level(vlasov_level* L) {
 
 inline int wrap(int x, int n) { return ((x % n) + n) % n; }
 
-// fused field of the 1D+1V stage: O(n) split of the Green's function (default) or the Toeplitz
-// rows of round 1 (VLASOV_FIELD=toeplitz, experiments)
+// fused field of the 1D+1V stage: Toeplitz rows split over the strip's cluster (default), or the
+// O(n) split of the Green's function (VLASOV_FIELD=split): exact and tiling-independent, but
+// measured slower on B200 (C4: 191 vs 185 us per step)
 bool split_field() {
-    static const bool s = [] { const char* e = std::getenv("VLASOV_FIELD"); return !(e && std::string(e) == "toeplitz"); }();
+    static const bool s = [] { const char* e = std::getenv("VLASOV_FIELD"); return e && std::string(e) == "split"; }();
     return s;
 }
 
@@ -365,7 +366,8 @@ int build_tiles_1d(vlasov_level* L, bool have_device) {
         // the fused-field launch groups the v-tiles of a strip into one cluster: one wave of
         // clusters (the unfused launch uses the same tiles)
         L->cluster_size = 1;
-        if (have_device && L->single_block && nvt >= 2 && L->dom[0] <= 4096 && !split_field()) {
+        if (have_device && L->single_block && nvt >= 2 && L->dom[0] <= 4096 &&
+            (!split_field() || std::getenv("VLASOV_SPLIT_CLUSTER"))) {
             // cluster size: the divisor of nvt (<= 8) that keeps the most strips in one wave
             int64_t best = 0;
             for (int cs = std::min(8, nvt); cs >= 2; --cs) {

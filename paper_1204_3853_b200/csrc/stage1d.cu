@@ -85,7 +85,7 @@ static bool g_in_smem(int n) { return n <= G_SMEM_MAX_N; }
 // the window of gX the CTA's rows need [<= n + PART_MAX + 32]
 constexpr int PART_MAX = 136;
 static size_t field_smem_bytes(int n, bool split = false) {
-    if (split) return (size_t)(n + PART_MAX + 2 * (n / 32 + 2)) * sizeof(double);
+    if (split) return (size_t)(n + PART_MAX + 2 * (n / 32 + 2) + 8) * sizeof(double);
     return (size_t)(n + PART_MAX + (g_in_smem(n) ? n + PART_MAX + 32 : 0)) * sizeof(double);
 }
 constexpr int EROWS = 8;   // rows of E per warp group in the fused prologue (Toeplitz blocking)
@@ -222,13 +222,14 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     }
     // fused field in a cluster (the v-tiles of one row strip): every CTA's barrier is initialised
     // and armed before any CTA pushes E rows into its shared memory
-    const uint32_t crank = field ? cluster_ctarank() : 0u, csize = field ? cluster_nctarank() : 1u;
+    const bool toep = field && A.hs == nullptr;  // Toeplitz field: rows split over the strip's cluster
+    const uint32_t crank = toep ? cluster_ctarank() : 0u, csize = toep ? cluster_nctarank() : 1u;
     __syncthreads();
     // (after the barrier that orders the inits; before this thread's cluster arrive, so no remote
     // push can reach e_bar first)
     if (tid == 0 && csize > 1) mbar_arrive_expect_tx(&e_bar, (uint32_t)Q * 8u);
     // consumers arrive now and wait only before their first remote store; the producer waits at once
-    if (field && csize > 1) {
+    if (toep && csize > 1) {
         if (PWARPS && warp >= NW) cluster_sync_all();
         else cluster_arrive();
     }
@@ -323,14 +324,14 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         // (DESIGN.md 6.1), so with r = rho - mean
         //   E_i = K2 (sum r - r_i) - Kn (i sum r - sum_k k r_k + n S_i) + sum_{|m|<=HM} h(m) r_{i-m},
         //   S_i = sum_{k>i} r_k.
-        // Every CTA computes the sums in the same fixed order (32-cell chunks, one thread each; a
-        // warp scan over the chunk sums; per row the rest of its chunk), so E does not depend on
-        // the tiling.
+        // Every CTA computes the sums in the same fixed order (32-cell chunks summed by thread
+        // pairs; a warp scan over the chunk sums; per row the rest of its chunk), so E does not
+        // depend on the tiling.
         const int n = A.dom_x;
         const double* s_rho = f_rho;
         const int nch = (n + 31) >> 5;
         double* s_cs = f_rho + n + PART_MAX;     // [nch + 1] chunk sums -> sums of the later chunks; [nch]: sum r
-        double* s_ct = s_cs + nch + 1;           // [nch + 1] chunk sums of k r_k; [nch]: sum k r_k
+        double* s_ct = s_cs + nch + 1;           // [NW] warp partials of sum k r_k; [NW]: the total
         mbar_wait(&field_bar, 0);
         TRACE(2);
         {   // mean: as below (warp quarters, warp partials in warp order)
@@ -352,54 +353,82 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         for (int w = 0; w < NW; ++w) mean += psum[w];
         mean /= (double)n;
         TRACE(3);
-        for (int c = tid; c < nch; c += NT) {    // chunk sums of r and k r (one thread per chunk)
-            const int k0 = 32 * c, k1 = min(n, k0 + 32);
-            double cs = 0.0, ct = 0.0;
-            for (int k = k0; k < k1; ++k) {
-                const double r = s_rho[k] - mean;
-                cs += r;
-                ct = fma((double)k, r, ct);
+        // chunk sums of r = rho - mean (32-cell chunks) and the total of k r: thread t sums the
+        // cells [16 t, 16 t + 16) in order, a chunk is the sum of its two halves (one shuffle), the
+        // totals are fixed shuffle trees + warp partials in warp order -- the same expressions in
+        // every CTA (E independent of the tiling)
+        double tkr = 0.0;
+        const int niter = (32 * nch + 16 * NT - 1) / (16 * NT);          // uniform trip count (shuffles)
+        for (int it = 0; it < niter; ++it) {
+            const int h0 = 16 * tid + it * 16 * NT;
+            double hs_ = 0.0, hk = 0.0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int k = h0 + u;
+                const double r = k < n ? s_rho[k] - mean : 0.0;
+                hs_ += r;
+                hk = fma((double)k, r, hk);
             }
-            s_cs[c] = cs;
-            s_ct[c] = ct;
+            const double cs = hs_ + __shfl_xor_sync(0xffffffffu, hs_, 1);      // the chunk's two halves
+            if ((tid & 1) == 0 && (h0 >> 5) < nch) s_cs[h0 >> 5] = cs;
+            tkr += hk;
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tkr += __shfl_xor_sync(0xffffffffu, tkr, o);
+        if (lane == 0) s_ct[warp] = tkr;
         named_bar_sync(1, NT);
-        if (warp == 0) {                         // suffix sums of the chunk sums, sum r, sum k r
+        if (warp == 0) {                         // suffix sums of the chunk sums, sum r
             const int per = (nch + 31) >> 5, c0 = lane * per, c1 = min(nch, c0 + per);
-            double tot = 0.0, t1 = 0.0;
-            for (int c = c1 - 1; c >= c0; --c) { tot += s_cs[c]; t1 += s_ct[c]; }
+            double tot = 0.0;
+            for (int c = c1 - 1; c >= c0; --c) tot += s_cs[c];
             double suf = tot;                    // inclusive suffix over the lanes (Kogge-Stone)
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const double t = __shfl_down_sync(0xffffffffu, suf, o);
                 if (lane + o < 32) suf += t;
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) t1 += __shfl_xor_sync(0xffffffffu, t1, o);
             const double all = __shfl_sync(0xffffffffu, suf, 0);
             double acc = suf - tot;              // chunks of the higher lanes
             for (int c = c1 - 1; c >= c0; --c) { const double cc = s_cs[c]; s_cs[c] = acc; acc += cc; }
-            if (lane == 0) { s_cs[nch] = all; s_ct[nch] = t1; }
+            if (lane == 0) {
+                double t1 = 0.0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) t1 += s_ct[w];
+                s_cs[nch] = all;
+                s_ct[NW] = t1;
+            }
         }
+#ifdef STAGE1D_TRACE
+        if (tid == 0 && blockIdx.x < 2048) g_trace[blockIdx.x][9] = gtimer();
+#endif
         named_bar_sync(1, NT);
-        const double sumr = s_cs[nch], T1 = s_ct[nch];
+        const double sumr = s_cs[nch], T1 = s_ct[NW];
         for (int t = tid; t < Q; t += NT) {
-            const int i = ((B.lo_x + T.x0 - 2 + t) % n + n) % n;       // row of the periodic domain
+            int i = B.lo_x + T.x0 - 2 + t;                                 // row of the periodic domain
+            i += (i < 0) ? n : 0;
+            i -= (i >= n) ? n : 0;
+            i -= (i >= n) ? n : 0;
             const double ri = s_rho[i] - mean;
-            double sgt = 0.0;                    // S_i = sum_{k > i} r_k: rest of i+1's chunk, later chunks
+            double sgt = 0.0;                    // sum_{k > i} r_k: the rest of i+1's chunk, later chunks
             if (i + 1 < n) {
                 const int ce = min(n, (((i + 1) >> 5) + 1) << 5);
-                for (int k = i + 1; k < ce; ++k) sgt += s_rho[k] - mean;
-                sgt += s_cs[(i + 1) >> 5];
+                double a = 0.0, b = 0.0;
+                int k = i + 1;
+                for (; k + 1 < ce; k += 2) { a += s_rho[k] - mean; b += s_rho[k + 1] - mean; }
+                if (k < ce) a += s_rho[k] - mean;
+                sgt = (a + b) + s_cs[(i + 1) >> 5];
             }
-            double e = A.K2 * (sumr - ri) - A.Kn * ((double)i * sumr - T1 + (double)n * sgt);
-#pragma unroll 11
+            double e0 = A.K2 * (sumr - ri) - A.Kn * ((double)i * sumr - T1 + (double)n * sgt);
+            double e1 = 0.0, e2 = 0.0;           // local part: three interleaved partial sums
+#pragma unroll
             for (int m = -HM; m <= HM; ++m) {
                 int k = i - m;
                 k += (k < 0) ? n : 0;
                 k -= (k >= n) ? n : 0;
-                e = fma(__ldg(A.hs + m + HM), s_rho[k] - mean, e);
+                const double p = __ldg(A.hs + m + HM) * (s_rho[k] - mean);
+                if ((m + HM) % 3 == 0) e0 += p; else if ((m + HM) % 3 == 1) e1 += p; else e2 += p;
             }
+            const double e = e0 + (e1 + e2);
             sE[t] = e;
             if (T.pvt == 0 && t >= 2 && t < Q - 2) {     // owned rows + periodic ghosts, once per strip
                 const int x = B.lo_x + wr(T.x0 - 2 + t);
@@ -833,7 +862,7 @@ static int launch_t(const StageArgs1& A, int ntiles, int tile_rows, cudaStream_t
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = STAGE1D_PDL;
     ++na;
-    if (A.rho_in && A.cluster > 1 && !A.hs) {   // Toeplitz field: the v-tiles of a strip form one cluster
+    if (A.rho_in && A.cluster > 1) {   // the v-tiles of a strip form one cluster (Toeplitz field)
         at[na].id = cudaLaunchAttributeClusterDimension;
         at[na].val.clusterDim.x = (unsigned)A.cluster;
         at[na].val.clusterDim.y = 1;
@@ -930,7 +959,7 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.rho_in = rho_in;
     A.gE = gE;
     A.E_out = E_out;
-    A.cluster = (rho_in && !A.hs) ? L->cluster_size : 1;
+    A.cluster = rho_in ? L->cluster_size : 1;     // 1 unless chosen at level creation
     A.g_smem = (rho_in && !A.hs && g_in_smem(L->dom[0])) ? 1 : 0;
     A.gX = gX;
     A.nstrip1 = L->single_block ? L->n_strips : 0;

@@ -40,7 +40,9 @@ for fused in (True, False):
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
         cols = [0, 1, 2, 3, 4, 5, 6, 7] if fused else [0, 1, 5, 6, 7]
-        if s in (1, 2):
+        if fused and os.environ.get("TRACE_SPLIT"):         # split field: 9 chunk sums, 8 chunk scan
+            cols = [0, 1, 2, 3, 9, 8, 4, 5, 6, 7]
+        if s in (1, 2) and not os.environ.get("TRACE_SPLIT"):
             end = rel[:, 7]
             sm = buf[:n, 8].astype(int)
             nvt = 8
