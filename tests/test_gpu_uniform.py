@@ -368,3 +368,35 @@ def test_stage_vp_rejects_aliasing():
                                 _lib.CENTERED4, S.rhos[1])
     with pytest.raises(_lib.VlasovError):
         api.vlasov_rk4_stage(L, 3, 0.01, S.A, S.C, S.U, S.C, S.E[1], None, S.f0v, _lib.CENTERED4, None)
+
+
+_SPLIT_SCRIPT = r"""
+import os, sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+os.environ["VLASOV_FIELD"] = "split"
+import inputs
+from paper_1204_3853_b200.solver import UniformVlasov1D
+w = inputs.scaled(inputs.get("C4"), ({nx}, 1024), (64, 64))
+S = UniformVlasov1D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), inputs.background_profile(w))
+S.set_state(inputs.initial_cell_averages(w))
+for _ in range(5):
+    S.step(inputs.fixed_dt(w))
+np.save({out!r}, S.get_state())
+"""
+
+
+@pytest.mark.parametrize("nx", [512, 300])
+def test_split_field_option_parity(tmp_path, nx):
+    """VLASOV_FIELD=split (the O(n) sawtooth + local split of the exact Green's function in the
+    fused stage prologue): 5 fused steps against the oracle within 1e-11."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "s.npy")
+    r = subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT.format(root=root, out=out, nx=nx)], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    w = inputs.scaled(inputs.get("C4"), (nx, 1024), (64, 64))
+    ref, _ = uniform.problem_for(w).run(inputs.initial_cell_averages(w), inputs.fixed_dt(w), 5)
+    assert relerr(np.load(out), ref) < 1e-11
