@@ -12,6 +12,8 @@
 #include <map>
 #include <mutex>
 #include <string>
+
+#include <nvtx3/nvToolsExt.h>
 #include <vector>
 
 #include "internal.h"
@@ -156,6 +158,14 @@ void free_red_plan(RedPlan* p) {
     delete p;
 }
 }  // namespace vk
+
+// NVTX range per C-ABI call (one named range per entry point, visible in nsys / ncu
+// --nvtx; near-zero cost without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define VK_NVTX() NvtxRange vk_nvtx_range_(__func__)
 
 // ====================================================================== device helpers
 namespace {
@@ -1080,6 +1090,7 @@ int vlasov_device_ok(void) { return device_ok_impl(); }
 
 int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4], const vlasov_box* boxes,
                         int32_t nboxes, const vlasov_level* coarser, void* cuda_stream, vlasov_level** out) {
+    VK_NVTX();
     if (!geom || !ratio_to_level0 || !boxes || !out) return vk::fail(VLASOV_EINVAL, "null argument");
     *out = nullptr;
     const int nd = geom->ndim;
@@ -1276,6 +1287,7 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
 }
 
 int vlasov_level_destroy(vlasov_level* level) {
+    VK_NVTX();
     if (level) {
         cudaStreamSynchronize(level->stream);
         free_level(level);
@@ -1284,6 +1296,7 @@ int vlasov_level_destroy(vlasov_level* level) {
 }
 
 int vlasov_level_get_info(const vlasov_level* L, vlasov_level_info* info) {
+    VK_NVTX();
     if (!L || !info) return vk::fail(VLASOV_EINVAL, "null argument");
     std::memset(info, 0, sizeof(*info));
     info->field_doubles = L->field_doubles;
@@ -1306,6 +1319,7 @@ int vlasov_level_get_info(const vlasov_level* L, vlasov_level_info* info) {
 }
 
 int vlasov_level_layout(const vlasov_level* L, int32_t patch, int64_t* offset, int64_t strides[4]) {
+    VK_NVTX();
     if (!L || !offset || !strides) return vk::fail(VLASOV_EINVAL, "null argument");
     if (patch < 0 || patch >= (int)L->boxes.size()) return vk::fail(VLASOV_EINVAL, "patch out of range");
     const int b = L->patch_block[patch];
@@ -1316,6 +1330,7 @@ int vlasov_level_layout(const vlasov_level* L, int32_t patch, int64_t* offset, i
 
 int vlasov_level_ghost_map(const vlasov_level* L, int32_t patch, int32_t* kind, int32_t* src_patch,
                            int64_t* src_cell) {
+    VK_NVTX();
     if (!L || !kind || !src_patch || !src_cell) return vk::fail(VLASOV_EINVAL, "null argument");
     if (patch < 0 || patch >= (int)L->boxes.size()) return vk::fail(VLASOV_EINVAL, "patch out of range");
     const int nd = L->ndim;
@@ -1357,6 +1372,7 @@ int vlasov_level_ghost_map(const vlasov_level* L, int32_t patch, int32_t* kind, 
 // Alg.7 ComputeSubPatches
 int vlasov_subpatches(const vlasov_level* const* levels, int32_t nlev, int32_t li, int32_t patch,
                       vlasov_box* out, int32_t cap, int32_t* n) {
+    VK_NVTX();
     if (!levels || !n || li < 0 || li >= nlev) return vk::fail(VLASOV_EINVAL, "bad arguments");
     const vlasov_level* L = levels[li];
     if (patch < 0 || patch >= (int)L->boxes.size()) return vk::fail(VLASOV_EINVAL, "patch out of range");
@@ -1374,6 +1390,7 @@ int vlasov_subpatches(const vlasov_level* const* levels, int32_t nlev, int32_t l
 
 int vlasov_tags_to_boxes(const uint8_t* tags, const int32_t domain_cells[4], int32_t ndim, const int32_t ratio[4],
                          int32_t tile, vlasov_box* out, int32_t cap, int32_t* n) {
+    VK_NVTX();
     if (!tags || !domain_cells || !ratio || !n || ndim != 2) return vk::fail(VLASOV_EINVAL, "bad arguments");
     int foot[2];
     for (int d = 0; d < 2; ++d) {
@@ -1500,6 +1517,7 @@ struct Clusterer {
 int vlasov_cluster_tags(const uint8_t* tags, const int32_t shape[2], const int32_t lo[2],
                         const int32_t smallest[2], const int32_t largest[2], double efficiency,
                         vlasov_box* out, int32_t cap, int32_t* n) {
+    VK_NVTX();
     if (!tags || !shape || !lo || !smallest || !largest || !n) return vk::fail(VLASOV_EINVAL, "null argument");
     if (shape[0] < 0 || shape[1] < 0 || !(efficiency > 0.0) || efficiency > 1.0)
         return vk::fail(VLASOV_EINVAL, "cluster_tags: bad shape or efficiency");
@@ -1527,6 +1545,7 @@ int vlasov_cluster_tags(const uint8_t* tags, const int32_t shape[2], const int32
 int vlasov_regrid_boxes(const vlasov_level* L, const uint8_t* tags, const int32_t ratio[2],
                         const int32_t smallest[2], const int32_t largest[2], double efficiency, int32_t nest,
                         vlasov_box* out, int32_t cap, int32_t* n) {
+    VK_NVTX();
     if (!L || !tags || !ratio || !smallest || !largest || !n) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "regrid_boxes: 1D+1V levels only");
     if (nest < 0 || ratio[0] < 1 || ratio[1] < 1) return vk::fail(VLASOV_EINVAL, "regrid_boxes: bad nest or ratio");
@@ -1604,6 +1623,7 @@ int vlasov_regrid_boxes(const vlasov_level* L, const uint8_t* tags, const int32_
 // ---------------------------------------------------------------- compute entry points
 int vlasov_fill_ghosts(vlasov_level* L, double* f, const vlasov_level* coarser, const double* f_coarse,
                        const double* E_bc, const double* f0v, int32_t interp) {
+    VK_NVTX();
     if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim == 4 && !L->ghost4_built) {
         // a 2D+2V level stored as one block (the stage kernel derives its ghosts itself): the task
@@ -1634,6 +1654,7 @@ int vlasov_fill_ghosts(vlasov_level* L, double* f, const vlasov_level* coarser, 
 }
 
 int vlasov_rhs(vlasov_level* L, const double* f, const double* E, double* k, int32_t recon) {
+    VK_NVTX();
     if (!L || !f || !E || !k) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "rhs: 2D+2V not in this build yet");
@@ -1643,6 +1664,7 @@ int vlasov_rhs(vlasov_level* L, const double* f, const double* E, double* k, int
 int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, const double* f_s, double* u,
                      double* f_next, const double* E, const double* E_bc, const double* f0v, int32_t recon,
                      double* rho_next) {
+    VK_NVTX();
     if (!L || !f_s || !f_next || !E) return vk::fail(VLASOV_EINVAL, "null argument");
     if (stage < 1 || stage > 4) return vk::fail(VLASOV_EINVAL, "stage must be 1..4");
     if (stage >= 2 && !f_n) return vk::fail(VLASOV_EINVAL, "f_n required");
@@ -1667,6 +1689,7 @@ int vlasov_rk4_stage(vlasov_level* L, int32_t stage, double dt, double* f_n, con
 int vlasov_rk4_stage_vp(vlasov_level* L, const vlasov_poisson* plan, int32_t stage, double dt, double* f_n,
                         const double* f_s, double* u, double* f_next, const double* rho_s, double* E_s,
                         const double* E_bc, const double* f0v, int32_t recon, double* rho_next) {
+    VK_NVTX();
     if (!L || !plan || !f_s || !f_next || !rho_s || !E_s || !f0v)
         return vk::fail(VLASOV_EINVAL, "null argument");
     if (stage < 1 || stage > 4) return vk::fail(VLASOV_EINVAL, "stage must be 1..4");
@@ -1691,6 +1714,7 @@ int vlasov_rk4_stage_vp(vlasov_level* L, const vlasov_poisson* plan, int32_t sta
 
 int vlasov_reduce_charge(const vlasov_level* const* levels, int32_t nlev, const double* const* f, double q,
                          double base, int32_t accumulate, double* rho_finest) {
+    VK_NVTX();
     if (!levels || nlev < 1 || !rho_finest || !f) return vk::fail(VLASOV_EINVAL, "null argument");
     if (nlev > vk::MAXLEV) return vk::fail(VLASOV_EUNSUPPORTED, "more than 8 levels");
     for (int l = 0; l < nlev; ++l)
@@ -1732,11 +1756,13 @@ int vlasov_reduce_charge(const vlasov_level* const* levels, int32_t nlev, const 
 
 int vlasov_reduce_moment(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
                          double* rho_finest) {
+    VK_NVTX();
     return vlasov_reduce_charge(levels, nlev, f, -1.0, 1.0, 0, rho_finest);
 }
 
 int vlasov_reduce_current(const vlasov_level* const* levels, int32_t nlev, const double* const* f, double q,
                           int32_t accumulate, double* j) {
+    VK_NVTX();
     if (!levels || nlev < 1 || !f || !j) return vk::fail(VLASOV_EINVAL, "null argument");
     if (nlev > vk::MAXLEV) return vk::fail(VLASOV_EUNSUPPORTED, "more than 8 levels");
     for (int l = 0; l < nlev; ++l) {
@@ -1761,6 +1787,7 @@ int vlasov_reduce_current(const vlasov_level* const* levels, int32_t nlev, const
 }
 
 int vlasov_level_set_moment_base(vlasov_level* L, double base) {
+    VK_NVTX();
     if (!L) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!L->single_block) return vk::fail(VLASOV_EUNSUPPORTED, "moment base: one periodic block only");
     L->moment_base = base;
@@ -1768,6 +1795,7 @@ int vlasov_level_set_moment_base(vlasov_level* L, double base) {
 }
 
 int vlasov_level_set_velocity_faces(vlasov_level* L, int32_t phys_lo, int32_t phys_hi) {
+    VK_NVTX();
     if (!L) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!L->single_block || L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "velocity faces: one periodic 1D+1V block only");
     L->vphys[0] = phys_lo ? 1 : 0;
@@ -1776,6 +1804,7 @@ int vlasov_level_set_velocity_faces(vlasov_level* L, int32_t phys_lo, int32_t ph
 }
 
 int vlasov_vslab_pack(const vlasov_level* L, const double* f, double* lo, double* hi) {
+    VK_NVTX();
     if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 2 || !L->single_block || L->dom[1] < 2)
         return vk::fail(VLASOV_EUNSUPPORTED, "vslab: one 1D+1V block with >= 2 velocity cells");
@@ -1784,6 +1813,7 @@ int vlasov_vslab_pack(const vlasov_level* L, const double* f, double* lo, double
 }
 
 int vlasov_vslab_unpack(const vlasov_level* L, double* f, const double* lo, const double* hi) {
+    VK_NVTX();
     if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 2 || !L->single_block || L->dom[1] < 2)
         return vk::fail(VLASOV_EUNSUPPORTED, "vslab: one 1D+1V block with >= 2 velocity cells");
@@ -1792,6 +1822,7 @@ int vlasov_vslab_unpack(const vlasov_level* L, double* f, const double* lo, cons
 }
 
 int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream) {
+    VK_NVTX();
     if (!x || !out || n < 0) return vk::fail(VLASOV_EINVAL, "null argument or n < 0");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     return vk::launch_absmax(x, n, out, (cudaStream_t)cuda_stream);
@@ -1802,6 +1833,7 @@ int vlasov_absmax(const double* x, int64_t n, double* out, void* cuda_stream) {
 // finest level's velocity domain; max|E_l| on the device (k_absmax), one 8-byte read per level.
 int vlasov_next_dt(const vlasov_level* const* levels, int32_t nlev, const double* const* E, double dt_prev,
                    double cfl, double growth, double* dt_out) {
+    VK_NVTX();
     if (!levels || !E || !dt_out || nlev < 1) return vk::fail(VLASOV_EINVAL, "null argument or nlev < 1");
     if (!(cfl > 0.0) || !(growth > 0.0) || !(dt_prev > 0.0)) return vk::fail(VLASOV_EINVAL, "next_dt: cfl, growth, dt_prev > 0");
     for (int l = 0; l < nlev; ++l)
@@ -1912,6 +1944,7 @@ static int build_mask_plan(const vlasov_level* const* levels, int nlev, vk::Mask
 
 int vlasov_reduce_moment_mask(const vlasov_level* const* levels, int32_t nlev, const double* const* f,
                               double* rho_finest) {
+    VK_NVTX();
     if (!levels || nlev < 1 || !rho_finest || !f) return vk::fail(VLASOV_EINVAL, "null argument");
     if (nlev > vk::MAXLEV) return vk::fail(VLASOV_EUNSUPPORTED, "more than 8 levels");
     for (int l = 0; l < nlev; ++l)
@@ -1949,6 +1982,7 @@ int vlasov_reduce_moment_mask(const vlasov_level* const* levels, int32_t nlev, c
 //   g_x(m, n) = (1/N) sum_{(p,q) != 0} S_x(p) / Lambda sin(th_p m) cos(th_q n),  S_x = (16 sin th - 2 sin 2th)/dx
 //   g_y(m, n) = (1/N) sum_{(p,q) != 0} S_y(q) / Lambda cos(th_p m) sin(th_q n)
 int vlasov_poisson2d_create(int32_t nx, int32_t ny, double dx, double dy, void* cuda_stream, vlasov_poisson2d** out) {
+    VK_NVTX();
     if (!out) return vk::fail(VLASOV_EINVAL, "null argument");
     *out = nullptr;
     if (nx < 5 || ny < 5 || !(dx > 0) || !(dy > 0)) return vk::fail(VLASOV_EINVAL, "poisson2d: need nx, ny >= 5 and dx, dy > 0");
@@ -2014,12 +2048,14 @@ int vlasov_poisson2d_create(int32_t nx, int32_t ny, double dx, double dy, void* 
 }
 
 int vlasov_poisson2d_solve(const vlasov_poisson2d* P, const double* rho, double* E) {
+    VK_NVTX();
     if (!P || !rho || !E) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     return vk::launch_poisson2d(P, rho, E);
 }
 
 int vlasov_poisson2d_destroy(vlasov_poisson2d* P) {
+    VK_NVTX();
     if (!P) return VLASOV_OK;
     vk::dfree(P->d_gx, P->stream);
     vk::dfree(P->d_gy, P->stream);
@@ -2028,6 +2064,7 @@ int vlasov_poisson2d_destroy(vlasov_poisson2d* P) {
 }
 
 int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisson** out) {
+    VK_NVTX();
     if (!out) return vk::fail(VLASOV_EINVAL, "null argument");
     *out = nullptr;
     if (n < 5 || !(dx > 0)) return vk::fail(VLASOV_EINVAL, "poisson: need n >= 5 and dx > 0");
@@ -2108,6 +2145,7 @@ int vlasov_poisson_create(int32_t n, double dx, void* cuda_stream, vlasov_poisso
 }
 
 int vlasov_poisson_solve(vlasov_poisson* P, const double* rho, double* phi, double* E, int32_t ghost) {
+    VK_NVTX();
     if (!P || !rho) return vk::fail(VLASOV_EINVAL, "null argument");
     if (ghost < 0 || ghost > P->n) return vk::fail(VLASOV_EINVAL, "bad ghost width");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
@@ -2115,6 +2153,7 @@ int vlasov_poisson_solve(vlasov_poisson* P, const double* rho, double* phi, doub
 }
 
 int vlasov_poisson_destroy(vlasov_poisson* P) {
+    VK_NVTX();
     if (P) {
         vk::dfree(P->d_gE, P->stream);
         vk::dfree(P->d_gphi, P->stream);
@@ -2127,6 +2166,7 @@ int vlasov_poisson_destroy(vlasov_poisson* P) {
 }
 
 int vlasov_inject_field(vlasov_level* L, const double* E_finest, const int32_t n_finest[2], double* E_lvl) {
+    VK_NVTX();
     if (!L || !E_finest || !n_finest || !E_lvl) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
     if (L->ndim == 2) return vk::launch_inject_1d(L, E_finest, n_finest[0], E_lvl);
@@ -2134,6 +2174,7 @@ int vlasov_inject_field(vlasov_level* L, const double* E_finest, const int32_t n
 }
 
 int vlasov_level_face_doubles(const vlasov_level* L, int64_t* n) {
+    VK_NVTX();
     if (!L || !n) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "face_doubles: 2D+2V levels (F* form)");
     *n = L->face_doubles;
@@ -2142,6 +2183,7 @@ int vlasov_level_face_doubles(const vlasov_level* L, int64_t* n) {
 
 int vlasov_rk4_stage_fstar(vlasov_level* L, int32_t stage, double dt, const double* f_n, const double* f_s,
                            double* f_next, const double* E, int32_t recon, double* Fstar) {
+    VK_NVTX();
     if (!L || !f_n || !f_s || !E || !Fstar) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "rk4_stage_fstar: 2D+2V levels");
     if (stage < 1 || stage > 4) return vk::fail(VLASOV_EINVAL, "stage must be 1..4");
@@ -2153,6 +2195,7 @@ int vlasov_rk4_stage_fstar(vlasov_level* L, int32_t stage, double dt, const doub
 }
 
 int vlasov_fstar_coarsen(const vlasov_level* fine, const double* F_fine, const vlasov_level* coarse, double* F_coarse) {
+    VK_NVTX();
     if (!fine || !F_fine || !coarse || !F_coarse) return vk::fail(VLASOV_EINVAL, "null argument");
     if (fine->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "fstar_coarsen: 2D+2V levels");
     if (fine->coarser != coarse || coarse->uid != fine->coarser_uid)
@@ -2162,6 +2205,7 @@ int vlasov_fstar_coarsen(const vlasov_level* fine, const double* F_fine, const v
 }
 
 int vlasov_fstar_update(vlasov_level* L, double dt, const double* f_n, const double* Fstar, double* f_new) {
+    VK_NVTX();
     if (!L || !f_n || !Fstar || !f_new) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "fstar_update: 2D+2V levels");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
@@ -2169,6 +2213,7 @@ int vlasov_fstar_update(vlasov_level* L, double dt, const double* f_n, const dou
 }
 
 int vlasov_inject_field_ghosted(vlasov_level* L, const double* E_finest, const int32_t n_finest[2], double* E_lvl) {
+    VK_NVTX();
     if (!L || !E_finest || !n_finest || !E_lvl) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 4) return vk::fail(VLASOV_EUNSUPPORTED, "inject_field_ghosted: 2D+2V levels");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
@@ -2177,6 +2222,7 @@ int vlasov_inject_field_ghosted(vlasov_level* L, const double* E_finest, const i
 
 int vlasov_inject_field_scaled(vlasov_level* L, const double* E_finest, const int32_t n_finest[2], double scale,
                                double* E_lvl) {
+    VK_NVTX();
     if (!L || !E_finest || !n_finest || !E_lvl) return vk::fail(VLASOV_EINVAL, "null argument");
     if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "inject_field_scaled: 1D+1V levels only");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
@@ -2186,6 +2232,7 @@ int vlasov_inject_field_scaled(vlasov_level* L, const double* E_finest, const in
 int vlasov_flux_register_accumulate(vlasov_level* fine, const double* f_fine, const double* E_fine,
                                     const double* f_coarse, const double* E_coarse, double b_s, double* regs,
                                     int32_t recon) {
+    VK_NVTX();
     if (!fine || !f_fine || !E_fine || !f_coarse || !E_coarse) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!fine->coarser) return vk::fail(VLASOV_EINVAL, "flux registers: level has no coarser level");
     if (fine->n_reflux > 0 && !regs) return vk::fail(VLASOV_EINVAL, "flux registers: regs required");
@@ -2196,6 +2243,7 @@ int vlasov_flux_register_accumulate(vlasov_level* fine, const double* f_fine, co
 }
 
 int vlasov_average_down(vlasov_level* fine, const double* f_fine, double* f_coarse, const double* regs, double dt) {
+    VK_NVTX();
     if (!fine || !f_fine || !f_coarse) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!fine->coarser) return vk::fail(VLASOV_EINVAL, "average_down: level has no coarser level");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
@@ -2207,6 +2255,7 @@ int vlasov_average_down(vlasov_level* fine, const double* f_fine, double* f_coar
 }
 
 int vlasov_tag_cells(vlasov_level* L, const double* f, double tol, int32_t buffer, uint8_t* tags) {
+    VK_NVTX();
     if (!L || !f || !tags) return vk::fail(VLASOV_EINVAL, "null argument");
     if (buffer < 0) return vk::fail(VLASOV_EINVAL, "tag buffer < 0");
     if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "tag_cells: 1D+1V levels only");
@@ -2216,6 +2265,7 @@ int vlasov_tag_cells(vlasov_level* L, const double* f, double tol, int32_t buffe
 
 int vlasov_level_fill_from(vlasov_level* L, double* f, const vlasov_level* old, const double* f_old,
                            const vlasov_level* coarser, const double* f_coarse, int32_t interp) {
+    VK_NVTX();
     if (!L || !f) return vk::fail(VLASOV_EINVAL, "null argument");
     if (old && !f_old) return vk::fail(VLASOV_EINVAL, "fill_from: f_old required with old");
     if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "fill_from: 1D+1V only");
