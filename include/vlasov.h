@@ -150,11 +150,14 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
  * rows are never read), and the velocity ghosts of f_s follow the characteristic v-boundary
  * condition (reading #6) either derived in-kernel from E_bc (E_bc non-NULL, exactly as
  * vlasov_fill_ghosts(E_bc, f0v) would) or, with E_bc == NULL ("carried ghosts"), read from f_s's
- * velocity ghost columns.  Stage 1 always derives them in-kernel from its own field E, which is
- * E(f_n), the end-of-step constraint evaluation of Alg.5 (reading #6b); E_bc is
- * ignored at stage 1.  With f0v non-NULL the stage also writes f_next's velocity ghost columns
- * (interior rows) for the field E of this stage -- the E_bc of the next stage (reading #6b) -- so a
- * chain of stages with E_bc == NULL needs no ghost fill at all.  Only the velocity faces the
+ * velocity ghost columns.  Stage 1 decides the direction with its own field E, which is E(f_n),
+ * the end-of-step constraint evaluation of Alg.5 (reading #6b); E_bc is ignored at
+ * stage 1 (with E_bc == NULL the carried ghost columns of f_n must hold the outgoing candidate,
+ * the cubic extrapolation, wherever E(f_n) is outgoing -- stage 4 writes it there, and so does
+ * vlasov_fill_ghosts with E(f_n)).  With f0v non-NULL the stage also writes f_next's velocity
+ * ghost columns (interior rows) for the field E of this stage -- the E_bc of the next stage
+ * (reading #6b); stage 4 writes the cubic extrapolation -- so a chain of steps with E_bc == NULL
+ * needs one vlasov_fill_ghosts of the initial state only.  Only the velocity faces the
  * level marks physical (vlasov_level_set_velocity_faces; default both) get the boundary
  * condition in-kernel; a non-physical face keeps the ghost columns stored in f_s.
  * With f0v == NULL (E_bc must be NULL too) the ghost frame of f_s must have been filled by

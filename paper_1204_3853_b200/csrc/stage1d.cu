@@ -568,13 +568,16 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     // the thread holding domain cells 0..3 / nv-4 .. nv-1 (SELF: level nv % 4 == 0)
     const bool edge_lo = SELF && (B.lo_v + c0 == 0);
     const bool edge_hi = SELF && (B.lo_v + c0 + CPT == A.dom_v);
-    // GM 1: input v-ghosts derived in-kernel from E_bc; GM 2: read from f_s's ghost columns, except
-    // at stage 1, whose boundary field is its own E = E(f_n) (the end-of-step constraint evaluation
-    // of Alg.5, reading #6b): derived in-kernel from E.  Only at physical velocity faces.
-    // SELF: the edge threads stage f_next's boundary cells; its velocity ghost columns for this
-    // stage's field E are written after the march, off the critical path
-    constexpr bool BC_IN = (GM == 1) || (GM == 2 && STAGE == 1);
-    const bool lo_edge = BC_IN && edge_lo && A.phys_lo, hi_edge = BC_IN && edge_hi && A.phys_hi;
+    // GM 1: input v-ghosts derived in-kernel from E_bc (at stage 1 from its own E = E(f_n), the
+    // end-of-step constraint evaluation of Alg.5, reading #6b).  GM 2: read from f_s's
+    // ghost columns, written by the stage that produced f_s for its own field -- except that
+    // stage 4 writes the outgoing candidate (the cubic extrapolation) and stage 1 decides with its
+    // own E: a branch-free select between the carried value and the unperturbed profile (SEL1).
+    // Only at physical velocity faces.  SELF: the edge threads stage f_next's boundary cells; its
+    // velocity ghost columns are written after the march, off the critical path
+    constexpr bool BC_IN = (GM == 1);
+    constexpr bool SEL1 = (GM == 2 && STAGE == 1);
+    const bool lo_edge = (BC_IN || SEL1) && edge_lo && A.phys_lo, hi_edge = (BC_IN || SEL1) && edge_hi && A.phys_hi;
     const double* Ebcf = (STAGE == 1) ? E : Ebc;   // the field deciding the direction
     constexpr bool GHOST_OUT = SELF && STAGE >= 1;
 
@@ -637,6 +640,15 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                     v[L + 2] = s_f0[3];
                 }
             }
+        }
+        if (SEL1) {                              // stage 1, carried ghosts: keep the extrapolation
+            const double a = -E[r];              // if outgoing, else the unperturbed profile
+            constexpr int L = CPT + 1;
+            const bool klo = !lo_edge || (a < 0.0), khi = !hi_edge || (a > 0.0);
+            v[1] = klo ? v[1] : s_f0[1];
+            v[0] = klo ? v[0] : s_f0[0];
+            v[L + 1] = khi ? v[L + 1] : s_f0[2];
+            v[L + 2] = khi ? v[L + 2] : s_f0[3];
         }
 #pragma unroll
         for (int b = 0; b < CPT + 2; ++b) W[K][b] = v[b + 1];   // register window: row r -> W[K]
@@ -798,7 +810,8 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
             if (side == 0 ? !has_lo : !has_hi) continue;
             const int i = T.x0 + rr;
             const double* se = s_edge + (rr * 2 + side) * CPT;
-            const double a = -E[i];
+            // stage 4: the outgoing candidate for the next stage 1 (SEL1 decides with E(f_n))
+            const double a = (STAGE == 4 && GM == 2) ? (side == 0 ? -1.0 : 1.0) : -E[i];
             double2 g;
             if (side == 0) {
                 g = a < 0.0 ? make_double2(10.0 * se[0] - 20.0 * se[1] + 15.0 * se[2] - 4.0 * se[3],

@@ -327,10 +327,11 @@ def test_strip_shift_changes_no_result(tmp_path):
 @pytest.mark.parametrize("mode", list(MODES))
 def test_stage1_boundary_uses_own_field(mode):
     """Reading #6b (Alg.5): stage 1's characteristic boundary condition uses E(f_n), the
-    stage's own field -- not whatever the velocity ghost columns of f_n hold (carried modes) nor
-    the E_bc buffer (in-kernel E_bc modes).  Both are made adversarial (junk ghost columns, E_bc of
-    the opposite sign) on a state with O(1) boundary values; the step must still equal the
-    oracle's (tests/test_oracle_alg5.py pins that the boundary field matters here)."""
+    stage's own field -- not the E_bc buffer.  In the in-kernel E_bc modes and with stored ghosts
+    the ghost columns of f_n are junk as well (they are derived, not read); in the carried modes
+    stage 1 keeps the carried outgoing candidate (written by stage 4 / set_state) or replaces it by
+    the profile, deciding with E(f_n).  State with O(1) boundary values (tests/test_oracle_alg5.py
+    pins that the boundary field matters here); the steps must equal the oracle's."""
     import test_oracle_alg5 as alg5
     w, prob, f0, dt = alg5.heavy_tail_problem()
     kw = MODES[mode]
@@ -340,9 +341,10 @@ def test_stage1_boundary_uses_own_field(mode):
                         carry_ghosts=kw.get("carry_ghosts", True))
     S.set_state(f0)
     with torch.cuda.stream(S.stream):
-        g = S.level.patch_view(S.A, 0, 2)
-        g[:, 0:2] = 1.0e3                    # junk velocity ghosts of f_n
-        g[:, -2:] = -1.0e3
+        if not kw.get("carry_ghosts", True) or not kw.get("self_ghost", True):
+            g = S.level.patch_view(S.A, 0, 2)
+            g[:, 0:2] = 1.0e3                # junk velocity ghosts of f_n
+            g[:, -2:] = -1.0e3
         S.E[0].neg_()                        # E_bc buffer of stage 1: the opposite sign
     f, E_bc = f0, prob.constraints(f0)
     for n in range(3):
