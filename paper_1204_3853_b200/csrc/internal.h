@@ -342,6 +342,9 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
 int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
                       double* rho);
+bool stage_2d2v_tel_ok(const vlasov_level* L);
+int launch_stage_2d2v_tel(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
+                          double* f_next, const double* E, double* rho_partials);
 int launch_moment_2d2v(const vlasov_level* L, const double* f, double* rho);
 int stage_1d1v_ctas_per_sm(bool wide, int tile_rows);
 int stage_1d1v_tile_width(bool wide);   // cells per v-tile of the stage kernel

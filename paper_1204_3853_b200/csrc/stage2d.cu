@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.h"
@@ -657,8 +658,14 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
         VK_CUDA(launch_pdl(k_vghost_2d2v, dim3((unsigned)(A.nx * A.ny)), dim3(128), 0, L->stream,
                            const_cast<double*>(f_s), A.org, A.s0, A.s1, A.s2, A.nx, A.ny, A.nvx, A.nvy, E_bc, f0v));
     }
-    rc = recon == VLASOV_UPWIND ? dispatch2<VLASOV_UPWIND>(stage, A, M, grid, L->stream)
-                                : dispatch2<VLASOV_CENTERED4>(stage, A, M, grid, L->stream);
+    static const bool faces = std::getenv("VLASOV_C5_FACES") != nullptr;   // experiment: face form
+    if (recon == VLASOV_CENTERED4 && !faces && stage_2d2v_tel_ok(L)) {
+        // CENTERED4: telescoped form (stage2d_tel.cu); the moment partials have the same layout
+        rc = launch_stage_2d2v_tel(L, stage, dt, f_n, f_s, u, f_next, E, rho ? L->d_partials : nullptr);
+    } else {
+        rc = recon == VLASOV_UPWIND ? dispatch2<VLASOV_UPWIND>(stage, A, M, grid, L->stream)
+                                    : dispatch2<VLASOV_CENTERED4>(stage, A, M, grid, L->stream);
+    }
     if (rc || !rho) return rc;
     const int ncfg = A.nx * A.ny;
     VK_CUDA(launch_pdl(k_moment_2d2v_finish, dim3((ncfg + 31) / 32), dim3(32, 8), 0, L->stream,
