@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <algorithm>
 #include <type_traits>
 
 #include "internal.h"
@@ -502,32 +503,47 @@ __global__ void k_vghost_2d2v(double* __restrict__ f, int64_t org, int64_t s0, i
                               int nvx, int nvy, const double* __restrict__ E_bc, const double* __restrict__ f0v) {
     griddep_wait();
     griddep_launch_dependents();
-    // block = one (x, y) column: threads [0, nvx) the vy ghosts of vx line li, threads
-    // [nvx, nvx + nvy) the vx ghosts at vy index li; all loads issued before the stores
+    // block = one (x, y) column: threads [0, nvx) the vy ghosts of vx line t (16-B loads of the
+    // 4 cells next to each end, one 16-B store per end), threads [nvx, nvx + nvy/2) the vx ghosts
+    // at the vy cell pair 2(t - nvx), +1 (16-B loads along vy, coalesced across threads).  Rows
+    // are 16-B aligned: org, the strides and nvy are even (level layout, nvy even).
     const int c = blockIdx.x;                                     // i * ny + k
     const int i = c / ny, k = c - (c / ny) * ny;
     const int nyg = ny + 4;
     const int64_t col = (int64_t)(i + 2) * nyg + (k + 2);
     double* base = f + org + (int64_t)i * s0 + (int64_t)k * s1;
-    for (int t = threadIdx.x; t < nvx + nvy; t += blockDim.x) {
-        const bool vy = t < nvx;
-        const int li = vy ? t : t - nvx;
-        const double a = -__ldg(E_bc + (vy ? (int64_t)(nx + 4) * nyg : 0) + col);
-        const int64_t st = vy ? 1 : s2;                           // stride along the ghosted dim
-        double* line = vy ? base + (int64_t)li * s2 : base + li;  // element 0 of the ghosted dim
-        const int n = vy ? nvy : nvx;
-        const double* pr = vy ? f0v + (int64_t)(li + 2) * (nvy + 4) + 2 : f0v + 2 * (int64_t)(nvy + 4) + (li + 2);
-        const int64_t pst = vy ? 1 : nvy + 4;                     // profile at ghosted index g: pr[g * pst]
-        double* e = line + (int64_t)(n - 1) * st;
-        const double l0 = line[0], l1 = line[st], l2 = line[2 * st], l3 = line[3 * st];
-        const double h0 = e[0], h1 = e[-st], h2 = e[-2 * st], h3 = e[-3 * st];
-        const double pm1 = __ldg(pr - pst), pm2 = __ldg(pr - 2 * pst);
-        const double pn = __ldg(pr + (int64_t)n * pst), pn1 = __ldg(pr + (int64_t)(n + 1) * pst);
+    auto ld2 = [](const double* q) { return *reinterpret_cast<const double2*>(q); };
+    auto st2 = [](double* q, double a, double b) { *reinterpret_cast<double2*>(q) = make_double2(a, b); };
+    auto ex1 = [](double f0, double f1, double f2, double f3) { return 4.0 * f0 - 6.0 * f1 + 4.0 * f2 - f3; };
+    auto ex2 = [](double f0, double f1, double f2, double f3) { return 10.0 * f0 - 20.0 * f1 + 15.0 * f2 - 4.0 * f3; };
+    for (int t = threadIdx.x; t < nvx + nvy / 2; t += blockDim.x) {
+      if (t < nvx) {
+        const double a = -__ldg(E_bc + (int64_t)(nx + 4) * nyg + col);
+        double* line = base + (int64_t)t * s2;                    // m = 0
+        const double2 l01 = ld2(line), l23 = ld2(line + 2);
+        const double2 h32 = ld2(line + nvy - 4), h10 = ld2(line + nvy - 2);
+        const double* pr = f0v + (int64_t)(t + 2) * (nvy + 4);     // profile at ghosted m index
+        const double2 plo = ld2(pr), phi = ld2(pr + nvy + 2);      // m = -2, -1 and nvy, nvy+1
         const bool out_lo = a < 0.0, out_hi = a > 0.0;
-        line[-st] = out_lo ? 4.0 * l0 - 6.0 * l1 + 4.0 * l2 - l3 : pm1;
-        line[-2 * st] = out_lo ? 10.0 * l0 - 20.0 * l1 + 15.0 * l2 - 4.0 * l3 : pm2;
-        e[st] = out_hi ? 4.0 * h0 - 6.0 * h1 + 4.0 * h2 - h3 : pn;
-        e[2 * st] = out_hi ? 10.0 * h0 - 20.0 * h1 + 15.0 * h2 - 4.0 * h3 : pn1;
+        st2(line - 2, out_lo ? ex2(l01.x, l01.y, l23.x, l23.y) : plo.x, out_lo ? ex1(l01.x, l01.y, l23.x, l23.y) : plo.y);
+        st2(line + nvy, out_hi ? ex1(h10.y, h10.x, h32.y, h32.x) : phi.x, out_hi ? ex2(h10.y, h10.x, h32.y, h32.x) : phi.y);
+      } else {
+        const double a = -__ldg(E_bc + col);
+        const int m = 2 * (t - nvx);
+        double* cm = base + m;                                    // (l = 0, m)
+        const double2 f0 = ld2(cm), f1 = ld2(cm + s2), f2 = ld2(cm + 2 * s2), f3 = ld2(cm + 3 * s2);
+        double* ce = cm + (int64_t)(nvx - 1) * s2;
+        const double2 g0 = ld2(ce), g1 = ld2(ce - s2), g2 = ld2(ce - 2 * s2), g3 = ld2(ce - 3 * s2);
+        const int64_t pst = nvy + 4;
+        const double* pr = f0v + 2 * pst + (m + 2);                // profile (l = 0, m)
+        const double2 pm1 = ld2(pr - pst), pm2 = ld2(pr - 2 * pst);
+        const double2 pn = ld2(pr + nvx * pst), pn1 = ld2(pr + (nvx + 1) * pst);
+        const bool out_lo = a < 0.0, out_hi = a > 0.0;
+        st2(cm - s2, out_lo ? ex1(f0.x, f1.x, f2.x, f3.x) : pm1.x, out_lo ? ex1(f0.y, f1.y, f2.y, f3.y) : pm1.y);
+        st2(cm - 2 * s2, out_lo ? ex2(f0.x, f1.x, f2.x, f3.x) : pm2.x, out_lo ? ex2(f0.y, f1.y, f2.y, f3.y) : pm2.y);
+        st2(ce + s2, out_hi ? ex1(g0.x, g1.x, g2.x, g3.x) : pn.x, out_hi ? ex1(g0.y, g1.y, g2.y, g3.y) : pn.y);
+        st2(ce + 2 * s2, out_hi ? ex2(g0.x, g1.x, g2.x, g3.x) : pn1.x, out_hi ? ex2(g0.y, g1.y, g2.y, g3.y) : pn1.y);
+      }
     }
 }
 
@@ -655,7 +671,7 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
         (rc = encode_map(L, f_n ? f_n : f_s, S2_TM, 4, &M.fn4)) || (rc = encode_map(L, u ? u : f_s, S2_TM, 4, &M.u4)))
         return rc;
     if (S2_GLOBAL_GHOSTS) {
-        VK_CUDA(launch_pdl(k_vghost_2d2v, dim3((unsigned)(A.nx * A.ny)), dim3(128), 0, L->stream,
+        VK_CUDA(launch_pdl(k_vghost_2d2v, dim3((unsigned)(A.nx * A.ny)), dim3((unsigned)std::min(1024, (A.nvx + A.nvy / 2 + 31) / 32 * 32)), 0, L->stream,
                            const_cast<double*>(f_s), A.org, A.s0, A.s1, A.s2, A.nx, A.ny, A.nvx, A.nvy, E_bc, f0v));
     }
     static const bool faces = std::getenv("VLASOV_C5_FACES") != nullptr;   // experiment: face form
