@@ -3,6 +3,8 @@
 // injection to a level.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -353,8 +355,148 @@ __global__ void __launch_bounds__(P2_THREADS) k_poisson2d(const double* __restri
     }
 }
 
+// Toeplitz-blocked variant (ny in {8, 16, ..., 256}): thread (subset s, output block b) sums, for the
+// i' of its subset (i' = s, s + S, ...), the 8 outputs k = 8b .. 8b+7 of row i with a sliding
+// register window of the Green's functions (one new g value per component and k', one broadcast
+// rho value, 16 FMAs); the S subset partials are added in subset order (deterministic).
+constexpr int P2T_K = 8;
+// Launched as clusters of P2T_SPLIT CTAs per output row: CTA rank c of the cluster takes the i'
+// of every P2T_SPLIT-th subset; rank 0 adds the ranks' partials (DSMEM) in rank order.
+constexpr int P2T_SPLIT = 2;
+__global__ void __launch_bounds__(P2_THREADS) k_poisson2d_tb(const double* __restrict__ rho, const double* __restrict__ gx,
+                                                              const double* __restrict__ gy, int nx, int ny,
+                                                              double* __restrict__ E) {
+    griddep_wait();
+    griddep_launch_dependents();
+    extern __shared__ double sm[];
+    const int n = nx * ny;
+    double* s_rho = sm;                                   // [n]
+    double* s_gx = sm + n;                                // [n]
+    double* s_gy = s_gx + n;                              // [n]
+    double* s_part = s_gy + n;                            // [2][P2_THREADS][8]
+    __shared__ double s_red[P2_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc = 0.0;
+    for (int t = tid; t < n; t += P2_THREADS) {
+        const double v = rho[t];
+        s_rho[t] = v;
+        acc += v;
+        s_gx[t] = gx[t];
+        s_gy[t] = gy[t];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) s_red[warp] = acc;
+    __syncthreads();
+    double mean = 0.0;
+#pragma unroll
+    for (int w = 0; w < P2_THREADS / 32; ++w) mean += s_red[w];
+    mean /= (double)n;
+    for (int t = tid; t < n; t += P2_THREADS) s_rho[t] -= mean;
+    __syncthreads();
+    const int i = blockIdx.x / P2T_SPLIT, crank = (int)cluster_ctarank();
+    const int nb = ny / P2T_K, S = P2_THREADS / nb;
+    const int b = tid % nb, sub = tid / nb;
+    double ax[P2T_K], ay[P2T_K];
+#pragma unroll
+    for (int j = 0; j < P2T_K; ++j) ax[j] = ay[j] = 0.0;
+    for (int ip = sub * P2T_SPLIT + crank; ip < nx; ip += S * P2T_SPLIT) {
+        const int di = i - ip < 0 ? i - ip + nx : i - ip;
+        const double* rr = s_rho + ip * ny;
+        const double* gxr = s_gx + di * ny;
+        const double* gyr = s_gy + di * ny;
+        // window w[j] = g[(8b + j - kp) mod ny]
+        double wx[P2T_K], wy[P2T_K];
+#pragma unroll
+        for (int j = 0; j < P2T_K; ++j) { wx[j] = gxr[P2T_K * b + j]; wy[j] = gyr[P2T_K * b + j]; }
+        for (int kp0 = 0; kp0 < ny; kp0 += P2T_K) {
+#pragma unroll
+            for (int u = 0; u < P2T_K; ++u) {
+                const int kp = kp0 + u;
+                const double r = rr[kp];
+#pragma unroll
+                for (int j = 0; j < P2T_K; ++j) {
+                    // slot of output j in the rotating window after u shifts
+                    const int sl = (j - u + P2T_K * 8) % P2T_K;
+                    ax[j] = fma(wx[sl], r, ax[j]);
+                    ay[j] = fma(wy[sl], r, ay[j]);
+                }
+                // shift: the slot of output 7 becomes the slot of output 0 with g[(8b - kp - 1) mod ny]
+                const int sl7 = (P2T_K - 1 - u + P2T_K * 8) % P2T_K;
+                int q = P2T_K * b - kp - 1;
+                q += (q < 0) ? ny : 0;
+                wx[sl7] = gxr[q];
+                wy[sl7] = gyr[q];
+            }
+        }
+    }
+    double* px = s_part + (size_t)tid * P2T_K;
+    double* py = s_part + (size_t)(P2_THREADS + tid) * P2T_K;
+#pragma unroll
+    for (int j = 0; j < P2T_K; ++j) { px[j] = ax[j]; py[j] = ay[j]; }
+    cluster_sync_all();                                   // partials of every rank visible
+    const int nyg = ny + 4;
+    for (int kk = tid; kk < ny && crank == 0; kk += P2_THREADS) {
+        const int bb = kk / P2T_K, jj = kk % P2T_K;
+        double ex = 0.0, ey = 0.0;
+        for (int c = 0; c < P2T_SPLIT; ++c) {
+            const uint32_t base = map_shared_rank(s_part, (uint32_t)c);
+            for (int g = 0; g < S; ++g) {
+                double vx, vy;
+                const uint32_t ox = base + (uint32_t)(((g * nb + bb) * P2T_K + jj) * 8);
+                const uint32_t oy = base + (uint32_t)(((P2_THREADS + g * nb + bb) * P2T_K + jj) * 8);
+                asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(vx) : "r"(ox) : "memory");
+                asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(vy) : "r"(oy) : "memory");
+                ex += vx;
+                ey += vy;
+            }
+        }
+        for (int c = 0; c < 2; ++c) {
+            const double e = c ? ey : ex;
+            double* Ec = E + (int64_t)c * (nx + 4) * nyg;
+            const int rows[3] = {i + 2, i + 2 + nx, i + 2 - nx};
+            for (int r = 0; r < 3; ++r) {
+                const int gr = rows[r];
+                if (gr < 0 || gr >= nx + 4) continue;
+                double* row = Ec + (int64_t)gr * nyg;
+                row[kk + 2] = e;
+                if (kk < 2) row[kk + 2 + ny] = e;
+                if (kk >= ny - 2) row[kk + 2 - ny] = e;
+            }
+        }
+    }
+    cluster_sync_all();                                   // rank 0 done reading the other ranks
+}
+
 int launch_poisson2d(const vlasov_poisson2d* P, const double* rho, double* E) {
     const int n = P->nx * P->ny;
+    const int ny = P->ny;
+    static const bool plain = std::getenv("VLASOV_POISSON2D_PLAIN") != nullptr;   // experiment switch
+    if (!plain && ny % P2T_K == 0 && ny / P2T_K <= 32 && (32 % (ny / P2T_K)) == 0 && n <= P2_SMEM_MAX) {
+        const size_t smem = (size_t)(3 * n + 2 * P2_THREADS * P2T_K) * sizeof(double);
+        static bool cfg = false;
+        if (!cfg) {
+            VK_CUDA(cudaFuncSetAttribute(k_poisson2d_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            cfg = true;
+        }
+        cudaLaunchConfig_t cfgl = {};
+        cfgl.gridDim = dim3(P->nx * P2T_SPLIT);
+        cfgl.blockDim = dim3(P2_THREADS);
+        cfgl.dynamicSmemBytes = smem;
+        cfgl.stream = P->stream;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = VK_PDL;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = P2T_SPLIT;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfgl.attrs = at;
+        cfgl.numAttrs = 2;
+        VK_CUDA(cudaLaunchKernelEx(&cfgl, k_poisson2d_tb, rho, (const double*)P->d_gx, (const double*)P->d_gy,
+                                   P->nx, P->ny, E));
+        return VLASOV_OK;
+    }
     if (n <= P2_SMEM_MAX) {
         const size_t smem = (size_t)(3 * n + 2 * P2_THREADS) * sizeof(double);
         static bool cfg = false;

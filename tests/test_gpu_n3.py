@@ -21,7 +21,7 @@ def relerr(a, b):
     return np.max(np.abs(a - b)) / np.max(np.abs(b))
 
 
-@pytest.mark.parametrize("nx,ny", [(16, 12), (20, 36), (64, 64), (128, 96)])
+@pytest.mark.parametrize("nx,ny", [(16, 12), (20, 36), (64, 64), (128, 96), (8, 16), (40, 32), (12, 128), (6, 8)])
 def test_poisson2d_parity(nx, ny):
     rng = np.random.default_rng(nx * 1000 + ny)
     dx, dy = 2 * np.pi / nx, 2 * np.pi / ny * 0.7
