@@ -55,6 +55,7 @@ class AmrVlasov1D:
         self.f0v = []
         self.regs = []            # per level (None for level 0)
         self.cur = 0              # which of E[l][0/1] holds E_bc
+        self._f0v_cache = {}
         with torch.cuda.stream(self.stream):
             for l, (bl, r) in enumerate(zip(level_boxes, ratios)):
                 self._append_level(bl, r)
@@ -67,8 +68,10 @@ class AmrVlasov1D:
         self.levels.append(L)
         self.bufs.append({k: L.field(0.0) for k in "ABCU"})
         self.E.append([L.efield(), L.efield()])
-        self.f0v.append(torch.as_tensor(np.ascontiguousarray(self.f0v_fn(tuple(ratio))),
-                                        dtype=torch.float64).cuda())
+        key = tuple(ratio)
+        if key not in self._f0v_cache:     # the unperturbed profile of a ratio (kept across regrids)
+            self._f0v_cache[key] = torch.as_tensor(np.ascontiguousarray(self.f0v_fn(key)), dtype=torch.float64).cuda()
+        self.f0v.append(self._f0v_cache[key])
         n = L.info.fluxreg_doubles
         self.regs.append(None if coarser is None else torch.zeros(max(1, n), dtype=torch.float64, device="cuda"))
 
@@ -167,13 +170,21 @@ class AmrVlasov1D:
         The E_bc ping-pong index returns to its value after 4 stages, so the graph is reusable."""
         key = (tuple(L.h.value for L in self.levels), float(dt))
         if getattr(self, "_graph_key", None) != key:
-            self.step(dt)
+            if getattr(self, "_graph_key", None) is None:
+                # first capture: one eager step builds the lazily created plans (Alg.8 reduction);
+                # after a regrid the constraint evaluation in regrid_to has built them already
+                self.step(dt)
+                self.stream.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._step_launches(dt)
+                self._graph, self._graph_key = g, key
+                return
             self.stream.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.stream):
                 self._step_launches(dt)
             self._graph, self._graph_key = g, key
-            return
         with torch.cuda.stream(self.stream):
             self._graph.replay()
 

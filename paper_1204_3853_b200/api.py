@@ -281,7 +281,14 @@ class Level:
         self.coarser = coarser
         self.h = vlasov_level_create(self.geom, ratio, self.boxes, coarser.h if coarser else None, stream)
         self.info = vlasov_level_get_info(self.h)
-        self.layouts = [vlasov_level_layout(self.h, p) for p in range(len(self.boxes))]
+        self._layouts = None
+
+    @property
+    def layouts(self):
+        """Per-patch (offset, strides), queried on first use (a regrid's new level needs none)."""
+        if self._layouts is None:
+            self._layouts = [vlasov_level_layout(self.h, p) for p in range(len(self.boxes))]
+        return self._layouts
 
     def __del__(self):
         try:

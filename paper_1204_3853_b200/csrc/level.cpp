@@ -1,5 +1,7 @@
 // libvlasov host side: errors, box calculus, level metadata (layout, tiles, ghost / transfer task
 // lists), Poisson plans, C ABI entry points.  See include/vlasov.h for the contract.
+#include <chrono>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -456,7 +458,7 @@ int build_ghost_tasks(vlasov_level* L, const vlasov_level* C, std::vector<int64_
     for (size_t b = 0; b < L->blocks.size(); ++b) {
         const Box& B = L->blocks[b];
         const Box GB = vk::box_grow(B, vk::G, nd);
-        for_each_cell(GB, nd, [&](const int* c) {
+        auto ghost_cell = [&](const int* c) {
             if (err) return;
             if (vk::box_contains(B, c, nd)) return;
             if (phys_code(L, c) >= 0) return;                     // PHYS: handled per column
@@ -488,7 +490,21 @@ int build_ghost_tasks(vlasov_level* L, const vlasov_level* C, std::vector<int64_
                 t.sub[d] = d < nd ? (int8_t)(w[d] - cc[d] * rr[d]) : 0;
             }
             cfs.push_back(t);
-        });
+        };
+        if (nd == 2) {
+            // the ghost frame only, row by row (x major, v fastest: the same task order as a
+            // sweep of the grown block), without visiting the interior
+            for (int x = GB.lo[0]; x <= GB.hi[0]; ++x) {
+                const bool xin = x >= B.lo[0] && x <= B.hi[0];
+                for (int v = GB.lo[1]; v <= GB.hi[1]; ++v) {
+                    if (xin && v == B.lo[1]) v = B.hi[1] + 1;
+                    const int c[4] = {x, v, 0, 0};
+                    ghost_cell(c);
+                }
+            }
+        } else {
+            for_each_cell(GB, nd, ghost_cell);
+        }
         if (err) return err;
         if (nd == 2) {
             const int nv = L->dom[1];
@@ -1209,10 +1225,23 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
     std::vector<int32_t> reflux_off;
     std::vector<vk::AvgTask> avg;
     std::vector<vk::PhysTask4> phys4;
+    static const bool prof = std::getenv("VLASOV_PROFILE_CREATE") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    const auto t0 = tnow();
+    auto t1 = t0, t2 = t0, t3 = t0;
     if (nd == 2) {
         rc = build_tiles_1d(L, device_ok_impl() != 0);
+        t1 = tnow();
         if (!rc) rc = build_ghost_tasks(L, coarser, copies, cfs, phys);
+        t2 = tnow();
         if (!rc && coarser) rc = build_amr_tasks(L, coarser, reflux, reflux_cells, reflux_off, avg);
+        t3 = tnow();
+        if (prof)
+            fprintf(stderr, "level_create build: tiles %.1f ghost %.1f amr %.1f us (copies %zu cf %zu phys %zu reflux %zu avg %zu)\n",
+                    us(t0, t1), us(t1, t2), us(t2, t3), copies.size() / 2, cfs.size(), phys.size(), reflux.size(), avg.size());
     } else if (!L->single_block) {
         // 2D+2V hierarchy level (N3): one block per patch, ghost tasks (siblings / periodic
         // images, coarse-fine) and the characteristic velocity tasks (v_x pass, then v_y pass)
@@ -1280,8 +1309,11 @@ int vlasov_level_create(const vlasov_geom* geom, const int32_t ratio_to_level0[4
         free_level(L);
         return rc;
     }
+    const auto t4 = tnow();
     cudaError_t e = cudaStreamSynchronize(L->stream);
     if (e != cudaSuccess) { free_level(L); return vk::cuda_check(e, "level_create upload"); }
+    if (prof)
+        fprintf(stderr, "level_create device: alloc+upload %.1f sync %.1f us\n", us(t3, t4), us(t4, tnow()));
     *out = L;
     return VLASOV_OK;
 }
