@@ -91,6 +91,9 @@ static size_t field_smem_bytes(int n, bool split = false) {
 constexpr int EROWS = 8;   // rows of E per warp group in the fused prologue (Toeplitz blocking)
 constexpr int HM = 16;     // half-width of the local part of the split Green's function
 
+#ifndef STAGE1D_SEL1
+#define STAGE1D_SEL1 1   // experiments: 0 drops stage 1's boundary select (wrong BC, timing only)
+#endif
 // CPT = 4 cells per consumer thread, TV = 4*NT cells per v-tile.
 #ifndef STAGE1D_CPT
 #define STAGE1D_CPT 4
@@ -165,7 +168,11 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     constexpr bool PWG = Roles<NT>::PWG;
     using SG = StageGeom<STAGE, NT>;
     constexpr int TV = SG::TV, SEG = SG::SEG, SLOT = SG::SLOT, NSLOT = SG::NSLOT, NW = SG::NW;
-    constexpr bool SELF = (GM != 0);
+    // GM bit 2: the O(n) split field (VLASOV_FIELD=split) instead of the cluster Toeplitz rows --
+    // a compile-time variant, so the default kernel carries none of its code or registers
+    constexpr bool SPLIT = (GM & 4) != 0;
+    constexpr int GMODE = GM & 3;
+    constexpr bool SELF = (GMODE != 0);
     constexpr bool NEED_FN = (STAGE >= 2);
     constexpr bool NEED_U = (STAGE == 4);
 
@@ -174,6 +181,8 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     __shared__ __align__(8) uint64_t empty_bar[NSLOT];
     __shared__ __align__(8) uint64_t field_bar;
     __shared__ __align__(8) uint64_t e_bar;      // fused field: all Q rows of E have landed
+    __shared__ __align__(8) uint64_t ready_bar[NSLOT];   // stage 1, carried ghosts: slot's ghosts decided
+    __shared__ __align__(8) uint64_t e_ready;    // stage 1, carried ghosts: the tile's E rows are in sE
     __shared__ unsigned s_ticket;
     __shared__ double s_f0[4];                   // f0v at v-ghost columns -2, -1, nv, nv + 1 (SELF)
     __shared__ uint32_t s_dep[NT];               // slot-release dependency sink (see the row step)
@@ -214,15 +223,26 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     const bool field = SELF && (A.rho_in != nullptr);
     // one mbarrier per thread (sequential inits by one thread cost ~35 ns each, ~1 us for a
     // 12-slot ring); every initialising thread fences its own inits
-    if (tid < 2 * NSLOT + 2) {
+    if (tid < 3 * NSLOT + 3) {
         uint64_t* bar = tid < NSLOT ? &full_bar[tid] : tid < 2 * NSLOT ? &empty_bar[tid - NSLOT]
-                      : tid == 2 * NSLOT ? &field_bar : &e_bar;
+                      : tid == 2 * NSLOT ? &field_bar : tid == 2 * NSLOT + 1 ? &e_bar
+                      : tid == 2 * NSLOT + 2 ? &e_ready : &ready_bar[tid - 2 * NSLOT - 3];
         mbar_init(bar, (tid >= NSLOT && tid < 2 * NSLOT) ? (uint32_t)NW : 1u);
         fence_mbar_init();
     }
+    // Stage 1 with carried ghosts (reading #6b): f_n's ghost columns hold the outgoing candidate
+    // (stage 4 wrote the cubic extrapolation); the direction is decided with this stage's own
+    // field E = E(f_n).  In the edge v-tiles a helper warp of the producer warpgroup keeps the
+    // candidate or puts the unperturbed profile into every landed slot, so the consumers of those
+    // tiles (which would otherwise set the stage time) do no per-row boundary work.
+    constexpr bool SEL1_ANY = STAGE1D_SEL1 && (GMODE == 2 && STAGE == 1);
+    constexpr bool SEL1H = SEL1_ANY && PWG;
+    const bool sel_lo = SEL1H && A.phys_lo && (B.lo_v + T.j0 == 0);
+    const bool sel_hi = SEL1H && A.phys_hi && (B.lo_v + T.j0 + T.ncols == A.dom_v);
+    const bool sel_cta = sel_lo || sel_hi;
     // fused field in a cluster (the v-tiles of one row strip): every CTA's barrier is initialised
     // and armed before any CTA pushes E rows into its shared memory
-    const bool toep = field && A.hs == nullptr;  // Toeplitz field: rows split over the strip's cluster
+    const bool toep = field && !SPLIT;  // Toeplitz field: rows split over the strip's cluster
     const uint32_t crank = toep ? cluster_ctarank() : 0u, csize = toep ? cluster_nctarank() : 1u;
     __syncthreads();
     // (after the barrier that orders the inits; before this thread's cluster arrive, so no remote
@@ -298,6 +318,21 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                 if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
             }
         }
+        if (SEL1H && sel_cta && warp == NW + 1 && lane == 0) {
+            mbar_wait(&e_ready, 0);
+            const double* Er = sE + 2 - T.x0;
+            int slot = 0;
+            uint32_t phase = 0;
+            for (int q = 0; q < Q; ++q) {
+                mbar_wait(&full_bar[slot], phase);
+                double* seg = smem + slot * SLOT;
+                const double a = -Er[T.x0 - 2 + q];
+                if (sel_lo && !(a < 0.0)) { seg[0] = s_f0[0]; seg[1] = s_f0[1]; }
+                if (sel_hi && !(a > 0.0)) { seg[T.ncols + 2] = s_f0[2]; seg[T.ncols + 3] = s_f0[3]; }
+                mbar_arrive(&ready_bar[slot]);
+                if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
+            }
+        }
         return;
     }
     if (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PWG_CONSUMER_REGS));
@@ -318,7 +353,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     }
 
     // ---------------------------------------------------------------- consumers
-    if (field && A.hs != nullptr) {
+    if (SPLIT && field) {
         // Constraint evaluation of the stage state (Alg.5) in O(n): the exact discrete
         // Green's function of E = -D4 phi is a sawtooth plus a part decaying like 0.0718^|m|
         // (DESIGN.md 6.1), so with r = rho - mean
@@ -548,7 +583,10 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         else named_bar_sync(1, NT);
         for (int t = tid; t < Q; t += NT) sE[t] = s_part[t];
         named_bar_sync(1, NT);
+    } else if (sel_cta) {
+        named_bar_sync(1, NT);                   // sE written by every consumer
     }
+    if (sel_cta && tid == 0) mbar_arrive(&e_ready);
     TRACE(5);
     const int cl = CPT * tid;                    // tile-local column of my first cell
     const int c0 = T.j0 + cl;                    // block-local interior column
@@ -575,8 +613,8 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     // own E: a branch-free select between the carried value and the unperturbed profile (SEL1).
     // Only at physical velocity faces.  SELF: the edge threads stage f_next's boundary cells; its
     // velocity ghost columns are written after the march, off the critical path
-    constexpr bool BC_IN = (GM == 1);
-    constexpr bool SEL1 = (GM == 2 && STAGE == 1);
+    constexpr bool BC_IN = (GMODE == 1);
+    constexpr bool SEL1 = SEL1_ANY && !PWG;      // no helper warp: the edge threads select per row
     const bool lo_edge = (BC_IN || SEL1) && edge_lo && A.phys_lo, hi_edge = (BC_IN || SEL1) && edge_hi && A.phys_hi;
     const double* Ebcf = (STAGE == 1) ? E : Ebc;   // the field deciding the direction
     constexpr bool GHOST_OUT = SELF && STAGE >= 1;
@@ -598,7 +636,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         constexpr int K = decltype(Kc)::value;
         constexpr bool OUT = decltype(OUTc)::value;
         const int r = T.x0 - 2 + q;
-        if (live) mbar_wait(&full_bar[slot], phase);
+        if (live) mbar_wait(sel_cta ? &ready_bar[slot] : &full_bar[slot], phase);
 #ifdef STAGE1D_TRACE
         if (q == 0) TRACE(6);
 #endif
@@ -641,8 +679,9 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                 }
             }
         }
-        if (SEL1) {                              // stage 1, carried ghosts: keep the extrapolation
+        if (SEL1 && (lo_edge || hi_edge)) {      // stage 1, carried ghosts: keep the extrapolation
             const double a = -E[r];              // if outgoing, else the unperturbed profile
+                                                 // (edge threads only: the other warps skip it)
             constexpr int L = CPT + 1;
             const bool klo = !lo_edge || (a < 0.0), khi = !hi_edge || (a > 0.0);
             v[1] = klo ? v[1] : s_f0[1];
@@ -811,7 +850,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
             const int i = T.x0 + rr;
             const double* se = s_edge + (rr * 2 + side) * CPT;
             // stage 4: the outgoing candidate for the next stage 1 (SEL1 decides with E(f_n))
-            const double a = (STAGE == 4 && GM == 2) ? (side == 0 ? -1.0 : 1.0) : -E[i];
+            const double a = (STAGE == 4 && GMODE == 2) ? (side == 0 ? -1.0 : 1.0) : -E[i];
             double2 g;
             if (side == 0) {
                 g = a < 0.0 ? make_double2(10.0 * se[0] - 20.0 * se[1] + 15.0 * se[2] - 4.0 * se[3],
@@ -1009,15 +1048,24 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     const int nt = (int)(wide ? L->h_tiles_wide.size() : L->h_tiles_narrow.size());
     if (nt == 0) return VLASOV_OK;
     const int rows = L->tile_rows;
-    const int gm = self ? (E_bc ? 1 : 2) : 0;
+    const int gm = (self ? (E_bc ? 1 : 2) : 0) | (A.hs != nullptr ? 4 : 0);
+    if (A.hs != nullptr && !self) return fail(VLASOV_EINVAL, "split field needs in-kernel ghosts");
     if (wide) {
-        return gm == 2 ? dispatch_recon<NT_WIDE, 2>(recon, stage, A, nt, rows, L->stream)
-             : gm == 1 ? dispatch_recon<NT_WIDE, 1>(recon, stage, A, nt, rows, L->stream)
-                       : dispatch_recon<NT_WIDE, 0>(recon, stage, A, nt, rows, L->stream);
+        switch (gm) {
+            case 6: return dispatch_recon<NT_WIDE, 6>(recon, stage, A, nt, rows, L->stream);
+            case 5: return dispatch_recon<NT_WIDE, 5>(recon, stage, A, nt, rows, L->stream);
+            case 2: return dispatch_recon<NT_WIDE, 2>(recon, stage, A, nt, rows, L->stream);
+            case 1: return dispatch_recon<NT_WIDE, 1>(recon, stage, A, nt, rows, L->stream);
+            default: return dispatch_recon<NT_WIDE, 0>(recon, stage, A, nt, rows, L->stream);
+        }
     }
-    return gm == 2 ? dispatch_recon<NT_NARROW, 2>(recon, stage, A, nt, rows, L->stream)
-         : gm == 1 ? dispatch_recon<NT_NARROW, 1>(recon, stage, A, nt, rows, L->stream)
-                   : dispatch_recon<NT_NARROW, 0>(recon, stage, A, nt, rows, L->stream);
+    switch (gm) {
+        case 6: return dispatch_recon<NT_NARROW, 6>(recon, stage, A, nt, rows, L->stream);
+        case 5: return dispatch_recon<NT_NARROW, 5>(recon, stage, A, nt, rows, L->stream);
+        case 2: return dispatch_recon<NT_NARROW, 2>(recon, stage, A, nt, rows, L->stream);
+        case 1: return dispatch_recon<NT_NARROW, 1>(recon, stage, A, nt, rows, L->stream);
+        default: return dispatch_recon<NT_NARROW, 0>(recon, stage, A, nt, rows, L->stream);
+    }
 }
 
 }  // namespace vk
