@@ -357,6 +357,33 @@ def test_three_level_regrid_run_parity():
         assert err < 1e-11, (n, err)
 
 
+def test_four_level_amr3_regrid_run_parity():
+    """N1: four levels with the paper's ratios [2,4], [4,2], [2,2] and the AMR3
+    parameter set of P:1495-1503 (smallest patch (8,8); largest patch level_1 (32,128),
+    level_2 (128,256), the finest specified value for level 3; tag buffer 8), multi-level regrid at
+    step 0 and step 2: boxes of every level bit-exact, f within 1e-11 after 4 steps."""
+    w = inputs.scaled(inputs.get("C3"), (16, 32), (8, 8))
+    args = (0.005, [8, 8, 8], [(2, 4), (4, 2), (2, 2)], [(8, 8)] * 3, [(32, 128), (128, 256), (128, 256)], 0.7)
+    dt = inputs.fixed_dt(w, (16, 16))
+    H = drv.hierarchy(w, [inputs.level0_boxes(w)], [(1, 1)])
+    data = _ic_data(H, w)
+    E_bc = drv.start(H, data)
+    G = AmrVlasov1D(w.ncells, w.lower, inputs.spacing(w), [inputs.level0_boxes(w)], [(1, 1)],
+                    lambda r: inputs.background_profile(w, r))
+    G.set_state([inputs.initial_cell_averages(w)])
+    for n in range(4):
+        if n % 2 == 0:
+            data, E_bc, nbs = drv.regrid_multilevel(H, data, E_bc, *args)
+            got = G.regrid_hierarchy(*args)
+            assert len(nbs) == 3                                  # four levels
+            assert [[tuple(map(tuple, b)) for b in lvl] for lvl in got] == \
+                [[tuple(map(tuple, b)) for b in lvl] for lvl in nbs]
+        data, E_bc, _ = amr.step(H, data, E_bc, dt)
+        G.step_graph(dt)
+        err = relerr_levels(G.get_state(), _interiors(data))
+        assert err < 1e-11, (n, err)
+
+
 def _golden_c3():
     import os
     p = os.path.join(os.path.dirname(__file__), "golden", "c3_100_steps.npz")

@@ -152,3 +152,43 @@ def test_cabi_regrid_boxes_bitexact_vs_oracle(seed):
     if exp:
         fine = boxes.LevelMeta(dom, tuple(a * b for a, b in zip(rat[k], ratio)), exp, (True, False))
         assert boxes.properly_nested(fine, metas[k])
+
+
+def test_four_level_amr3_hierarchy_invariants():
+    """The oracle's multi-level regrid with the paper's four-level ratios [2,4], [4,2], [2,2]
+     and the AMR3 parameters (smallest (8,8); largest level_1 (32,128),
+    level_2 (128,256), the finest specified value for level 3; tag buffer 8) on a C3-shaped
+    16x32 base: four levels, every fine box a union of refined coarser cells, within the patch-size
+    limits, pairwise disjoint, and properly nested in the next coarser level."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(__file__))
+    import amr_drivers as drv
+    import inputs
+    w = inputs.scaled(inputs.get("C3"), (16, 32), (8, 8))
+    ratios = [(2, 4), (4, 2), (2, 2)]
+    smallest, largest = [(8, 8)] * 3, [(32, 128), (128, 256), (128, 256)]
+    H = drv.hierarchy(w, [inputs.level0_boxes(w)], [(1, 1)])
+    data = H.new_data()
+    for p, b in enumerate(H.levels[0].boxes):
+        data[0][p][2:-2, 2:-2] = inputs.initial_cell_averages(w, (1, 1), b)
+    E_bc = drv.start(H, data)
+    _, _, nbs = drv.regrid_multilevel(H, data, E_bc, 0.005, [8, 8, 8], ratios, smallest, largest, 0.7)
+    assert len(nbs) == 3 and len(H.levels) == 4
+    for k, nb in enumerate(nbs):
+        r = ratios[k]
+        dom = [w.ncells[d] * H.levels[k + 1].ratio[d] for d in range(2)]
+        coarse = H.levels[k].boxes
+        for i, b in enumerate(nb):
+            lo, hi = b
+            for d in range(2):
+                n = hi[d] - lo[d] + 1
+                assert 0 <= lo[d] <= hi[d] < dom[d]
+                assert lo[d] % r[d] == 0 and (hi[d] + 1) % r[d] == 0          # refined coarse cells
+                assert n <= largest[k][d] and (n >= smallest[k][d] or n == dom[d])
+            for b2 in nb[i + 1:]:
+                assert boxes.is_empty(boxes.intersect(b, b2))                   # disjoint
+            # proper nesting: every coarsened cell lies in a level-k box
+            cb = boxes.coarsen(b, r)
+            covered = sum(boxes.ncells(boxes.intersect(cb, c)) for c in coarse)
+            assert covered == boxes.ncells(cb)
