@@ -164,7 +164,14 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
  * vlasov_fill_ghosts.
  * rho_next (nullable; single block covering the domain only): receives the velocity moment of
  * f_next, rho = 1 - dv sum_v f_next, fused into the stage: per-(row, v-tile) partial
- * sums combined in a fixed order by the last CTA of each row strip (deterministic).            */
+ * sums combined in a fixed order by the last CTA of each row strip (deterministic).
+ * 2D+2V levels (ndim 4): one block covering the periodic (x, y) domain, n_vx % 4 == 0, n_vy even;
+ * f0v ([(n_vx + 4)(n_vy + 4)], the unperturbed profile on the ghosted velocity range) and E_bc
+ * (the level's ghosted E array) required; the velocity ghosts of f_s follow the characteristic
+ * condition with E_bc (reading #6), derived into f_s's velocity ghost frame by a pass before the
+ * stage kernel (f_s's ghost frame is written; its interior is not).  rho_next receives
+ * 1 - dvx dvy sum_v f_next per (x, y) cell ([nx][ny]), from per-(vx line, vy tile) partials summed
+ * in a fixed order (deterministic).                                                             */
 int vlasov_rhs(vlasov_level* level, const double* f, const double* E, double* k, int32_t recon);
 
 /* vlasov_rk4_stage_vp: the constraint evaluation of Alg.5 fused into the stage for a
