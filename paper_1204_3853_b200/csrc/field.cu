@@ -377,12 +377,29 @@ __global__ void __launch_bounds__(P2_THREADS) k_poisson2d_tb(const double* __res
     __shared__ double s_red[P2_THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double acc = 0.0;
-    for (int t = tid; t < n; t += P2_THREADS) {
-        const double v = rho[t];
-        s_rho[t] = v;
-        acc += v;
-        s_gx[t] = gx[t];
-        s_gy[t] = gy[t];
+    // 16-byte loads, 4 in flight per thread per array (n = nx ny is a multiple of 8: ny % 8 == 0)
+    const int n2 = n / 2;
+    for (int t0 = tid; t0 < n2; t0 += 4 * P2_THREADS) {
+        double2 r[4], a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u * P2_THREADS;
+            if (t < n2) {
+                r[u] = __ldg(reinterpret_cast<const double2*>(rho) + t);
+                a[u] = __ldg(reinterpret_cast<const double2*>(gx) + t);
+                b[u] = __ldg(reinterpret_cast<const double2*>(gy) + t);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u * P2_THREADS;
+            if (t < n2) {
+                reinterpret_cast<double2*>(s_rho)[t] = r[u];
+                reinterpret_cast<double2*>(s_gx)[t] = a[u];
+                reinterpret_cast<double2*>(s_gy)[t] = b[u];
+                acc += r[u].x + r[u].y;
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -434,35 +451,35 @@ __global__ void __launch_bounds__(P2_THREADS) k_poisson2d_tb(const double* __res
     double* py = s_part + (size_t)(P2_THREADS + tid) * P2T_K;
 #pragma unroll
     for (int j = 0; j < P2T_K; ++j) { px[j] = ax[j]; py[j] = ay[j]; }
-    cluster_sync_all();                                   // partials of every rank visible
+    __syncthreads();
+    // per-rank sums over the S subsets (fixed order), into the dead rho area: s_sum[c][k]
+    double* s_sum = s_rho;
+    for (int t = tid; t < 2 * ny; t += P2_THREADS) {
+        const int c = t / ny, kk = t - c * ny, bb = kk / P2T_K, jj = kk % P2T_K;
+        const double* pp = s_part + (size_t)c * P2_THREADS * P2T_K;
+        double e = 0.0;
+        for (int g = 0; g < S; ++g) e += pp[(size_t)(g * nb + bb) * P2T_K + jj];
+        s_sum[t] = e;
+    }
+    cluster_sync_all();                                   // every rank's sums visible
     const int nyg = ny + 4;
-    for (int kk = tid; kk < ny && crank == 0; kk += P2_THREADS) {
-        const int bb = kk / P2T_K, jj = kk % P2T_K;
-        double ex = 0.0, ey = 0.0;
-        for (int c = 0; c < P2T_SPLIT; ++c) {
-            const uint32_t base = map_shared_rank(s_part, (uint32_t)c);
-            for (int g = 0; g < S; ++g) {
-                double vx, vy;
-                const uint32_t ox = base + (uint32_t)(((g * nb + bb) * P2T_K + jj) * 8);
-                const uint32_t oy = base + (uint32_t)(((P2_THREADS + g * nb + bb) * P2T_K + jj) * 8);
-                asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(vx) : "r"(ox) : "memory");
-                asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(vy) : "r"(oy) : "memory");
-                ex += vx;
-                ey += vy;
-            }
+    for (int t = tid; t < 2 * ny && crank == 0; t += P2_THREADS) {
+        const int c = t / ny, kk = t - c * ny;
+        double e = s_sum[t];
+        for (int r = 1; r < P2T_SPLIT; ++r) {             // ranks in order (deterministic)
+            double v;
+            asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(map_shared_rank(s_sum + t, (uint32_t)r)) : "memory");
+            e += v;
         }
-        for (int c = 0; c < 2; ++c) {
-            const double e = c ? ey : ex;
-            double* Ec = E + (int64_t)c * (nx + 4) * nyg;
-            const int rows[3] = {i + 2, i + 2 + nx, i + 2 - nx};
-            for (int r = 0; r < 3; ++r) {
-                const int gr = rows[r];
-                if (gr < 0 || gr >= nx + 4) continue;
-                double* row = Ec + (int64_t)gr * nyg;
-                row[kk + 2] = e;
-                if (kk < 2) row[kk + 2 + ny] = e;
-                if (kk >= ny - 2) row[kk + 2 - ny] = e;
-            }
+        double* Ec = E + (int64_t)c * (nx + 4) * nyg;
+        const int rows[3] = {i + 2, i + 2 + nx, i + 2 - nx};
+        for (int r = 0; r < 3; ++r) {
+            const int gr = rows[r];
+            if (gr < 0 || gr >= nx + 4) continue;
+            double* row = Ec + (int64_t)gr * nyg;
+            row[kk + 2] = e;
+            if (kk < 2) row[kk + 2 + ny] = e;
+            if (kk >= ny - 2) row[kk + 2 - ny] = e;
         }
     }
     cluster_sync_all();                                   // rank 0 done reading the other ranks
@@ -472,7 +489,8 @@ int launch_poisson2d(const vlasov_poisson2d* P, const double* rho, double* E) {
     const int n = P->nx * P->ny;
     const int ny = P->ny;
     static const bool plain = std::getenv("VLASOV_POISSON2D_PLAIN") != nullptr;   // experiment switch
-    if (!plain && ny % P2T_K == 0 && ny / P2T_K <= 32 && (32 % (ny / P2T_K)) == 0 && n <= P2_SMEM_MAX) {
+    if (!plain && ny % P2T_K == 0 && ny / P2T_K <= 32 && (32 % (ny / P2T_K)) == 0 && n <= P2_SMEM_MAX &&
+        ((uintptr_t)rho & 15) == 0) {
         const size_t smem = (size_t)(3 * n + 2 * P2_THREADS * P2T_K) * sizeof(double);
         static bool cfg = false;
         if (!cfg) {
