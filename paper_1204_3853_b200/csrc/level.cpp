@@ -455,6 +455,11 @@ int build_ghost_tasks(vlasov_level* L, const vlasov_level* C, std::vector<int64_
     if (C)
         for (int d = 0; d < nd; ++d) rr[d] = L->ratio[d] / C->ratio[d];
     int err = VLASOV_OK;
+    {   // capacity: the ghost frames of all blocks (avoids reallocating the task lists)
+        int64_t fr = 0;
+        for (const Box& B : L->blocks) fr += vk::box_ncells(vk::box_grow(B, vk::G, nd), nd) - vk::box_ncells(B, nd);
+        copies.reserve((size_t)(2 * fr));
+    }
     for (size_t b = 0; b < L->blocks.size(); ++b) {
         const Box& B = L->blocks[b];
         const Box GB = vk::box_grow(B, vk::G, nd);
@@ -493,12 +498,29 @@ int build_ghost_tasks(vlasov_level* L, const vlasov_level* C, std::vector<int64_
         };
         if (nd == 2) {
             // the ghost frame only, row by row (x major, v fastest: the same task order as a
-            // sweep of the grown block), without visiting the interior
-            for (int x = GB.lo[0]; x <= GB.hi[0]; ++x) {
+            // sweep of the grown block), without visiting the interior; runs of sibling copies
+            // from one source box take one owner lookup (the copy addresses are consecutive)
+            for (int x = GB.lo[0]; x <= GB.hi[0] && !err; ++x) {
                 const bool xin = x >= B.lo[0] && x <= B.hi[0];
-                for (int v = GB.lo[1]; v <= GB.hi[1]; ++v) {
+                for (int v = GB.lo[1]; v <= GB.hi[1] && !err; ++v) {
                     if (xin && v == B.lo[1]) v = B.hi[1] + 1;
                     const int c[4] = {x, v, 0, 0};
+                    if (phys_code(L, c) < 0 && !L->single_block) {
+                        int w[4];
+                        wrap_cfg(L, c, w);
+                        const int q = own.find(w);
+                        if (q >= 0) {
+                            // the run: up to the end of box q in v, of this row's ghost range
+                            const int vend = std::min(L->blocks[q].hi[1], (xin && v < B.lo[1]) ? B.lo[1] - 1 : GB.hi[1]);
+                            const int64_t d0 = cell_addr(L, (int)b, c), s0 = cell_addr(L, q, w);
+                            for (int k = 0; k <= vend - v; ++k) {
+                                copies.push_back(d0 + k);
+                                copies.push_back(s0 + k);
+                            }
+                            v = vend;
+                            continue;
+                        }
+                    }
                     ghost_cell(c);
                 }
             }
