@@ -137,7 +137,9 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
 /* ---- right-hand side and RK4 stage ------------------------------------------------- *
  * vlasov_rhs: k = L(f) on every interior cell (face averages P:322-368, fluxes P:263-282 with
  * the +1/48 reading #3, divergence P:246-250); `f` ghosts must be filled; `E` is this level's
- * E array.  k has the level layout (ghost cells of k untouched).
+ * E array.  k has the level layout (ghost cells of k untouched); k must not alias f.  2D+2V: one
+ * block covering the periodic (x, y) domain (x, y wrapped in-kernel; the velocity ghost frame of f
+ * filled, e.g. by vlasov_fill_ghosts with E_bc and f0v); CENTERED4 in the telescoped form.
  *
  * vlasov_rk4_stage: one stage of classic RK4 in the minimum-traffic rearrangement
  * (identical to the flux-accumulation form P:399-410 in exact arithmetic):

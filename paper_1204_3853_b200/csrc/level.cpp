@@ -1711,7 +1711,14 @@ int vlasov_rhs(vlasov_level* L, const double* f, const double* E, double* k, int
     VK_NVTX();
     if (!L || !f || !E || !k) return vk::fail(VLASOV_EINVAL, "null argument");
     if (!device_ok_impl()) return vk::fail(VLASOV_ECUDA, "no sm_100 CUDA device");
-    if (L->ndim != 2) return vk::fail(VLASOV_EUNSUPPORTED, "rhs: 2D+2V not in this build yet");
+    if (recon != VLASOV_CENTERED4 && recon != VLASOV_UPWIND) return vk::fail(VLASOV_EINVAL, "bad recon");
+    if (k == f) return vk::fail(VLASOV_EINVAL, "k must not alias f");
+    if (L->ndim == 4) {
+        // 2D+2V: one periodic block (x, y wrapped in-kernel), velocity ghost frame of f current
+        if (!L->self_ghost_ok) return vk::fail(VLASOV_EUNSUPPORTED, "rhs: 2D+2V needs one periodic block");
+        return vk::launch_stage_2d2v(L, 0, 0.0, const_cast<double*>(f), f, nullptr, k, E, nullptr, nullptr, recon,
+                                     nullptr);
+    }
     return vk::launch_stage_1d1v(L, 0, 0.0, nullptr, f, nullptr, k, E, nullptr, nullptr, recon, nullptr);
 }
 

@@ -147,13 +147,13 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(const StageArgs2 A
         gEf[2 * t] = __ldg(A.E + (int64_t)(xx + 2) * nyg + (yy + 2));
         gEf[2 * t + 1] = __ldg(A.E + ecomp + (int64_t)(xx + 2) * nyg + (yy + 2));
     }
-    if (tid < 32) {
+    if (tid < 32 && A.f0v != nullptr) {
         const int Lg = tid >> 2, which = tid & 3;
         const int ll = min(max(l0 - 2 + Lg, 0), A.nvx - 1);
         const int mm = which < 2 ? which : A.nvy + which;
         gPv[tid] = __ldg(A.f0v + (int64_t)(ll + 2) * (A.nvy + 4) + mm);
     }
-    for (int t = tid; t < 4 * S2_TM; t += blockDim.x) {
+    for (int t = tid; t < 4 * S2_TM && A.f0v != nullptr; t += blockDim.x) {
         const int g = t / S2_TM, c = t % S2_TM;
         const int lg = g < 2 ? g - 2 : A.nvx + (g - 2);
         const int m = min(mt * S2_TM + c, A.nvy - 1);
@@ -644,7 +644,7 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.u_out = u;
     A.f_next = f_next;
     A.E = E;
-    A.E_bc = E_bc;
+    A.E_bc = E_bc ? E_bc : E;           // staged by the face-form kernel (rhs: its field)
     A.f0v = f0v;
     A.s0 = L->block_str[0][0];
     A.s1 = L->block_str[0][1];
@@ -670,7 +670,8 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
     if ((rc = encode_map(L, f_s, S2_LW, 8, &M.fs8)) || (rc = encode_map(L, f_s, S2_LW, 4, &M.fs4)) ||
         (rc = encode_map(L, f_n ? f_n : f_s, S2_TM, 4, &M.fn4)) || (rc = encode_map(L, u ? u : f_s, S2_TM, 4, &M.u4)))
         return rc;
-    if (S2_GLOBAL_GHOSTS) {
+    // the velocity ghost frame of f_s from E_bc (vlasov_rhs, stage 0: the frame must be current)
+    if (S2_GLOBAL_GHOSTS && E_bc != nullptr && f0v != nullptr) {
         VK_CUDA(launch_pdl(k_vghost_2d2v, dim3((unsigned)(A.nx * A.ny)), dim3((unsigned)std::min(1024, (A.nvx + A.nvy / 2 + 31) / 32 * 32)), 0, L->stream,
                            const_cast<double*>(f_s), A.org, A.s0, A.s1, A.s2, A.nx, A.ny, A.nvx, A.nvy, E_bc, f0v));
     }

@@ -115,3 +115,26 @@ def test_c5_full_size_ten_steps_bench_launch():
     got = S.get_state()
     ref, _ = uniform.problem_for(w).run(f0, dt, 10)
     assert relerr(got, ref) < 1e-11
+
+
+@pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
+@pytest.mark.parametrize("shape", [(8, 8, 12, 16), (10, 6, 8, 70), (6, 12, 16, 130)])
+def test_rhs_parity_2d2v(shape, recon):
+    # vlasov_rhs on a 2D+2V level (the boundary call of SURVEY 8(b)): ghost frame by
+    # vlasov_fill_ghosts(E_bc, f0v), then k = L(f) against the oracle's face -> flux -> divergence
+    # form on a noisy state with the prescribed field
+    w = inputs.scaled(inputs.get("C5"), shape, shape)
+    f0 = inputs.initial_cell_averages(w) * (1.0 + 0.05 * inputs.random_field(shape, 17))
+    S = _solver(w, recon)
+    S.set_state(f0)
+    h = S.level.h
+    k = S.level.field(0.0)
+    with torch.cuda.stream(S.stream):
+        api.vlasov_fill_ghosts(h, S.A, None, None, S.E, S.f0v)
+        api.vlasov_rhs(h, S.A, S.E, k, RECON[recon])
+    S.stream.synchronize()
+    got = S.level.get_domain(k)
+    prob = uniform.problem_for(w, recon)
+    E = prob.constraints(f0)
+    ref, _ = prob.rhs(f0, E, E)
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
