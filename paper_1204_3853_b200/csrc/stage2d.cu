@@ -661,6 +661,8 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
     A.hvy = L->h[3];
     A.vx_lo = L->lower[2];
     A.vy_lo = L->lower[3];
+    // the row march wraps x once on either side (rows x0-4 .. x1+1): at least 4 x cells
+    if (A.nx < 4) return fail(VLASOV_EINVAL, "2D+2V stage: need >= 4 cells along x");
     const int nmt = (A.nvy + S2_TM - 1) / S2_TM, nlg = (A.nvx + S2_LT - 1) / S2_LT;
     A.nstrips = L->strips2;
     A.partials = rho ? L->d_partials : nullptr;

@@ -138,3 +138,37 @@ def test_rhs_parity_2d2v(shape, recon):
     E = prob.constraints(f0)
     ref, _ = prob.rhs(f0, E, E)
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
+def test_constant_state_rhs_is_exactly_zero_2d2v(recon):
+    # free-stream preservation: f == c (and the unperturbed profile == c,
+    # so every velocity ghost is c whatever the direction) gives k == 0 bitwise for any field --
+    # every difference of equal values is an exact zero in the telescoped form as in the face form
+    w = inputs.scaled(inputs.get("C5"), (8, 6, 12, 70), (8, 6, 12, 70))
+    c = 0.3125
+    f0v = np.full_like(inputs.background_profile(w), c)
+    S = UniformVlasov2D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), f0v,
+                        inputs.prescribed_field(w), RECON[recon])
+    S.set_state(np.full(w.ncells, c))
+    k = S.level.field(1.0)
+    with torch.cuda.stream(S.stream):
+        api.vlasov_fill_ghosts(S.level.h, S.A, None, None, S.E, S.f0v)
+        api.vlasov_rhs(S.level.h, S.A, S.E, k, RECON[recon])
+    S.stream.synchronize()
+    assert np.all(S.level.get_domain(k) == 0.0)
+
+
+def test_stage_kernels_deterministic_2d2v():
+    # two runs of the same 3 steps are bitwise equal (fixed-order moment partials, no atomics)
+    w = inputs.scaled(inputs.get("C5"), (8, 10, 12, 70), (8, 10, 12, 70))
+    f0 = inputs.initial_cell_averages(w) * (1.0 + 0.05 * inputs.random_field(w.ncells, 23))
+    dt = inputs.fixed_dt(w)
+    outs = []
+    for _ in range(2):
+        S = _solver(w)
+        S.set_state(f0)
+        for _ in range(3):
+            S.step(dt)
+        outs.append((S.get_state(), S.moment()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
