@@ -130,9 +130,12 @@ class AmrVlasov1D:
 
     def _constraints(self, fs, E_out):
         api.vlasov_reduce_moment(self.handles, fs, self.rho)
-        self.poisson.solve(self.rho, None, self.E_f, 0)
-        for l, L in enumerate(self.levels):
-            api.vlasov_inject_field(L.h, self.E_f, (self.nxf,), E_out[l])
+        # the finest level is at the finest x resolution: the solve writes its ghosted E directly
+        # (ghost = 2, vlasov_poisson_solve), the coarser levels are injected from its interior
+        E_fin = E_out[-1]
+        self.poisson.solve(self.rho, None, E_fin, 2)
+        for l in range(len(self.levels) - 1):
+            api.vlasov_inject_field(self.levels[l].h, E_fin[2:], (self.nxf,), E_out[l])
 
     def _stage(self, s, dt):
         order = {1: ("A", "B"), 2: ("B", "C"), 3: ("C", "B"), 4: ("B", "A")}[s]
@@ -195,10 +198,10 @@ class AmrVlasov1D:
 
     def launches_per_step(self) -> int:
         nl = len(self.levels)
-        # per stage: fill (copy/CF + phys) per level, reduction (2), Poisson (1), inject per level,
-        # stage kernel per level, flux registers per fine level; then refluxing + average-down and
-        # the end-of-step constraint evaluation (fill, reduction, Poisson, inject)
-        return 4 * (2 * nl + 2 + 1 + nl + nl + (nl - 1)) + 2 * (nl - 1) + (2 * nl + 2 + 1 + nl)
+        # per stage: fill (copy/CF + phys) per level, reduction (2), Poisson (1, into the finest
+        # level's E), inject per coarser level, stage kernel per level, flux registers per fine
+        # level; then refluxing + average-down and the end-of-step constraint evaluation
+        return 4 * (2 * nl + 2 + 1 + (nl - 1) + nl + (nl - 1)) + 2 * (nl - 1) + (2 * nl + 2 + 1 + (nl - 1))
 
     # ------------------------------------------------------------------ regrid (C3 rule)
     def tags_level0(self, tol, buffer):
