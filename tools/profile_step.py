@@ -23,7 +23,7 @@ if w.ncfg == 1:
     S = UniformVlasov1D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), inputs.background_profile(w), rc)
 else:
     S = UniformVlasov2D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), inputs.background_profile(w),
-                        inputs.prescribed_field(w), rc)
+                        inputs.prescribed_field(w) if w.field == "prescribed" else None, rc, field=w.field)
 S.set_state(inputs.initial_cell_averages(w))
 dt = inputs.fixed_dt(w)
 for _ in range(a.steps):
