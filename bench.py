@@ -30,9 +30,9 @@ sys.path.insert(0, ROOT)
 #   stage 1: read f_n, write f2                    16 B
 #   stage 2: read f2, f_n; write u, f3             32 B
 #   stage 3: read f3, f_n; write f4                24 B
-#   stage 4: read f4, u, f_n; write f_{n+1}        32 B
-STAGE_BYTES = {1: 16, 2: 32, 3: 24, 4: 32}
-STEP_BYTES = sum(STAGE_BYTES.values())          # 104 B per cell per RK4 step
+#   stage 4: read f4, u; write f_{n+1}             24 B   (u = (f2 + 2 f3 - f_n)/3 holds the f_n term)
+STAGE_BYTES = {1: 16, 2: 32, 3: 24, 4: 24}
+STEP_BYTES = sum(STAGE_BYTES.values())          # 96 B per cell per RK4 step
 
 
 def read_peaks():
@@ -340,7 +340,7 @@ def run_amr(args, w, rank, world, local):
                        "l2": "L2-resident (a few MiB): small-config, latency-bound"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "whole AMR step (104 B/cell algorithmic; L2-resident, latency-bound)"},
+                         "kernel": "whole AMR step (96 B/cell algorithmic; L2-resident, latency-bound)"},
             "gpu_launches": G.launches_per_step() * args.steps,
             "clocks": clk, "cpu_baseline": None if (args.no_cpu_baseline or world > 1) else cpu_baseline(w.name),
         }

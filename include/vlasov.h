@@ -144,9 +144,12 @@ int vlasov_fill_ghosts(vlasov_level* level, double* f, const vlasov_level* coars
  * vlasov_rk4_stage: one stage of classic RK4 in the minimum-traffic rearrangement
  * (identical to the flux-accumulation form P:399-410 in exact arithmetic):
  *   stage 1: f_next = f_n + dt/2 k(f_n)                         (f_s == f_n)
- *   stage 2: u = f_n + (f_s - f_n)/3 + dt/3 k(f_s);  f_next = f_n + dt/2 k(f_s)
+ *   stage 2: u = (f_n + f_s)/3 + dt/3 k(f_s);  f_next = f_n + dt/2 k(f_s)
  *   stage 3: f_next = f_n + dt k(f_s)
- *   stage 4: f_next = u + (f_s - f_n)/3 + dt/6 k(f_s)           (f_next may alias f_n)
+ *   stage 4: f_next = u + f_s/3 + dt/6 k(f_s)      (f_n is not read; f_next may alias f_n)
+ * (u = (f_2 + 2 f_3 - f_n)/3 is everything of the RK4 sum f_{n+1} = (f_2 + 2 f_3 + f_4 - f_n)/3 +
+ * dt/6 k(f_4) that stage 4 cannot form from f_s = f_4, so stage 4 reads two fields only:
+ * 16 + 32 + 24 + 24 = 96 B per cell per step.)
  * Ghosts of f_s: if f0v is non-NULL the level must be ONE block covering the (periodic) domain
  * with a number of velocity cells divisible by 4; x is wrapped periodically in-kernel (the ghost
  * rows are never read), and the velocity ghosts of f_s follow the characteristic v-boundary

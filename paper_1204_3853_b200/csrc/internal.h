@@ -308,6 +308,10 @@ struct vlasov_level {
     // 2D+2V
     int64_t e_doubles = 0;
     int strips2 = 1;                      // x strips of the 2D+2V stage kernel
+    int tel_ns = 0;                       // strips of the telescoped 2D+2V kernel (0: not chosen yet)
+    int tel_xb[33] = {0};                 // their boundaries (stage2d_tel.cu)
+    int acc_ns = 0;                       // the same for the accumulator-form kernel (stage2d_acc.cu)
+    int acc_xb[33] = {0};
     // scratch (device): interpolation tables
     double* d_b5 = nullptr;               // linear5 weights for coarse_ratio, [dim][s][5]
 };
@@ -343,6 +347,10 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
                       double* f_next, const double* E, const double* E_bc, const double* f0v, int recon,
                       double* rho);
 bool stage_2d2v_tel_ok(const vlasov_level* L);
+int stage_2d2v_choose_strips(int64_t tiles, int nx, int rmax, int smax, const char* env, int* xb);
+bool stage_2d2v_acc_ok(const vlasov_level* L);
+int launch_stage_2d2v_acc(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
+                          double* f_next, const double* E, double* rho_partials);
 int launch_stage_2d2v_tel(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
                           double* f_next, const double* E, double* rho_partials);
 int launch_moment_2d2v(const vlasov_level* L, const double* f, double* rho);

@@ -139,7 +139,7 @@ template <int STAGE, int NT>
 struct StageGeom {
     static constexpr int TV = CPT * NT;
     static constexpr int SEG = TV + 4;                       // f_s row segment incl. 2+2 halo columns
-    static constexpr int NFN = (STAGE >= 2 ? 1 : 0) + (STAGE == 4 ? 1 : 0);
+    static constexpr int NFN = STAGE >= 2 ? 1 : 0;           // f_n row (stages 2, 3) or u row (stage 4)
     static constexpr int SLOT = SEG + NFN * TV;              // doubles per ring slot
     // ring depth: ~RING_KB of row data per CTA, 3..16 slots (a slot is consumed in one row step)
     // ring size per stage (measured on C4: stage 2 best at 48 KB, stages 3 and 4 at 64 KB)
@@ -156,8 +156,8 @@ struct StageGeom {
     }
 };
 
-// Ring slot of row step q (row r = x0 - 2 + q): [ f_s(r, j0-2 .. j0+TV+1) | f_n(r-2, j0..) | u(r-2, j0..) ];
-// the f_n / u rows are those of the output row i = r - 2 (q >= 4), so every slot is consumed
+// Ring slot of row step q (row r = x0 - 2 + q): [ f_s(r, j0-2 .. j0+TV+1) | f_n(r-2, j0..) or u(r-2, j0..) ];
+// the f_n / u row is that of the output row i = r - 2 (q >= 4), so every slot is consumed
 // completely in its own row step and released at once.
 // GM (ghost mode of f_s): 0 = ghost frame read from memory (any level); 1 = one periodic block,
 // x wrapped in-kernel, velocity ghosts derived from E_bc; 2 = one periodic block, velocity ghosts
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     constexpr bool SPLIT = (GM & 4) != 0;
     constexpr int GMODE = GM & 3;
     constexpr bool SELF = (GMODE != 0);
-    constexpr bool NEED_FN = (STAGE >= 2);
+    constexpr bool NEED_FN = (STAGE == 2 || STAGE == 3);     // stage 4 reads u only (u holds no f_n term)
     constexpr bool NEED_U = (STAGE == 4);
 
     extern __shared__ __align__(128) double smem[];
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         mbar_arrive_expect_tx(&full_bar[sl], bytes);
         bulk_g2s(dst, A.f_s + rowbase(rs) + T.j0 - 2, seg_bytes, &full_bar[sl]);
         if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl]);
-        if (NEED_U && out_row) bulk_g2s(dst + SEG + TV, A.u_in + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl]);
+        if (NEED_U && out_row) bulk_g2s(dst + SEG, A.u_in + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl]);
     };
     // fused field: this CTA computes rows [tb, te) of the tile's Q rows of E (the strip's v-tiles
     // of a cluster split them); row tb + t is x = gxu0 + t (unwrapped, gxu0 in [0, n)); they read
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         }
         if (OUT && NEED_U) {
 #pragma unroll
-            for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + TV + cl + m); uu[m] = p.x; uu[m + 1] = p.y; }
+            for (int m = 0; m < CPT; m += 2) { const double2 p = lds2(seg + SEG + cl + m); uu[m] = p.x; uu[m + 1] = p.y; }
         }
         if (BC_IN && (lo_edge || hi_edge)) {     // characteristic BC (reading #6), a = -E_bc
             const double a = -Ebcf[r];
@@ -717,13 +717,13 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                     o[n] = fma((0.5 * A.dt) * rdv12, dFv, fma(-(0.5 * A.dt) * rdx12, dFx, fs));
                 } else if (STAGE == 2) {
                     const double k = dFv * rdv12 - dFx * rdx12;
-                    uu[n] = fn[n] + (fs - fn[n]) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * k;
+                    uu[n] = (fn[n] + fs) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * k;
                     o[n] = fn[n] + (0.5 * A.dt) * k;
                 } else if (STAGE == 3) {
                     o[n] = fma(A.dt * rdv12, dFv, fma(-A.dt * rdx12, dFx, fn[n]));
                 } else {
                     o[n] = fma((A.dt * (1.0 / 6.0)) * rdv12, dFv,
-                               fma(-(A.dt * (1.0 / 6.0)) * rdx12, dFx, fma(fs - fn[n], 1.0 / 3.0, uu[n])));
+                               fma(-(A.dt * (1.0 / 6.0)) * rdx12, dFx, fma(fs, 1.0 / 3.0, uu[n])));
                 }
             }
             if (NEED_FN) fnuu ^= __double2hiint(fn[0]) ^ __double2hiint(fn[2]);

@@ -79,7 +79,7 @@ struct StageArgs2 {
 
 template <int STAGE>
 struct Slot2 {
-    static constexpr int NFU = (STAGE >= 2 ? 1 : 0) + (STAGE == 4 ? 1 : 0);
+    static constexpr int NFU = STAGE >= 2 ? 1 : 0;           // f_n (stages 2, 3) or u (stage 4)
     static constexpr int SIZE = S2_NLINE * S2_LW + NFU * S2_LT * S2_TM;   // doubles (multiple of 16: 128-B parts)
     static size_t smem_bytes(int qmax) {
         return ((size_t)S2_NSLOT * SIZE + 20 * (size_t)qmax + 32 + 4 * S2_TM) * sizeof(double);  // ring + staging
@@ -186,10 +186,8 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(const StageArgs2 A
                     tma_load_4d(dst + 24 * S2_LW, &M.fs4, cm, l0 + 2, kmm + 2, i + 2, fb);        // C0
                     tma_load_4d(dst + 28 * S2_LW, &M.fs4, cm, l0 + 2, kpp + 2, i + 2, fb);        // C1
                     tma_load_4d(dst + 32 * S2_LW, &M.fs4, cm, l0 + 2, k + 2, i + 2, fb);          // D
-                    if (SL::NFU >= 1)
-                        tma_load_4d(dst + S2_NLINE * S2_LW, &M.fn4, cm + 2, l0 + 2, k + 2, i + 2, fb);   // F
-                    if (SL::NFU >= 2)
-                        tma_load_4d(dst + S2_NLINE * S2_LW + S2_LT * S2_TM, &M.u4, cm + 2, l0 + 2, k + 2, i + 2, fb);  // U
+                    if (SL::NFU >= 1)                                          // F: f_n, or u in stage 4
+                        tma_load_4d(dst + S2_NLINE * S2_LW, STAGE == 4 ? &M.u4 : &M.fn4, cm + 2, l0 + 2, k + 2, i + 2, fb);
                 }
                 if (++slot == S2_NSLOT) { slot = 0; phase ^= 1u; }
             }
@@ -315,7 +313,6 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(const StageArgs2 A
         const double* SC = SB + 16 * S2_LW;
         const double* SD = SC + 8 * S2_LW;
         const double* SF = SA + S2_NLINE * S2_LW;
-        const double* SU = SF + S2_LT * S2_TM;
         // ---- row r: x window, vx faces, vy faces
         const double axr = -Ebx(q, 2);
         const double2 c01 = lds2(SA + (w + 2) * S2_LW + cl - 2), c23 = lds2(SA + (w + 2) * S2_LW + cl),
@@ -403,8 +400,8 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(const StageArgs2 A
                 for (int fc = 0; fc < 3; ++fc)
                     Fvy[fc] = eyi * VY[R1][fc] + cyi * (VY[R2][fc] - VY[R0][fc]) + cyk * (VYk[1][fc] - VYk[0][fc]);
                 double2 fn = make_double2(0.0, 0.0), uu = make_double2(0.0, 0.0);
-                if (STAGE >= 2) fn = lds2(SF + w * S2_TM + 2 * lane);
-                if (STAGE == 4) uu = lds2(SU + w * S2_TM + 2 * lane);
+                if (STAGE == 2 || STAGE == 3) fn = lds2(SF + w * S2_TM + 2 * lane);
+                if (STAGE == 4) uu = lds2(SF + w * S2_TM + 2 * lane);
                 dep ^= __double2hiint(fn.x) ^ __double2hiint(uu.x);
                 double o[2], un[2];
 #pragma unroll
@@ -426,12 +423,12 @@ __global__ void __launch_bounds__(S2_THREADS, 2) k_stage_2d2v(const StageArgs2 A
                     } else if (STAGE == 1) {
                         o[mm] = fs + (0.5 * A.dt) * kk;
                     } else if (STAGE == 2) {
-                        un[mm] = fnm + (fs - fnm) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * kk;
+                        un[mm] = (fnm + fs) * (1.0 / 3.0) + (A.dt * (1.0 / 3.0)) * kk;
                         o[mm] = fnm + (0.5 * A.dt) * kk;
                     } else if (STAGE == 3) {
                         o[mm] = fnm + A.dt * kk;
                     } else {
-                        o[mm] = um + (fs - fnm) * (1.0 / 3.0) + (A.dt * (1.0 / 6.0)) * kk;
+                        o[mm] = um + fs * (1.0 / 3.0) + (A.dt * (1.0 / 6.0)) * kk;
                     }
                 }
                 if (live && act) {
@@ -678,7 +675,10 @@ int launch_stage_2d2v(vlasov_level* L, int stage, double dt, double* f_n, const 
                            const_cast<double*>(f_s), A.org, A.s0, A.s1, A.s2, A.nx, A.ny, A.nvx, A.nvy, E_bc, f0v));
     }
     static const bool faces = std::getenv("VLASOV_C5_FACES") != nullptr;   // experiment: face form
-    if (recon == VLASOV_CENTERED4 && !faces && stage_2d2v_tel_ok(L)) {
+    if (recon == VLASOV_CENTERED4 && !faces && stage_2d2v_acc_ok(L)) {
+        // CENTERED4: telescoped form with per-output accumulators (stage2d_acc.cu)
+        rc = launch_stage_2d2v_acc(L, stage, dt, f_n, f_s, u, f_next, E, rho ? L->d_partials : nullptr);
+    } else if (recon == VLASOV_CENTERED4 && !faces && stage_2d2v_tel_ok(L)) {
         // CENTERED4: telescoped form (stage2d_tel.cu); the moment partials have the same layout
         rc = launch_stage_2d2v_tel(L, stage, dt, f_n, f_s, u, f_next, E, rho ? L->d_partials : nullptr);
     } else {

@@ -29,7 +29,7 @@
 //   A   row r,     y = k0, k0+1,   vx l0-2 .. l0+5   (P, D_vx f, D_vy f, Q, f of the own lines)
 //   B   row i,     y = k0-1, k0+2, vx l0-2 .. l0+5   (D_vx f, D_vy f, Q of the y neighbours)
 //   C   row i,     y = k0-2, k0+3, vx l0 .. l0+3     (Q for D_y)
-//   F,U row i,     y = k0, k0+1,   vx l0 .. l0+3     (f_n, u: RK4 combine, stages 2-4)
+//   F   row i,     y = k0, k0+1,   vx l0 .. l0+3     (f_n in stages 2-3, u in stage 4: RK4 combine)
 // with output row i = r - 2.  Own-line quantities are kept in register windows along x (the
 // x-differences come from the window).  Per-(x, y) velocity coefficients are tabulated in shared
 // memory at kernel start.
@@ -39,6 +39,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 #include <type_traits>
 
 #include "internal.h"
@@ -51,6 +53,7 @@ constexpr int T2_TM = 64;                   // vy cells per tile (2 per lane)
 constexpr int T2_LW = T2_TM + 4;            // doubles per line segment
 constexpr int T2_THREADS = 256;             // 4 consumer warps + producer warpgroup
 constexpr int T2_RMAX = 64;                 // rows per strip (coefficient table capacity)
+constexpr int T2_SMAX = 16;                 // strips along x
 // slot layout (doubles); every part offset is a multiple of 16 doubles (128-B TMA destinations)
 constexpr int T2_A = 0;                     // [2 y][8 vx][68]
 constexpr int T2_B0 = 16 * T2_LW;           // [8][68]
@@ -62,7 +65,7 @@ constexpr int T2_FU = 2 * T2_LT * T2_TM;    // doubles of one F or U part
 
 template <int STAGE>
 struct SlotT {
-    static constexpr int NFU = (STAGE >= 2 ? 1 : 0) + (STAGE == 4 ? 1 : 0);
+    static constexpr int NFU = STAGE >= 2 ? 1 : 0;                             // f_n (stages 2, 3) or u (stage 4)
     static constexpr int SIZE = T2_F + NFU * T2_FU;                           // doubles
     static constexpr int NSLOT = STAGE == 4 ? 3 : 4;                          // 2 CTAs per SM
     static constexpr size_t smem_bytes() { return ((size_t)NSLOT * SIZE + 16 * T2_RMAX) * sizeof(double); }
@@ -83,6 +86,7 @@ struct StageArgsT {
     double* partials;          // [nvx * nmt][nx][ny] moment partials (nullable)
     int64_t s0, s1, s2, org;
     int nx, ny, nvx, nvy, nmt, nstrips;
+    int xb[T2_SMAX + 1];       // strip s covers rows xb[s] .. xb[s+1]-1 (strip lengths may differ)
     double hx, hy, hvx, hvy, vx_lo, vy_lo;
     double sc;                 // stage factor of k (0.5 dt, 0.5 dt, dt, dt/6; 1 for STAGE 0)
 };
@@ -114,8 +118,8 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_stage_2d2v_tel(const StageArg
     b /= nlt;
     const int k0 = 2 * (b % (A.ny / 2));
     const int strip = b / (A.ny / 2);
-    const int x0 = (int)((int64_t)A.nx * strip / A.nstrips);
-    const int x1 = (int)((int64_t)A.nx * (strip + 1) / A.nstrips);
+    const int x0 = A.nstrips <= T2_SMAX ? A.xb[strip] : (int)((int64_t)A.nx * strip / A.nstrips);
+    const int x1 = A.nstrips <= T2_SMAX ? A.xb[strip + 1] : (int)((int64_t)A.nx * (strip + 1) / A.nstrips);
     const int rows = x1 - x0, Q = rows + 4;
     const int ncols = min(T2_TM, A.nvy - mt * T2_TM);
     const int nyg = A.ny + 4;
@@ -172,8 +176,8 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_stage_2d2v_tel(const StageArg
                     tma_load_4d(dst + T2_B1, &M.b, cm, l0, yp2, i, fb);
                     tma_load_4d(dst + T2_C0, &M.c, cm, l0 + 2, ym2, i, fb);
                     tma_load_4d(dst + T2_C1, &M.c, cm, l0 + 2, yp3, i, fb);
-                    if (SL::NFU >= 1) tma_load_4d(dst + T2_F, &M.fn, cm + 2, l0 + 2, k0 + 2, i, fb);
-                    if (SL::NFU >= 2) tma_load_4d(dst + T2_F + T2_FU, &M.u, cm + 2, l0 + 2, k0 + 2, i, fb);
+                    if (STAGE == 2 || STAGE == 3) tma_load_4d(dst + T2_F, &M.fn, cm + 2, l0 + 2, k0 + 2, i, fb);
+                    if (STAGE == 4) tma_load_4d(dst + T2_F, &M.u, cm + 2, l0 + 2, k0 + 2, i, fb);
                 }
                 if (++slot == NSLOT) { slot = 0; phase ^= 1u; }
             }
@@ -261,8 +265,8 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_stage_2d2v_tel(const StageArg
             double2 uu[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
 #pragma unroll
             for (int y = 0; y < 2; ++y) {
-                if (STAGE >= 2) fn[y] = lds2(S + T2_F + (y * T2_LT + w) * T2_TM + 2 * lane);
-                if (STAGE == 4) uu[y] = lds2(S + T2_F + T2_FU + (y * T2_LT + w) * T2_TM + 2 * lane);
+                if (STAGE == 2 || STAGE == 3) fn[y] = lds2(S + T2_F + (y * T2_LT + w) * T2_TM + 2 * lane);
+                if (STAGE == 4) uu[y] = lds2(S + T2_F + (y * T2_LT + w) * T2_TM + 2 * lane);
             }
             const double* ce = cE + 16 * j;
             double o[2][2], un[2][2];
@@ -296,12 +300,12 @@ __global__ void __launch_bounds__(T2_THREADS, 2) k_stage_2d2v_tel(const StageArg
                     if (STAGE == 0 || STAGE == 1) {
                         o[y][mm] = STAGE == 0 ? kk : fs + kk;
                     } else if (STAGE == 2) {
-                        un[y][mm] = fma(2.0 / 3.0, kk, fma(fs - fnm, 1.0 / 3.0, fnm));
+                        un[y][mm] = fma(2.0 / 3.0, kk, (fnm + fs) * (1.0 / 3.0));
                         o[y][mm] = fnm + kk;
                     } else if (STAGE == 3) {
                         o[y][mm] = fnm + kk;
                     } else {
-                        o[y][mm] = fma(fs - fnm, 1.0 / 3.0, um) + kk;
+                        o[y][mm] = fma(fs, 1.0 / 3.0, um) + kk;
                     }
                 }
                 dep ^= __double2hiint(o[y][0]);
@@ -422,13 +426,99 @@ bool stage_2d2v_tel_ok(const vlasov_level* L) {
     return L->dom[1] % 2 == 0 && L->dom[2] % T2_LT == 0 && L->dom[3] % 2 == 0;
 }
 
-// strips of at most T2_RMAX rows, about one wave of 2 CTAs per SM (ragged waves cost less than the
-// 4 warm-up rows of a shorter strip)
-int stage_2d2v_tel_strips(const vlasov_level* L) {
-    const int nx = L->dom[0];
-    int ns = (nx + T2_RMAX - 1) / T2_RMAX;
-    if (const char* e = std::getenv("VLASOV_STRIPS2T")) ns = std::max(ns, atoi(e));
-    return std::max(1, std::min(ns, nx));
+// Strip boundaries along x.  All CTAs of a strip take the same time (rows + warm-up), and the block
+// scheduler hands CTAs out in blockIdx order (strip-major) to 2 slots per SM, so the stage time is
+// the makespan of that list schedule.  Equal strips quantise badly when tiles / slots is far from an
+// integer (C5: 512 tiles on 296 slots = 1.73 waves); two strips of unequal length (long first) fill
+// the last wave.  Candidates: ns equal strips (ns from the T2_RMAX minimum up), and for a level that
+// fits one strip every split (a, nx - a); cost of a CTA = its row steps (rows + 4, rounded up to the
+// unroll group of 4: the dead steps of a ragged group still execute) - 2 (the 4 warm-up rows load
+// the A part only).  Measured on C5 (B200, 3 interleaved runs each, +-0.1): one strip 29.55 G
+// cell-updates/s, (52,12) 31.24, (56,8) 31.46, (60,4) 30.95, (54,10) 30.0, (49,15) 29.6.  CTAs of one strip march in lockstep, so neighbouring tiles still share halo lines
+// through the L2.
+static double strips_makespan(const int* len, int ns, int64_t tiles, int slots) {
+    std::vector<double> heap((size_t)slots, 0.0);                          // min-heap of slot end times
+    auto cmp = [](double a, double b) { return a > b; };
+    double end = 0.0;
+    for (int s = 0; s < ns; ++s)
+        for (int64_t t = 0; t < tiles; ++t) {
+            std::pop_heap(heap.begin(), heap.end(), cmp);
+            const double e = heap.back() + (len[s] + 4 + 3) / 4 * 4 - 2.0;   // row steps run in groups of 4
+            heap.back() = e;
+            std::push_heap(heap.begin(), heap.end(), cmp);
+            end = std::max(end, e);
+        }
+    return end;
+}
+
+int stage_2d2v_choose_strips(int64_t tiles, int nx, int rmax, int smax, const char* env, int* xb) {
+    static int slots = 0;
+    if (!slots) {
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            sms = 148;
+        }
+        slots = 2 * sms;
+    }
+    const int nsmin = (nx + rmax - 1) / rmax;
+    if (nsmin > smax) return nsmin;                                        // equal strips, bounds computed in the kernel
+    std::vector<int> best_len((size_t)smax), len((size_t)smax);
+    int best_ns = 0;
+    double best = 0.0;
+    auto consider = [&](int ns) {
+        const double m = strips_makespan(len.data(), ns, tiles, slots);
+        if (best_ns == 0 || m < (best_ns == nsmin ? best * 0.97 : best)) { // the default must be beaten by 3 %
+            best = m;
+            best_ns = ns;
+            std::copy(len.begin(), len.begin() + ns, best_len.begin());
+        }
+    };
+    auto equal = [&](int ns) {
+        for (int s = 0; s < ns; ++s) len[s] = (int)((int64_t)nx * (s + 1) / ns - (int64_t)nx * s / ns);
+    };
+    const char* e = env ? std::getenv(env) : nullptr;                      // experiments: "ns" or "a,b,..."
+    if (e && std::strchr(e, ',')) {
+        int ns = 0, sum = 0;
+        for (const char* p = e; ns < smax; ++p) {
+            len[ns] = atoi(p);
+            sum += len[ns++];
+            p = std::strchr(p, ',');
+            if (!p) break;
+        }
+        bool ok = sum == nx;
+        for (int s = 0; s < ns; ++s) ok = ok && len[s] >= 1 && len[s] <= rmax;
+        if (ok) consider(ns);
+    } else if (e) {
+        const int ns = std::min(std::max(nsmin, std::min(atoi(e), nx)), smax);
+        equal(ns);
+        consider(ns);
+    }
+    if (best_ns == 0 && tiles * nsmin <= 65536) {                          // bound the host-side search
+        for (int ns = nsmin; ns <= std::min({nsmin + 3, nx, smax}); ++ns) {
+            equal(ns);
+            consider(ns);
+        }
+        if (nsmin == 1 && nx <= 256)
+            for (int a = nx - 1; 2 * a >= nx; --a) {                       // long strip first
+                len[0] = a;
+                len[1] = nx - a;
+                consider(2);
+            }
+    }
+    if (best_ns == 0) {
+        best_ns = nsmin;
+        equal(best_ns);
+        std::copy(len.begin(), len.begin() + best_ns, best_len.begin());
+    }
+    xb[0] = 0;
+    for (int s = 0; s < best_ns; ++s) xb[s + 1] = xb[s] + best_len[s];
+    return best_ns;
+}
+
+int stage_2d2v_tel_strips(const vlasov_level* L, int* xb) {
+    const int64_t tiles = (int64_t)((L->dom[3] + T2_TM - 1) / T2_TM) * (L->dom[2] / T2_LT) * (L->dom[1] / 2);
+    return stage_2d2v_choose_strips(tiles, L->dom[0], T2_RMAX, T2_SMAX, "VLASOV_STRIPS2T", xb);
 }
 
 int launch_stage_2d2v_tel(vlasov_level* L, int stage, double dt, double* f_n, const double* f_s, double* u,
@@ -446,7 +536,9 @@ int launch_stage_2d2v_tel(vlasov_level* L, int stage, double dt, double* f_n, co
     A.nvx = L->dom[2];
     A.nvy = L->dom[3];
     A.nmt = (A.nvy + T2_TM - 1) / T2_TM;
-    A.nstrips = stage_2d2v_tel_strips(L);
+    if (L->tel_ns == 0) L->tel_ns = stage_2d2v_tel_strips(L, L->tel_xb);
+    A.nstrips = L->tel_ns;
+    std::copy(L->tel_xb, L->tel_xb + T2_SMAX + 1, A.xb);
     A.hx = L->h[0];
     A.hy = L->h[1];
     A.hvx = L->h[2];

@@ -45,7 +45,7 @@ tot = sum(p["dram_read_bytes"] + max(p["dram_write_bytes"], p["l2_write_bytes_fr
 if len(per) != 4:
     sys.exit(f"need the 4 stage launches of one step, found {len(per)}")
 res = {"source": f"ncu --set full --clock-control none, {len(per)} stage launches of one {wname} RK4 step ({rep})",
-       "bytes_per_step": tot, "bytes_per_step_per_cell": tot / cells, "algorithmic_bytes_per_step_per_cell": 104,
+       "bytes_per_step": tot, "bytes_per_step_per_cell": tot / cells, "algorithmic_bytes_per_step_per_cell": 96,
        "definition": "per launch: dram__bytes_read.sum + max(dram__bytes_write.sum, 32 x "
                      "lts__t_sectors_srcunit_tex_op_write.sum) (every sector the kernel dirties in L2 is "
                      "written back once, during or after the launch)",
