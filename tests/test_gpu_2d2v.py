@@ -140,12 +140,13 @@ def test_rhs_parity_2d2v(shape, recon):
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("shape", [(8, 6, 12, 70), (8, 8, 12, 70)])
 @pytest.mark.parametrize("recon", [scheme.CENTERED4, scheme.UPWIND])
-def test_constant_state_rhs_is_exactly_zero_2d2v(recon):
+def test_constant_state_rhs_is_exactly_zero_2d2v(recon, shape):
     # free-stream preservation: f == c (and the unperturbed profile == c,
     # so every velocity ghost is c whatever the direction) gives k == 0 bitwise for any field --
     # every difference of equal values is an exact zero in the telescoped form as in the face form
-    w = inputs.scaled(inputs.get("C5"), (8, 6, 12, 70), (8, 6, 12, 70))
+    w = inputs.scaled(inputs.get("C5"), shape, shape)
     c = 0.3125
     f0v = np.full_like(inputs.background_profile(w), c)
     S = UniformVlasov2D(w.ncells, w.lower, inputs.spacing(w), inputs.level0_boxes(w), f0v,
@@ -172,3 +173,22 @@ def test_stage_kernels_deterministic_2d2v():
             S.step(dt)
         outs.append((S.get_state(), S.moment()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_accumulator_form_kernel_parity_subprocess():
+    """The opt-in accumulator-form CENTERED4 kernel (stage2d_acc.cu, VLASOV_C5_ACC=1; the choice is
+    read once per process): the stage, rhs, one-step, ten-step, constant-state and determinism tests of this file
+    re-run with it in a child process."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("VLASOV_C5_ACC"):
+        pytest.skip("already running with the accumulator-form kernel")
+    env = dict(os.environ, VLASOV_C5_ACC="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_2d2v.py"), "-m", "gpu", "-q", "-x",
+                        "-p", "no:cacheprovider", "-k",
+                        "test_one_step or test_ten_steps_and_moment or constant_state or deterministic or half_step or rhs_parity"],
+                       env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
