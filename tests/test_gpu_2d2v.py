@@ -101,19 +101,19 @@ def test_c5_full_size_one_step():
     assert relerr(got, ref) < 1e-12
 
 
-def test_c5_full_size_ten_steps_bench_launch():
-    # BASELINE.json C5 at full size in the bench's launch configuration (one-step CUDA graph,
-    # replayed): 10 steps within 1e-11
+def test_c5_full_size_eleven_steps_bench_launch():
+    # BASELINE.json C5 at full size in the bench's launch configuration (a CUDA graph of 5 RK4
+    # steps, replayed): 1 eager + 2 x 5 graph steps within 1e-11
     w = inputs.get("C5")
     f0 = inputs.initial_cell_averages(w)
     dt = inputs.fixed_dt(w)
     S = _solver(w)
     S.set_state(f0)
-    S.capture(dt, steps=1)                   # runs one eager step first
-    for _ in range(9):
+    S.capture(dt, steps=5)                   # runs one eager step first
+    for _ in range(2):
         S.replay()
     got = S.get_state()
-    ref, _ = uniform.problem_for(w).run(f0, dt, 10)
+    ref, _ = uniform.problem_for(w).run(f0, dt, 11)
     assert relerr(got, ref) < 1e-11
 
 
