@@ -366,7 +366,12 @@ def run_vslab(args, w, rank, world, local):
     wg = replace(w, ncells=(w.ncells[0], w.ncells[1] * world), name=f"{w.name}-vslab{world}")
     h = inputs.spacing(wg)
     dt = inputs.fixed_dt(wg)
-    comm = DistComm.with_p2p_group(rank, world) if world > 1 else LocalComm()
+    # VLASOV_VSLAB_DIST=1 under torchrun --nproc-per-node 1: the NCCL transport with one rank (the
+    # all-reduce and its stream-ordered wait inside the graph capture; no neighbours to exchange with)
+    use_dist = world > 1 or (os.environ.get("VLASOV_VSLAB_DIST") and "RANK" in os.environ)
+    if use_dist and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = DistComm.with_p2p_group(rank, world) if use_dist else LocalComm()
     G = VSlabVlasov1D(wg.ncells, wg.lower, h, inputs.background_profile(wg), world, [rank], comm)
     G.set_state(lambda vr: inputs.initial_cell_averages(
         wg, None, ((0, vr.start), (wg.ncells[0] - 1, vr.stop - 1))))

@@ -75,6 +75,7 @@ struct StageArgs1 {
     int nstrip1;               // > 0: single block, tiles computed from blockIdx (no table load)
     Block1 blk0;               // that block
     int xshift;                // single block: strips start xshift rows later (periodic wrap; L2 reuse)
+    int l2hint;                // L2 eviction priorities per field (single periodic block; see `issue`)
 };
 
 // the fused prologue stages the whole (periodically extended) Green's function in shared memory
@@ -278,6 +279,17 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         if (NEED_U && out_row) bytes += row_bytes;
         double* dst = smem + sl * SLOT;
         mbar_arrive_expect_tx(&full_bar[sl], bytes);
+        if (A.l2hint) {
+            // L2 residency by reuse distance (4 fields of the level size, an L2 of about two): f_n
+            // is read by stages 1-3 and overwritten in place by stage 4 -> kept (evict_last, the
+            // stage-4 store too); a stage state f_2, f_3, f_4 and u are dead once read -> evict_first;
+            // f_next is stored with the default priority (the next stage reads it, strip-shifted).
+            bulk_g2s_hint(dst, A.f_s + rowbase(rs) + T.j0 - 2, seg_bytes, &full_bar[sl], STAGE <= 1 ? l2_evict_last() : l2_evict_first());
+            if (NEED_FN && out_row)
+                bulk_g2s_hint(dst + SEG, A.f_n + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl], STAGE == 2 ? l2_evict_last() : l2_evict_first());
+            if (NEED_U && out_row) bulk_g2s_hint(dst + SEG, A.u_in + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl], l2_evict_first());
+            return;
+        }
         bulk_g2s(dst, A.f_s + rowbase(rs) + T.j0 - 2, seg_bytes, &full_bar[sl]);
         if (NEED_FN && out_row) bulk_g2s(dst + SEG, A.f_n + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl]);
         if (NEED_U && out_row) bulk_g2s(dst + SEG, A.u_in + rowbase(wr(r - 2)) + T.j0, row_bytes, &full_bar[sl]);
@@ -589,6 +601,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
     if (sel_cta && tid == 0) mbar_arrive(&e_ready);
     TRACE(5);
     const int cl = CPT * tid;                    // tile-local column of my first cell
+    const uint64_t pol_st = STAGE == 4 ? l2_evict_last() : l2_evict_first();   // f_{n+1} (stage 4), u (stage 2) stores
     const int c0 = T.j0 + cl;                    // block-local interior column
     const int nact = min(CPT, T.ncols - cl);     // active cells of this thread (may be <= 0)
     // SELF levels have nv % 4 == 0: a thread is either fully active or idle
@@ -735,8 +748,12 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                 if (live && act) {
 #pragma unroll
                     for (int m = 0; m < CPT; m += 2) {
-                        *reinterpret_cast<double2*>(op + m) = make_double2(o[m], o[m + 1]);
-                        if (STAGE == 2) *reinterpret_cast<double2*>(up + m) = make_double2(uu[m], uu[m + 1]);
+                        if (STAGE == 4 && A.l2hint) stg2_hint(op + m, o[m], o[m + 1], pol_st);
+                        else *reinterpret_cast<double2*>(op + m) = make_double2(o[m], o[m + 1]);
+                        if (STAGE == 2) {
+                            if (A.l2hint) stg2_hint(up + m, uu[m], uu[m + 1], pol_st);
+                            else *reinterpret_cast<double2*>(up + m) = make_double2(uu[m], uu[m + 1]);
+                        }
                     }
                 }
             } else if (live) {
@@ -995,6 +1012,12 @@ int stage_1d1v_max_clusters(bool wide, int tile_rows, int cs, int n) {
 }
 
 // strip shift of the even stages in quarters of a strip (VLASOV_XSHIFT, experiments; default 2)
+// L2 eviction priorities (VLASOV_L2HINT=0 disables; experiments)
+static int l2hint_on() {
+    static const int q = [] { const char* e = getenv("VLASOV_L2HINT"); return e ? atoi(e) : 1; }();
+    return q;
+}
+
 static int shift_quarters() {
     static const int q = [] { const char* e = getenv("VLASOV_XSHIFT"); return e ? atoi(e) : 2; }();
     return q;
@@ -1018,6 +1041,7 @@ int launch_stage_1d1v(vlasov_level* L, int stage, double dt, double* f_n, const 
     // L2 reuse between stages: even stages start their strips half a strip later, so each CTA
     // first reads the rows the previous stage wrote last (still in L2)
     A.xshift = (A.nstrip1 > 0 && (stage % 2) == 0) ? L->dom[0] / A.nstrip1 * shift_quarters() / 4 : 0;
+    A.l2hint = (A.nstrip1 > 0 && stage >= 1) ? l2hint_on() : 0;
     if (!L->h_blocks1.empty()) A.blk0 = L->h_blocks1[0];
     A.f_s = f_s;
     A.f_n = f_n;

@@ -16,6 +16,8 @@ timeout 600 python bench.py --workload C5 --steps 10 --no-cpu-baseline > $O/benc
 timeout 600 python bench.py --workload C5P --steps 10 --no-cpu-baseline > $O/bench_c5p.json 2> $O/bench_c5p.err
 timeout 900 python bench.py --workload C3 --steps 20 > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 600 python bench.py --shard vslab --steps 10 --no-cpu-baseline > $O/bench_vslab1.json 2> $O/bench_vslab1.err
+VLASOV_VSLAB_DIST=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 \
+  bench.py --gpus 1 --shard vslab --steps 10 --no-cpu-baseline > $O/bench_vslab1_nccl.json 2> $O/bench_vslab1_nccl.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 300 python tools/time_regrid.py > $O/regrid_phases.txt 2>&1
 PS="python tools/profile_step.py --steps 3"
