@@ -35,6 +35,11 @@ STAGE_BYTES = {1: 16, 2: 32, 3: 24, 4: 24}
 STEP_BYTES = sum(STAGE_BYTES.values())          # 96 B per cell per RK4 step
 
 
+# a rank's stdout must hold the JSON line only: NCCL_DEBUG=VERSION makes NCCL print its version there
+if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
+
+
 def read_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
