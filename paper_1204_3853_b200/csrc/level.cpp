@@ -212,11 +212,11 @@ void free_level(vlasov_level* L) {
 
 inline int wrap(int x, int n) { return ((x % n) + n) % n; }
 
-// fused field of the 1D+1V stage: Toeplitz rows split over the strip's cluster (default), or the
-// O(n) split of the Green's function (VLASOV_FIELD=split): exact and tiling-independent, but
-// measured slower on B200 (C4: 191 vs 185 us per step)
+// fused field of the 1D+1V stage: the O(n) split of the Green's function, each CTA for its own rows
+// (default for n >= 64; C4 on B200: 151 us per step), or the Toeplitz rows split over the strip's
+// cluster (VLASOV_FIELD=toeplitz: 160 us)
 bool split_field() {
-    static const bool s = [] { const char* e = std::getenv("VLASOV_FIELD"); return e && std::string(e) == "split"; }();
+    static const bool s = [] { const char* e = std::getenv("VLASOV_FIELD"); return !(e && std::string(e) == "toeplitz"); }();
     return s;
 }
 

@@ -366,22 +366,20 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
 
     // ---------------------------------------------------------------- consumers
     if (SPLIT && field) {
-        // Constraint evaluation of the stage state (Alg.5) in O(n): the exact discrete
-        // Green's function of E = -D4 phi is a sawtooth plus a part decaying like 0.0718^|m|
-        // (DESIGN.md 6.1), so with r = rho - mean
+        // Constraint evaluation of the stage state (Alg.5) in O(n) per CTA: the exact
+        // discrete Green's function of E = -D4 phi is a sawtooth plus a part decaying like
+        // 0.0718^|m|, so with r = rho - mean
         //   E_i = K2 (sum r - r_i) - Kn (i sum r - sum_k k r_k + n S_i) + sum_{|m|<=HM} h(m) r_{i-m},
         //   S_i = sum_{k>i} r_k.
-        // Every CTA computes the sums in the same fixed order (32-cell chunks summed by thread
-        // pairs; a warp scan over the chunk sums; per row the rest of its chunk), so E does not
-        // depend on the tiling.
+        // A CTA needs S_i for its Q consecutive rows only: S of its first row i0 is one more block
+        // reduction (with sum r and sum k r_k), the others follow from S_{i+1} = S_i - r_{i+1}
+        // (periodic rows: + sum r past the wrap).  No cluster, no scan; fixed summation orders.
         const int n = A.dom_x;
         const double* s_rho = f_rho;
-        const int nch = (n + 31) >> 5;
-        double* s_cs = f_rho + n + PART_MAX;     // [nch + 1] chunk sums -> sums of the later chunks; [nch]: sum r
-        double* s_ct = s_cs + nch + 1;           // [NW] warp partials of sum k r_k; [NW]: the total
+        double* s_w = f_rho + n + PART_MAX;      // [3 NW] warp partials of sum r, sum k r, S_{i0}
         mbar_wait(&field_bar, 0);
         TRACE(2);
-        {   // mean: as below (warp quarters, warp partials in warp order)
+        {   // mean: warp quarters, warp partials in warp order
             const int kb = (int)((int64_t)n * warp / NW), ke = (int)((int64_t)n * (warp + 1) / NW);
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             int k = kb + lane;
@@ -400,71 +398,48 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         for (int w = 0; w < NW; ++w) mean += psum[w];
         mean /= (double)n;
         TRACE(3);
-        // chunk sums of r = rho - mean (32-cell chunks) and the total of k r: thread t sums the
-        // cells [16 t, 16 t + 16) in order, a chunk is the sum of its two halves (one shuffle), the
-        // totals are fixed shuffle trees + warp partials in warp order -- the same expressions in
-        // every CTA (E independent of the tiling)
-        double tkr = 0.0;
-        const int niter = (32 * nch + 16 * NT - 1) / (16 * NT);          // uniform trip count (shuffles)
-        for (int it = 0; it < niter; ++it) {
-            const int h0 = 16 * tid + it * 16 * NT;
-            double hs_ = 0.0, hk = 0.0;
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int k = h0 + u;
-                const double r = k < n ? s_rho[k] - mean : 0.0;
-                hs_ += r;
-                hk = fma((double)k, r, hk);
+        int i0 = B.lo_x + T.x0 - 2;              // periodic row of tile row 0
+        i0 += (i0 < 0) ? n : 0;
+        i0 -= (i0 >= n) ? n : 0;
+        i0 -= (i0 >= n) ? n : 0;
+        {   // sum r, sum k r_k, S_{i0}: thread-strided partial sums, shuffle trees, warp order
+            double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+            for (int k = tid; k < n; k += NT) {
+                const double r = s_rho[k] - mean;
+                q0 += r;
+                q1 = fma((double)k, r, q1);
+                q2 += (k > i0) ? r : 0.0;
             }
-            const double cs = hs_ + __shfl_xor_sync(0xffffffffu, hs_, 1);      // the chunk's two halves
-            if ((tid & 1) == 0 && (h0 >> 5) < nch) s_cs[h0 >> 5] = cs;
-            tkr += hk;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                q0 += __shfl_xor_sync(0xffffffffu, q0, o);
+                q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+                q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+            }
+            if (lane == 0) { s_w[3 * warp] = q0; s_w[3 * warp + 1] = q1; s_w[3 * warp + 2] = q2; }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tkr += __shfl_xor_sync(0xffffffffu, tkr, o);
-        if (lane == 0) s_ct[warp] = tkr;
         named_bar_sync(1, NT);
-        if (warp == 0) {                         // suffix sums of the chunk sums, sum r
-            const int per = (nch + 31) >> 5, c0 = lane * per, c1 = min(nch, c0 + per);
-            double tot = 0.0;
-            for (int c = c1 - 1; c >= c0; --c) tot += s_cs[c];
-            double suf = tot;                    // inclusive suffix over the lanes (Kogge-Stone)
+        double sumr = 0.0, T1 = 0.0, S0 = 0.0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double t = __shfl_down_sync(0xffffffffu, suf, o);
-                if (lane + o < 32) suf += t;
-            }
-            const double all = __shfl_sync(0xffffffffu, suf, 0);
-            double acc = suf - tot;              // chunks of the higher lanes
-            for (int c = c1 - 1; c >= c0; --c) { const double cc = s_cs[c]; s_cs[c] = acc; acc += cc; }
-            if (lane == 0) {
-                double t1 = 0.0;
-#pragma unroll
-                for (int w = 0; w < NW; ++w) t1 += s_ct[w];
-                s_cs[nch] = all;
-                s_ct[NW] = t1;
-            }
-        }
-#ifdef STAGE1D_TRACE
-        if (tid == 0 && blockIdx.x < 2048) g_trace[blockIdx.x][9] = gtimer();
-#endif
-        named_bar_sync(1, NT);
-        const double sumr = s_cs[nch], T1 = s_ct[NW];
+        for (int w = 0; w < NW; ++w) { sumr += s_w[3 * w]; T1 += s_w[3 * w + 1]; S0 += s_w[3 * w + 2]; }
         for (int t = tid; t < Q; t += NT) {
-            int i = B.lo_x + T.x0 - 2 + t;                                 // row of the periodic domain
-            i += (i < 0) ? n : 0;
-            i -= (i >= n) ? n : 0;
-            i -= (i >= n) ? n : 0;
-            const double ri = s_rho[i] - mean;
-            double sgt = 0.0;                    // sum_{k > i} r_k: the rest of i+1's chunk, later chunks
-            if (i + 1 < n) {
-                const int ce = min(n, (((i + 1) >> 5) + 1) << 5);
-                double a = 0.0, b = 0.0;
-                int k = i + 1;
-                for (; k + 1 < ce; k += 2) { a += s_rho[k] - mean; b += s_rho[k + 1] - mean; }
-                if (k < ce) a += s_rho[k] - mean;
-                sgt = (a + b) + s_cs[(i + 1) >> 5];
+            const bool wrapped = i0 + t >= n;
+            const int i = wrapped ? i0 + t - n : i0 + t;                   // row of the periodic domain (Q <= n)
+            double pa = 0.0, pb = 0.0;           // sum_{s=1..t} r_{i0+s}: two interleaved partial sums
+            {
+                int k = i0 + 1;
+                k -= (k >= n) ? n : 0;
+                int sidx = 1;
+                for (; sidx + 1 <= t; sidx += 2) {
+                    const int k1 = (k + 1 >= n) ? k + 1 - n : k + 1;
+                    pa += s_rho[k] - mean;
+                    pb += s_rho[k1] - mean;
+                    k = (k1 + 1 >= n) ? k1 + 1 - n : k1 + 1;
+                }
+                if (sidx <= t) pa += s_rho[k] - mean;
             }
+            const double sgt = S0 - (pa + pb) + (wrapped ? sumr : 0.0);    // S_i
+            const double ri = s_rho[i] - mean;
             double e0 = A.K2 * (sumr - ri) - A.Kn * ((double)i * sumr - T1 + (double)n * sgt);
             double e1 = 0.0, e2 = 0.0;           // local part: three interleaved partial sums
 #pragma unroll

@@ -23,7 +23,11 @@
 // neighbour lines per 4 own lines instead of per 2) and ~30 % fewer TMA bytes (56 line segments per
 // 16 output lines instead of 40 per 8).  A constant f still gives k == 0 exactly (every e, D and d
 // of equal values is an exact zero).  The stage's f_s enters the RK4 combine through the
-// accumulator (stages 1, 4) or is re-read with f_n / u from global memory when the row completes.
+// accumulator (stages 1, 4) or a two-row register window (stage 2).
+//
+// Measured on B200: parity-green but not faster than stage2d_tel.cu in any variant
+// tried, so it is opt-in (VLASOV_C5_ACC=1): at 8 warps per SM the row step is a latency chain, and
+// fewer shared-memory wavefronts do not shorten it.
 //
 // Layout: [x][y][vx][vy], vy contiguous, ghost frame 2; the velocity ghost frame of f_s is derived
 // before the stage by k_vghost_2d2v (reading #6); x, y periodic by coordinates.  CTA = 4 y lines
@@ -34,8 +38,8 @@
 //   B   y = k0-1, k0+4,   vx l0-2 .. l0+5   (D_vx f, D_vy f, Q of the y neighbours)
 //   C   y = k0-2, k0+5,   vx l0 .. l0+3     (Q for D_y)
 // B and C only for rows inside the strip (the 2+2 rows around it contribute through x only).
-// f_n, u (and f_s of the completing row, stage 2) arrive in a single-buffered part of their own
-// (issued when the previous row's has been consumed, prefetched into the L2 two rows earlier).
+// f_n (stages 2, 3) or u (stage 4) of the completing row arrives in a single-buffered part of its
+// own (issued when the previous row's has been consumed, prefetched into the L2 earlier).
 // The per-(x, y) velocity coefficients are produced row by row by a helper warp of the producer
 // warpgroup into an 8-row ring (they ride on the slot's full barrier), so a strip may have any
 // number of rows.

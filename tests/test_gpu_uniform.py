@@ -310,20 +310,28 @@ np.save({out!r}, np.concatenate([S.get_state().ravel(), S.rhos[0].cpu().numpy()]
 
 def test_strip_shift_changes_no_result(tmp_path):
     """The even stages' strip shift (L2 reuse, DESIGN 6.1) is a reordering of independent row
-    work: three fused RK4 steps with and without it (VLASOV_XSHIFT) are bitwise equal."""
+    work: three fused RK4 steps with and without it (VLASOV_XSHIFT) are bitwise equal with the
+    Toeplitz field (a row's E does not depend on its position in the strip) and equal to rounding
+    with the default O(n) field (the summation order of S_i starts at the strip's first row)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for q in ("0", "2", "1"):
-        out = str(tmp_path / f"s{q}.npy")
-        code = _SHIFT_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), out=out)
-        env = dict(os.environ, VLASOV_XSHIFT=q)
-        subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
-        res[q] = np.load(out)
-    assert np.array_equal(res["0"], res["2"])
-    assert np.array_equal(res["0"], res["1"])
+    for field in ("toeplitz", "split"):
+        res = {}
+        for q in ("0", "2", "1"):
+            out = str(tmp_path / f"s{field}{q}.npy")
+            code = _SHIFT_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), out=out)
+            env = dict(os.environ, VLASOV_XSHIFT=q, VLASOV_FIELD=field)
+            subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+            res[q] = np.load(out)
+        if field == "toeplitz":
+            assert np.array_equal(res["0"], res["2"])
+            assert np.array_equal(res["0"], res["1"])
+        else:
+            tol = 1e-13 * np.abs(res["0"]).max()
+            np.testing.assert_allclose(res["2"], res["0"], rtol=0, atol=tol)
+            np.testing.assert_allclose(res["1"], res["0"], rtol=0, atol=tol)
 
 
 @pytest.mark.parametrize("mode", list(MODES))
@@ -377,7 +385,7 @@ def test_stage_vp_rejects_aliasing():
 _SPLIT_SCRIPT = r"""
 import os, sys, numpy as np, torch
 sys.path.insert(0, {root!r})
-os.environ["VLASOV_FIELD"] = "split"
+os.environ["VLASOV_FIELD"] = {field!r}
 import inputs
 from paper_1204_3853_b200.solver import UniformVlasov1D
 w = inputs.scaled(inputs.get("C4"), ({nx}, 1024), (64, 64))
@@ -389,16 +397,19 @@ np.save({out!r}, S.get_state())
 """
 
 
+@pytest.mark.parametrize("field", ["toeplitz", "split"])
 @pytest.mark.parametrize("nx", [512, 300])
-def test_split_field_option_parity(tmp_path, nx):
-    """VLASOV_FIELD=split (the O(n) sawtooth + local split of the exact Green's function in the
-    fused stage prologue): 5 fused steps against the oracle within 1e-11."""
+def test_fused_field_variants_parity(tmp_path, nx, field):
+    """Both variants of the fused stage prologue's field: the O(n) sawtooth + local
+    split of the exact Green's function (default) and the cluster Toeplitz rows
+    (VLASOV_FIELD=toeplitz; the choice is read once per process): 5 fused steps against the oracle
+    within 1e-11."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = str(tmp_path / "s.npy")
-    r = subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT.format(root=root, out=out, nx=nx)], capture_output=True,
+    r = subprocess.run([sys.executable, "-c", _SPLIT_SCRIPT.format(root=root, out=out, nx=nx, field=field)], capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     w = inputs.scaled(inputs.get("C4"), (nx, 1024), (64, 64))
