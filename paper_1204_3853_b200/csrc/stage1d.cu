@@ -143,11 +143,11 @@ struct StageGeom {
     static constexpr int NFN = STAGE >= 2 ? 1 : 0;           // f_n row (stages 2, 3) or u row (stage 4)
     static constexpr int SLOT = SEG + NFN * TV;              // doubles per ring slot
     // ring depth: ~RING_KB of row data per CTA, 3..16 slots (a slot is consumed in one row step)
-    // ring size per stage (measured on C4: stage 2 best at 48 KB, stages 3 and 4 at 64 KB)
+    // ring size per stage (measured on C4: stage 2 best at 48 KB, stages 1, 3 and 4 at 64 KB)
 #ifdef RING_KB_ALL
     static constexpr int RKB = RING_KB_ALL;
 #else
-    static constexpr int RKB = STAGE >= 3 ? 64 : RING_KB;
+    static constexpr int RKB = STAGE == 2 ? RING_KB : 64;
 #endif
     static constexpr int NSLOT_RAW = (RKB * 1024) / (SLOT * 8);
     static constexpr int NSLOT = NSLOT_RAW < 4 ? 4 : (NSLOT_RAW > 16 ? 16 : NSLOT_RAW);
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
         //   S_i = sum_{k>i} r_k.
         // A CTA needs S_i for its Q consecutive rows only: S of its first row i0 is one more block
         // reduction (with sum r and sum k r_k), the others follow from S_{i+1} = S_i - r_{i+1}
-        // (periodic rows: + sum r past the wrap).  No cluster, no scan; fixed summation orders.
+        // (periodic rows: + sum r per wrap).  No cluster, no scan; fixed summation orders.
         const int n = A.dom_x;
         const double* s_rho = f_rho;
         double* s_w = f_rho + n + PART_MAX;      // [3 NW] warp partials of sum r, sum k r, S_{i0}
@@ -423,8 +423,8 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
 #pragma unroll
         for (int w = 0; w < NW; ++w) { sumr += s_w[3 * w]; T1 += s_w[3 * w + 1]; S0 += s_w[3 * w + 2]; }
         for (int t = tid; t < Q; t += NT) {
-            const bool wrapped = i0 + t >= n;
-            const int i = wrapped ? i0 + t - n : i0 + t;                   // row of the periodic domain (Q <= n)
+            const int wraps = (i0 + t) / n;                                // periodic wraps (Q may exceed n)
+            const int i = i0 + t - wraps * n;                              // row of the periodic domain
             double pa = 0.0, pb = 0.0;           // sum_{s=1..t} r_{i0+s}: two interleaved partial sums
             {
                 int k = i0 + 1;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(Roles<NT>::THREADS, STAGE1D_MINB) k_stage_1d1v
                 }
                 if (sidx <= t) pa += s_rho[k] - mean;
             }
-            const double sgt = S0 - (pa + pb) + (wrapped ? sumr : 0.0);    // S_i
+            const double sgt = S0 - (pa + pb) + (double)wraps * sumr;      // S_i
             const double ri = s_rho[i] - mean;
             double e0 = A.K2 * (sumr - ri) - A.Kn * ((double)i * sumr - T1 + (double)n * sgt);
             double e1 = 0.0, e2 = 0.0;           // local part: three interleaved partial sums
