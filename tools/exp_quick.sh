@@ -1,10 +1,12 @@
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/quick; mkdir -p $O; : > $O/exp.log
-timeout 900 python -m pytest tests/test_gpu_uniform.py tests/test_gpu_vslab.py -m gpu -x -q -p no:cacheprovider > $O/pytest.txt 2>&1
-tail -3 $O/pytest.txt >> $O/exp.log
-for rep in 1 2 3; do
-  timeout 300 python bench.py --no-cpu-baseline > $O/b.json 2> $O/b.err
-  python -c "
-import json; d=json.load(open('$O/b.json')); print(round(d['value']/1e9,2), round(d['ms_per_step'],4), d['roofline']['frac'], [round(x*1e3,1) for x in d['roofline']['stage_ms_eager']])" >> $O/exp.log 2>&1
-done
-cat $O/exp.log
+O=gpurun_out/fin; mkdir -p $O
+timeout 900 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err
+timeout 600 python bench.py --workload C5 --steps 10 --no-cpu-baseline > $O/bench_c5.json 2> $O/bench_c5.err
+timeout 600 python bench.py --workload C5P --steps 10 --no-cpu-baseline > $O/bench_c5p.json 2> $O/bench_c5p.err
+timeout 300 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "bench or smoke or c1_one_step" > $O/pytest_small.txt 2>&1
+tail -2 $O/pytest_small.txt
+python -c "
+import json
+for n in ('c4','c5','c5p'):
+    d=json.load(open('$O/bench_%s.json'%n)); print(n, round(d['value']/1e9,2), d['ms_per_step'], d['roofline']['frac'], d['e2e']['value'], (d.get('cpu_baseline') or {}).get('value'))
+"
